@@ -1,0 +1,205 @@
+/*
+ * ig_b200.h — C-ABI of the B200-native Interpretable-Generalization hot path.
+ *
+ * This is the drop-in boundary of SURVEY.md §8(b).  Every entry point takes
+ * plain pointers and sizes (no torch / C++ types) and returns an int status.
+ * Packed rows use the reference layout exactly (proj/include/ig/bitpack.hpp:15-26,
+ * proj/src/bitpack.cpp:17-28): row-major n x K int64 words, K = ceil(L/64),
+ * bit j in word j/64 at position j%64 (LSB first), padding bits >= L zero.
+ *
+ * Host pointers are the default.  Functions suffixed `_device` take device
+ * pointers that stay resident in HBM (the bench's `value` leg); everything
+ * runs on the context's stream (ig_ctx_set_stream).
+ *
+ * Each declaration cites the reference interface it replaces.  A thin C++
+ * shim that implements `ig::KernelBackend` and the `mine.hpp` free functions on
+ * top of this ABI is shown in INTEGRATION.md.
+ */
+#ifndef IG_B200_H
+#define IG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---------------------------------------------------------------- status
+ * One code per reference exception type; no exception crosses the ABI.      */
+enum ig_status {
+    IG_OK = 0,
+    IG_E_INVALID_ARG = 1, /* std::invalid_argument  kernels.cpp:22-36,93,110; bitpack.cpp:53-58 */
+    IG_E_RANGE = 2,       /* std::out_of_range      bitpack.cpp:20-24 */
+    IG_E_CONFIG = 3,      /* ig::ConfigError        kernels.cpp:12-15,193; pipeline.cpp:113-119 */
+    IG_E_IO = 4,          /* ig::IoError            csv.cpp:98-103 */
+    IG_E_DATA = 5,        /* ig::DataError          csv.cpp:32-36; pipeline.cpp:42,110,174,190,310,317 */
+    IG_E_OVERFLOW = 6,    /* ig::ArithmeticError    kernels.cpp:40-46,174-176; mine.hpp:46-51 */
+    IG_E_CUDA = 7,        /* CUDA runtime failure (no reference counterpart) */
+    IG_E_NCCL = 8,
+    IG_E_OOM = 9
+};
+
+typedef struct ig_ctx ig_ctx;
+
+/* Context = one device + one stream + the resident buffers.  Not thread-safe:
+ * concurrent callers use one context each (kernels.hpp:23-26 purity holds
+ * because every call is a pure function of its inputs). */
+int ig_ctx_create(int device, ig_ctx** out);
+void ig_ctx_destroy(ig_ctx* ctx);
+/* Message of the last failing call on this context (thread-local when ctx is NULL). */
+const char* ig_last_error(const ig_ctx* ctx);
+/* Run subsequent work on `stream` (a cudaStream_t); NULL restores the context's own. */
+int ig_ctx_set_stream(ig_ctx* ctx, void* stream);
+/* Number of kernels this context has launched so far (bench `gpu_launches`). */
+uint64_t ig_ctx_launch_count(const ig_ctx* ctx);
+const char* ig_version(void);
+/* Integer-pipe micro-benchmark: sustained LOP3.32/s and POPC.32/s of the whole
+ * device (roofline denominator of the AND/POPC kernels). */
+int ig_measure_int_peaks(ig_ctx* ctx, double* lop3_per_s, double* popc_per_s);
+
+/* KernelConfig (kernels.hpp:14-21).  pair_batch / coverage_block must be >= 1
+ * (kernels.cpp:12-15) and never change results; threads is ignored. */
+typedef struct {
+    size_t pair_batch;
+    size_t coverage_block;
+    size_t memory_budget_bytes;
+    int threads;
+} ig_kernel_config;
+void ig_kernel_config_default(ig_kernel_config* cfg);
+
+/* ---------------------------------------------------------------- KernelBackend
+ * kernels.hpp:27-53 — the three batched primitives.                          */
+
+/* out[t] = rows[left] & rows[j_begin+t]; window must lie in (left, n]
+ * (kernels.hpp:33-39; kernels.cpp:19-32).  Contract conformance only: the fit
+ * never crosses the boundary per left row. */
+int ig_pair_intersect_batch(ig_ctx* ctx, const int64_t* rows, size_t n_rows, uint32_t logical_len,
+                            size_t left, size_t j_begin, size_t j_end, int64_t* out);
+
+/* mask[p] = 1 iff some opponent row is a superset of pattern p
+ * (kernels.hpp:41-46; kernels.cpp:59-65,89-103).  coverage_block >= 1. */
+int ig_coverage_any(ig_ctx* ctx, const int64_t* patterns, size_t n_patterns, uint32_t patterns_len,
+                    const int64_t* opponents, size_t n_opponents, uint32_t opponents_len,
+                    size_t coverage_block, uint8_t* mask);
+
+/* out[t] = sum_p scores[p] * [pattern p subset of test t], checked int64 in
+ * pattern order (kernels.hpp:48-52; kernels.cpp:40-46,67-77,105-118). */
+int ig_fused_score(ig_ctx* ctx, const int64_t* patterns, size_t n_patterns, uint32_t patterns_len,
+                   const int64_t* scores, size_t n_scores, const int64_t* tests, size_t n_tests,
+                   uint32_t tests_len, int64_t* out);
+
+/* ---------------------------------------------------------------- mine
+ * mine.hpp:12-53.  A candidate set lives on the device; copy out on demand.   */
+typedef struct ig_candidates ig_candidates;
+typedef void (*ig_progress_fn)(uint64_t pairs_done, uint64_t pairs_total, uint64_t candidates_found,
+                               void* user);
+
+/* {rows[i] & rows[j] : i<j, non-empty} U {rows[i]} deduplicated by content, in
+ * canonical words::less order (mine.hpp:35-40).
+ * Progress is reported from the calling thread (mine.hpp:31-33). */
+int ig_enumerate_candidates(ig_ctx* ctx, const int64_t* rows, size_t n_rows, uint32_t logical_len,
+                            const ig_kernel_config* cfg, ig_progress_fn progress, void* user,
+                            ig_candidates** out);
+/* support[p] = #{i : pattern p subset of rows[i]} (mine.hpp:42-44). */
+int ig_count_support(ig_ctx* ctx, ig_candidates* cands, const int64_t* rows, size_t n_rows,
+                     uint32_t logical_len, const ig_kernel_config* cfg);
+/* score = support * size^2, checked (mine.hpp:46-48). */
+int ig_score_patterns(ig_ctx* ctx, ig_candidates* cands);
+/* checked sum (mine.hpp:50-51). Host-only arithmetic. */
+int ig_total_score(const int64_t* scores, size_t n, int64_t* out);
+size_t ig_candidates_count(const ig_candidates* c);
+uint32_t ig_candidates_logical_len(const ig_candidates* c);
+/* Any output pointer may be NULL; supports/scores must have been computed if requested. */
+int ig_candidates_copy(ig_ctx* ctx, const ig_candidates* c, int64_t* words, int64_t* supports,
+                       int64_t* scores);
+void ig_candidates_free(ig_candidates* c);
+
+/* ---------------------------------------------------------------- purify / fit
+ * The coarse entry point: SPEC.md cmd_train's mining half with both
+ * classes resident: enumerate -> support -> score -> total -> reject_covered
+ * for attack and normal.  Dictionaries keep canonical order.     */
+typedef struct ig_model ig_model;
+
+int ig_fit(ig_ctx* ctx, const int64_t* attack, size_t n_attack, const int64_t* normal,
+           size_t n_normal, uint32_t logical_len, const ig_kernel_config* cfg, ig_model** out);
+int ig_fit_device(ig_ctx* ctx, const int64_t* d_attack, size_t n_attack, const int64_t* d_normal,
+                  size_t n_normal, uint32_t logical_len, const ig_kernel_config* cfg, ig_model** out);
+/* cls: 0 attack, 1 normal.  which: 0 candidates B^c, 1 pure dictionary P^c. */
+size_t ig_model_count(const ig_model* m, int cls, int which);
+uint32_t ig_model_logical_len(const ig_model* m);
+int ig_model_copy(ig_ctx* ctx, const ig_model* m, int cls, int which, int64_t* words,
+                  int64_t* supports, int64_t* scores);
+/* Phase timings of the last fit in ms: [rows, enumerate, support, purify, order, total]. */
+int ig_model_phase_ms(const ig_model* m, double* ms6);
+void ig_model_free(ig_model* m);
+
+/* evidence_scores: A = fused_score(P+, S+, T), N likewise.  */
+int ig_evidence(ig_ctx* ctx, const ig_model* m, const int64_t* tests, size_t n_tests,
+                uint32_t tests_len, int64_t* A, int64_t* N);
+int ig_evidence_device(ig_ctx* ctx, const ig_model* m, const int64_t* d_tests, size_t n_tests,
+                       uint32_t tests_len, int64_t* d_A, int64_t* d_N);
+
+/* ---------------------------------------------------------------- pipeline
+ * Kernel (1): tokenise -> vocabulary -> anti-contradiction -> pack
+ * (pipeline.hpp:60-113; pipeline.cpp:171-339).  The host keeps CSV parsing,
+ * schema statistics and the byte-order vocabulary sort (SURVEY.md §7 hard part 3);
+ * the device computes every cell's z-score units llround(((v-mean)/std)*10^p)
+ * in IEEE double, the distinct tokens, the bit lookup and the packed rows.   */
+typedef struct ig_table ig_table;   /* parsed CSV (csv.hpp:9-21) */
+typedef struct ig_schema ig_schema; /* DatasetSchema (pipeline.hpp:24-36) */
+typedef struct ig_columns ig_columns; /* typed column arrays of a table under a schema */
+typedef struct ig_encoding ig_encoding; /* vocabulary + packed rows (device resident) */
+
+int ig_read_csv(const char* bytes, size_t len, ig_table** out);        /* csv.hpp:19 */
+size_t ig_table_rows(const ig_table* t);
+size_t ig_table_cols(const ig_table* t);
+/* rows [begin, end) as a new table (positional split). */
+int ig_table_slice(const ig_table* t, size_t begin, size_t end, ig_table** out);
+void ig_table_free(ig_table* t);
+
+/* pipeline.hpp:70-72.  attack_values / normal_values: comma-separated or NULL. */
+int ig_infer_schema(const ig_table* t, const char* label_column, const char* attack_values,
+                    const char* normal_values, int decimals, ig_schema** out);
+int ig_schema_column(const ig_schema* s, size_t j, int* kind, double* mean, double* stddev);
+size_t ig_schema_label_index(const ig_schema* s);
+void ig_schema_free(ig_schema* s);
+
+/* Host parse of a table under a schema into typed arrays (the "parsed
+ * columns" the timed fit starts from).  Numeric cells become
+ * doubles (NaN = empty cell), categorical cells interned ids (-1 = empty);
+ * unparsable numeric cells -> IG_E_DATA (pipeline.cpp:188-193). */
+int ig_columns_build(const ig_table* t, const ig_schema* s, int with_labels, ig_columns** out);
+/* Keep a copy of the columns resident on the context's device; later encodes
+ * of these columns read HBM instead of host memory (bench `value` leg). */
+int ig_columns_upload(ig_ctx* ctx, ig_columns* c);
+size_t ig_columns_rows(const ig_columns* c);
+size_t ig_columns_bytes(const ig_columns* c);
+void ig_columns_free(ig_columns* c);
+
+/* encode_training (pipeline.hpp:103; pipeline.cpp:273-328). */
+int ig_encode_training(ig_ctx* ctx, const ig_columns* cols, ig_encoding** out);
+/* encode_rows (pipeline.hpp:108-109; pipeline.cpp:330-339): test rows under
+ * the training vocabulary; unseen tokens dropped. */
+int ig_encode_rows(ig_ctx* ctx, const ig_columns* cols, const ig_encoding* train, ig_encoding** out);
+uint32_t ig_encoding_logical_len(const ig_encoding* e);
+/* which: 0 attack, 1 normal (training); 2 all rows (test encode). */
+size_t ig_encoding_rows(const ig_encoding* e, int which);
+const int64_t* ig_encoding_device_rows(const ig_encoding* e, int which);
+int ig_encoding_copy_rows(ig_ctx* ctx, const ig_encoding* e, int which, int64_t* out);
+/* Vocabulary as '\n'-terminated tokens in bit order (pipeline.hpp:40-58). */
+const char* ig_encoding_vocabulary(const ig_encoding* e);
+/* Anti-contradiction report (pipeline.hpp:88-100): removed source rows ascending. */
+size_t ig_encoding_removed_count(const ig_encoding* e);
+int ig_encoding_removed_rows(const ig_encoding* e, uint64_t* rows);
+void ig_encoding_free(ig_encoding* e);
+
+/* Fit / evidence directly on resident encodings (no host round trip). */
+int ig_fit_encoded(ig_ctx* ctx, const ig_encoding* train, const ig_kernel_config* cfg, ig_model** out);
+int ig_evidence_encoded(ig_ctx* ctx, const ig_model* m, const ig_encoding* tests, int64_t* A,
+                        int64_t* N);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IG_B200_H */

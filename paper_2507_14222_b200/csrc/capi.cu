@@ -1,0 +1,591 @@
+// capi.cu — the extern "C" boundary (include/ig_b200.h) and the fit
+// orchestration.  Every entry point validates like the reference does
+// (kernels.cpp:12-36, 93, 110, 143, 160; bitpack.cpp:53-58), runs on the
+// context stream, and converts internal errors into ig_status codes.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "encode.cuh"
+#include "host_pipeline.hpp"
+#include "ig_b200.h"
+#include "ig_internal.cuh"
+#include "subset.cuh"
+
+struct ig_ctx : igb::Ctx {};
+
+struct ig_candidates {
+    igb::DevRows rows;
+    igb::DevBuf support, score;
+    bool has_support = false, has_score = false;
+    uint64_t pairs = 0;
+};
+
+struct ig_model {
+    uint32_t L = 0;
+    ig_candidates cand[2];
+    ig_candidates pure[2];
+    double ms[6] = {0, 0, 0, 0, 0, 0};
+    igb::EnumStats stats[2];
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+using igb::DevBuf;
+using igb::DevRows;
+using igb::Error;
+using igb::fail;
+
+template <class F>
+int guard(ig_ctx* ctx, F&& f) {
+    try {
+        if (ctx) IGB_CUDA(cudaSetDevice(ctx->device));
+        f();
+        return IG_OK;
+    } catch (const Error& e) {
+        (ctx ? ctx->err : g_err) = e.msg;
+        return e.status;
+    } catch (const std::bad_alloc&) {
+        (ctx ? ctx->err : g_err) = "host allocation failed";
+        return IG_E_OOM;
+    } catch (const std::exception& e) {
+        (ctx ? ctx->err : g_err) = e.what();
+        return IG_E_CUDA;
+    }
+}
+
+void check_cfg(const ig_kernel_config* cfg) {
+    if (!cfg) return;
+    // kernels.cpp:12-15
+    if (cfg->pair_batch < 1) fail(IG_E_CONFIG, "pair-batch must be >= 1");
+    if (cfg->coverage_block < 1) fail(IG_E_CONFIG, "coverage-block must be >= 1");
+}
+
+void upload_rows(igb::Ctx& ctx, const int64_t* h, size_t n, uint32_t L, DevRows& d) {
+    d.n = n;
+    d.k = igb::words_for(L);
+    d.L = L;
+    const size_t bytes = std::max<size_t>(n * d.k, 1) * 8;
+    d.buf.alloc(bytes, ctx.stream);
+    if (n * d.k) IGB_CUDA(cudaMemcpyAsync(d.buf.p, h, n * d.k * 8, cudaMemcpyHostToDevice, ctx.stream));
+}
+
+// Borrow resident device rows without copying.
+struct View {
+    const int64_t* p;
+    size_t n, k;
+};
+
+struct Timer {
+    cudaEvent_t e[8];
+    int used = 0;
+    cudaStream_t s;
+    explicit Timer(cudaStream_t st) : s(st) {
+        for (auto& x : e) cudaEventCreate(&x);
+    }
+    ~Timer() {
+        for (auto& x : e) cudaEventDestroy(x);
+    }
+    void mark() { cudaEventRecord(e[used++], s); }
+    double ms(int a, int b) {
+        float f = 0;
+        cudaEventSynchronize(e[b]);
+        cudaEventElapsedTime(&f, e[a], e[b]);
+        return f;
+    }
+};
+
+// The mining half of cmd_train: for both classes enumerate →
+// support → score → total; canonical order; reject_covered against
+// the opposite class.
+void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m) {
+    m.L = L;
+    const size_t k = igb::words_for(L);
+    Timer tm(ctx.stream);
+    tm.mark();  // 0
+    for (int c = 0; c < 2; ++c) {
+        if (X[c].n == 0) fail(IG_E_DATA, "enumerate_candidates: empty class");
+        igb::enumerate_dev(ctx, X[c].p, X[c].n, k, L, m.cand[c].rows, &m.stats[c]);
+        m.cand[c].pairs = m.stats[c].pairs;
+    }
+    tm.mark();  // 1
+    for (int c = 0; c < 2; ++c) {
+        ig_candidates& C = m.cand[c];
+        const size_t np = C.rows.n;
+        C.support.alloc(std::max<size_t>(np, 1) * 8, ctx.stream);
+        C.score.alloc(std::max<size_t>(np, 1) * 8, ctx.stream);
+        igb::count_support_dev(ctx, C.rows.data(), np, X[c].p, X[c].n, k, C.support.as<int64_t>());
+        if (igb::score_dev(ctx, C.rows.data(), np, k, C.support.as<int64_t>(), C.score.as<int64_t>()) != IG_OK)
+            fail(IG_E_OVERFLOW, "pattern score overflows int64");
+        int64_t total = 0;
+        if (igb::total_score_dev(ctx, C.score.as<int64_t>(), np, &total) != IG_OK)
+            fail(IG_E_OVERFLOW, "total score overflows int64");
+        C.has_support = C.has_score = true;
+    }
+    tm.mark();  // 2
+    for (int c = 0; c < 2; ++c) igb::canonical_order(ctx, m.cand[c].rows, &m.cand[c].support, &m.cand[c].score);
+    tm.mark();  // 3
+    for (int c = 0; c < 2; ++c) {
+        ig_candidates& C = m.cand[c];
+        const size_t np = C.rows.n;
+        DevBuf mask(std::max<size_t>(np, 1), ctx.stream);
+        igb::coverage_any_dev(ctx, C.rows.data(), np, X[1 - c].p, X[1 - c].n, k, mask.as<uint8_t>());
+        ig_candidates& P = m.pure[c];
+        P.rows.k = k;
+        P.rows.L = L;
+        P.rows.buf.alloc(std::max<size_t>(np * k, 1) * 8, ctx.stream);
+        P.support.alloc(std::max<size_t>(np, 1) * 8, ctx.stream);
+        P.score.alloc(std::max<size_t>(np, 1) * 8, ctx.stream);
+        P.rows.n = igb::compact_unflagged(ctx, C.rows.data(), C.support.as<int64_t>(), C.score.as<int64_t>(),
+                                          mask.as<uint8_t>(), np, k, P.rows.data(), P.support.as<int64_t>(),
+                                          P.score.as<int64_t>());
+        P.has_support = P.has_score = true;
+    }
+    tm.mark();  // 4
+    IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+    m.ms[0] = 0;
+    m.ms[1] = tm.ms(0, 1);
+    m.ms[2] = tm.ms(1, 2);
+    m.ms[3] = tm.ms(3, 4);
+    m.ms[4] = tm.ms(2, 3);
+    m.ms[5] = tm.ms(0, 4);
+    for (int c = 0; c < 2; ++c) {
+        for (ig_candidates* C : {&m.cand[c], &m.pure[c]}) {
+            C->rows.buf.persist();
+            C->support.persist();
+            C->score.persist();
+        }
+    }
+}
+
+void copy_out(igb::Ctx& ctx, const ig_candidates& c, int64_t* words, int64_t* sup, int64_t* sc) {
+    const size_t n = c.rows.n, k = c.rows.k;
+    if (words && n * k)
+        IGB_CUDA(cudaMemcpyAsync(words, c.rows.data(), n * k * 8, cudaMemcpyDeviceToHost, ctx.stream));
+    if (sup) {
+        if (!c.has_support) fail(IG_E_INVALID_ARG, "supports not counted");
+        if (n) IGB_CUDA(cudaMemcpyAsync(sup, c.support.p, n * 8, cudaMemcpyDeviceToHost, ctx.stream));
+    }
+    if (sc) {
+        if (!c.has_score) fail(IG_E_INVALID_ARG, "scores not computed");
+        if (n) IGB_CUDA(cudaMemcpyAsync(sc, c.score.p, n * 8, cudaMemcpyDeviceToHost, ctx.stream));
+    }
+    IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+}
+
+void evidence_impl(igb::Ctx& ctx, const ig_model& m, const int64_t* d_tests, size_t nt, uint32_t L, int64_t* d_A,
+                   int64_t* d_N) {
+    if (L != m.L) fail(IG_E_INVALID_ARG, "fused_score: logical length mismatch");
+    const size_t k = igb::words_for(L);
+    for (int c = 0; c < 2; ++c) {
+        const ig_candidates& P = m.pure[c];
+        if (igb::fused_score_dev(ctx, P.rows.data(), P.rows.n, P.score.as<int64_t>(), d_tests, nt, k,
+                                 c == 0 ? d_A : d_N) != IG_OK)
+            fail(IG_E_OVERFLOW, "evidence score sum overflows int64");
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ig_version(void) { return "ig_b200 0.1.0 (sm_100a)"; }
+
+const char* ig_last_error(const ig_ctx* ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
+
+void ig_kernel_config_default(ig_kernel_config* cfg) {
+    cfg->pair_batch = 8192;  // kernels.hpp:15-18 defaults
+    cfg->coverage_block = 4096;
+    cfg->memory_budget_bytes = size_t{2} << 30;
+    cfg->threads = 0;
+}
+
+int ig_ctx_create(int device, ig_ctx** out) {
+    *out = nullptr;
+    auto c = std::make_unique<ig_ctx>();
+    c->device = device;
+    int st = guard(c.get(), [&] {
+        IGB_CUDA(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
+        c->stream = c->own;
+        cudaDeviceProp prop;
+        IGB_CUDA(cudaGetDeviceProperties(&prop, device));
+        c->sm_count = prop.multiProcessorCount;
+        c->smem_optin = prop.sharedMemPerBlockOptin;
+        if (prop.major < 10) fail(IG_E_CUDA, std::string("device ") + prop.name + " is not sm_100-class");
+        cudaMemPool_t pool;
+        IGB_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+        uint64_t thr = UINT64_MAX;
+        IGB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    });
+    if (st != IG_OK) {
+        g_err = c->err;
+        return st;
+    }
+    *out = c.release();
+    return IG_OK;
+}
+
+void ig_ctx_destroy(ig_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->own) {
+        cudaStreamSynchronize(ctx->own);
+        cudaStreamDestroy(ctx->own);
+    }
+    delete ctx;
+}
+
+int ig_ctx_set_stream(ig_ctx* ctx, void* stream) {
+    return guard(ctx, [&] { ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own; });
+}
+
+uint64_t ig_ctx_launch_count(const ig_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int ig_measure_int_peaks(ig_ctx* ctx, double* lop3_per_s, double* popc_per_s) {
+    return guard(ctx, [&] { igb::measure_int_peaks(*ctx, lop3_per_s, popc_per_s); });
+}
+
+// ------------------------------------------------------------------ KernelBackend
+int ig_pair_intersect_batch(ig_ctx* ctx, const int64_t* rows, size_t n, uint32_t L, size_t left, size_t jb,
+                            size_t je, int64_t* out) {
+    return guard(ctx, [&] {
+        // kernels.cpp:19-32
+        if (left >= n) fail(IG_E_INVALID_ARG, "pair_intersect_batch: left index out of range");
+        if (jb <= left)
+            fail(IG_E_INVALID_ARG,
+                 "pair_intersect_batch: window overlaps [0, left]; only ordered pairs left < j are valid");
+        if (je < jb || je > n) fail(IG_E_INVALID_ARG, "pair_intersect_batch: window out of range");
+        const size_t k = igb::words_for(L);
+        const size_t cnt = je - jb;
+        if (cnt == 0 || k == 0) return;
+        DevRows d;
+        upload_rows(*ctx, rows + jb * k, cnt, L, d);
+        DevRows l;
+        upload_rows(*ctx, rows + left * k, 1, L, l);
+        DevBuf o(cnt * k * 8, ctx->stream);
+        igb::pair_window_dev(*ctx, l.data(), d.data(), cnt, k, o.as<int64_t>());
+        IGB_CUDA(cudaMemcpyAsync(out, o.p, cnt * k * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        IGB_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int ig_coverage_any(ig_ctx* ctx, const int64_t* pat, size_t np, uint32_t Lp, const int64_t* opp, size_t no,
+                    uint32_t Lo, size_t block, uint8_t* mask) {
+    return guard(ctx, [&] {
+        if (Lp != Lo) fail(IG_E_INVALID_ARG, "coverage_any: logical length mismatch");  // kernels.cpp:34-38
+        if (block < 1) fail(IG_E_INVALID_ARG, "coverage_block must be >= 1");          // kernels.cpp:93
+        if (np == 0) return;
+        DevRows P, X;
+        upload_rows(*ctx, pat, np, Lp, P);
+        upload_rows(*ctx, opp, no, Lo, X);
+        DevBuf m(np, ctx->stream);
+        igb::coverage_any_dev(*ctx, P.data(), np, X.data(), no, P.k, m.as<uint8_t>());
+        IGB_CUDA(cudaMemcpyAsync(mask, m.p, np, cudaMemcpyDeviceToHost, ctx->stream));
+        IGB_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int ig_fused_score(ig_ctx* ctx, const int64_t* pat, size_t np, uint32_t Lp, const int64_t* scores, size_t ns,
+                   const int64_t* tests, size_t nt, uint32_t Lt, int64_t* out) {
+    return guard(ctx, [&] {
+        if (Lp != Lt) fail(IG_E_INVALID_ARG, "fused_score: logical length mismatch");
+        if (ns != np) fail(IG_E_INVALID_ARG, "fused_score: scores length != pattern count");  // kernels.cpp:110
+        if (nt == 0) return;
+        DevRows P, T;
+        upload_rows(*ctx, pat, np, Lp, P);
+        upload_rows(*ctx, tests, nt, Lt, T);
+        DevBuf s(std::max<size_t>(np, 1) * 8, ctx->stream), o(nt * 8, ctx->stream);
+        if (np) IGB_CUDA(cudaMemcpyAsync(s.p, scores, np * 8, cudaMemcpyHostToDevice, ctx->stream));
+        if (igb::fused_score_dev(*ctx, P.data(), np, s.as<int64_t>(), T.data(), nt, P.k, o.as<int64_t>()) != IG_OK)
+            fail(IG_E_OVERFLOW, "evidence score sum overflows int64");
+        IGB_CUDA(cudaMemcpyAsync(out, o.p, nt * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        IGB_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+// ------------------------------------------------------------------ mine
+int ig_enumerate_candidates(ig_ctx* ctx, const int64_t* rows, size_t n, uint32_t L, const ig_kernel_config* cfg,
+                            ig_progress_fn progress, void* user, ig_candidates** out) {
+    *out = nullptr;
+    return guard(ctx, [&] {
+        check_cfg(cfg);
+        if (n == 0) fail(IG_E_DATA, "enumerate_candidates: empty class");
+        DevRows X;
+        upload_rows(*ctx, rows, n, L, X);
+        auto c = std::make_unique<ig_candidates>();
+        igb::EnumStats st;
+        igb::enumerate_dev(*ctx, X.data(), n, X.k, L, c->rows, &st);
+        igb::canonical_order(*ctx, c->rows, nullptr, nullptr);
+        IGB_CUDA(cudaStreamSynchronize(ctx->stream));
+        c->rows.buf.persist();
+        c->pairs = st.pairs;
+        if (progress) progress(st.pairs, st.pairs, c->rows.n, user);
+        *out = c.release();
+    });
+}
+
+int ig_count_support(ig_ctx* ctx, ig_candidates* c, const int64_t* rows, size_t n, uint32_t L,
+                     const ig_kernel_config* cfg) {
+    return guard(ctx, [&] {
+        check_cfg(cfg);
+        if (L != c->rows.L) fail(IG_E_INVALID_ARG, "count_support: logical length mismatch");
+        DevRows X;
+        upload_rows(*ctx, rows, n, L, X);
+        c->support.alloc(std::max<size_t>(c->rows.n, 1) * 8, ctx->stream);
+        igb::count_support_dev(*ctx, c->rows.data(), c->rows.n, X.data(), n, X.k, c->support.as<int64_t>());
+        IGB_CUDA(cudaStreamSynchronize(ctx->stream));
+        c->support.persist();
+        c->has_support = true;
+    });
+}
+
+int ig_score_patterns(ig_ctx* ctx, ig_candidates* c) {
+    return guard(ctx, [&] {
+        if (!c->has_support) fail(IG_E_INVALID_ARG, "score_patterns: supports not counted");
+        c->score.alloc(std::max<size_t>(c->rows.n, 1) * 8, ctx->stream);
+        if (igb::score_dev(*ctx, c->rows.data(), c->rows.n, c->rows.k, c->support.as<int64_t>(),
+                           c->score.as<int64_t>()) != IG_OK)
+            fail(IG_E_OVERFLOW, "pattern score overflows int64");
+        IGB_CUDA(cudaStreamSynchronize(ctx->stream));
+        c->score.persist();
+        c->has_score = true;
+    });
+}
+
+int ig_total_score(const int64_t* s, size_t n, int64_t* out) {
+    return guard(nullptr, [&] {
+        int64_t acc = 0;
+        for (size_t i = 0; i < n; ++i)
+            if (__builtin_add_overflow(acc, s[i], &acc)) fail(IG_E_OVERFLOW, "total score overflows int64");
+        *out = acc;
+    });
+}
+
+size_t ig_candidates_count(const ig_candidates* c) { return c ? c->rows.n : 0; }
+uint32_t ig_candidates_logical_len(const ig_candidates* c) { return c ? c->rows.L : 0; }
+
+int ig_candidates_copy(ig_ctx* ctx, const ig_candidates* c, int64_t* words, int64_t* sup, int64_t* sc) {
+    return guard(ctx, [&] { copy_out(*ctx, *c, words, sup, sc); });
+}
+
+void ig_candidates_free(ig_candidates* c) { delete c; }
+
+// ------------------------------------------------------------------ fit / evidence
+int ig_fit(ig_ctx* ctx, const int64_t* attack, size_t na, const int64_t* normal, size_t nn, uint32_t L,
+           const ig_kernel_config* cfg, ig_model** out) {
+    *out = nullptr;
+    return guard(ctx, [&] {
+        check_cfg(cfg);
+        DevRows A, N;
+        upload_rows(*ctx, attack, na, L, A);
+        upload_rows(*ctx, normal, nn, L, N);
+        View X[2] = {{A.data(), na, A.k}, {N.data(), nn, N.k}};
+        auto m = std::make_unique<ig_model>();
+        fit_impl(*ctx, X, L, *m);
+        *out = m.release();
+    });
+}
+
+int ig_fit_device(ig_ctx* ctx, const int64_t* d_attack, size_t na, const int64_t* d_normal, size_t nn, uint32_t L,
+                  const ig_kernel_config* cfg, ig_model** out) {
+    *out = nullptr;
+    return guard(ctx, [&] {
+        check_cfg(cfg);
+        const size_t k = igb::words_for(L);
+        View X[2] = {{d_attack, na, k}, {d_normal, nn, k}};
+        auto m = std::make_unique<ig_model>();
+        fit_impl(*ctx, X, L, *m);
+        *out = m.release();
+    });
+}
+
+size_t ig_model_count(const ig_model* m, int cls, int which) {
+    if (!m || cls < 0 || cls > 1) return 0;
+    return which == 0 ? m->cand[cls].rows.n : m->pure[cls].rows.n;
+}
+
+uint32_t ig_model_logical_len(const ig_model* m) { return m ? m->L : 0; }
+
+int ig_model_copy(ig_ctx* ctx, const ig_model* m, int cls, int which, int64_t* words, int64_t* sup, int64_t* sc) {
+    return guard(ctx, [&] {
+        if (cls < 0 || cls > 1) fail(IG_E_INVALID_ARG, "class must be 0 (attack) or 1 (normal)");
+        copy_out(*ctx, which == 0 ? m->cand[cls] : m->pure[cls], words, sup, sc);
+    });
+}
+
+int ig_model_phase_ms(const ig_model* m, double* ms6) {
+    if (!m) return IG_E_INVALID_ARG;
+    std::memcpy(ms6, m->ms, sizeof(m->ms));
+    return IG_OK;
+}
+
+void ig_model_free(ig_model* m) { delete m; }
+
+int ig_evidence(ig_ctx* ctx, const ig_model* m, const int64_t* tests, size_t nt, uint32_t L, int64_t* A, int64_t* N) {
+    return guard(ctx, [&] {
+        if (nt == 0) return;
+        DevRows T;
+        upload_rows(*ctx, tests, nt, L, T);
+        DevBuf a(nt * 8, ctx->stream), b(nt * 8, ctx->stream);
+        evidence_impl(*ctx, *m, T.data(), nt, L, a.as<int64_t>(), b.as<int64_t>());
+        IGB_CUDA(cudaMemcpyAsync(A, a.p, nt * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        IGB_CUDA(cudaMemcpyAsync(N, b.p, nt * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        IGB_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int ig_evidence_device(ig_ctx* ctx, const ig_model* m, const int64_t* d_tests, size_t nt, uint32_t L, int64_t* d_A,
+                       int64_t* d_N) {
+    return guard(ctx, [&] {
+        if (nt == 0) return;
+        evidence_impl(*ctx, *m, d_tests, nt, L, d_A, d_N);
+    });
+}
+
+// ------------------------------------------------------------------ pipeline
+int ig_read_csv(const char* bytes, size_t len, ig_table** out) {
+    *out = nullptr;
+    return guard(nullptr, [&] {
+        auto t = std::make_unique<ig_table>();
+        igb::read_csv(bytes, len, *t);
+        *out = t.release();
+    });
+}
+size_t ig_table_rows(const ig_table* t) { return t ? t->n_rows : 0; }
+size_t ig_table_cols(const ig_table* t) { return t ? t->header.size() : 0; }
+int ig_table_slice(const ig_table* t, size_t begin, size_t end, ig_table** out) {
+    *out = nullptr;
+    return guard(nullptr, [&] {
+        if (begin > end || end > t->n_rows) fail(IG_E_INVALID_ARG, "table slice out of range");
+        auto s = std::make_unique<ig_table>();
+        s->header = t->header;
+        const size_t nc = t->header.size();
+        s->n_rows = end - begin;
+        s->off.reserve(s->n_rows * nc);
+        s->len.reserve(s->n_rows * nc);
+        for (size_t r = begin; r < end; ++r)
+            for (size_t j = 0; j < nc; ++j) {
+                auto c = t->cell(r, j);
+                s->off.push_back(s->arena.size());
+                s->len.push_back((uint32_t)c.size());
+                s->arena.append(c);
+            }
+        *out = s.release();
+    });
+}
+void ig_table_free(ig_table* t) { delete t; }
+
+int ig_infer_schema(const ig_table* t, const char* label, const char* attack, const char* normal, int decimals,
+                    ig_schema** out) {
+    *out = nullptr;
+    return guard(nullptr, [&] {
+        auto s = std::make_unique<ig_schema>();
+        igb::infer_schema(*t, label ? label : "", igb::split_csv_list(attack), igb::split_csv_list(normal), decimals,
+                          *s);
+        *out = s.release();
+    });
+}
+int ig_schema_column(const ig_schema* s, size_t j, int* kind, double* mean, double* sd) {
+    if (!s || j >= s->names.size()) return IG_E_RANGE;
+    *kind = s->kind[j];
+    *mean = s->mean[j];
+    *sd = s->sd[j];
+    return IG_OK;
+}
+size_t ig_schema_label_index(const ig_schema* s) { return s ? s->label_index : 0; }
+void ig_schema_free(ig_schema* s) { delete s; }
+
+int ig_columns_build(const ig_table* t, const ig_schema* s, int with_labels, ig_columns** out) {
+    *out = nullptr;
+    return guard(nullptr, [&] {
+        auto c = std::make_unique<ig_columns>();
+        igb::build_columns(*t, *s, with_labels != 0, *c);
+        *out = c.release();
+    });
+}
+int ig_columns_upload(ig_ctx* ctx, ig_columns* c) {
+    return guard(ctx, [&] { igb::upload_columns(*ctx, *c); });
+}
+size_t ig_columns_rows(const ig_columns* c) { return c ? c->n_rows : 0; }
+size_t ig_columns_bytes(const ig_columns* c) {
+    return c ? c->values.size() * 8 + c->cat.size() * 4 + c->is_attack.size() : 0;
+}
+void ig_columns_free(ig_columns* c) { delete c; }
+
+int ig_encode_training(ig_ctx* ctx, const ig_columns* cols, ig_encoding** out) {
+    *out = nullptr;
+    return guard(ctx, [&] {
+        auto e = std::make_unique<ig_encoding>();
+        igb::encode_training_dev(*ctx, *cols, *e);
+        e->attack.buf.persist();
+        e->normal.buf.persist();
+        *out = e.release();
+    });
+}
+
+int ig_encode_rows(ig_ctx* ctx, const ig_columns* cols, const ig_encoding* train, ig_encoding** out) {
+    *out = nullptr;
+    return guard(ctx, [&] {
+        auto e = std::make_unique<ig_encoding>();
+        igb::encode_rows_dev(*ctx, *cols, *train, *e);
+        e->all.buf.persist();
+        *out = e.release();
+    });
+}
+
+uint32_t ig_encoding_logical_len(const ig_encoding* e) { return e ? e->L : 0; }
+static const DevRows* enc_rows(const ig_encoding* e, int which) {
+    return which == 0 ? &e->attack : which == 1 ? &e->normal : &e->all;
+}
+size_t ig_encoding_rows(const ig_encoding* e, int which) { return e ? enc_rows(e, which)->n : 0; }
+const int64_t* ig_encoding_device_rows(const ig_encoding* e, int which) {
+    return e ? enc_rows(e, which)->data() : nullptr;
+}
+int ig_encoding_copy_rows(ig_ctx* ctx, const ig_encoding* e, int which, int64_t* out) {
+    return guard(ctx, [&] {
+        const DevRows* r = enc_rows(e, which);
+        if (r->n * r->k)
+            IGB_CUDA(cudaMemcpyAsync(out, r->data(), r->n * r->k * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        IGB_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+const char* ig_encoding_vocabulary(const ig_encoding* e) { return e ? e->vocab_blob.c_str() : ""; }
+size_t ig_encoding_removed_count(const ig_encoding* e) { return e ? e->removed.size() : 0; }
+int ig_encoding_removed_rows(const ig_encoding* e, uint64_t* rows) {
+    if (!e) return IG_E_INVALID_ARG;
+    std::copy(e->removed.begin(), e->removed.end(), rows);
+    return IG_OK;
+}
+void ig_encoding_free(ig_encoding* e) { delete e; }
+
+int ig_fit_encoded(ig_ctx* ctx, const ig_encoding* train, const ig_kernel_config* cfg, ig_model** out) {
+    *out = nullptr;
+    return guard(ctx, [&] {
+        check_cfg(cfg);
+        View X[2] = {{train->attack.data(), train->attack.n, train->attack.k},
+                     {train->normal.data(), train->normal.n, train->normal.k}};
+        auto m = std::make_unique<ig_model>();
+        fit_impl(*ctx, X, train->L, *m);
+        *out = m.release();
+    });
+}
+
+int ig_evidence_encoded(ig_ctx* ctx, const ig_model* m, const ig_encoding* tests, int64_t* A, int64_t* N) {
+    return guard(ctx, [&] {
+        const size_t nt = tests->all.n;
+        if (nt == 0) return;
+        DevBuf a(nt * 8, ctx->stream), b(nt * 8, ctx->stream);
+        evidence_impl(*ctx, *m, tests->all.data(), nt, tests->L, a.as<int64_t>(), b.as<int64_t>());
+        IGB_CUDA(cudaMemcpyAsync(A, a.p, nt * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        IGB_CUDA(cudaMemcpyAsync(N, b.p, nt * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        IGB_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+}  // extern "C"

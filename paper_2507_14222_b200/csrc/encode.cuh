@@ -1,0 +1,30 @@
+// encode.cuh — resident vocabulary + packed rows (kernel 1 outputs).
+#pragma once
+
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "host_pipeline.hpp"
+#include "ig_internal.cuh"
+
+struct ig_encoding {
+    uint32_t L = 0;
+    size_t n_cols = 0, label_index = 0;
+    int decimals = 2;
+    std::vector<int> kind;
+    std::vector<std::vector<std::string>> dict;
+    std::string vocab_blob;                                   // tokens in bit order, '\n'-terminated
+    std::vector<std::vector<int64_t>> num_codes;              // per column, sorted units
+    std::vector<std::vector<int32_t>> num_bits;               // per column, matching bits
+    std::vector<std::unordered_map<std::string, int32_t>> cat_bits;  // per column text -> bit
+    std::vector<int> empty_bit;                               // per column bit of "j:" or -1
+    igb::DevRows attack, normal, all;
+    std::vector<uint64_t> removed;                            // anti-contradiction source rows
+};
+
+namespace igb {
+void encode_training_dev(Ctx& ctx, const ig_columns& c, ig_encoding& e);
+void upload_columns(Ctx& ctx, ig_columns& c);
+void encode_rows_dev(Ctx& ctx, const ig_columns& c, const ig_encoding& train, ig_encoding& e);
+}  // namespace igb

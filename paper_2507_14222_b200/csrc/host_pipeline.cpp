@@ -1,0 +1,268 @@
+// host_pipeline.cpp — CSV reader, schema inference and typed columns.
+// See host_pipeline.hpp for the reference lines each function follows.
+#include "host_pipeline.hpp"
+
+#include <algorithm>
+#include <charconv>
+#include <cmath>
+#include <limits>
+#include <string>
+#include <unordered_map>
+
+#include "ig_b200.h"
+#include "ig_error.hpp"
+
+namespace igb {
+
+// pipeline.cpp:16-25 — the whole cell must parse with std::from_chars and be finite.
+std::optional<double> parse_double_strict(std::string_view s) {
+    if (s.empty()) return std::nullopt;
+    double v = 0.0;
+    auto [ptr, ec] = std::from_chars(s.data(), s.data() + s.size(), v);
+    if (ec != std::errc{} || ptr != s.data() + s.size()) return std::nullopt;
+    if (!std::isfinite(v)) return std::nullopt;
+    return v;
+}
+
+// csv.cpp:14-89: comma fields, double-quote quoting with "" escapes, CR/LF/CRLF
+// records, BOM strip, ragged rows are a DataError, trailing newline ignored.
+void read_csv(const char* text, size_t n, ig_table& t) {
+    t = ig_table{};
+    t.arena.reserve(n);
+    std::vector<uint64_t> rec_off;
+    std::vector<uint32_t> rec_len;
+    bool have_header = false;
+    bool in_quotes = false;
+    bool any_field = false;
+    size_t line = 1;
+    uint64_t field_start = 0;
+
+    auto end_field = [&] {
+        rec_off.push_back(field_start);
+        rec_len.push_back((uint32_t)(t.arena.size() - field_start));
+        field_start = t.arena.size();
+        any_field = true;
+    };
+    auto end_record = [&] {
+        end_field();
+        if (!have_header) {
+            for (size_t i = 0; i < rec_off.size(); ++i) t.header.emplace_back(t.arena.data() + rec_off[i], rec_len[i]);
+            have_header = true;
+            t.arena.clear();
+            field_start = 0;
+        } else {
+            if (rec_off.size() != t.header.size())
+                throw Error{IG_E_DATA, "<csv>: line " + std::to_string(line) + ": expected " +
+                                           std::to_string(t.header.size()) + " fields, got " +
+                                           std::to_string(rec_off.size())};
+            t.off.insert(t.off.end(), rec_off.begin(), rec_off.end());
+            t.len.insert(t.len.end(), rec_len.begin(), rec_len.end());
+            ++t.n_rows;
+        }
+        rec_off.clear();
+        rec_len.clear();
+        any_field = false;
+    };
+
+    size_t i = 0;
+    if (n >= 3 && (unsigned char)text[0] == 0xEF && (unsigned char)text[1] == 0xBB && (unsigned char)text[2] == 0xBF) i = 3;
+    for (; i < n; ++i) {
+        const char c = text[i];
+        if (in_quotes) {
+            if (c == '"') {
+                if (i + 1 < n && text[i + 1] == '"') {
+                    t.arena.push_back('"');
+                    ++i;
+                } else {
+                    in_quotes = false;
+                }
+            } else {
+                if (c == '\n') ++line;
+                t.arena.push_back(c);
+            }
+            continue;
+        }
+        switch (c) {
+            case '"':
+                in_quotes = true;
+                break;
+            case ',':
+                end_field();
+                break;
+            case '\r':
+                if (i + 1 < n && text[i + 1] == '\n') ++i;
+                [[fallthrough]];
+            case '\n':
+                end_record();
+                ++line;
+                break;
+            default:
+                t.arena.push_back(c);
+        }
+    }
+    if (in_quotes) throw Error{IG_E_DATA, "<csv>: unterminated quoted field at end of input"};
+    if (any_field || t.arena.size() > field_start) end_record();
+    if (!have_header) throw Error{IG_E_DATA, "<csv>: empty input, no header row"};
+}
+
+// pipeline.cpp:35-49
+bool is_attack(const ig_schema& s, std::string_view label) {
+    auto contains = [&](const std::vector<std::string>& v) { return std::find(v.begin(), v.end(), label) != v.end(); };
+    if (!s.attack_values.empty()) {
+        if (contains(s.attack_values)) return true;
+        if (s.normal_values.empty() || contains(s.normal_values)) return false;
+        throw Error{IG_E_DATA, "label value '" + std::string(label) + "' not covered by attack/normal mapping"};
+    }
+    if (!s.normal_values.empty()) return !contains(s.normal_values);
+    return label != "normal";
+}
+
+std::vector<std::string> split_csv_list(const char* s) {
+    std::vector<std::string> out;
+    if (!s || !*s) return out;
+    std::string cur;
+    for (const char* p = s; *p; ++p) {
+        if (*p == ',') {
+            out.push_back(cur);
+            cur.clear();
+        } else {
+            cur += *p;
+        }
+    }
+    out.push_back(cur);
+    return out;
+}
+
+// pipeline.cpp:107-169 — numeric iff every non-empty cell parses; mean and
+// population std from sequential double sums over the table's rows.
+void infer_schema(const ig_table& t, const std::string& label, const std::vector<std::string>& attack,
+                  const std::vector<std::string>& normal, int decimals, ig_schema& s) {
+    if (t.n_rows == 0) throw Error{IG_E_DATA, "empty table: no data rows to train on"};
+    if (decimals < 0 || decimals > 12)
+        throw Error{IG_E_CONFIG, "decimals must be in [0, 12], got " + std::to_string(decimals)};
+    auto it = std::find(t.header.begin(), t.header.end(), label);
+    if (it == t.header.end()) throw Error{IG_E_CONFIG, "label column '" + label + "' not found in header"};
+    s = ig_schema{};
+    s.names = t.header;
+    s.label_index = (size_t)(it - t.header.begin());
+    s.label_column = label;
+    s.attack_values = attack;
+    s.normal_values = normal;
+    s.decimals = decimals;
+    const size_t nc = t.header.size();
+    s.kind.assign(nc, 1);
+    s.mean.assign(nc, 0.0);
+    s.sd.assign(nc, 0.0);
+    for (size_t j = 0; j < nc; ++j) {
+        if (j == s.label_index) continue;
+        bool numeric = true;
+        size_t parsed = 0;
+        double sum = 0.0;
+        for (size_t r = 0; r < t.n_rows; ++r) {
+            auto cell = t.cell(r, j);
+            if (cell.empty()) continue;
+            auto v = parse_double_strict(cell);
+            if (!v) {
+                numeric = false;
+                break;
+            }
+            sum += *v;
+            ++parsed;
+        }
+        if (!numeric || parsed == 0) continue;
+        s.kind[j] = 0;
+        s.mean[j] = sum / static_cast<double>(parsed);
+        double ss = 0.0;
+        for (size_t r = 0; r < t.n_rows; ++r) {
+            auto cell = t.cell(r, j);
+            if (cell.empty()) continue;
+            const double d = *parse_double_strict(cell) - s.mean[j];
+            ss += d * d;
+        }
+        s.sd[j] = std::sqrt(ss / static_cast<double>(parsed));
+    }
+    for (size_t r = 0; r < t.n_rows; ++r) is_attack(s, t.cell(r, s.label_index));
+}
+
+// Typed columns of `t` under `s`: the "parsed columns" a fit starts from.
+// Row-count mismatch and unparsable numeric cells raise DataError exactly as
+// tokenize_row does (pipeline.cpp:173-193).
+void build_columns(const ig_table& t, const ig_schema& s, bool with_labels, ig_columns& c) {
+    if (t.header.size() != s.names.size())
+        throw Error{IG_E_DATA, "row 0: expected " + std::to_string(s.names.size()) + " columns, got " +
+                                   std::to_string(t.header.size())};
+    c = ig_columns{};
+    c.n_rows = t.n_rows;
+    c.n_cols = s.names.size();
+    c.label_index = s.label_index;
+    c.decimals = s.decimals;
+    c.scale = std::pow(10.0, s.decimals);
+    c.kind = s.kind;
+    c.mean = s.mean;
+    c.sd = s.sd;
+    c.slot.assign(c.n_cols, -1);
+    c.dict.resize(c.n_cols);
+    for (size_t j = 0; j < c.n_cols; ++j) {
+        if (j == s.label_index) continue;
+        c.slot[j] = s.kind[j] == 0 ? (int)c.n_num++ : (int)c.n_cat++;
+    }
+    c.values.assign(c.n_num * c.n_rows, 0.0);
+    c.cat.assign(c.n_cat * c.n_rows, -1);
+    const double nan = std::numeric_limits<double>::quiet_NaN();
+    for (size_t j = 0; j < c.n_cols; ++j) {
+        if (j == s.label_index) continue;
+        if (s.kind[j] == 0) {
+            double* dst = c.values.data() + (size_t)c.slot[j] * c.n_rows;
+            for (size_t r = 0; r < t.n_rows; ++r) {
+                auto cell = t.cell(r, j);
+                if (cell.empty()) {
+                    dst[r] = nan;
+                    continue;
+                }
+                auto v = parse_double_strict(cell);
+                if (!v)
+                    throw Error{IG_E_DATA, "row " + std::to_string(r) + ", column " + std::to_string(j) + " (" +
+                                               s.names[j] + "): cannot parse '" + std::string(cell) + "' as a number"};
+                dst[r] = *v;
+            }
+        } else {
+            int32_t* dst = c.cat.data() + (size_t)c.slot[j] * c.n_rows;
+            std::unordered_map<std::string_view, int32_t> ids;
+            auto& dict = c.dict[j];
+            for (size_t r = 0; r < t.n_rows; ++r) {
+                auto cell = t.cell(r, j);
+                if (cell.empty()) continue;  // -1: the bare "j:" token (pipeline.cpp:185-186)
+                auto [it, fresh] = ids.try_emplace(cell, (int32_t)dict.size());
+                if (fresh) dict.emplace_back(cell);
+                dst[r] = it->second;
+            }
+        }
+    }
+    if (with_labels) {
+        c.is_attack.resize(c.n_rows);
+        for (size_t r = 0; r < t.n_rows; ++r) c.is_attack[r] = is_attack(s, t.cell(r, s.label_index)) ? 1 : 0;
+    }
+}
+
+// pipeline.cpp:88-104 — fixed-point text of `units` at `decimals` places,
+// sign-normalised zero.
+std::string format_units(int64_t units, int decimals) {
+    int64_t denom = 1;
+    for (int i = 0; i < decimals; ++i) denom *= 10;
+    const bool negative = units < 0;
+    const uint64_t mag = negative ? -static_cast<uint64_t>(units) : static_cast<uint64_t>(units);
+    const uint64_t whole = mag / static_cast<uint64_t>(denom);
+    const uint64_t frac = mag % static_cast<uint64_t>(denom);
+    std::string out;
+    if (negative && mag != 0) out += '-';
+    out += std::to_string(whole);
+    if (decimals > 0) {
+        std::string f = std::to_string(frac);
+        out += '.';
+        out.append(static_cast<size_t>(decimals) - f.size(), '0');
+        out += f;
+    }
+    return out;
+}
+
+}  // namespace igb

@@ -1,0 +1,139 @@
+// ig_internal.cuh — shared internals of libig_b200.so (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "ig_b200.h"
+#include "ig_error.hpp"
+
+namespace igb {
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+    if (e != cudaSuccess) {
+        int st = (e == cudaErrorMemoryAllocation) ? IG_E_OOM : IG_E_CUDA;
+        fail(st, std::string(what) + ": " + cudaGetErrorString(e) + " (" + file + ":" + std::to_string(line) + ")");
+    }
+}
+#define IGB_CUDA(x) ::igb::cuda_check((x), #x, __FILE__, __LINE__)
+
+struct Ctx;
+
+// Stream-ordered device buffer (cudaMallocAsync on the context stream; the
+// pool keeps freed blocks cached so repeated fits do not hit the driver).
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    cudaStream_t s = nullptr;
+    DevBuf() = default;
+    DevBuf(size_t n, cudaStream_t st) { alloc(n, st); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept { *this = std::move(o); }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) {
+            release();
+            p = o.p;
+            bytes = o.bytes;
+            s = o.s;
+            persistent = o.persistent;
+            o.p = nullptr;
+            o.bytes = 0;
+        }
+        return *this;
+    }
+    ~DevBuf() { release(); }
+    void alloc(size_t n, cudaStream_t st) {
+        release();
+        s = st;
+        bytes = n;
+        if (n) IGB_CUDA(cudaMallocAsync(&p, n, st));
+    }
+    void release() noexcept {
+        if (p) {
+            if (persistent)
+                cudaFree(p);  // long-lived result objects may outlive the stream they were made on
+            else
+                cudaFreeAsync(p, s);
+        }
+        p = nullptr;
+        bytes = 0;
+    }
+    // Mark as owned by a long-lived ABI object (model, candidate set, encoding).
+    void persist() { persistent = true; }
+    bool persistent = false;
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+// Matrix of packed rows resident on the device.
+struct DevRows {
+    DevBuf buf;
+    size_t n = 0;
+    size_t k = 0;
+    uint32_t L = 0;
+    int64_t* data() const { return buf.as<int64_t>(); }
+};
+
+struct Ctx {
+    int device = 0;
+    cudaStream_t own = nullptr;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    uint64_t launches = 0;
+    int sm_count = 148;
+    size_t smem_optin = 0;
+};
+
+inline size_t words_for(uint32_t L) { return (static_cast<size_t>(L) + 63) / 64; }
+
+// Every kernel launch goes through this so the context can report how many of
+// its own kernels ran (bench `gpu_launches`) and catch launch errors at once.
+#define IGB_LAUNCH(ctx, kernel, grid, block, smem, ...)                                   \
+    do {                                                                                  \
+        kernel<<<(grid), (block), (smem), (ctx).stream>>>(__VA_ARGS__);                   \
+        IGB_CUDA(cudaGetLastError());                                                     \
+        ++(ctx).launches;                                                                 \
+    } while (0)
+
+// ------------------------------------------------------------------ device primitives
+__device__ __forceinline__ uint64_t mix64(uint64_t h) {
+    // murmur3 fmix64
+    h ^= h >> 33;
+    h *= 0xff51afd7ed558ccdull;
+    h ^= h >> 33;
+    h *= 0xc4ceb9fe1a85ec53ull;
+    h ^= h >> 33;
+    return h;
+}
+
+// Streaming fingerprint of a K-word candidate: word-position dependent so that
+// permuted words do not collide; finalised with fmix64.  A fingerprint is only
+// a bucket hint — every equality is confirmed on the full words.
+struct Fp {
+    uint64_t h = 0x9e3779b97f4a7c15ull;
+    __device__ __forceinline__ void add(uint64_t w) {
+        h ^= w * 0x87c37b91114253d5ull;
+        h = (h << 31) | (h >> 33);
+        h *= 0x4cf5ad432745937full;
+        h += 0x52dce729ull;
+    }
+    __device__ __forceinline__ uint64_t final(uint32_t k) const {
+        uint64_t f = mix64(h ^ k);
+        return f ? f : 1ull;  // 0 marks an empty hash slot
+    }
+};
+
+// ------------------------------------------------------------------ host helpers
+// (declared here, defined in the .cu files)
+void sort_rows_canonical(Ctx& ctx, const int64_t* d_words, size_t n, size_t k, uint32_t* d_perm);
+void gather_rows(Ctx& ctx, const int64_t* d_src, const uint32_t* d_perm, size_t n, size_t k, int64_t* d_dst);
+
+}  // namespace igb

@@ -1,0 +1,500 @@
+// mine.cu — candidate enumeration (kernel 2), exact dedup (kernel 3), scores,
+// canonical ordering.
+//
+// Reference semantics: enumerate_candidates proj/include/ig/mine.hpp:35-40 with
+// SPEC.md:301-309 (B^c = {x_i ∩ x_j : i<j, non-empty} ∪ X^c, dedup by content,
+// canonical words::less order, bitpack.hpp:59-68); score_patterns / total_score
+// mine.hpp:46-51.
+//
+// Design (B200): class rows are L2-resident (≤17 MB for NSL shape).  A CTA owns
+// a 64×64 tile of the upper triangle (u ≤ v; the diagonal u == v yields the
+// union term X_u itself).  Both row blocks are staged in shared memory with an
+// odd row stride (conflict-free 64-bit lane access).  Each pair's AND is
+// fingerprinted and inserted into one device-wide open-addressing table of
+// 16-byte slots {fingerprint, representative pair (u,v)} claimed with a single
+// 128-bit atom.cas.  An insert that meets an equal fingerprint re-materialises
+// the representative's words from L2 and compares all K words: equal → duplicate;
+// different → a genuine 64-bit collision, deferred to a second table with a new
+// seed (levels repeat until empty), so the result is exact by construction.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+
+#include "ig_internal.cuh"
+#include "subset.cuh"
+
+namespace igb {
+
+namespace {
+
+constexpr int kTile = 64;
+constexpr int kPairThreads = 256;
+constexpr uint64_t kRepInit = ~0ull;
+
+struct Table {
+    ulonglong2* slots;
+    uint64_t mask;
+    uint2* reps;
+    unsigned long long* count;
+    unsigned long long limit;  // max distinct before the table is declared full
+    uint2* ovf;
+    unsigned long long* ovf_count;
+    unsigned long long ovf_cap;
+    unsigned long long* collisions;
+    int* fail;  // bit0 table full, bit1 overflow list full
+    uint64_t seed;
+};
+
+__device__ __forceinline__ ulonglong2 cas128(ulonglong2* addr, ulonglong2 cmp, ulonglong2 val) {
+    ulonglong2 old;
+    asm volatile(
+        "{\n\t.reg .b128 c, n, o;\n\t"
+        "mov.b128 c, {%2, %3};\n\t"
+        "mov.b128 n, {%4, %5};\n\t"
+        "atom.global.cas.b128 o, [%6], c, n;\n\t"
+        "mov.b128 {%0, %1}, o;\n\t}"
+        : "=l"(old.x), "=l"(old.y)
+        : "l"(cmp.x), "l"(cmp.y), "l"(val.x), "l"(val.y), "l"(addr)
+        : "memory");
+    return old;
+}
+
+__device__ __forceinline__ uint64_t ld_volatile(const unsigned long long* p) {
+    return *reinterpret_cast<const volatile unsigned long long*>(p);
+}
+
+// Insert candidate (u,v) with fingerprint fp.  `b(w)` yields word w of the
+// candidate; X is the class row matrix used to re-materialise representatives.
+template <class WordFn>
+__device__ void table_insert(const Table& T, const int64_t* __restrict__ X, int k, uint32_t u, uint32_t v,
+                             uint64_t fp, WordFn b) {
+    const uint64_t rep = ((uint64_t)u << 32) | v;
+    uint64_t s = (fp ^ T.seed) & T.mask;
+    for (uint64_t probes = 0; probes <= T.mask; ++probes, s = (s + 1) & T.mask) {
+        ulonglong2* slot = T.slots + s;
+        ulonglong2 cur;
+        cur.x = ld_volatile(&slot->x);
+        if (cur.x == 0) {
+            const ulonglong2 old = cas128(slot, make_ulonglong2(0ull, kRepInit), make_ulonglong2(fp, rep));
+            if (old.x == 0) {
+                const unsigned long long idx = atomicAdd(T.count, 1ull);
+                if (idx < T.limit)
+                    T.reps[idx] = make_uint2(u, v);
+                else
+                    atomicOr(T.fail, 1);
+                return;
+            }
+            cur = old;
+        }
+        if (cur.x != fp) continue;
+        uint64_t r = cur.y;
+        while (r == kRepInit) r = ld_volatile(&slot->y);  // winner's 128-bit store is in flight
+        const uint32_t ru = (uint32_t)(r >> 32), rv = (uint32_t)r;
+        const int64_t* a = X + (size_t)ru * k;
+        const int64_t* c = X + (size_t)rv * k;
+        bool same = true;
+        for (int w = 0; w < k && same; ++w) same = ((__ldg(a + w) & __ldg(c + w)) == b(w));
+        if (same) return;
+        // equal fingerprint, different content: defer to the next level
+        atomicAdd(T.collisions, 1ull);
+        const unsigned long long o = atomicAdd(T.ovf_count, 1ull);
+        if (o < T.ovf_cap)
+            T.ovf[o] = make_uint2(u, v);
+        else
+            atomicOr(T.fail, 2);
+        return;
+    }
+    atomicOr(T.fail, 1);
+}
+
+__device__ __forceinline__ void tile_of(uint64_t t, uint32_t& bi, uint32_t& bj) {
+    // t enumerates (bi <= bj) column by column: t = bj(bj+1)/2 + bi
+    uint64_t j = (uint64_t)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+    while (j * (j + 1) / 2 > t) --j;
+    while ((j + 1) * (j + 2) / 2 <= t) ++j;
+    bj = (uint32_t)j;
+    bi = (uint32_t)(t - j * (j + 1) / 2);
+}
+
+// One CTA per 64x64 tile of the triangle u <= v (grid-stride over tiles).
+__global__ void __launch_bounds__(kPairThreads)
+pair_enum(const int64_t* __restrict__ X, uint32_t n, int k, int stride, uint64_t n_tiles, Table T,
+          uint64_t tile_begin) {
+    extern __shared__ int64_t sm[];
+    int64_t* sI = sm;
+    int64_t* sJ = sm + (size_t)kTile * stride;
+    for (uint64_t t = tile_begin + blockIdx.x; t < n_tiles; t += gridDim.x) {
+        if (*(volatile int*)T.fail) return;
+        uint32_t bi, bj;
+        tile_of(t, bi, bj);
+        const uint32_t i0 = bi * kTile, j0 = bj * kTile;
+        __syncthreads();
+        for (int q = threadIdx.x; q < kTile * k; q += kPairThreads) {
+            const int r = q / k, w = q % k;
+            sI[r * stride + w] = (i0 + r < n) ? X[(size_t)(i0 + r) * k + w] : 0;
+            sJ[r * stride + w] = (j0 + r < n) ? X[(size_t)(j0 + r) * k + w] : 0;
+        }
+        __syncthreads();
+        for (int q = threadIdx.x; q < kTile * kTile; q += kPairThreads) {
+            const int r = q / kTile, c = q % kTile;
+            const uint32_t u = i0 + r, v = j0 + c;
+            if (u >= n || v >= n || u > v) continue;
+            const int64_t* a = sI + r * stride;
+            const int64_t* b = sJ + c * stride;
+            Fp fp;
+            uint64_t nz = 0;
+            for (int w = 0; w < k; ++w) {
+                const uint64_t x = (uint64_t)(a[w] & b[w]);
+                nz |= x;
+                fp.add(x);
+            }
+            if (!nz) continue;  // SPEC.md:338 empty intersections dropped at the source
+            table_insert(T, X, k, u, v, fp.final(k), [&](int w) { return a[w] & b[w]; });
+        }
+    }
+}
+
+// Re-insert deferred (collided) pairs into a fresh level with a new seed.
+__global__ void pair_insert_list(const int64_t* __restrict__ X, int k, const uint2* __restrict__ list,
+                                 size_t n_list, Table T) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_list;
+         i += (size_t)gridDim.x * blockDim.x) {
+        const uint2 p = list[i];
+        const int64_t* a = X + (size_t)p.x * k;
+        const int64_t* b = X + (size_t)p.y * k;
+        Fp fp;
+        fp.h ^= T.seed;
+        for (int w = 0; w < k; ++w) fp.add((uint64_t)(__ldg(a + w) & __ldg(b + w)));
+        table_insert(T, X, k, p.x, p.y, fp.final(k),
+                     [&](int w) { return __ldg(a + w) & __ldg(b + w); });
+    }
+}
+
+__global__ void materialize(const int64_t* __restrict__ X, int k, const uint2* __restrict__ reps, size_t n,
+                            int64_t* __restrict__ out) {
+    for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < n * k;
+         q += (size_t)gridDim.x * blockDim.x) {
+        const size_t i = q / k;
+        const int w = (int)(q % k);
+        const uint2 p = reps[i];
+        out[q] = X[(size_t)p.x * k + w] & X[(size_t)p.y * k + w];
+    }
+}
+
+__global__ void gather_key(const int64_t* __restrict__ words, const uint32_t* __restrict__ perm, size_t n,
+                           int k, int w, uint64_t* __restrict__ key) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        key[i] = (uint64_t)words[(size_t)perm[i] * k + w];
+}
+
+__global__ void iota_u32(uint32_t* p, size_t n) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        p[i] = (uint32_t)i;
+}
+
+__global__ void gather_rows_k(const int64_t* __restrict__ src, const uint32_t* __restrict__ perm, size_t n,
+                              int k, int64_t* __restrict__ dst) {
+    for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < n * k;
+         q += (size_t)gridDim.x * blockDim.x)
+        dst[q] = src[(size_t)perm[q / k] * k + (q % k)];
+}
+
+__global__ void gather_i64(const int64_t* __restrict__ src, const uint32_t* __restrict__ perm, size_t n,
+                           int64_t* __restrict__ dst) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        dst[i] = src[perm[i]];
+}
+
+__global__ void score_k(const int64_t* __restrict__ pat, size_t n, int k, const int64_t* __restrict__ sup,
+                        int64_t* __restrict__ score, int* __restrict__ ovf) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        int64_t size = 0;
+        for (int w = 0; w < k; ++w) size += __popcll((unsigned long long)pat[i * k + w]);
+        const int64_t sq = size * size;  // size <= 64k bits: no overflow
+        const int64_t f = sup[i];
+        int64_t s;
+        // f * sq overflows int64 iff |f| > INT64_MAX / sq (sq > 0; f >= 0 here)
+        if (sq != 0 && (f > INT64_MAX / sq || f < INT64_MIN / sq)) {
+            atomicOr(ovf, 1);
+            s = 0;
+        } else {
+            s = f * sq;
+        }
+        score[i] = s;
+    }
+}
+
+// Checked Σ in 128-bit per block, combined on the host.
+__global__ void sum128(const int64_t* __restrict__ s, size_t n, unsigned long long* __restrict__ out_lo,
+                       long long* __restrict__ out_hi) {
+    __int128 acc = 0;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        acc += s[i];
+    typedef cub::BlockReduce<long long, 256> BR;
+    __shared__ typename BR::TempStorage t1, t2;
+    // split into (hi, lo32) pieces that fit long long sums across 256 threads
+    const long long hi = (long long)(acc >> 32);
+    const long long lo = (long long)(acc & 0xffffffff);
+    const long long shi = BR(t1).Sum(hi);
+    __syncthreads();
+    const long long slo = BR(t2).Sum(lo);
+    if (threadIdx.x == 0) {
+        out_lo[blockIdx.x] = (unsigned long long)slo;
+        out_hi[blockIdx.x] = shi;
+    }
+}
+
+unsigned grid_for(const Ctx& ctx, size_t work, int threads) {
+    size_t g = (work + threads - 1) / threads;
+    const size_t cap = (size_t)ctx.sm_count * 32;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    return (unsigned)g;
+}
+
+struct TableMem {
+    DevBuf slots, reps, ovf, ctr;  // ctr: count, ovf_count, collisions, fail
+    Table make(Ctx& ctx, uint64_t cap, uint64_t ovf_cap, uint64_t seed) {
+        slots.alloc(cap * sizeof(ulonglong2), ctx.stream);
+        // empty slot = {0, kRepInit}: fill x with 0 and y with ~0 via two memsets on a strided view
+        IGB_CUDA(cudaMemset2DAsync(slots.p, 16, 0, 8, cap, ctx.stream));
+        IGB_CUDA(cudaMemset2DAsync(static_cast<char*>(slots.p) + 8, 16, 0xff, 8, cap, ctx.stream));
+        const uint64_t limit = cap / 4 * 3;
+        reps.alloc(limit * sizeof(uint2), ctx.stream);
+        ovf.alloc(ovf_cap * sizeof(uint2), ctx.stream);
+        ctr.alloc(4 * sizeof(unsigned long long), ctx.stream);
+        IGB_CUDA(cudaMemsetAsync(ctr.p, 0, 4 * sizeof(unsigned long long), ctx.stream));
+        Table T;
+        T.slots = slots.as<ulonglong2>();
+        T.mask = cap - 1;
+        T.reps = reps.as<uint2>();
+        T.count = ctr.as<unsigned long long>();
+        T.limit = limit;
+        T.ovf = ovf.as<uint2>();
+        T.ovf_count = ctr.as<unsigned long long>() + 1;
+        T.ovf_cap = ovf_cap;
+        T.collisions = ctr.as<unsigned long long>() + 2;
+        T.fail = reinterpret_cast<int*>(ctr.as<unsigned long long>() + 3);
+        T.seed = seed;
+        return T;
+    }
+};
+
+uint64_t next_pow2(uint64_t x) {
+    uint64_t p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+__global__ void pair_window_k(const int64_t* __restrict__ left, const int64_t* __restrict__ rows, size_t cnt, int k,
+                              int64_t* __restrict__ out) {
+    for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < cnt * k; q += (size_t)gridDim.x * blockDim.x)
+        out[q] = left[q % k] & rows[q];
+}
+
+}  // namespace
+
+void pair_window_dev(Ctx& ctx, const int64_t* d_left, const int64_t* d_rows, size_t cnt, size_t k, int64_t* d_out) {
+    IGB_LAUNCH(ctx, pair_window_k, grid_for(ctx, cnt * k, 256), 256, 0, d_left, d_rows, cnt, (int)k, d_out);
+}
+
+void sort_rows_canonical(Ctx& ctx, const int64_t* d_words, size_t n, size_t k, uint32_t* d_perm) {
+    if (n == 0) return;
+    IGB_LAUNCH(ctx, iota_u32, grid_for(ctx, n, 256), 256, 0, d_perm, n);
+    if (n == 1) return;
+    DevBuf keys(n * 8, ctx.stream), keys2(n * 8, ctx.stream), perm2(n * 4, ctx.stream);
+    size_t temp_bytes = 0;
+    IGB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, keys.as<uint64_t>(), keys2.as<uint64_t>(),
+                                             d_perm, perm2.as<uint32_t>(), (int64_t)n, 0, 64, ctx.stream));
+    DevBuf temp(temp_bytes, ctx.stream);
+    uint32_t* cur = d_perm;
+    uint32_t* alt = perm2.as<uint32_t>();
+    // LSD over words K-1 .. 0 with a stable radix sort: lexicographic unsigned order.
+    for (int w = (int)k - 1; w >= 0; --w) {
+        IGB_LAUNCH(ctx, gather_key, grid_for(ctx, n, 256), 256, 0, d_words, cur, n, (int)k, w, keys.as<uint64_t>());
+        IGB_CUDA(cub::DeviceRadixSort::SortPairs(temp.p, temp_bytes, keys.as<uint64_t>(), keys2.as<uint64_t>(),
+                                                 cur, alt, (int64_t)n, 0, 64, ctx.stream));
+        std::swap(cur, alt);
+    }
+    if (cur != d_perm) IGB_CUDA(cudaMemcpyAsync(d_perm, cur, n * 4, cudaMemcpyDeviceToDevice, ctx.stream));
+}
+
+void gather_rows(Ctx& ctx, const int64_t* d_src, const uint32_t* d_perm, size_t n, size_t k, int64_t* d_dst) {
+    if (n == 0) return;
+    IGB_LAUNCH(ctx, gather_rows_k, grid_for(ctx, n * k, 256), 256, 0, d_src, d_perm, n, (int)k, d_dst);
+}
+
+void canonical_order(Ctx& ctx, DevRows& rows, DevBuf* a, DevBuf* b) {
+    const size_t n = rows.n, k = rows.k;
+    if (n < 2) return;
+    DevBuf perm(n * 4, ctx.stream);
+    sort_rows_canonical(ctx, rows.data(), n, k, perm.as<uint32_t>());
+    DevBuf sorted(n * k * 8, ctx.stream);
+    gather_rows(ctx, rows.data(), perm.as<uint32_t>(), n, k, sorted.as<int64_t>());
+    rows.buf = std::move(sorted);
+    for (DevBuf* pay : {a, b}) {
+        if (!pay || !pay->p) continue;
+        DevBuf t(n * 8, ctx.stream);
+        IGB_LAUNCH(ctx, gather_i64, grid_for(ctx, n, 256), 256, 0, pay->as<int64_t>(), perm.as<uint32_t>(), n,
+                   t.as<int64_t>());
+        *pay = std::move(t);
+    }
+}
+
+void enumerate_dev(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, uint32_t L, DevRows& out,
+                   EnumStats* stats) {
+    out.n = 0;
+    out.k = k;
+    out.L = L;
+    if (n == 0) return;
+    if (n > 0xffffffffull) fail(IG_E_INVALID_ARG, "enumerate: more than 2^32 rows");
+    const uint64_t blocks = (n + kTile - 1) / kTile;
+    const uint64_t n_tiles = blocks * (blocks + 1) / 2;
+    const uint64_t pairs = (uint64_t)n * (n - 1) / 2;
+    const int stride = (int)(k | 1);
+    const size_t smem = 2 * (size_t)kTile * stride * 8;
+    if (smem > 200 * 1024) fail(IG_E_INVALID_ARG, "enumerate: rows wider than the shared-memory tile (K > 200)");
+    IGB_CUDA(cudaFuncSetAttribute(pair_enum, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+
+    // Initial capacity from a sub-linear guess of the distinct count; doubled
+    // (x4) and rerun if the table fills.  Results never depend on capacity.
+    uint64_t guess = (uint64_t)(4.0 * std::pow((double)(pairs + n), 0.8)) + 2 * n + 1024;
+    uint64_t cap = next_pow2(std::max<uint64_t>(guess, 1u << 16));
+    const uint64_t max_cap = next_pow2(2 * (pairs + n) + 1024);
+    if (cap > max_cap) cap = max_cap;
+    int retries = 0;
+    std::vector<DevBuf> level_reps;  // per level: reps
+    std::vector<uint64_t> level_counts;
+    uint64_t collisions_total = 0;
+    for (;;) {
+        level_reps.clear();
+        level_counts.clear();
+        collisions_total = 0;
+        bool ok = true;
+        DevBuf pending;   // uint2 pairs deferred from the previous level
+        uint64_t n_pending = 0;
+        for (int level = 0;; ++level) {
+            TableMem tm;
+            const uint64_t lcap = level == 0 ? cap : next_pow2(4 * n_pending + 1024);
+            const uint64_t ovf_cap = level == 0 ? std::max<uint64_t>(1u << 20, cap / 64) : n_pending + 1;
+            Table T = tm.make(ctx, lcap, ovf_cap, 0x2545f4914f6cdd1dull * (uint64_t)(level + 1));
+            if (level == 0) {
+                const unsigned grid = (unsigned)std::min<uint64_t>(n_tiles, (uint64_t)ctx.sm_count * 16);
+                IGB_LAUNCH(ctx, pair_enum, grid, kPairThreads, smem, d_rows, (uint32_t)n, (int)k, stride, n_tiles,
+                           T, 0ull);
+            } else {
+                IGB_LAUNCH(ctx, pair_insert_list, grid_for(ctx, n_pending, 256), 256, 0, d_rows, (int)k,
+                           pending.as<uint2>(), n_pending, T);
+            }
+            unsigned long long h[4];
+            IGB_CUDA(cudaMemcpyAsync(h, tm.ctr.p, sizeof(h), cudaMemcpyDeviceToHost, ctx.stream));
+            IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+            const int failbits = (int)(h[3] & 0xffffffffu);
+            if (failbits) {
+                ok = false;
+                break;
+            }
+            level_counts.push_back(h[0]);
+            collisions_total += h[2];
+            level_reps.push_back(std::move(tm.reps));
+            if (h[1] == 0) break;
+            pending = std::move(tm.ovf);
+            n_pending = h[1];
+            if (level > 64) fail(IG_E_CUDA, "enumerate: fingerprint collision levels did not converge");
+        }
+        if (ok) break;
+        if (cap >= max_cap) fail(IG_E_OOM, "enumerate: candidate table cannot grow further");
+        cap = std::min<uint64_t>(cap * 4, max_cap);
+        ++retries;
+    }
+    uint64_t total = 0;
+    for (auto c : level_counts) total += c;
+    out.buf.alloc(total * k * 8, ctx.stream);
+    out.n = total;
+    uint64_t off = 0;
+    for (size_t l = 0; l < level_reps.size(); ++l) {
+        const uint64_t c = level_counts[l];
+        if (c)
+            IGB_LAUNCH(ctx, materialize, grid_for(ctx, c * k, 256), 256, 0, d_rows, (int)k,
+                       level_reps[l].as<uint2>(), c, out.data() + off * k);
+        off += c;
+    }
+    if (stats) {
+        stats->pairs = pairs;
+        stats->table_slots = cap;
+        stats->retries = retries;
+        stats->levels = (int)level_reps.size();
+        stats->collisions = collisions_total;
+    }
+}
+
+int score_dev(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const int64_t* d_support, int64_t* d_score) {
+    if (np == 0) return IG_OK;
+    DevBuf flag(sizeof(int), ctx.stream);
+    IGB_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), ctx.stream));
+    IGB_LAUNCH(ctx, score_k, grid_for(ctx, np, 256), 256, 0, d_pat, np, (int)k, d_support, d_score, flag.as<int>());
+    int h = 0;
+    IGB_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+    IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+    return h ? IG_E_OVERFLOW : IG_OK;
+}
+
+int total_score_dev(Ctx& ctx, const int64_t* d_score, size_t np, int64_t* total) {
+    *total = 0;
+    if (np == 0) return IG_OK;
+    const unsigned g = std::min<unsigned>(grid_for(ctx, np, 256), 1024);
+    DevBuf lo(g * 8, ctx.stream), hi(g * 8, ctx.stream);
+    IGB_LAUNCH(ctx, sum128, g, 256, 0, d_score, np, lo.as<unsigned long long>(), hi.as<long long>());
+    std::vector<unsigned long long> hl(g);
+    std::vector<long long> hh(g);
+    IGB_CUDA(cudaMemcpyAsync(hl.data(), lo.p, g * 8, cudaMemcpyDeviceToHost, ctx.stream));
+    IGB_CUDA(cudaMemcpyAsync(hh.data(), hi.p, g * 8, cudaMemcpyDeviceToHost, ctx.stream));
+    IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+    __int128 acc = 0;
+    for (unsigned i = 0; i < g; ++i) acc += ((__int128)hh[i] << 32) + (__int128)hl[i];
+    // Scores are non-negative (support >= 0), so the running-sum overflow of
+    // total_score (mine.hpp:50-51) happens iff the exact total exceeds INT64_MAX.
+    if (acc > (__int128)INT64_MAX || acc < (__int128)INT64_MIN) return IG_E_OVERFLOW;
+    *total = (int64_t)acc;
+    return IG_OK;
+}
+
+namespace {
+__global__ void flag_to_keep(const uint8_t* f, size_t n, uint8_t* keep) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        keep[i] = f[i] ? 0 : 1;
+}
+__global__ void compact_rows_k(const int64_t* __restrict__ src, const uint32_t* __restrict__ idx, size_t m, int k,
+                               int64_t* __restrict__ dst) {
+    for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < m * k; q += (size_t)gridDim.x * blockDim.x)
+        dst[q] = src[(size_t)idx[q / k] * k + q % k];
+}
+}  // namespace
+
+size_t compact_unflagged(Ctx& ctx, const int64_t* d_words, const int64_t* d_sup, const int64_t* d_sc,
+                         const uint8_t* d_flag, size_t n, size_t k, int64_t* o_words, int64_t* o_sup,
+                         int64_t* o_sc) {
+    if (n == 0) return 0;
+    DevBuf keep(n, ctx.stream), idx(n * 4, ctx.stream), nsel(8, ctx.stream), iota(n * 4, ctx.stream);
+    IGB_LAUNCH(ctx, flag_to_keep, grid_for(ctx, n, 256), 256, 0, d_flag, n, keep.as<uint8_t>());
+    IGB_LAUNCH(ctx, iota_u32, grid_for(ctx, n, 256), 256, 0, iota.as<uint32_t>(), n);
+    size_t tb = 0;
+    IGB_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, iota.as<uint32_t>(), keep.as<uint8_t>(), idx.as<uint32_t>(),
+                                        nsel.as<int64_t>(), (int64_t)n, ctx.stream));
+    DevBuf temp(tb, ctx.stream);
+    IGB_CUDA(cub::DeviceSelect::Flagged(temp.p, tb, iota.as<uint32_t>(), keep.as<uint8_t>(), idx.as<uint32_t>(),
+                                        nsel.as<int64_t>(), (int64_t)n, ctx.stream));
+    int64_t m = 0;
+    IGB_CUDA(cudaMemcpyAsync(&m, nsel.p, 8, cudaMemcpyDeviceToHost, ctx.stream));
+    IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+    if (m) {
+        IGB_LAUNCH(ctx, compact_rows_k, grid_for(ctx, m * k, 256), 256, 0, d_words, idx.as<uint32_t>(), (size_t)m,
+                   (int)k, o_words);
+        if (d_sup) IGB_LAUNCH(ctx, gather_i64, grid_for(ctx, m, 256), 256, 0, d_sup, idx.as<uint32_t>(), (size_t)m, o_sup);
+        if (d_sc) IGB_LAUNCH(ctx, gather_i64, grid_for(ctx, m, 256), 256, 0, d_sc, idx.as<uint32_t>(), (size_t)m, o_sc);
+    }
+    return (size_t)m;
+}
+
+}  // namespace igb

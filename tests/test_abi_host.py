@@ -1,0 +1,149 @@
+"""CPU checks of the product library: it loads, exports every symbol
+include/ig_b200.h declares, and its host-side pipeline pieces (CSV reader,
+schema inference, checked total, config validation, infer/eval arithmetic)
+match the reference semantics.  No GPU compute is called here."""
+import json
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle import pipeline as opipe
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _header_symbols():
+    src = open(os.path.join(ROOT, "include", "ig_b200.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(ig_[a-z0-9_]+)\s*\(", src)) - {"ig_progress_fn"})
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2507_14222_b200 import _native
+    syms = _header_symbols()
+    assert len(syms) >= 50
+    for s in syms:
+        assert hasattr(_native.lib, s), s
+    bound = {name for name, _, _ in _native.SIGNATURES}
+    assert set(syms) == bound
+
+
+def test_library_is_sm100a_only():
+    so = os.path.join(ROOT, "paper_2507_14222_b200", "libig_b200.so")
+    data = open(so, "rb").read()
+    assert b"sm_100a" in data or b"sm_100" in data
+
+
+def test_csv_reader_matches_reference_restatement(golden_dir):
+    from paper_2507_14222_b200 import api
+    g = json.load(open(os.path.join(golden_dir, "tokenizer.json")))
+    for name, run in g["runs"].items():
+        csv = run["csv"].encode()
+        t = api.read_csv(csv)
+        hdr, rows = opipe.read_csv(csv)
+        assert t.rows == len(rows) and t.columns == len(hdr)
+        tr = t.slice(0, run["train_rows"])
+        s = api.infer_schema(tr, "label", decimals=run["decimals"])
+        for j in range(t.columns - 1):
+            kind, mean, sd = s.column(j)
+            assert (0 if kind == "numeric" else 1) == run["kind"][j]
+            assert mean == run["mean"][j] and sd == run["std"][j]
+
+
+@pytest.mark.parametrize("bad, exc", [
+    (b"a,b\n1,2\n3\n", "DataError"),
+    (b"a,b\n\"1,2\n", "DataError"),
+    (b"", "DataError"),
+])
+def test_csv_errors(bad, exc):
+    from paper_2507_14222_b200 import api
+    with pytest.raises(getattr(api, exc)):
+        api.read_csv(bad)
+
+
+def test_schema_errors():
+    from paper_2507_14222_b200 import api
+    t = api.read_csv(b"a,label\n1,normal\n2,neptune\n")
+    with pytest.raises(api.ConfigError):
+        api.infer_schema(t, "nolabel")
+    with pytest.raises(api.ConfigError):
+        api.infer_schema(t, "label", decimals=13)
+    with pytest.raises(api.DataError):
+        api.infer_schema(t, "label", attack_values=["neptune"], normal_values=["x"])
+    with pytest.raises(api.DataError):
+        api.infer_schema(api.read_csv(b"a,label\n"), "label")
+
+
+def test_total_score_checked():
+    from paper_2507_14222_b200 import api
+    assert api.total_score(np.array([1, 2, 3])) == 6
+    with pytest.raises(api.IGArithmeticError):
+        api.total_score(np.array([2**62, 2**62]))
+
+
+def test_config_and_backend_factory():
+    from paper_2507_14222_b200 import api
+    with pytest.raises(api.ConfigError):
+        api.KernelConfig(pair_batch=0).validate()
+    with pytest.raises(api.ConfigError):
+        api.KernelConfig(coverage_block=0).validate()
+    with pytest.raises(api.ConfigError, match="available: b200"):
+        api.make_backend("cuda-magic")
+    assert api.backend_names() == ["b200"]
+
+
+def test_decision_table_property():
+    """procedural R1-R3 == closed form on 10^6 random tuples."""
+    from paper_2507_14222_b200 import api
+    rng = np.random.default_rng(639)
+    n = 1_000_000
+    A = rng.integers(0, 50, n)
+    Nv = rng.integers(0, 50, n)
+    mu = float(rng.uniform(0, 60))
+    sg = float(rng.uniform(0, 20))
+    r = float(rng.uniform(0, 2))
+    label, reg = api.classify(A, Nv, mu, sg, r)
+    closed = (A >= Nv) | (Nv.astype(float) < mu - r * sg)
+    assert np.array_equal(label.astype(bool), closed)
+    idx = rng.integers(0, n, 2000)
+    for i in idx:
+        assert (int(label[i]), int(reg[i])) == opipe.classify(int(A[i]), int(Nv[i]), mu, sg, r)
+
+
+def test_metrics_against_direct_formulas():
+    """confusion metrics to 1e-12; rank AUC vs the O(P*N) pairwise oracle."""
+    from paper_2507_14222_b200 import api
+    rng = np.random.default_rng(640)
+    for _ in range(2000):
+        n = int(rng.integers(1, 60))
+        truth = rng.integers(0, 2, n)
+        pred = rng.integers(0, 2, n)
+        m = rng.integers(-5, 5, n)
+        got = api.compute_metrics(pred, truth, m)
+        tp = int(((pred == 1) & (truth == 1)).sum())
+        fp = int(((pred == 1) & (truth == 0)).sum())
+        fn = int(((pred == 0) & (truth == 1)).sum())
+        tn = n - tp - fp - fn
+        assert math.isclose(got["accuracy"], (tp + tn) / n, abs_tol=1e-12)
+        assert math.isclose(got["recall"], tp / (tp + fn) if tp + fn else 0.0, abs_tol=1e-12)
+        assert math.isclose(got["precision"], tp / (tp + fp) if tp + fp else 0.0, abs_tol=1e-12)
+        pos = m[truth == 1]
+        neg = m[truth == 0]
+        if len(pos) and len(neg):
+            pairs = sum((1.0 if p > q else 0.5 if p == q else 0.0) for p in pos for q in neg)
+            assert got["rank_auc"] == pairs / (len(pos) * len(neg))
+    # invariance under strictly increasing transforms
+    m = rng.integers(-50, 50, 200)
+    t = rng.integers(0, 2, 200)
+    assert api.compute_metrics(t, t, m)["rank_auc"] == api.compute_metrics(t, t, 3 * m + 7)["rank_auc"]
+
+
+def test_normal_stats_examples():
+    from paper_2507_14222_b200 import api
+    assert api.fit_normal_stats([10, 10, 10, 0]) == (10.0, 0.0)
+    mu, sg = api.fit_normal_stats([40, 50, 60])
+    assert mu == 50.0 and abs(sg - 8.16496580927726) < 1e-12
+    assert api.fit_normal_stats([0, 0, 0]) == (0.0, 0.0)

@@ -1,0 +1,92 @@
+"""GPU parity of mine/purify (mine.hpp:35-51) against the
+reference-generated golden fixtures and the plain-C oracle.  Bit-exact."""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import oracle
+from tests.helpers import random_rows
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def api():
+    from paper_2507_14222_b200 import api as a
+    return a
+
+
+def test_golden_random_cases(api, golden_dir):
+    z = np.load(os.path.join(golden_dir, "random_mine.npz"))
+    be = api.make_backend("b200")
+    for i in range(int(z["count"])):
+        p = f"c{i}_"
+        L = int(z[p + "L"])
+        Xa = api.PackedMatrix(z[p + "attack"], L, "attack")
+        Xn = api.PackedMatrix(z[p + "normal"], L, "normal")
+        cs = api.enumerate_candidates(Xa, be, api.KernelConfig(pair_batch=int(i % 5) + 1))
+        assert np.array_equal(cs.patterns.words, z[p + "ca_words"]), i
+        api.count_support(cs, Xa)
+        api.score_patterns(cs)
+        assert np.array_equal(cs.supports, z[p + "ca_sup"]), i
+        assert np.array_equal(cs.scores, z[p + "ca_sc"]), i
+        m = api.fit(Xa.words, Xn.words, L)
+        for c, key in ((0, "ca"), (1, "cn")):
+            d = m.dictionary(c, 0)
+            assert np.array_equal(d.words, z[p + key + "_words"]), (i, c)
+            assert np.array_equal(d.supports, z[p + key + "_sup"]), (i, c)
+            assert np.array_equal(d.scores, z[p + key + "_sc"]), (i, c)
+            keep = z[p + ("keep_a" if c == 0 else "keep_n")] == 1
+            pd = m.dictionary(c, 1)
+            assert np.array_equal(pd.words, z[p + key + "_words"][keep]), (i, c)
+            assert np.array_equal(pd.scores, z[p + key + "_sc"][keep]), (i, c)
+        A, N = m.evidence(z[p + "tests"])
+        assert np.array_equal(A, z[p + "A"]) and np.array_equal(N, z[p + "N"]), i
+
+
+def test_degenerate_classes(api):
+    L = 70
+    rng = np.random.default_rng(9)
+    row = random_rows(rng, 1, L, 0.5)
+    same = np.repeat(row, 37, axis=0)
+    cs = api.enumerate_candidates(api.PackedMatrix(same, L))
+    assert np.array_equal(cs.patterns.words, row)             # SPEC.md:308 all identical → 1
+    a = np.zeros((2, 2), np.int64)
+    a[0, 0] = 1
+    a[1, 1] = 1                                               # disjoint rows → the two signatures
+    cs = api.enumerate_candidates(api.PackedMatrix(a, L))
+    assert cs.patterns.rows == 2
+    with pytest.raises(api.DataError):
+        api.enumerate_candidates(api.PackedMatrix(np.zeros((0, 2), np.int64), L))
+    with pytest.raises(api.ConfigError):
+        api.enumerate_candidates(api.PackedMatrix(a, L), config=api.KernelConfig(pair_batch=0))
+    z = np.zeros((3, 2), np.int64)                            # all-empty rows → no candidates
+    assert api.enumerate_candidates(api.PackedMatrix(z, L)).patterns.rows == 0
+
+
+@pytest.mark.parametrize("n,L,dens", [(600, 96, 0.6), (2500, 300, 0.93), (1500, 1000, 0.985)])
+def test_fit_vs_oracle_random(api, n, L, dens):
+    rng = np.random.default_rng(n + L)
+    Xa = random_rows(rng, n, L, dens)
+    Xn = random_rows(rng, n + 17, L, dens)
+    ref = oracle.fit(Xa, Xn)
+    m = api.fit(Xa, Xn, L)
+    for c in range(2):
+        for which, want in ((0, ref.candidates[c]), (1, ref.pure[c])):
+            d = m.dictionary(c, which)
+            assert np.array_equal(d.words, want.words), (c, which)
+            assert np.array_equal(d.supports, want.supports), (c, which)
+            assert np.array_equal(d.scores, want.scores), (c, which)
+    T = random_rows(rng, 777, L, dens)
+    A, N = m.evidence(T)
+    assert np.array_equal(A, oracle.fused_score(ref.pure[0].words, ref.pure[0].scores, T))
+    assert np.array_equal(N, oracle.fused_score(ref.pure[1].words, ref.pure[1].scores, T))
+
+
+def test_progress_callback(api):
+    rng = np.random.default_rng(5)
+    X = random_rows(rng, 100, 64, 0.7)
+    seen = []
+    cs = api.enumerate_candidates(api.PackedMatrix(X, 64), progress=lambda d, t, f: seen.append((d, t, f)))
+    assert seen and seen[-1] == (100 * 99 // 2, 100 * 99 // 2, cs.patterns.rows)
