@@ -75,6 +75,7 @@ __device__ void table_insert(const Table& T, const int64_t* __restrict__ X, int 
         ulonglong2* slot = T.slots + s;
         ulonglong2 cur;
         cur.x = ld_volatile(&slot->x);
+        cur.y = kRepInit;  // loaded below only when the fingerprint matches
         if (cur.x == 0) {
             const ulonglong2 old = cas128(slot, make_ulonglong2(0ull, kRepInit), make_ulonglong2(fp, rep));
             if (old.x == 0) {
@@ -89,7 +90,7 @@ __device__ void table_insert(const Table& T, const int64_t* __restrict__ X, int 
         }
         if (cur.x != fp) continue;
         uint64_t r = cur.y;
-        while (r == kRepInit) r = ld_volatile(&slot->y);  // winner's 128-bit store is in flight
+        while (r == kRepInit) r = ld_volatile(&slot->y);  // not loaded yet, or the winner's store is in flight
         const uint32_t ru = (uint32_t)(r >> 32), rv = (uint32_t)r;
         const int64_t* a = X + (size_t)ru * k;
         const int64_t* c = X + (size_t)rv * k;
