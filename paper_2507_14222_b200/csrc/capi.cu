@@ -14,6 +14,7 @@
 #include "host_pipeline.hpp"
 #include "ig_b200.h"
 #include "ig_internal.cuh"
+#include "posting.cuh"
 #include "subset.cuh"
 
 struct ig_ctx : igb::Ctx {};
@@ -115,12 +116,20 @@ void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m) {
         m.cand[c].pairs = m.stats[c].pairs;
     }
     tm.mark();  // 1
+    // Row postings of each class, shared by support (own class) and coverage (opposite class).
+    const bool vertical = igb::postings_supported(L, std::max(X[0].n, X[1].n));
+    igb::Postings PX[2];
+    if (vertical)
+        for (int c = 0; c < 2; ++c) igb::build_postings(ctx, X[c].p, X[c].n, k, L, PX[c]);
     for (int c = 0; c < 2; ++c) {
         ig_candidates& C = m.cand[c];
         const size_t np = C.rows.n;
         C.support.alloc(std::max<size_t>(np, 1) * 8, ctx.stream);
         C.score.alloc(std::max<size_t>(np, 1) * 8, ctx.stream);
-        igb::count_support_dev(ctx, C.rows.data(), np, X[c].p, X[c].n, k, C.support.as<int64_t>());
+        if (vertical)
+            igb::posting_support(ctx, C.rows.data(), np, k, PX[c], C.support.as<int64_t>());
+        else
+            igb::count_support_dev(ctx, C.rows.data(), np, X[c].p, X[c].n, k, C.support.as<int64_t>());
         if (igb::score_dev(ctx, C.rows.data(), np, k, C.support.as<int64_t>(), C.score.as<int64_t>()) != IG_OK)
             fail(IG_E_OVERFLOW, "pattern score overflows int64");
         int64_t total = 0;
@@ -135,7 +144,10 @@ void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m) {
         ig_candidates& C = m.cand[c];
         const size_t np = C.rows.n;
         DevBuf mask(std::max<size_t>(np, 1), ctx.stream);
-        igb::coverage_any_dev(ctx, C.rows.data(), np, X[1 - c].p, X[1 - c].n, k, mask.as<uint8_t>());
+        if (vertical && X[1 - c].n > 0)
+            igb::posting_cover(ctx, C.rows.data(), np, k, PX[1 - c], mask.as<uint8_t>());
+        else
+            igb::coverage_any_dev(ctx, C.rows.data(), np, X[1 - c].p, X[1 - c].n, k, mask.as<uint8_t>());
         ig_candidates& P = m.pure[c];
         P.rows.k = k;
         P.rows.L = L;
@@ -183,6 +195,24 @@ void evidence_impl(igb::Ctx& ctx, const ig_model& m, const int64_t* d_tests, siz
                    int64_t* d_N) {
     if (L != m.L) fail(IG_E_INVALID_ARG, "fused_score: logical length mismatch");
     const size_t k = igb::words_for(L);
+    // Fit scores are support * size^2 >= 0, so the vertical matcher applies;
+    // test-row postings are built once and shared by both dictionaries.
+    if (igb::postings_supported(L, nt)) {
+        igb::Postings PT;
+        igb::build_postings(ctx, d_tests, nt, k, L, PT);
+        DevBuf flag(sizeof(int), ctx.stream);
+        IGB_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), ctx.stream));
+        for (int c = 0; c < 2; ++c) {
+            const ig_candidates& P = m.pure[c];
+            igb::posting_match(ctx, P.rows.data(), P.rows.n, k, P.score.as<int64_t>(), PT, c == 0 ? d_A : d_N,
+                               flag.as<int>());
+        }
+        int h = 0;
+        IGB_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+        IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+        if (h) fail(IG_E_OVERFLOW, "evidence score sum overflows int64");
+        return;
+    }
     for (int c = 0; c < 2; ++c) {
         const ig_candidates& P = m.pure[c];
         if (igb::fused_score_dev(ctx, P.rows.data(), P.rows.n, P.score.as<int64_t>(), d_tests, nt, k,

@@ -16,6 +16,7 @@
 #include <cub/cub.cuh>
 
 #include "ig_internal.cuh"
+#include "posting.cuh"
 #include "subset.cuh"
 
 namespace igb {
@@ -244,6 +245,12 @@ void coverage_any_dev(Ctx& ctx, const int64_t* d_pat, size_t np, const int64_t* 
                       size_t k, uint8_t* d_mask) {
     IGB_CUDA(cudaMemsetAsync(d_mask, 0, np, ctx.stream));
     if (np == 0 || no == 0) return;
+    if (postings_supported((uint32_t)(64 * k), no)) {
+        Postings P;
+        build_postings(ctx, d_opp, no, k, (uint32_t)(64 * k), P);
+        posting_cover(ctx, d_pat, np, k, P, d_mask);
+        return;
+    }
     // The opponent side is never sliced: each candidate stops at its first cover.
     launch_scan<kCover, false>(ctx, d_pat, np, d_opp, no, k, nullptr, 1, no, nullptr, nullptr, d_mask,
                                nullptr);
@@ -254,6 +261,12 @@ void count_support_dev(Ctx& ctx, const int64_t* d_pat, size_t np, const int64_t*
     if (np == 0) return;
     if (n == 0) {
         IGB_CUDA(cudaMemsetAsync(d_support, 0, np * 8, ctx.stream));
+        return;
+    }
+    if (postings_supported((uint32_t)(64 * k), n)) {
+        Postings P;
+        build_postings(ctx, d_rows, n, k, (uint32_t)(64 * k), P);
+        posting_support(ctx, d_pat, np, k, P, d_support);
         return;
     }
     size_t slice_rows;
@@ -286,6 +299,10 @@ int fused_score_dev(Ctx& ctx, const int64_t* d_pat, size_t np, const int64_t* d_
         // every test row walks the patterns in index order (kernels.cpp:70-75).
         launch_scan<kMatch, true>(ctx, d_tests, nt, d_pat, np, k, d_scores, 1, np, d_out, nullptr, nullptr,
                                   d_flags);
+    } else if (postings_supported((uint32_t)(64 * k), nt)) {
+        Postings P;
+        build_postings(ctx, d_tests, nt, k, (uint32_t)(64 * k), P);
+        posting_match(ctx, d_pat, np, k, d_scores, P, d_out, d_flags);
     } else {
         size_t slice_rows;
         const int slices = choose_slices(ctx, nt, np, &slice_rows);
