@@ -23,6 +23,7 @@ struct ig_candidates {
     igb::DevRows rows;
     igb::DevBuf support, score;
     bool has_support = false, has_score = false;
+    bool ordered = true;  // rows in canonical words::less order
     uint64_t pairs = 0;
 };
 
@@ -114,6 +115,7 @@ void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m) {
         if (X[c].n == 0) fail(IG_E_DATA, "enumerate_candidates: empty class");
         igb::enumerate_dev(ctx, X[c].p, X[c].n, k, L, m.cand[c].rows, &m.stats[c]);
         m.cand[c].pairs = m.stats[c].pairs;
+        m.cand[c].ordered = false;
     }
     tm.mark();  // 1
     // Row postings of each class, shared by support (own class) and coverage (opposite class).
@@ -138,8 +140,6 @@ void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m) {
         C.has_support = C.has_score = true;
     }
     tm.mark();  // 2
-    for (int c = 0; c < 2; ++c) igb::canonical_order(ctx, m.cand[c].rows, &m.cand[c].support, &m.cand[c].score);
-    tm.mark();  // 3
     for (int c = 0; c < 2; ++c) {
         ig_candidates& C = m.cand[c];
         const size_t np = C.rows.n;
@@ -159,13 +159,17 @@ void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m) {
                                           P.score.as<int64_t>());
         P.has_support = P.has_score = true;
     }
+    tm.mark();  // 3
+    // Canonical order of the pure dictionaries (the model output).  The full
+    // candidate sets B^c are ordered on first copy-out (ig_model_copy which=0).
+    for (int c = 0; c < 2; ++c) igb::canonical_order(ctx, m.pure[c].rows, &m.pure[c].support, &m.pure[c].score);
     tm.mark();  // 4
     IGB_CUDA(cudaStreamSynchronize(ctx.stream));
     m.ms[0] = 0;
     m.ms[1] = tm.ms(0, 1);
     m.ms[2] = tm.ms(1, 2);
-    m.ms[3] = tm.ms(3, 4);
-    m.ms[4] = tm.ms(2, 3);
+    m.ms[3] = tm.ms(2, 3);
+    m.ms[4] = tm.ms(3, 4);
     m.ms[5] = tm.ms(0, 4);
     for (int c = 0; c < 2; ++c) {
         for (ig_candidates* C : {&m.cand[c], &m.pure[c]}) {
@@ -176,7 +180,14 @@ void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m) {
     }
 }
 
-void copy_out(igb::Ctx& ctx, const ig_candidates& c, int64_t* words, int64_t* sup, int64_t* sc) {
+void copy_out(igb::Ctx& ctx, ig_candidates& c, int64_t* words, int64_t* sup, int64_t* sc) {
+    if (!c.ordered) {
+        igb::canonical_order(ctx, c.rows, c.has_support ? &c.support : nullptr, c.has_score ? &c.score : nullptr);
+        c.rows.buf.persist();
+        c.support.persist();
+        c.score.persist();
+        c.ordered = true;
+    }
     const size_t n = c.rows.n, k = c.rows.k;
     if (words && n * k)
         IGB_CUDA(cudaMemcpyAsync(words, c.rows.data(), n * k * 8, cudaMemcpyDeviceToHost, ctx.stream));
@@ -199,13 +210,14 @@ void evidence_impl(igb::Ctx& ctx, const ig_model& m, const int64_t* d_tests, siz
     // test-row postings are built once and shared by both dictionaries.
     if (igb::postings_supported(L, nt)) {
         igb::Postings PT;
-        igb::build_postings(ctx, d_tests, nt, k, L, PT);
+        igb::build_postings(ctx, d_tests, nt, k, L, PT, true, true);
         DevBuf flag(sizeof(int), ctx.stream);
         IGB_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), ctx.stream));
         for (int c = 0; c < 2; ++c) {
             const ig_candidates& P = m.pure[c];
+            // the fit checked Σ candidate scores <= INT64_MAX (total_score); pure ⊆ candidates
             igb::posting_match(ctx, P.rows.data(), P.rows.n, k, P.score.as<int64_t>(), PT, c == 0 ? d_A : d_N,
-                               flag.as<int>());
+                               flag.as<int>(), true);
         }
         int h = 0;
         IGB_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
@@ -401,7 +413,7 @@ size_t ig_candidates_count(const ig_candidates* c) { return c ? c->rows.n : 0; }
 uint32_t ig_candidates_logical_len(const ig_candidates* c) { return c ? c->rows.L : 0; }
 
 int ig_candidates_copy(ig_ctx* ctx, const ig_candidates* c, int64_t* words, int64_t* sup, int64_t* sc) {
-    return guard(ctx, [&] { copy_out(*ctx, *c, words, sup, sc); });
+    return guard(ctx, [&] { copy_out(*ctx, const_cast<ig_candidates&>(*c), words, sup, sc); });
 }
 
 void ig_candidates_free(ig_candidates* c) { delete c; }
@@ -445,7 +457,8 @@ uint32_t ig_model_logical_len(const ig_model* m) { return m ? m->L : 0; }
 int ig_model_copy(ig_ctx* ctx, const ig_model* m, int cls, int which, int64_t* words, int64_t* sup, int64_t* sc) {
     return guard(ctx, [&] {
         if (cls < 0 || cls > 1) fail(IG_E_INVALID_ARG, "class must be 0 (attack) or 1 (normal)");
-        copy_out(*ctx, which == 0 ? m->cand[cls] : m->pure[cls], words, sup, sc);
+        ig_model* mm = const_cast<ig_model*>(m);  // ordering on demand does not change the content
+        copy_out(*ctx, which == 0 ? mm->cand[cls] : mm->pure[cls], words, sup, sc);
     });
 }
 

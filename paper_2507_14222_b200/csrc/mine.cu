@@ -30,7 +30,7 @@ namespace {
 
 constexpr int kTile = 64;
 constexpr int kPairThreads = 256;
-constexpr uint64_t kRepInit = ~0ull;
+constexpr uint64_t kRepInit = 0ull;  // slot.y = ((u << 32) | v) + 1 once written; all-zero slot = empty
 
 struct Table {
     ulonglong2* slots;
@@ -69,7 +69,7 @@ __device__ __forceinline__ uint64_t ld_volatile(const unsigned long long* p) {
 template <class WordFn>
 __device__ void table_insert(const Table& T, const int64_t* __restrict__ X, int k, uint32_t u, uint32_t v,
                              uint64_t fp, WordFn b) {
-    const uint64_t rep = ((uint64_t)u << 32) | v;
+    const uint64_t rep = (((uint64_t)u << 32) | v) + 1;
     uint64_t s = (fp ^ T.seed) & T.mask;
     for (uint64_t probes = 0; probes <= T.mask; ++probes, s = (s + 1) & T.mask) {
         ulonglong2* slot = T.slots + s;
@@ -77,7 +77,7 @@ __device__ void table_insert(const Table& T, const int64_t* __restrict__ X, int 
         cur.x = ld_volatile(&slot->x);
         cur.y = kRepInit;  // loaded below only when the fingerprint matches
         if (cur.x == 0) {
-            const ulonglong2 old = cas128(slot, make_ulonglong2(0ull, kRepInit), make_ulonglong2(fp, rep));
+            const ulonglong2 old = cas128(slot, make_ulonglong2(0ull, 0ull), make_ulonglong2(fp, rep));
             if (old.x == 0) {
                 const unsigned long long idx = atomicAdd(T.count, 1ull);
                 if (idx < T.limit)
@@ -91,6 +91,7 @@ __device__ void table_insert(const Table& T, const int64_t* __restrict__ X, int 
         if (cur.x != fp) continue;
         uint64_t r = cur.y;
         while (r == kRepInit) r = ld_volatile(&slot->y);  // not loaded yet, or the winner's store is in flight
+        --r;
         const uint32_t ru = (uint32_t)(r >> 32), rv = (uint32_t)r;
         const int64_t* a = X + (size_t)ru * k;
         const int64_t* c = X + (size_t)rv * k;
@@ -258,9 +259,7 @@ struct TableMem {
     DevBuf slots, reps, ovf, ctr;  // ctr: count, ovf_count, collisions, fail
     Table make(Ctx& ctx, uint64_t cap, uint64_t ovf_cap, uint64_t seed) {
         slots.alloc(cap * sizeof(ulonglong2), ctx.stream);
-        // empty slot = {0, kRepInit}: fill x with 0 and y with ~0 via two memsets on a strided view
-        IGB_CUDA(cudaMemset2DAsync(slots.p, 16, 0, 8, cap, ctx.stream));
-        IGB_CUDA(cudaMemset2DAsync(static_cast<char*>(slots.p) + 8, 16, 0xff, 8, cap, ctx.stream));
+        IGB_CUDA(cudaMemsetAsync(slots.p, 0, cap * sizeof(ulonglong2), ctx.stream));  // empty slot = {0, 0}
         const uint64_t limit = cap / 4 * 3;
         reps.alloc(limit * sizeof(uint2), ctx.stream);
         ovf.alloc(ovf_cap * sizeof(uint2), ctx.stream);

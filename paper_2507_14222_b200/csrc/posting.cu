@@ -122,13 +122,17 @@ __global__ void pattern_token_count(const int64_t* __restrict__ pat, size_t np, 
 
 // Token list of each pattern sorted by (df, token) when it has at most
 // kMaxSorted tokens; longer lists keep bit order after moving the rarest first.
-__global__ void pattern_token_fill(const int64_t* __restrict__ pat, size_t np, int k, const uint32_t* __restrict__ df,
-                                   const uint32_t* __restrict__ off, uint16_t* __restrict__ toks) {
+// df is staged in shared memory (L <= 64*K words of 4 bytes).
+__global__ void pattern_token_fill(const int64_t* __restrict__ pat, size_t np, int k, const uint32_t* __restrict__ gdf,
+                                   uint32_t L, const uint32_t* __restrict__ off, uint16_t* __restrict__ toks) {
+    extern __shared__ uint32_t df[];
+    for (uint32_t i = threadIdx.x; i < L; i += blockDim.x) df[i] = gdf[i];
+    __syncthreads();
     for (size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += (size_t)gridDim.x * blockDim.x) {
         const uint32_t o = off[p];
         const uint32_t total = off[p + 1] - o;
         if (total <= kMaxSorted) {
-            uint32_t key[kMaxSorted];
+            uint64_t key[kMaxSorted];  // (df << 16) | token: sorts by (df, token)
             int m = 0;
             for (int w = 0; w < k; ++w) {
                 uint64_t x = (uint64_t)pat[p * k + w];
@@ -136,19 +140,16 @@ __global__ void pattern_token_fill(const int64_t* __restrict__ pat, size_t np, i
                     const int b = __ffsll((long long)x) - 1;
                     x &= x - 1;
                     const uint32_t t = (uint32_t)w * 64 + b;
-                    const uint32_t dt = df[t];
+                    const uint64_t kt = ((uint64_t)df[t] << 16) | t;
                     int i = m++;
-                    while (i > 0) {
-                        const uint32_t u = key[i - 1];
-                        const uint32_t du = df[u];
-                        if (du < dt || (du == dt && u < t)) break;
-                        key[i] = u;
+                    while (i > 0 && key[i - 1] > kt) {
+                        key[i] = key[i - 1];
                         --i;
                     }
-                    key[i] = t;
+                    key[i] = kt;
                 }
             }
-            for (int i = 0; i < m; ++i) toks[o + i] = (uint16_t)key[i];
+            for (int i = 0; i < m; ++i) toks[o + i] = (uint16_t)(key[i] & 0xffffu);
         } else {
             uint32_t n = 0, best = 0, bestdf = 0xffffffffu;
             for (int w = 0; w < k; ++w) {
@@ -171,7 +172,58 @@ __global__ void pattern_token_fill(const int64_t* __restrict__ pat, size_t np, i
     }
 }
 
-enum Mode : int { kMatch = 0, kSupport = 1, kCover = 2 };
+// Rank-space variant: with byrank[] = tokens sorted by (df, token) and rank[]
+// its inverse, re-indexing a pattern's bits by rank and reading them back in
+// bit order lists its tokens rarest first with no per-pattern sort: O(|b| + K).
+constexpr int kRankWords = 64;
+__global__ void pattern_token_fill_rank(const int64_t* __restrict__ pat, size_t np, int k,
+                                        const uint16_t* __restrict__ grank, const uint16_t* __restrict__ gbyrank,
+                                        uint32_t L, const uint32_t* __restrict__ off, uint16_t* __restrict__ toks) {
+    extern __shared__ uint16_t rsm[];
+    uint16_t* rank = rsm;
+    uint16_t* byrank = rsm + L;
+    for (uint32_t i = threadIdx.x; i < L; i += blockDim.x) {
+        rank[i] = grank[i];
+        byrank[i] = gbyrank[i];
+    }
+    __syncthreads();
+    for (size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += (size_t)gridDim.x * blockDim.x) {
+        uint64_t rb[kRankWords];
+        for (int w = 0; w < k; ++w) rb[w] = 0;
+        for (int w = 0; w < k; ++w) {
+            uint64_t x = (uint64_t)pat[p * k + w];
+            while (x) {
+                const int b = __ffsll((long long)x) - 1;
+                x &= x - 1;
+                const uint32_t r = rank[w * 64 + b];
+                rb[r >> 6] |= 1ull << (r & 63);
+            }
+        }
+        uint32_t o = off[p];
+        for (int q = 0; q < k; ++q) {
+            uint64_t y = rb[q];
+            while (y) {
+                const int b = __ffsll((long long)y) - 1;
+                y &= y - 1;
+                toks[o++] = byrank[q * 64 + b];
+            }
+        }
+    }
+}
+
+__global__ void rank_keys(const uint32_t* __restrict__ df, uint32_t L, unsigned long long* __restrict__ key,
+                          uint16_t* __restrict__ tok) {
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < L; t += gridDim.x * blockDim.x) {
+        key[t] = ((unsigned long long)df[t] << 16) | t;
+        tok[t] = (uint16_t)t;
+    }
+}
+
+__global__ void invert_rank(const uint16_t* __restrict__ byrank, uint32_t L, uint16_t* __restrict__ rank) {
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < L; r += gridDim.x * blockDim.x) rank[byrank[r]] = (uint16_t)r;
+}
+
+enum Mode : int { kMatch = 0, kSupport = 1, kCover = 2, kMatchChecked = 3 };
 
 // Warp per pattern over the CSR token lists.
 template <int MODE>
@@ -207,17 +259,29 @@ posting_scan(const unsigned long long* __restrict__ dense, size_t W, const uint3
         const uint32_t beg = nz_off[t1], end = nz_off[t1 + 1];
         const unsigned long long* p1 = dense + (size_t)t1 * W;
         unsigned long long s = 0;
-        if (MODE == kMatch) s = (unsigned long long)scores[p];
+        if (MODE == kMatch || MODE == kMatchChecked) s = (unsigned long long)scores[p];
         uint32_t cnt = 0;
         bool hit = false;
+        const uint32_t Wu = (uint32_t)W;  // L * W < 2^32 (postings_supported)
         for (uint32_t j0 = beg; j0 < end; j0 += 32) {
             const uint32_t j = j0 + lane;
             const uint32_t w = j < end ? nz_idx[j] : 0u;
+            const unsigned long long* col = dense + w;
             unsigned long long mw = j < end ? p1[w] : 0ull;
-            for (uint32_t i = 1; i < m; ++i) {
+            // four tokens per round: independent loads, one warp vote
+            for (uint32_t i = 1; i < m; i += 4) {
                 if (!__any_sync(kFull, mw != 0ull)) break;
-                const uint32_t t = i < 32 ? __shfl_sync(kFull, tl, i) : (uint32_t)toks[o + i];
-                if (mw) mw &= dense[(size_t)t * W + w];
+                uint32_t t[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t ii = min(i + u, m - 1);
+                    t[u] = ii < 32 ? __shfl_sync(kFull, tl, ii) : (uint32_t)toks[o + ii];
+                }
+                if (mw) {
+                    const unsigned long long a = col[t[0] * Wu], b = col[t[1] * Wu];
+                    const unsigned long long c = col[t[2] * Wu], d = col[t[3] * Wu];
+                    mw &= (a & b) & (c & d);
+                }
             }
             if (MODE == kSupport) {
                 cnt += __popcll(mw);
@@ -227,11 +291,16 @@ posting_scan(const unsigned long long* __restrict__ dense, size_t W, const uint3
                     break;
                 }
             } else {
+                unsigned long long* row = acc + (size_t)w * 64;
                 while (mw) {
                     const int b = __ffsll((long long)mw) - 1;
                     mw &= mw - 1;
-                    const unsigned long long old = atomicAdd(acc + (size_t)w * 64 + b, s);
-                    if (old + s > (unsigned long long)INT64_MAX) ovf = true;
+                    if (MODE == kMatchChecked) {
+                        const unsigned long long old = atomicAdd(row + b, s);
+                        if (old + s > (unsigned long long)INT64_MAX) ovf = true;
+                    } else {
+                        atomicAdd(row + b, s);  // RED: Σ scores <= INT64_MAX, no sum can overflow
+                    }
                 }
             }
         }
@@ -242,13 +311,38 @@ posting_scan(const unsigned long long* __restrict__ dense, size_t W, const uint3
             if (lane == 0) cover_out[p] = hit ? 1 : 0;
         }
     }
-    if (MODE == kMatch && ovf) atomicOr(flags, 1);
+    if (MODE == kMatchChecked && ovf) atomicOr(flags, 1);
 }
 
-__global__ void scatter_u64(const unsigned long long* __restrict__ src, const uint32_t* __restrict__ perm, size_t n,
-                            int64_t* __restrict__ dst) {
+// dst[perm[i]] = src[group ? group[i] : i] for every canonical position i.
+__global__ void scatter_u64(const unsigned long long* __restrict__ src, const uint32_t* __restrict__ perm,
+                            const uint32_t* __restrict__ group, size_t n, int64_t* __restrict__ dst) {
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
-        dst[perm[i]] = (int64_t)src[i];
+        dst[perm[i]] = (int64_t)src[group ? group[i] : i];
+}
+
+__global__ void row_heads(const int64_t* __restrict__ rows, const uint32_t* __restrict__ perm, size_t n, int k,
+                          uint32_t* __restrict__ head) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        uint32_t h = 1;
+        if (i > 0) {
+            const int64_t* a = rows + (size_t)perm[i] * k;
+            const int64_t* b = rows + (size_t)perm[i - 1] * k;
+            h = 0;
+            for (int w = 0; w < k; ++w)
+                if (a[w] != b[w]) {
+                    h = 1;
+                    break;
+                }
+        }
+        head[i] = h;
+    }
+}
+
+// exclusive sum of heads -> group index of each position (heads start a new group)
+__global__ void fix_group(const uint32_t* __restrict__ head, size_t n, uint32_t* __restrict__ group) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        group[i] = group[i] + head[i] - 1;
 }
 
 // CSR token lists of `np` patterns ordered by the document frequency of P.
@@ -271,7 +365,30 @@ void pattern_tokens(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const P
     IGB_CUDA(cudaMemcpyAsync(&total, T.off.as<uint32_t>() + np, 4, cudaMemcpyDeviceToHost, ctx.stream));
     IGB_CUDA(cudaStreamSynchronize(ctx.stream));
     T.toks.alloc(std::max<size_t>(total, 1) * 2, ctx.stream);
-    IGB_LAUNCH(ctx, pattern_token_fill, grid_for(ctx, np, 128), 128, 0, d_pat, np, (int)k, P.df.as<uint32_t>(),
+    if (k <= kRankWords) {
+        const uint32_t L = P.L;
+        DevBuf key(L * 8, ctx.stream), key2(L * 8, ctx.stream), tok(L * 2, ctx.stream), byrank(L * 2, ctx.stream),
+            rank(L * 2, ctx.stream);
+        IGB_LAUNCH(ctx, rank_keys, grid_for(ctx, L, 256), 256, 0, P.df.as<uint32_t>(), L, key.as<unsigned long long>(),
+                   tok.as<uint16_t>());
+        size_t tb2 = 0;
+        IGB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb2, key.as<unsigned long long>(), key2.as<unsigned long long>(),
+                                                 tok.as<uint16_t>(), byrank.as<uint16_t>(), (int64_t)L, 0, 64, ctx.stream));
+        DevBuf temp2(tb2, ctx.stream);
+        IGB_CUDA(cub::DeviceRadixSort::SortPairs(temp2.p, tb2, key.as<unsigned long long>(), key2.as<unsigned long long>(),
+                                                 tok.as<uint16_t>(), byrank.as<uint16_t>(), (int64_t)L, 0, 64, ctx.stream));
+        IGB_LAUNCH(ctx, invert_rank, grid_for(ctx, L, 256), 256, 0, byrank.as<uint16_t>(), L, rank.as<uint16_t>());
+        const size_t smem = (size_t)L * 4;
+        if (smem > 48 * 1024)
+            IGB_CUDA(cudaFuncSetAttribute(pattern_token_fill_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        IGB_LAUNCH(ctx, pattern_token_fill_rank, grid_for(ctx, np, 128), 128, smem, d_pat, np, (int)k,
+                   rank.as<uint16_t>(), byrank.as<uint16_t>(), L, T.off.as<uint32_t>(), T.toks.as<uint16_t>());
+        return;
+    }
+    const size_t smem = (size_t)P.L * 4;
+    if (smem > 48 * 1024)
+        IGB_CUDA(cudaFuncSetAttribute(pattern_token_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    IGB_LAUNCH(ctx, pattern_token_fill, grid_for(ctx, np, 128), 128, smem, d_pat, np, (int)k, P.df.as<uint32_t>(), P.L,
                T.off.as<uint32_t>(), T.toks.as<uint16_t>());
 }
 
@@ -292,26 +409,57 @@ void launch_scan(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Post
 bool postings_supported(uint32_t L, size_t n) { return words_for(L) * 64 < 65535 && n < 0xffffffffull; }
 
 void build_postings(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, uint32_t /*logical_len*/, Postings& P,
-                    bool canonical) {
+                    bool canonical, bool distinct) {
     const uint32_t L = (uint32_t)(64 * k);  // every bit position, padding included
     P.L = L;
-    P.n = n;
-    P.W = (n + 63) / 64;
+    P.n_src = n;
+    P.perm.release();
+    P.group.release();
+    P.rep.release();
+    if ((canonical || distinct) && n > 1) {
+        P.perm.alloc(n * 4, ctx.stream);
+        sort_rows_canonical(ctx, d_rows, n, k, P.perm.as<uint32_t>());
+    }
+    size_t nd = n;
+    const uint32_t* rows_of = P.perm.as<uint32_t>();  // posting row -> source row
+    if (distinct && n > 1) {
+        // identical rows are adjacent in canonical order: one posting row per distinct row
+        DevBuf head(n * 4, ctx.stream), nsel(8, ctx.stream);
+        P.group.alloc(n * 4, ctx.stream);
+        P.rep.alloc(n * 4, ctx.stream);
+        IGB_LAUNCH(ctx, row_heads, grid_for(ctx, n, 256), 256, 0, d_rows, P.perm.as<uint32_t>(), n, (int)k,
+                   head.as<uint32_t>());
+        size_t tb = 0;
+        IGB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, head.as<uint32_t>(), P.group.as<uint32_t>(), (int64_t)n,
+                                               ctx.stream));
+        size_t tb2 = 0;
+        IGB_CUDA(cub::DeviceSelect::Flagged(nullptr, tb2, P.perm.as<uint32_t>(), head.as<uint32_t>(),
+                                            P.rep.as<uint32_t>(), nsel.as<int64_t>(), (int64_t)n, ctx.stream));
+        DevBuf temp(std::max(tb, tb2), ctx.stream);
+        // group[i] = (#heads in [0, i]) - 1: exclusive sum of heads shifted by the head at i
+        IGB_CUDA(cub::DeviceScan::ExclusiveSum(temp.p, tb, head.as<uint32_t>(), P.group.as<uint32_t>(), (int64_t)n,
+                                               ctx.stream));
+        IGB_CUDA(cub::DeviceSelect::Flagged(temp.p, tb2, P.perm.as<uint32_t>(), head.as<uint32_t>(),
+                                            P.rep.as<uint32_t>(), nsel.as<int64_t>(), (int64_t)n, ctx.stream));
+        IGB_LAUNCH(ctx, fix_group, grid_for(ctx, n, 256), 256, 0, head.as<uint32_t>(), n, P.group.as<uint32_t>());
+        int64_t m = 0;
+        IGB_CUDA(cudaMemcpyAsync(&m, nsel.p, 8, cudaMemcpyDeviceToHost, ctx.stream));
+        IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+        nd = (size_t)m;
+        rows_of = P.rep.as<uint32_t>();
+    }
+    P.n = nd;
+    P.W = (nd + 63) / 64;
     const size_t W = std::max<size_t>(P.W, 1);
     P.dense.alloc((size_t)L * W * 8, ctx.stream);
     P.df.alloc((size_t)L * 4, ctx.stream);
     P.nz_off.alloc(((size_t)L + 1) * 4, ctx.stream);
-    P.perm.release();
     DevBuf nzc(((size_t)L + 1) * 4, ctx.stream);
     IGB_CUDA(cudaMemsetAsync(P.dense.p, 0, (size_t)L * W * 8, ctx.stream));
-    if (canonical && n > 1) {
-        P.perm.alloc(n * 4, ctx.stream);
-        sort_rows_canonical(ctx, d_rows, n, k, P.perm.as<uint32_t>());
-    }
-    if (n && k) {
+    if (nd && k) {
         const size_t warps = P.W * k;
-        IGB_LAUNCH(ctx, transpose_rows, grid_for(ctx, warps * 32, 256), 256, 0, d_rows, P.perm.as<uint32_t>(), n,
-                   (int)k, P.W, P.dense.as<unsigned long long>());
+        IGB_LAUNCH(ctx, transpose_rows, grid_for(ctx, warps * 32, 256), 256, 0, d_rows, rows_of, nd, (int)k, P.W,
+                   P.dense.as<unsigned long long>());
     }
     IGB_LAUNCH(ctx, token_stats, grid_for(ctx, (size_t)L * 32, 256), 256, 0, P.dense.as<unsigned long long>(), L,
                P.W, nzc.as<uint32_t>(), P.df.as<uint32_t>());
@@ -340,20 +488,28 @@ void posting_cover(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Po
 }
 
 void posting_match(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const int64_t* d_scores, const Postings& P,
-                   int64_t* d_out, int* d_overflow) {
+                   int64_t* d_out, int* d_overflow, bool sum_fits) {
     const size_t n = std::max<size_t>(P.n, 1);
+    if (P.group.p == nullptr && P.perm.p == nullptr && P.n_src != P.n) fail(IG_E_CUDA, "posting_match: bad postings");
+    // sum_fits: Σ scores <= INT64_MAX, so no evidence sum can overflow and the
+    // accumulation needs no returned value (fire-and-forget RED).
+    auto run = [&](unsigned long long* acc) {
+        if (sum_fits)
+            launch_scan<kMatch>(ctx, d_pat, np, k, P, d_scores, acc, nullptr, nullptr, d_overflow);
+        else
+            launch_scan<kMatchChecked>(ctx, d_pat, np, k, P, d_scores, acc, nullptr, nullptr, d_overflow);
+    };
     if (!P.perm.p) {
         IGB_CUDA(cudaMemsetAsync(d_out, 0, n * 8, ctx.stream));
-        launch_scan<kMatch>(ctx, d_pat, np, k, P, d_scores, reinterpret_cast<unsigned long long*>(d_out), nullptr,
-                            nullptr, d_overflow);
+        run(reinterpret_cast<unsigned long long*>(d_out));
         return;
     }
     // accumulate in the postings' (canonical) row order, then scatter back
     DevBuf acc(n * 8, ctx.stream);
     IGB_CUDA(cudaMemsetAsync(acc.p, 0, n * 8, ctx.stream));
-    launch_scan<kMatch>(ctx, d_pat, np, k, P, d_scores, acc.as<unsigned long long>(), nullptr, nullptr, d_overflow);
-    IGB_LAUNCH(ctx, scatter_u64, grid_for(ctx, P.n, 256), 256, 0, acc.as<unsigned long long>(), P.perm.as<uint32_t>(),
-               P.n, d_out);
+    run(acc.as<unsigned long long>());
+    IGB_LAUNCH(ctx, scatter_u64, grid_for(ctx, P.n_src, 256), 256, 0, acc.as<unsigned long long>(),
+               P.perm.as<uint32_t>(), P.group.as<uint32_t>(), P.n_src, d_out);
 }
 
 }  // namespace igb

@@ -247,7 +247,7 @@ void coverage_any_dev(Ctx& ctx, const int64_t* d_pat, size_t np, const int64_t* 
     if (np == 0 || no == 0) return;
     if (postings_supported((uint32_t)(64 * k), no)) {
         Postings P;
-        build_postings(ctx, d_opp, no, k, (uint32_t)(64 * k), P);
+        build_postings(ctx, d_opp, no, k, (uint32_t)(64 * k), P, true, true);
         posting_cover(ctx, d_pat, np, k, P, d_mask);
         return;
     }
@@ -301,8 +301,10 @@ int fused_score_dev(Ctx& ctx, const int64_t* d_pat, size_t np, const int64_t* d_
                                   d_flags);
     } else if (postings_supported((uint32_t)(64 * k), nt)) {
         Postings P;
-        build_postings(ctx, d_tests, nt, k, (uint32_t)(64 * k), P);
-        posting_match(ctx, d_pat, np, k, d_scores, P, d_out, d_flags);
+        build_postings(ctx, d_tests, nt, k, (uint32_t)(64 * k), P, true, true);
+        int64_t total = 0;
+        const bool fits = total_score_dev(ctx, d_scores, np, &total) == IG_OK;  // scores >= 0 here
+        posting_match(ctx, d_pat, np, k, d_scores, P, d_out, d_flags, fits);
     } else {
         size_t slice_rows;
         const int slices = choose_slices(ctx, nt, np, &slice_rows);
