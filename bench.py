@@ -24,12 +24,12 @@ CSV parsing and schema statistics (host) are reported separately (`host_prep_s`)
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
 import subprocess
 import sys
-import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -54,43 +54,46 @@ def parse_args():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line).
+
+    One `nvidia-smi -lms 200` child is started before the timed region and
+    stopped after it, so no fork happens while steps are being issued."""
 
     def __init__(self):
-        self.samples = []
-        self._stop = threading.Event()
-        self._t = None
+        self.proc = None
+        self.lines = []
 
     def start(self):
-        def run():
-            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_power_cap")
-            while not self._stop.is_set():
-                try:
-                    out = subprocess.run(["nvidia-smi", "-i", os.environ.get("LOCAL_RANK", "0"),
-                                          f"--query-gpu={q}", "--format=csv,noheader,nounits"],
-                                         capture_output=True, text=True, timeout=5).stdout.strip()
-                    if out:
-                        self.samples.append([x.strip() for x in out.split(",")])
-                except Exception:
-                    pass
-                self._stop.wait(0.2)
-        self._t = threading.Thread(target=run, daemon=True)
-        self._t.start()
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", os.environ.get("LOCAL_RANK", "0"), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.3)  # first sample lands before the timed region
+        except OSError:
+            self.proc = None
 
     def stop(self):
-        self._stop.set()
-        if self._t:
-            self._t.join(timeout=6)
-        if not self.samples:
+        if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        samples = [[x.strip() for x in ln.split(",")] for ln in out.splitlines() if ln.count(",") >= 5]
+        if not samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(s[0]) for s in samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in samples if s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].strip() == "Active"})
+        reasons = sorted({names[i] for s in samples for i in range(4) if s[2 + i].strip() == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(samples)}
 
 
 def workload_config(args, n_train, n_test, extra=None):
@@ -235,12 +238,15 @@ def run_b200(args):
     launches0 = ctx.launches
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     barrier()
+    gc.disable()
     for i in range(args.steps):
+        enc = model = tenc = None  # release the previous step's results outside the timed window
         ev[i][0].record(stream)
         enc, model, tenc = step_resident()
         ev[i][1].record(stream)
     barrier()
     clk = clocks.stop()
+    gc.enable()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     launches = (ctx.launches - launches0) / args.steps
     ms = statistics.median(step_ms)
@@ -255,7 +261,10 @@ def run_b200(args):
         step_e2e()
     barrier()
     e2e_ms = []
+    model_e = A = N = None
+    gc.disable()
     for _ in range(args.steps):
+        model_e = A = N = None
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         w0 = time.perf_counter()
         a.record(stream)
@@ -263,6 +272,7 @@ def run_b200(args):
         b.record(stream)
         torch.cuda.synchronize()
         e2e_ms.append(max(a.elapsed_time(b), (time.perf_counter() - w0) * 1e3))
+    gc.enable()
     e2e = statistics.median(e2e_ms)
     if dist is not None:
         t = torch.tensor([e2e], device="cuda")
@@ -271,28 +281,31 @@ def run_b200(args):
     h2d = cols_tr.nbytes + cols_te.nbytes
     d2h = 2 * n_test * 8
 
-    # ---- roofline of the dominant kernel: the matcher (kernel 6)
+    # ---- roofline of the dominant kernel: the matcher (kernel 6, posting_scan<kMatch>)
     P = [model.count(0, 1), model.count(1, 1)]
     K = (tenc.logical_len + 63) // 64
-    words = (P[0] + P[1]) * n_test * K
-    mt = []
-    for _ in range(3):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
+    ctx.set_diagnostics(True)
+    reps = 3
+    for _ in range(reps):
         model.evidence_device(tenc.device_rows(2), n_test, dA.data_ptr(), dN.data_ptr())
-        b.record(stream)
-        torch.cuda.synchronize()
-        mt.append(a.elapsed_time(b))
-    match_ms = min(mt)
+    kms, words, nl = ctx.diag_match()
+    ctx.set_diagnostics(False)
     lop3_s, popc_s = ctx.int_peaks()
-    peak_words = lop3_s / 2 / 1e9   # one 64-bit word test = 2 LOP3.32 (acc | p & ~x per half)
-    achieved = words / (match_ms * 1e-3) / 1e9
-    roofline = {"bound": "int", "kernel": "subset_scan<kMatch> (evidence, kernel 6)", "achieved": achieved,
+    peak_words = lop3_s / 2 / 1e9   # a 64-bit word AND = 2 LOP3.32
+    achieved = words / (kms * 1e-3) / 1e9
+    horiz = (P[0] + P[1]) * n_test * K * reps
+    roofline = {"bound": "int", "kernel": "posting_scan<kMatch> (matcher, kernel 6)", "achieved": achieved,
                 "peak": peak_words, "unit": "Gword/s", "frac": achieved / peak_words, "traffic": None,
-                "algorithmic_work": f"(|P+|+|P-|) x n_test x K = ({P[0]}+{P[1]}) x {n_test} x {K} 64-bit word-tests",
-                "peak_source": f"measured lop3 micro-kernel {lop3_s / 1e12:.2f} T LOP3.32/s (diag.cu), "
-                               "2 LOP3 per 64-bit word", "kernel_ms": match_ms,
-                "share_of_step": match_ms / ms}
+                "algorithmic_work": (f"posting-list intersection: sum over pure patterns of |b| x nnz-words(rarest "
+                                     f"token) = {words // reps} 64-bit word-ANDs per evidence call "
+                                     f"({nl // reps} launches)"),
+                "horizontal_equivalent": {"word_tests": horiz // reps,
+                                          "effective_Gword_s": horiz / (kms * 1e-3) / 1e9,
+                                          "note": "dense (b&x)==b work the posting form avoids"},
+                "peak_source": f"measured lop3 micro-kernel {lop3_s / 1e12:.2f} T LOP3.32/s (diag.cu)",
+                "kernel_ms_per_launch": kms / max(nl, 1), "launches_per_step": nl // reps,
+                "share_of_step": kms / reps / ms,
+                "ncu": "profiles/ (issue-slot utilisation of the same kernel)"}
 
     line = {"metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",

@@ -54,6 +54,11 @@ int ig_ctx_set_stream(ig_ctx* ctx, void* stream);
 /* Number of kernels this context has launched so far (bench `gpu_launches`). */
 uint64_t ig_ctx_launch_count(const ig_ctx* ctx);
 const char* ig_version(void);
+/* Diagnostics for the bench roofline (off by default; adds syncs when on):
+ * matcher kernel time (CUDA events) and its posting word-ANDs
+ * Σ_p |b_p| * nnz_words(rarest token of p), accumulated since the last reset. */
+int ig_ctx_set_diagnostics(ig_ctx* ctx, int on);
+int ig_ctx_diag_match(ig_ctx* ctx, double* kernel_ms, uint64_t* word_ands, uint64_t* launches);
 /* Integer-pipe micro-benchmark: sustained LOP3.32/s and POPC.32/s of the whole
  * device (roofline denominator of the AND/POPC kernels). */
 int ig_measure_int_peaks(ig_ctx* ctx, double* lop3_per_s, double* popc_per_s);
@@ -104,6 +109,9 @@ int ig_enumerate_candidates(ig_ctx* ctx, const int64_t* rows, size_t n_rows, uin
 /* support[p] = #{i : pattern p subset of rows[i]} (mine.hpp:42-44). */
 int ig_count_support(ig_ctx* ctx, ig_candidates* cands, const int64_t* rows, size_t n_rows,
                      uint32_t logical_len, const ig_kernel_config* cfg);
+/* Same on plain host arrays (patterns not produced by ig_enumerate_candidates). */
+int ig_count_support_rows(ig_ctx* ctx, const int64_t* patterns, size_t n_patterns, uint32_t patterns_len,
+                          const int64_t* rows, size_t n_rows, uint32_t rows_len, int64_t* support);
 /* score = support * size^2, checked (mine.hpp:46-48). */
 int ig_score_patterns(ig_ctx* ctx, ig_candidates* cands);
 /* checked sum (mine.hpp:50-51). Host-only arithmetic. */

@@ -15,6 +15,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 REF_SO = os.path.join(HERE, "_ref", "libigref.so")
+REF_B200_SO = os.path.join(HERE, "_ref", "libigref_b200.so")  # + integration/ shim on libig_b200.so
 
 STATUS = {1: ValueError, 2: IndexError, 3: "ConfigError", 4: OSError, 5: "DataError",
           6: "ArithmeticError", 7: RuntimeError}
@@ -27,19 +28,20 @@ class RefError(RuntimeError):
         self.msg = msg
 
 
-_lib = None
+_libs = {}
 
 
-def available() -> bool:
-    return os.path.exists(REF_SO)
+def available(b200: bool = False) -> bool:
+    return os.path.exists(REF_B200_SO if b200 else REF_SO)
 
 
-def lib():
-    global _lib
-    if _lib is None:
-        if not available():
-            raise FileNotFoundError(f"{REF_SO} not built (make -C oracle ref)")
-        L = C.CDLL(REF_SO)
+def lib(b200: bool = False):
+    key = bool(b200)
+    if key not in _libs:
+        path = REF_B200_SO if b200 else REF_SO
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"{path} not built (make -C oracle ref / refb200)")
+        L = C.CDLL(path)
         p64 = C.POINTER(C.c_int64)
         sz = C.c_size_t
         L.igref_last_error.restype = C.c_char_p
@@ -89,13 +91,13 @@ def lib():
         L.igref_run_cols.restype = sz
         L.igref_run_schema.argtypes = [C.c_void_p, C.POINTER(C.c_uint8), C.POINTER(C.c_double),
                                        C.POINTER(C.c_double), C.POINTER(C.c_size_t)]
-        _lib = L
-    return _lib
+        _libs[key] = L
+    return _libs[key]
 
 
-def _check(status: int):
+def _check(status: int, b200: bool = False):
     if status:
-        raise RefError(status, lib().igref_last_error().decode())
+        raise RefError(status, lib(b200).igref_last_error().decode())
 
 
 def _p64(a: np.ndarray):
@@ -117,8 +119,9 @@ def pair_intersect_batch(rows: np.ndarray, L: int, left: int, jb: int, je: int,
     rows = _words(rows)
     k = (L + 63) // 64
     out = np.zeros((max(je - jb, 0), k), np.int64)
-    _check(lib().igref_pair_intersect_batch(backend.encode(), threads, _p64(rows), rows.shape[0], L,
-                                            left, jb, je, _p64(out)))
+    b = backend == "b200"
+    _check(lib(b).igref_pair_intersect_batch(backend.encode(), threads, _p64(rows), rows.shape[0], L,
+                                             left, jb, je, _p64(out)), b)
     return out
 
 
@@ -126,8 +129,9 @@ def coverage_any(pat: np.ndarray, Lp: int, opp: np.ndarray, Lo: int, block: int 
                  backend: str = "parallel-cpu", threads: int = 0) -> np.ndarray:
     pat, opp = _words(pat), _words(opp)
     mask = np.zeros(pat.shape[0], np.uint8)
-    _check(lib().igref_coverage_any(backend.encode(), threads, _p64(pat), pat.shape[0], Lp, _p64(opp),
-                                    opp.shape[0], Lo, block, mask.ctypes.data_as(C.POINTER(C.c_uint8))))
+    b = backend == "b200"
+    _check(lib(b).igref_coverage_any(backend.encode(), threads, _p64(pat), pat.shape[0], Lp, _p64(opp),
+                                     opp.shape[0], Lo, block, mask.ctypes.data_as(C.POINTER(C.c_uint8))), b)
     return mask
 
 
@@ -136,8 +140,9 @@ def fused_score(pat: np.ndarray, Lp: int, scores: np.ndarray, tests: np.ndarray,
     pat, tests = _words(pat), _words(tests)
     scores = np.ascontiguousarray(scores, np.int64)
     out = np.zeros(tests.shape[0], np.int64)
-    _check(lib().igref_fused_score(backend.encode(), threads, _p64(pat), pat.shape[0], Lp, _p64(scores),
-                                   scores.shape[0], _p64(tests), tests.shape[0], Lt, _p64(out)))
+    b = backend == "b200"
+    _check(lib(b).igref_fused_score(backend.encode(), threads, _p64(pat), pat.shape[0], Lp, _p64(scores),
+                                    scores.shape[0], _p64(tests), tests.shape[0], Lt, _p64(out)), b)
     return out
 
 
@@ -152,23 +157,24 @@ def mine(rows: np.ndarray, L: int, pair_batch: int = 8192, backend: str = "refer
          threads: int = 0, support: bool = True) -> Candidates:
     """enumerate_candidates → count_support → score_patterns (mine.hpp:38-48)."""
     rows = _words(rows)
+    b200 = backend == "b200"
     h = C.c_void_p()
-    _check(lib().igref_enumerate(backend.encode(), threads, pair_batch, _p64(rows), rows.shape[0], L,
-                                 C.byref(h)))
+    _check(lib(b200).igref_enumerate(backend.encode(), threads, pair_batch, _p64(rows), rows.shape[0], L,
+                                 C.byref(h)), b200)
     try:
-        n = lib().igref_cand_count(h)
+        n = lib(b200).igref_cand_count(h)
         k = (L + 63) // 64
-        words = np.ctypeslib.as_array(lib().igref_cand_words(h), (n * k,)).reshape(n, k).copy() if n else \
+        words = np.ctypeslib.as_array(lib(b200).igref_cand_words(h), (n * k,)).reshape(n, k).copy() if n else \
             np.zeros((0, k), np.int64)
         if not support:
             return Candidates(words)
-        _check(lib().igref_count_support(h, threads, _p64(rows), rows.shape[0], L))
-        _check(lib().igref_score_patterns(h))
-        sup = np.ctypeslib.as_array(lib().igref_cand_supports(h), (n,)).copy() if n else np.zeros(0, np.int64)
-        sc = np.ctypeslib.as_array(lib().igref_cand_scores(h), (n,)).copy() if n else np.zeros(0, np.int64)
+        _check(lib(b200).igref_count_support(h, threads, _p64(rows), rows.shape[0], L), b200)
+        _check(lib(b200).igref_score_patterns(h), b200)
+        sup = np.ctypeslib.as_array(lib(b200).igref_cand_supports(h), (n,)).copy() if n else np.zeros(0, np.int64)
+        sc = np.ctypeslib.as_array(lib(b200).igref_cand_scores(h), (n,)).copy() if n else np.zeros(0, np.int64)
         return Candidates(words, sup, sc)
     finally:
-        lib().igref_cand_free(h)
+        lib(b200).igref_cand_free(h)
 
 
 def total_score(scores: np.ndarray) -> int:
@@ -208,12 +214,13 @@ def run(csv: bytes, label_col: str = "label", attack_values: str = "", normal_va
         threads: int = 0, pair_batch: int = 8192, coverage_block: int = 4096,
         test_limit: int | None = None, stages: int = 2, r: float = 0.568) -> RefRun:
     """Full reference pipeline: parse → schema → encode → mine → purify → evidence."""
-    L_ = lib()
+    b200 = backend == "b200"
+    L_ = lib(b200)
     h = C.c_void_p()
     tl = (1 << 63) if test_limit is None else test_limit
     _check(L_.igref_run_create(csv, len(csv), label_col.encode(), attack_values.encode(),
                                normal_values.encode(), decimals, ratio_k, train_rows, backend.encode(),
-                               threads, pair_batch, coverage_block, tl, stages, r, C.byref(h)))
+                               threads, pair_batch, coverage_block, tl, stages, r, C.byref(h)), b200)
     try:
         L = L_.igref_run_L(h)
         k = (L + 63) // 64

@@ -41,6 +41,10 @@
 #include "ig/pipeline.hpp"
 #include "ig/version.hpp"
 
+#ifdef IG_WITH_B200
+#include "ig_b200_backend.hpp"  // integration/: the reference-side binding of libig_b200.so
+#endif
+
 namespace ig {
 
 // ---------------------------------------------------------------------------
@@ -265,6 +269,15 @@ namespace {
 
 thread_local std::string g_err;
 
+// make_backend (kernels.cpp:188-194) plus the "b200" registration a maintainer
+// adds when this shim is linked against libig_b200.so.
+std::unique_ptr<ig::KernelBackend> backend_for(const char* name, int threads) {
+#ifdef IG_WITH_B200
+    if (std::string(name) == "b200") return ig::make_b200_backend(0);
+#endif
+    return ig::make_backend(name, threads);
+}
+
 enum Status : int {
     OK = 0,
     E_INVALID = 1,
@@ -375,7 +388,7 @@ int igref_pair_intersect_batch(const char* backend, int threads, const std::int6
                                std::size_t n, std::uint32_t L, std::size_t left, std::size_t jb,
                                std::size_t je, std::int64_t* out) {
     return guard([&] {
-        auto be = ig::make_backend(backend, threads);
+        auto be = backend_for(backend, threads);
         be->pair_intersect_batch(to_matrix(rows, n, L), left, jb, je, out);
     });
 }
@@ -384,7 +397,7 @@ int igref_coverage_any(const char* backend, int threads, const std::int64_t* pat
                        std::uint32_t Lp, const std::int64_t* opp, std::size_t no, std::uint32_t Lo,
                        std::size_t block, std::uint8_t* mask) {
     return guard([&] {
-        auto be = ig::make_backend(backend, threads);
+        auto be = backend_for(backend, threads);
         auto m = be->coverage_any(to_matrix(pat, np, Lp), to_matrix(opp, no, Lo), block);
         std::memcpy(mask, m.data(), m.size());
     });
@@ -395,7 +408,7 @@ int igref_fused_score(const char* backend, int threads, const std::int64_t* pat,
                       const std::int64_t* tests, std::size_t nt, std::uint32_t Lt,
                       std::int64_t* out) {
     return guard([&] {
-        auto be = ig::make_backend(backend, threads);
+        auto be = backend_for(backend, threads);
         auto v = be->fused_score(to_matrix(pat, np, Lp), std::span<const std::int64_t>(scores, ns),
                                  to_matrix(tests, nt, Lt));
         std::memcpy(out, v.data(), v.size() * sizeof(std::int64_t));
@@ -406,7 +419,7 @@ int igref_fused_score(const char* backend, int threads, const std::int64_t* pat,
 int igref_enumerate(const char* backend, int threads, std::size_t pair_batch,
                     const std::int64_t* rows, std::size_t n, std::uint32_t L, void** out) {
     return guard([&] {
-        auto be = ig::make_backend(backend, threads);
+        auto be = backend_for(backend, threads);
         ig::KernelConfig cfg;
         cfg.pair_batch = pair_batch;
         cfg.threads = threads;
@@ -476,7 +489,7 @@ int igref_run_create(const char* csv, std::size_t len, const char* label_col,
             return;
         }
 
-        auto be = ig::make_backend(backend, threads);
+        auto be = backend_for(backend, threads);
         ig::KernelConfig cfg;
         cfg.pair_batch = pair_batch;
         cfg.coverage_block = coverage_block;

@@ -47,6 +47,8 @@ SIGNATURES = [
     ("ig_ctx_set_stream", C.c_int, [vp, vp]),
     ("ig_ctx_launch_count", C.c_uint64, [vp]),
     ("ig_version", C.c_char_p, []),
+    ("ig_ctx_set_diagnostics", C.c_int, [vp, C.c_int]),
+    ("ig_ctx_diag_match", C.c_int, [vp, C.POINTER(C.c_double), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     ("ig_measure_int_peaks", C.c_int, [vp, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     ("ig_kernel_config_default", None, [C.POINTER(KernelConfigC)]),
     ("ig_pair_intersect_batch", C.c_int, [vp, p64, sz, u32, sz, sz, sz, p64]),
@@ -54,6 +56,7 @@ SIGNATURES = [
     ("ig_fused_score", C.c_int, [vp, p64, sz, u32, p64, sz, p64, sz, u32, p64]),
     ("ig_enumerate_candidates", C.c_int, [vp, p64, sz, u32, C.POINTER(KernelConfigC), PROGRESS, vp, C.POINTER(vp)]),
     ("ig_count_support", C.c_int, [vp, vp, p64, sz, u32, C.POINTER(KernelConfigC)]),
+    ("ig_count_support_rows", C.c_int, [vp, p64, sz, u32, p64, sz, u32, p64]),
     ("ig_score_patterns", C.c_int, [vp, vp]),
     ("ig_total_score", C.c_int, [p64, sz, p64]),
     ("ig_candidates_count", sz, [vp]),

@@ -111,6 +111,15 @@ class Context:
     def launches(self) -> int:
         return int(lib.ig_ctx_launch_count(self.handle))
 
+    def set_diagnostics(self, on: bool) -> None:
+        self.check(lib.ig_ctx_set_diagnostics(self.handle, 1 if on else 0))
+
+    def diag_match(self) -> tuple[float, int, int]:
+        """(matcher kernel ms, posting word-ANDs, launches) since set_diagnostics(True)."""
+        ms, w, n = C.c_double(), C.c_uint64(), C.c_uint64()
+        self.check(lib.ig_ctx_diag_match(self.handle, C.byref(ms), C.byref(w), C.byref(n)))
+        return ms.value, int(w.value), int(n.value)
+
     def int_peaks(self) -> tuple[float, float]:
         """Measured (LOP3.32/s, POPC.32/s) of this device (diag.cu)."""
         a, b = C.c_double(), C.c_double()

@@ -289,6 +289,23 @@ int ig_ctx_set_stream(ig_ctx* ctx, void* stream) {
 
 uint64_t ig_ctx_launch_count(const ig_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+int ig_ctx_set_diagnostics(ig_ctx* ctx, int on) {
+    return guard(ctx, [&] {
+        ctx->diag = on != 0;
+        ctx->diag_match_ms = 0;
+        ctx->diag_match_words = 0;
+        ctx->diag_match_launches = 0;
+    });
+}
+
+int ig_ctx_diag_match(ig_ctx* ctx, double* kernel_ms, uint64_t* word_ands, uint64_t* launches) {
+    return guard(ctx, [&] {
+        *kernel_ms = ctx->diag_match_ms;
+        *word_ands = ctx->diag_match_words;
+        *launches = ctx->diag_match_launches;
+    });
+}
+
 int ig_measure_int_peaks(ig_ctx* ctx, double* lop3_per_s, double* popc_per_s) {
     return guard(ctx, [&] { igb::measure_int_peaks(*ctx, lop3_per_s, popc_per_s); });
 }
@@ -384,6 +401,21 @@ int ig_count_support(ig_ctx* ctx, ig_candidates* c, const int64_t* rows, size_t 
         IGB_CUDA(cudaStreamSynchronize(ctx->stream));
         c->support.persist();
         c->has_support = true;
+    });
+}
+
+int ig_count_support_rows(ig_ctx* ctx, const int64_t* pat, size_t np, uint32_t Lp, const int64_t* rows, size_t n,
+                          uint32_t Lr, int64_t* support) {
+    return guard(ctx, [&] {
+        if (Lp != Lr) fail(IG_E_INVALID_ARG, "count_support: logical length mismatch");
+        if (np == 0) return;
+        DevRows P, X;
+        upload_rows(*ctx, pat, np, Lp, P);
+        upload_rows(*ctx, rows, n, Lr, X);
+        DevBuf s(np * 8, ctx->stream);
+        igb::count_support_dev(*ctx, P.data(), np, X.data(), n, P.k, s.as<int64_t>());
+        IGB_CUDA(cudaMemcpyAsync(support, s.p, np * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        IGB_CUDA(cudaStreamSynchronize(ctx->stream));
     });
 }
 

@@ -90,6 +90,11 @@ struct Ctx {
     uint64_t launches = 0;
     int sm_count = 148;
     size_t smem_optin = 0;
+    // diagnostics (bench roofline only; off on the timed path)
+    bool diag = false;
+    double diag_match_ms = 0;      // CUDA-event time of the matcher kernels
+    uint64_t diag_match_words = 0; // posting word-ANDs of the matcher (Σ_p |b_p| * nnz(rarest token))
+    uint64_t diag_match_launches = 0;
 };
 
 inline size_t words_for(uint32_t L) { return (static_cast<size_t>(L) + 63) / 64; }

@@ -392,6 +392,22 @@ void pattern_tokens(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const P
                T.off.as<uint32_t>(), T.toks.as<uint16_t>());
 }
 
+// Σ_p m_p * nnz(first token of p): the posting-intersection word-ANDs of a
+// launch without early exit (roofline numerator; diagnostics only).
+__global__ void vertical_work(const uint32_t* __restrict__ tok_off, const uint16_t* __restrict__ toks,
+                              const uint32_t* __restrict__ nz_off, size_t np, unsigned long long* __restrict__ out) {
+    unsigned long long acc = 0;
+    for (size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += (size_t)gridDim.x * blockDim.x) {
+        const uint32_t o = tok_off[p], m = tok_off[p + 1] - o;
+        if (m) {
+            const uint32_t t = toks[o];
+            acc += (unsigned long long)m * (nz_off[t + 1] - nz_off[t]);
+        }
+    }
+    for (int s = 16; s; s >>= 1) acc += __shfl_xor_sync(kFull, acc, s);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
+}
+
 template <int MODE>
 void launch_scan(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Postings& P, const int64_t* scores,
                  unsigned long long* acc, int64_t* support, uint8_t* cover, int* flags) {
@@ -399,9 +415,33 @@ void launch_scan(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Post
     PatternTokens T;
     pattern_tokens(ctx, d_pat, np, k, P, T);
     const size_t blocks = std::min<size_t>((np + 7) / 8, (size_t)ctx.sm_count * 64);
+    const bool diag = ctx.diag && (MODE == kMatch || MODE == kMatchChecked);
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (diag) {
+        IGB_CUDA(cudaEventCreate(&e0));
+        IGB_CUDA(cudaEventCreate(&e1));
+        IGB_CUDA(cudaEventRecord(e0, ctx.stream));
+    }
     IGB_LAUNCH(ctx, posting_scan<MODE>, (unsigned)blocks, 256, 0, P.dense.as<unsigned long long>(), P.W,
                P.nz_off.as<uint32_t>(), P.nz_idx.as<uint32_t>(), P.n, T.off.as<uint32_t>(), T.toks.as<uint16_t>(), np,
                scores, acc, support, cover, flags);
+    if (diag) {
+        IGB_CUDA(cudaEventRecord(e1, ctx.stream));
+        DevBuf w(8, ctx.stream);
+        IGB_CUDA(cudaMemsetAsync(w.p, 0, 8, ctx.stream));
+        IGB_LAUNCH(ctx, vertical_work, grid_for(ctx, np, 256), 256, 0, T.off.as<uint32_t>(), T.toks.as<uint16_t>(),
+                   P.nz_off.as<uint32_t>(), np, w.as<unsigned long long>());
+        unsigned long long hw = 0;
+        IGB_CUDA(cudaMemcpyAsync(&hw, w.p, 8, cudaMemcpyDeviceToHost, ctx.stream));
+        IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+        float ms = 0;
+        IGB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        ctx.diag_match_ms += ms;
+        ctx.diag_match_words += hw;
+        ctx.diag_match_launches += 1;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+    }
 }
 
 }  // namespace
