@@ -120,12 +120,19 @@ __device__ __forceinline__ void tile_of(uint64_t t, uint32_t& bi, uint32_t& bj) 
 }
 
 // One CTA per 64x64 tile of the triangle u <= v (grid-stride over tiles).
+// Pairs are first deduplicated inside the tile (shared-memory hash of
+// fingerprint tags, exact compare on the tile's staged rows), so only the first
+// pair of each distinct content in a tile probes the device-wide table.
+constexpr int kLocalSlots = 4096;
+constexpr int kLocalProbes = 64;
+
 __global__ void __launch_bounds__(kPairThreads)
 pair_enum(const int64_t* __restrict__ X, uint32_t n, int k, int stride, uint64_t n_tiles, Table T,
           uint64_t tile_begin) {
     extern __shared__ int64_t sm[];
-    int64_t* sI = sm;
-    int64_t* sJ = sm + (size_t)kTile * stride;
+    unsigned long long* local = reinterpret_cast<unsigned long long*>(sm);  // kLocalSlots
+    int64_t* sI = sm + kLocalSlots;
+    int64_t* sJ = sI + (size_t)kTile * stride;
     for (uint64_t t = tile_begin + blockIdx.x; t < n_tiles; t += gridDim.x) {
         if (*(volatile int*)T.fail) return;
         uint32_t bi, bj;
@@ -137,6 +144,7 @@ pair_enum(const int64_t* __restrict__ X, uint32_t n, int k, int stride, uint64_t
             sI[r * stride + w] = (i0 + r < n) ? X[(size_t)(i0 + r) * k + w] : 0;
             sJ[r * stride + w] = (j0 + r < n) ? X[(size_t)(j0 + r) * k + w] : 0;
         }
+        for (int q = threadIdx.x; q < kLocalSlots; q += kPairThreads) local[q] = 0ull;
         __syncthreads();
         for (int q = threadIdx.x; q < kTile * kTile; q += kPairThreads) {
             const int r = q / kTile, c = q % kTile;
@@ -152,7 +160,30 @@ pair_enum(const int64_t* __restrict__ X, uint32_t n, int k, int stride, uint64_t
                 fp.add(x);
             }
             if (!nz) continue;  // SPEC.md:338 empty intersections dropped at the source
-            table_insert(T, X, k, u, v, fp.final(k), [&](int w) { return a[w] & b[w]; });
+            const uint64_t f = fp.final(k);
+            // local entry: 51-bit tag (never zero) | 12-bit pair index within the tile
+            const unsigned long long entry = ((((f >> 13) | (1ull << 50))) << 12) | (unsigned)q;
+            bool dup = false;
+            uint32_t s = (uint32_t)(f & (kLocalSlots - 1));
+            for (int probe = 0; probe < kLocalProbes; ++probe, s = (s + 1) & (kLocalSlots - 1)) {
+                unsigned long long cur = local[s];
+                if (cur == 0ull) {
+                    cur = atomicCAS(local + s, 0ull, entry);
+                    if (cur == 0ull) break;  // first of its content in this tile
+                }
+                if ((cur >> 12) != (entry >> 12)) continue;
+                const int q2 = (int)(cur & 0xfffu);
+                const int64_t* a2 = sI + (q2 / kTile) * stride;
+                const int64_t* b2 = sJ + (q2 % kTile) * stride;
+                bool same = true;
+                for (int w = 0; w < k && same; ++w) same = ((a2[w] & b2[w]) == (a[w] & b[w]));
+                if (same) {
+                    dup = true;
+                    break;
+                }
+            }
+            if (dup) continue;
+            table_insert(T, X, k, u, v, f, [&](int w) { return a[w] & b[w]; });
         }
     }
 }
@@ -299,7 +330,7 @@ void pair_window_dev(Ctx& ctx, const int64_t* d_left, const int64_t* d_rows, siz
     IGB_LAUNCH(ctx, pair_window_k, grid_for(ctx, cnt * k, 256), 256, 0, d_left, d_rows, cnt, (int)k, d_out);
 }
 
-void sort_rows_canonical(Ctx& ctx, const int64_t* d_words, size_t n, size_t k, uint32_t* d_perm) {
+void sort_rows_canonical_lsd(Ctx& ctx, const int64_t* d_words, size_t n, size_t k, uint32_t* d_perm) {
     if (n == 0) return;
     IGB_LAUNCH(ctx, iota_u32, grid_for(ctx, n, 256), 256, 0, d_perm, n);
     if (n == 1) return;
@@ -342,8 +373,27 @@ void canonical_order(Ctx& ctx, DevRows& rows, DevBuf* a, DevBuf* b) {
     }
 }
 
+namespace {
+void enumerate_rows(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, uint32_t L, DevRows& out, EnumStats* stats);
+}
+
+// Identical rows give identical intersections, so B^c over the distinct rows
+// (canonical order, which also groups similar rows into the same tiles) equals
+// B^c over all rows with up to quadratically fewer pairs.
 void enumerate_dev(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, uint32_t L, DevRows& out,
                    EnumStats* stats) {
+    DevBuf U;
+    const size_t m = distinct_rows(ctx, d_rows, n, k, U);
+    enumerate_rows(ctx, U.as<int64_t>(), m, k, L, out, stats);
+    if (stats) {
+        stats->pairs = n ? (uint64_t)n * (n - 1) / 2 : 0;
+        stats->distinct_rows = m;
+    }
+}
+
+namespace {
+void enumerate_rows(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, uint32_t L, DevRows& out,
+                    EnumStats* stats) {
     out.n = 0;
     out.k = k;
     out.L = L;
@@ -353,7 +403,7 @@ void enumerate_dev(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, uint32_t
     const uint64_t n_tiles = blocks * (blocks + 1) / 2;
     const uint64_t pairs = (uint64_t)n * (n - 1) / 2;
     const int stride = (int)(k | 1);
-    const size_t smem = 2 * (size_t)kTile * stride * 8;
+    const size_t smem = (size_t)kLocalSlots * 8 + 2 * (size_t)kTile * stride * 8;
     if (smem > 200 * 1024) fail(IG_E_INVALID_ARG, "enumerate: rows wider than the shared-memory tile (K > 200)");
     IGB_CUDA(cudaFuncSetAttribute(pair_enum, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
 
@@ -428,6 +478,8 @@ void enumerate_dev(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, uint32_t
         stats->collisions = collisions_total;
     }
 }
+
+}  // namespace
 
 int score_dev(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const int64_t* d_support, int64_t* d_score) {
     if (np == 0) return IG_OK;

@@ -1,0 +1,318 @@
+// sort.cu — canonical (words::less, bitpack.hpp:59-68) ordering of K-word rows
+// with rank-compressed keys.
+//
+// Lexicographic order over K unsigned 64-bit words only depends on the order of
+// the values inside each word column.  Each column of a candidate / pattern set
+// takes few distinct values (C3 pure dictionaries: 63..1,970 per column, ~135
+// bits of dense ranks for all 14 words), so every word is replaced by its dense
+// rank among the column's distinct values and the ranks are packed MSB-first
+// into ceil(B/64) 64-bit keys.  One stable radix sort per packed key word
+// (LSD) then yields exactly the canonical order, with ~B/8 radix digit passes
+// instead of 8·K.  Distinct values are found with one open-addressing hash set
+// per column (16-byte slots claimed by a 128-bit CAS), ranked by sorting the
+// (column, value) list, and written back into the slots.  Falls back to the
+// K-pass LSD sort when the tables would be too large.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <vector>
+
+#include "ig_internal.cuh"
+
+namespace igb {
+namespace {
+
+unsigned grid_for(const Ctx& ctx, size_t work, int threads) {
+    size_t g = (work + threads - 1) / threads;
+    const size_t cap = (size_t)ctx.sm_count * 32;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    return (unsigned)g;
+}
+
+__device__ __forceinline__ ulonglong2 cas128(ulonglong2* addr, ulonglong2 cmp, ulonglong2 val) {
+    ulonglong2 old;
+    asm volatile(
+        "{\n\t.reg .b128 c, n, o;\n\t"
+        "mov.b128 c, {%2, %3};\n\t"
+        "mov.b128 n, {%4, %5};\n\t"
+        "atom.global.cas.b128 o, [%6], c, n;\n\t"
+        "mov.b128 {%0, %1}, o;\n\t}"
+        : "=l"(old.x), "=l"(old.y)
+        : "l"(cmp.x), "l"(cmp.y), "l"(val.x), "l"(val.y), "l"(addr)
+        : "memory");
+    return old;
+}
+
+__device__ __forceinline__ unsigned long long ldv(const unsigned long long* p) {
+    return *reinterpret_cast<const volatile unsigned long long*>(p);
+}
+
+// slot = {value, tag}; tag 0 = empty, 1 = present, 2 + rank after ranking.
+__global__ void column_insert(const int64_t* __restrict__ words, size_t n, int k, ulonglong2* __restrict__ tables,
+                              uint32_t slots, unsigned int* __restrict__ counts, int* __restrict__ full) {
+    const size_t total = n * (size_t)k;
+    for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += (size_t)gridDim.x * blockDim.x) {
+        const int w = (int)(q % k);
+        const unsigned long long v = (unsigned long long)words[q];
+        ulonglong2* T = tables + (size_t)w * slots;
+        uint32_t s = (uint32_t)(mix64(v) & (slots - 1));
+        for (uint32_t probe = 0;; ++probe, s = (s + 1) & (slots - 1)) {
+            if (probe >= slots || counts[w] >= slots / 2) {
+                atomicOr(full, 1);
+                return;
+            }
+            unsigned long long tag = ldv(&T[s].y);
+            if (tag == 0) {
+                const ulonglong2 old = cas128(T + s, make_ulonglong2(0ull, 0ull), make_ulonglong2(v, 1ull));
+                if (old.y == 0) {
+                    atomicAdd(counts + w, 1u);
+                    break;
+                }
+                if (old.x == v) break;
+                continue;
+            }
+            unsigned long long x = ldv(&T[s].x);
+            if (x == v) break;
+        }
+    }
+}
+
+// Occupied slots -> (column, value, slot) entries.
+__global__ void column_collect(const ulonglong2* __restrict__ tables, int k, uint32_t slots,
+                               unsigned long long* __restrict__ vals, uint32_t* __restrict__ where,
+                               unsigned int* __restrict__ n_out) {
+    const size_t total = (size_t)k * slots;
+    for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += (size_t)gridDim.x * blockDim.x) {
+        const ulonglong2 e = tables[q];
+        if (e.y != 0) {
+            const unsigned int o = atomicAdd(n_out, 1u);
+            vals[o] = e.x;
+            where[o] = (uint32_t)q;
+        }
+    }
+}
+
+__global__ void column_of(const uint32_t* __restrict__ where, size_t m, uint32_t slots, uint32_t* __restrict__ col) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (size_t)gridDim.x * blockDim.x)
+        col[i] = where[i] / slots;
+}
+
+// After sorting entries by (column, value): rank = position - column start.
+__global__ void write_ranks(const uint32_t* __restrict__ where, size_t m, uint32_t slots,
+                            const unsigned int* __restrict__ col_start, ulonglong2* __restrict__ tables) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (size_t)gridDim.x * blockDim.x) {
+        const uint32_t q = where[i];
+        const uint32_t w = q / slots;
+        tables[q].y = 2ull + (i - col_start[w]);
+    }
+}
+
+struct Field {
+    int key;    // packed key word
+    int shift;  // bit position of the field's LSB inside that key word
+};
+
+// Packed keys, MSB-first by word: keys[j][i] for key word j of row i.
+__global__ void pack_keys(const int64_t* __restrict__ words, size_t n, int k, const ulonglong2* __restrict__ tables,
+                          uint32_t slots, const Field* __restrict__ fields, int n_keys,
+                          unsigned long long* __restrict__ keys) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        unsigned long long acc[8];
+        for (int j = 0; j < n_keys; ++j) acc[j] = 0;
+        for (int w = 0; w < k; ++w) {
+            const unsigned long long v = (unsigned long long)words[i * k + w];
+            const ulonglong2* T = tables + (size_t)w * slots;
+            uint32_t s = (uint32_t)(mix64(v) & (slots - 1));
+            while (T[s].x != v || T[s].y == 0) s = (s + 1) & (slots - 1);
+            const unsigned long long r = T[s].y - 2;
+            const Field f = fields[w];
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (j == f.key) acc[j] |= r << f.shift;
+        }
+        for (int j = 0; j < n_keys; ++j) keys[(size_t)j * n + i] = acc[j];
+    }
+}
+
+__global__ void iota32(uint32_t* p, size_t n) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        p[i] = (uint32_t)i;
+}
+
+__global__ void gather_u64(const unsigned long long* __restrict__ src, const uint32_t* __restrict__ perm, size_t n,
+                           unsigned long long* __restrict__ dst) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        dst[i] = src[perm[i]];
+}
+
+__global__ void row_heads_k(const int64_t* __restrict__ rows, const uint32_t* __restrict__ perm, size_t n, int k,
+                            uint8_t* __restrict__ head) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        uint8_t h = 1;
+        if (i > 0) {
+            const int64_t* a = rows + (size_t)perm[i] * k;
+            const int64_t* b = rows + (size_t)perm[i - 1] * k;
+            h = 0;
+            for (int w = 0; w < k; ++w)
+                if (a[w] != b[w]) {
+                    h = 1;
+                    break;
+                }
+        }
+        head[i] = h;
+    }
+}
+
+__global__ void gather_rows_u32(const int64_t* __restrict__ src, const uint32_t* __restrict__ idx, size_t m, int k,
+                                int64_t* __restrict__ dst) {
+    for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < m * k; q += (size_t)gridDim.x * blockDim.x)
+        dst[q] = src[(size_t)idx[q / k] * k + q % k];
+}
+
+uint32_t next_pow2_u32(uint64_t x) {
+    uint64_t p = 1;
+    while (p < x) p <<= 1;
+    return (uint32_t)p;
+}
+
+}  // namespace
+
+void sort_rows_canonical(Ctx& ctx, const int64_t* d_words, size_t n, size_t k, uint32_t* d_perm) {
+    if (n == 0) return;
+    if (n == 1 || k == 0) {
+        IGB_LAUNCH(ctx, iota32, 1, 32, 0, d_perm, n);
+        return;
+    }
+    // Per-column hash sets; start small (columns usually hold a few thousand
+    // distinct words) and grow x16 when a column passes half load.
+    uint32_t slots = next_pow2_u32(std::min<uint64_t>(2 * n + 16, 1ull << 16));
+    DevBuf tables, counts((k + 1) * 4, ctx.stream), full(4, ctx.stream);
+    std::vector<unsigned int> hc(k + 1);
+    for (;;) {
+        if ((uint64_t)slots * k * 16 > (1ull << 31) || k > 512) {
+            sort_rows_canonical_lsd(ctx, d_words, n, k, d_perm);
+            return;
+        }
+        tables.alloc((size_t)slots * k * 16, ctx.stream);
+        IGB_CUDA(cudaMemsetAsync(tables.p, 0, (size_t)slots * k * 16, ctx.stream));
+        IGB_CUDA(cudaMemsetAsync(counts.p, 0, (k + 1) * 4, ctx.stream));
+        IGB_CUDA(cudaMemsetAsync(full.p, 0, 4, ctx.stream));
+        IGB_LAUNCH(ctx, column_insert, grid_for(ctx, n * k, 256), 256, 0, d_words, n, (int)k, tables.as<ulonglong2>(),
+                   slots, counts.as<unsigned int>(), full.as<int>());
+        int hfull = 0;
+        IGB_CUDA(cudaMemcpyAsync(hc.data(), counts.p, k * 4, cudaMemcpyDeviceToHost, ctx.stream));
+        IGB_CUDA(cudaMemcpyAsync(&hfull, full.p, 4, cudaMemcpyDeviceToHost, ctx.stream));
+        IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+        if (!hfull) break;
+        if (slots >= (1u << 20) || slots >= 2 * n + 16) {
+            sort_rows_canonical_lsd(ctx, d_words, n, k, d_perm);
+            return;
+        }
+        slots *= 16;
+    }
+    // Field layout: ceil(log2 D_w) bits per word, MSB-first, never straddling a key word.
+    std::vector<Field> fields(k);
+    int n_keys = 1, used = 0;
+    std::vector<int> used_bits;
+    for (size_t w = 0; w < k; ++w) {
+        int b = 1;
+        while ((1ull << b) < hc[w]) ++b;
+        if (used + b > 64) {
+            used_bits.push_back(used);
+            ++n_keys;
+            used = 0;
+        }
+        fields[w].key = n_keys - 1;
+        used += b;
+        fields[w].shift = 64 - used;
+    }
+    used_bits.push_back(used);
+    if (n_keys > 8 || n_keys >= (int)k) {
+        sort_rows_canonical_lsd(ctx, d_words, n, k, d_perm);
+        return;
+    }
+    // Rank the distinct values of every column.
+    uint64_t m = 0;
+    for (size_t w = 0; w < k; ++w) m += hc[w];
+    DevBuf vals(m * 8, ctx.stream), vals2(m * 8, ctx.stream), where(m * 4, ctx.stream), where2(m * 4, ctx.stream),
+        col(m * 4, ctx.stream), col2(m * 4, ctx.stream), nout(4, ctx.stream), cstart((k + 1) * 4, ctx.stream);
+    IGB_CUDA(cudaMemsetAsync(nout.p, 0, 4, ctx.stream));
+    IGB_LAUNCH(ctx, column_collect, grid_for(ctx, (size_t)k * slots, 256), 256, 0, tables.as<ulonglong2>(), (int)k,
+               slots, vals.as<unsigned long long>(), where.as<uint32_t>(), nout.as<unsigned int>());
+    size_t tb1 = 0, tb2 = 0;
+    IGB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb1, vals.as<unsigned long long>(),
+                                             vals2.as<unsigned long long>(), where.as<uint32_t>(),
+                                             where2.as<uint32_t>(), (int64_t)m, 0, 64, ctx.stream));
+    IGB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb2, col.as<uint32_t>(), col2.as<uint32_t>(),
+                                             where2.as<uint32_t>(), where.as<uint32_t>(), (int64_t)m, 0, 32,
+                                             ctx.stream));
+    DevBuf temp(std::max(tb1, tb2), ctx.stream);
+    IGB_CUDA(cub::DeviceRadixSort::SortPairs(temp.p, tb1, vals.as<unsigned long long>(),
+                                             vals2.as<unsigned long long>(), where.as<uint32_t>(),
+                                             where2.as<uint32_t>(), (int64_t)m, 0, 64, ctx.stream));
+    IGB_LAUNCH(ctx, column_of, grid_for(ctx, m, 256), 256, 0, where2.as<uint32_t>(), m, slots, col.as<uint32_t>());
+    int cbits = 1;
+    while ((1ull << cbits) < k) ++cbits;
+    IGB_CUDA(cub::DeviceRadixSort::SortPairs(temp.p, tb2, col.as<uint32_t>(), col2.as<uint32_t>(),
+                                             where2.as<uint32_t>(), where.as<uint32_t>(), (int64_t)m, 0, cbits,
+                                             ctx.stream));
+    std::vector<unsigned int> hstart(k + 1, 0);
+    for (size_t w = 0; w < k; ++w) hstart[w + 1] = hstart[w] + hc[w];
+    IGB_CUDA(cudaMemcpyAsync(cstart.p, hstart.data(), (k + 1) * 4, cudaMemcpyHostToDevice, ctx.stream));
+    IGB_LAUNCH(ctx, write_ranks, grid_for(ctx, m, 256), 256, 0, where.as<uint32_t>(), m, slots,
+               cstart.as<unsigned int>(), tables.as<ulonglong2>());
+    // Packed keys and LSD over the key words (least significant word first).
+    DevBuf dfields(k * sizeof(Field), ctx.stream), keys((size_t)n_keys * n * 8, ctx.stream);
+    IGB_CUDA(cudaMemcpyAsync(dfields.p, fields.data(), k * sizeof(Field), cudaMemcpyHostToDevice, ctx.stream));
+    IGB_LAUNCH(ctx, pack_keys, grid_for(ctx, n, 128), 128, 0, d_words, n, (int)k, tables.as<ulonglong2>(), slots,
+               dfields.as<Field>(), n_keys, keys.as<unsigned long long>());
+    DevBuf k1(n * 8, ctx.stream), k2(n * 8, ctx.stream), p2(n * 4, ctx.stream);
+    IGB_LAUNCH(ctx, iota32, grid_for(ctx, n, 256), 256, 0, d_perm, n);
+    size_t tb3 = 0;
+    IGB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb3, k1.as<unsigned long long>(), k2.as<unsigned long long>(),
+                                             d_perm, p2.as<uint32_t>(), (int64_t)n, 0, 64, ctx.stream));
+    DevBuf temp3(tb3, ctx.stream);
+    uint32_t* cur = d_perm;
+    uint32_t* alt = p2.as<uint32_t>();
+    for (int j = n_keys - 1; j >= 0; --j) {
+        const unsigned long long* kj = keys.as<unsigned long long>() + (size_t)j * n;
+        if (j == n_keys - 1) {
+            IGB_CUDA(cudaMemcpyAsync(k1.p, kj, n * 8, cudaMemcpyDeviceToDevice, ctx.stream));
+        } else {
+            IGB_LAUNCH(ctx, gather_u64, grid_for(ctx, n, 256), 256, 0, kj, cur, n, k1.as<unsigned long long>());
+        }
+        const int begin = 64 - used_bits[j];
+        IGB_CUDA(cub::DeviceRadixSort::SortPairs(temp3.p, tb3, k1.as<unsigned long long>(),
+                                                 k2.as<unsigned long long>(), cur, alt, (int64_t)n, begin, 64,
+                                                 ctx.stream));
+        std::swap(cur, alt);
+    }
+    if (cur != d_perm) IGB_CUDA(cudaMemcpyAsync(d_perm, cur, n * 4, cudaMemcpyDeviceToDevice, ctx.stream));
+}
+
+size_t distinct_rows(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, DevBuf& out) {
+    if (n == 0) {
+        out.alloc(8, ctx.stream);
+        return 0;
+    }
+    DevBuf perm(n * 4, ctx.stream), head(n, ctx.stream), rep(n * 4, ctx.stream), nsel(8, ctx.stream);
+    sort_rows_canonical(ctx, d_rows, n, k, perm.as<uint32_t>());
+    IGB_LAUNCH(ctx, row_heads_k, grid_for(ctx, n, 256), 256, 0, d_rows, perm.as<uint32_t>(), n, (int)k,
+               head.as<uint8_t>());
+    size_t tb = 0;
+    IGB_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, perm.as<uint32_t>(), head.as<uint8_t>(), rep.as<uint32_t>(),
+                                        nsel.as<int64_t>(), (int64_t)n, ctx.stream));
+    DevBuf temp(tb, ctx.stream);
+    IGB_CUDA(cub::DeviceSelect::Flagged(temp.p, tb, perm.as<uint32_t>(), head.as<uint8_t>(), rep.as<uint32_t>(),
+                                        nsel.as<int64_t>(), (int64_t)n, ctx.stream));
+    int64_t m = 0;
+    IGB_CUDA(cudaMemcpyAsync(&m, nsel.p, 8, cudaMemcpyDeviceToHost, ctx.stream));
+    IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+    out.alloc(std::max<size_t>((size_t)m * k, 1) * 8, ctx.stream);
+    IGB_LAUNCH(ctx, gather_rows_u32, grid_for(ctx, (size_t)m * k, 256), 256, 0, d_rows, rep.as<uint32_t>(), (size_t)m,
+               (int)k, out.as<int64_t>());
+    return (size_t)m;
+}
+
+}  // namespace igb

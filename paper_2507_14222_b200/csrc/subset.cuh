@@ -25,7 +25,8 @@ void pair_window_dev(Ctx& ctx, const int64_t* d_left, const int64_t* d_rows, siz
 // Distinct non-empty {X_u & X_v : u <= v} of one class (u == v gives the
 // union term X^c), unordered.  Exact: fingerprints only pick the bucket.
 struct EnumStats {
-    uint64_t pairs = 0;       // unordered pairs examined (i < j)
+    uint64_t pairs = 0;       // unordered pairs of the input rows (i < j), as the reference counts them
+    uint64_t distinct_rows = 0;  // rows actually paired (identical rows collapse)
     uint64_t table_slots = 0; // final hash capacity
     int retries = 0;          // capacity growths
     int levels = 0;           // collision levels used (1 = no fingerprint collision)
