@@ -207,6 +207,28 @@ int ig_fit_encoded(ig_ctx* ctx, const ig_encoding* train, const ig_kernel_config
 int ig_evidence_encoded(ig_ctx* ctx, const ig_model* m, const ig_encoding* tests, int64_t* A,
                         int64_t* N);
 
+/* ---------------------------------------------------------------- multi-GPU
+ * SURVEY.md §8(e).  One shard per rank (one process per GPU); training rows
+ * are replicated (every rank runs ig_encode_training on the same columns).
+ * Per class: ig_shard_enumerate dedups the pairs of this rank's tiles
+ * (round-robin over the u <= v tile triangle of the distinct canonical rows)
+ * and buckets the distinct candidates by owner (content fingerprint mod
+ * world) as 8-byte (u, v) row-pair records; the caller exchanges them
+ * (all-to-all, e.g. NCCL over NVLink) and hands each rank what it received to
+ * ig_shard_receive, which dedups exactly across ranks.  ig_shard_finish runs
+ * support / score / coverage / order on the owned candidates; its partial
+ * totals must be summed across ranks and checked <= INT64_MAX (mine.hpp:50-51).
+ * Evidence of the owned dictionaries (ig_evidence* on ig_shard_model) are
+ * partial sums; their sum over ranks is the full A / N.                    */
+typedef struct ig_shard ig_shard;
+int ig_shard_create(ig_ctx* ctx, const ig_encoding* train, int rank, int world, const ig_kernel_config* cfg,
+                    ig_shard** out);
+int ig_shard_enumerate(ig_ctx* ctx, ig_shard* s, int cls, uint64_t* counts, const void** d_send);
+int ig_shard_receive(ig_ctx* ctx, ig_shard* s, int cls, const void* d_recv, uint64_t n_records);
+int ig_shard_finish(ig_ctx* ctx, ig_shard* s, uint64_t* partial_totals);
+const ig_model* ig_shard_model(const ig_shard* s);
+void ig_shard_free(ig_shard* s);
+
 #ifdef __cplusplus
 }
 #endif

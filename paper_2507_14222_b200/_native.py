@@ -97,6 +97,12 @@ SIGNATURES = [
     ("ig_encoding_removed_rows", C.c_int, [vp, pu64]),
     ("ig_encoding_free", None, [vp]),
     ("ig_fit_encoded", C.c_int, [vp, vp, C.POINTER(KernelConfigC), C.POINTER(vp)]),
+    ("ig_shard_create", C.c_int, [vp, vp, C.c_int, C.c_int, C.POINTER(KernelConfigC), C.POINTER(vp)]),
+    ("ig_shard_enumerate", C.c_int, [vp, vp, C.c_int, pu64, C.POINTER(vp)]),
+    ("ig_shard_receive", C.c_int, [vp, vp, C.c_int, vp, C.c_uint64]),
+    ("ig_shard_finish", C.c_int, [vp, vp, pu64]),
+    ("ig_shard_model", vp, [vp]),
+    ("ig_shard_free", None, [vp]),
     ("ig_evidence_encoded", C.c_int, [vp, vp, vp, p64, p64]),
 ]
 

@@ -9,6 +9,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <vector>
 
 #include "encode.cuh"
 #include "host_pipeline.hpp"
@@ -29,6 +30,7 @@ struct ig_candidates {
 
 struct ig_model {
     uint32_t L = 0;
+    uint64_t partial_total[2] = {0, 0};  // Σ candidate scores per class (checked)
     ig_candidates cand[2];
     ig_candidates pure[2];
     double ms[6] = {0, 0, 0, 0, 0, 0};
@@ -106,12 +108,14 @@ struct Timer {
 // The mining half of cmd_train: for both classes enumerate →
 // support → score → total; canonical order; reject_covered against
 // the opposite class.
-void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m) {
+// enumerate = false: m.cand[c].rows already hold the candidates (multi-GPU
+// owner shard); only support -> score -> purify -> order run.
+void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m, bool enumerate = true) {
     m.L = L;
     const size_t k = igb::words_for(L);
     Timer tm(ctx.stream);
     tm.mark();  // 0
-    for (int c = 0; c < 2; ++c) {
+    for (int c = 0; c < 2 && enumerate; ++c) {
         if (X[c].n == 0) fail(IG_E_DATA, "enumerate_candidates: empty class");
         igb::enumerate_dev(ctx, X[c].p, X[c].n, k, L, m.cand[c].rows, &m.stats[c]);
         m.cand[c].pairs = m.stats[c].pairs;
@@ -137,6 +141,7 @@ void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m) {
         int64_t total = 0;
         if (igb::total_score_dev(ctx, C.score.as<int64_t>(), np, &total) != IG_OK)
             fail(IG_E_OVERFLOW, "total score overflows int64");
+        m.partial_total[c] = (uint64_t)total;
         C.has_support = C.has_score = true;
     }
     tm.mark();  // 2
@@ -662,5 +667,94 @@ int ig_evidence_encoded(ig_ctx* ctx, const ig_model* m, const ig_encoding* tests
         IGB_CUDA(cudaStreamSynchronize(ctx->stream));
     });
 }
+
+
+// ------------------------------------------------------------------ multi-GPU shards
+// rows replicated, pair tiles split round-robin, candidates
+// routed to the owner of their content fingerprint, owner-local support /
+// coverage / scores, matcher partials summed by the caller.
+struct ig_shard {
+    int rank = 0, world = 1;
+    uint32_t L = 0;
+    size_t k = 0;
+    const ig_encoding* train = nullptr;
+    igb::DevBuf U[2];
+    size_t m[2] = {0, 0};
+    igb::DevBuf send[2];
+    std::vector<uint64_t> counts[2];
+    bool received[2] = {false, false};
+    ig_model model;
+};
+
+int ig_shard_create(ig_ctx* ctx, const ig_encoding* train, int rank, int world, const ig_kernel_config* cfg,
+                    ig_shard** out) {
+    *out = nullptr;
+    return guard(ctx, [&] {
+        check_cfg(cfg);
+        if (world < 1 || rank < 0 || rank >= world) fail(IG_E_INVALID_ARG, "shard: rank must be in [0, world)");
+        auto s = std::make_unique<ig_shard>();
+        s->rank = rank;
+        s->world = world;
+        s->train = train;
+        s->L = train->L;
+        s->k = igb::words_for(train->L);
+        const igb::DevRows* X[2] = {&train->attack, &train->normal};
+        for (int c = 0; c < 2; ++c) {
+            if (X[c]->n == 0) fail(IG_E_DATA, "enumerate_candidates: empty class");
+            s->m[c] = igb::distinct_rows(*ctx, X[c]->data(), X[c]->n, s->k, s->U[c]);
+            s->U[c].persist();
+        }
+        IGB_CUDA(cudaStreamSynchronize(ctx->stream));
+        *out = s.release();
+    });
+}
+
+int ig_shard_enumerate(ig_ctx* ctx, ig_shard* s, int cls, uint64_t* counts, const void** d_send) {
+    return guard(ctx, [&] {
+        if (cls < 0 || cls > 1) fail(IG_E_INVALID_ARG, "class must be 0 (attack) or 1 (normal)");
+        igb::PairSource src;
+        src.tile_begin = (uint64_t)s->rank;
+        src.tile_step = (uint64_t)s->world;
+        igb::DevBuf reps;
+        const uint64_t c = igb::dedup_pairs(*ctx, s->U[cls].as<int64_t>(), s->m[cls], s->k, src, reps, nullptr);
+        igb::bucket_by_owner(*ctx, s->U[cls].as<int64_t>(), s->k, reps.as<uint2>(), c, s->world, s->send[cls],
+                             s->counts[cls]);
+        s->send[cls].persist();
+        for (int r = 0; r < s->world; ++r) counts[r] = s->counts[cls][r];
+        *d_send = s->send[cls].p;
+    });
+}
+
+int ig_shard_receive(ig_ctx* ctx, ig_shard* s, int cls, const void* d_recv, uint64_t n_records) {
+    return guard(ctx, [&] {
+        if (cls < 0 || cls > 1) fail(IG_E_INVALID_ARG, "class must be 0 (attack) or 1 (normal)");
+        igb::PairSource src;
+        src.list = static_cast<const uint2*>(d_recv);
+        src.n_list = n_records;
+        igb::DevBuf reps;
+        const uint64_t c = igb::dedup_pairs(*ctx, s->U[cls].as<int64_t>(), s->m[cls], s->k, src, reps,
+                                            &s->model.stats[cls]);
+        ig_candidates& C = s->model.cand[cls];
+        igb::materialize_pairs(*ctx, s->U[cls].as<int64_t>(), s->k, reps.as<uint2>(), c, s->L, C.rows);
+        C.ordered = false;
+        IGB_CUDA(cudaStreamSynchronize(ctx->stream));
+        s->received[cls] = true;
+    });
+}
+
+int ig_shard_finish(ig_ctx* ctx, ig_shard* s, uint64_t* partial_totals) {
+    return guard(ctx, [&] {
+        if (!s->received[0] || !s->received[1]) fail(IG_E_INVALID_ARG, "shard: receive both classes first");
+        View X[2] = {{s->train->attack.data(), s->train->attack.n, s->train->attack.k},
+                     {s->train->normal.data(), s->train->normal.n, s->train->normal.k}};
+        fit_impl(*ctx, X, s->L, s->model, /*enumerate=*/false);
+        partial_totals[0] = s->model.partial_total[0];
+        partial_totals[1] = s->model.partial_total[1];
+    });
+}
+
+const ig_model* ig_shard_model(const ig_shard* s) { return s ? &s->model : nullptr; }
+
+void ig_shard_free(ig_shard* s) { delete s; }
 
 }  // extern "C"

@@ -128,12 +128,14 @@ constexpr int kLocalProbes = 64;
 
 __global__ void __launch_bounds__(kPairThreads)
 pair_enum(const int64_t* __restrict__ X, uint32_t n, int k, int stride, uint64_t n_tiles, Table T,
-          uint64_t tile_begin) {
+          uint64_t tile_begin, uint64_t tile_step) {
     extern __shared__ int64_t sm[];
     unsigned long long* local = reinterpret_cast<unsigned long long*>(sm);  // kLocalSlots
     int64_t* sI = sm + kLocalSlots;
     int64_t* sJ = sI + (size_t)kTile * stride;
-    for (uint64_t t = tile_begin + blockIdx.x; t < n_tiles; t += gridDim.x) {
+    for (uint64_t it = blockIdx.x;; it += gridDim.x) {
+        const uint64_t t = tile_begin + it * tile_step;  // this rank's tiles: begin, begin + step, ...
+        if (t >= n_tiles) break;
         if (*(volatile int*)T.fail) return;
         uint32_t bi, bj;
         tile_of(t, bi, bj);
@@ -373,10 +375,6 @@ void canonical_order(Ctx& ctx, DevRows& rows, DevBuf* a, DevBuf* b) {
     }
 }
 
-namespace {
-void enumerate_rows(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, uint32_t L, DevRows& out, EnumStats* stats);
-}
-
 // Identical rows give identical intersections, so B^c over the distinct rows
 // (canonical order, which also groups similar rows into the same tiles) equals
 // B^c over all rows with up to quadratically fewer pairs.
@@ -384,24 +382,35 @@ void enumerate_dev(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, uint32_t
                    EnumStats* stats) {
     DevBuf U;
     const size_t m = distinct_rows(ctx, d_rows, n, k, U);
-    enumerate_rows(ctx, U.as<int64_t>(), m, k, L, out, stats);
+    PairSource src;  // every tile of the triangle
+    DevBuf reps;
+    const uint64_t c = dedup_pairs(ctx, U.as<int64_t>(), m, k, src, reps, stats);
+    materialize_pairs(ctx, U.as<int64_t>(), k, reps.as<uint2>(), c, L, out);
     if (stats) {
         stats->pairs = n ? (uint64_t)n * (n - 1) / 2 : 0;
         stats->distinct_rows = m;
     }
 }
 
-namespace {
-void enumerate_rows(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, uint32_t L, DevRows& out,
-                    EnumStats* stats) {
-    out.n = 0;
+void materialize_pairs(Ctx& ctx, const int64_t* d_rows, size_t k, const uint2* d_reps, uint64_t count, uint32_t L,
+                       DevRows& out) {
     out.k = k;
     out.L = L;
-    if (n == 0) return;
+    out.n = count;
+    out.buf.alloc(std::max<uint64_t>(count * k, 1) * 8, ctx.stream);
+    if (count * k)
+        IGB_LAUNCH(ctx, materialize, grid_for(ctx, count * k, 256), 256, 0, d_rows, (int)k, d_reps, count, out.data());
+}
+
+uint64_t dedup_pairs(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, const PairSource& src, DevBuf& reps_out,
+                     EnumStats* stats) {
+    reps_out.alloc(8, ctx.stream);
+    if (n == 0) return 0;
     if (n > 0xffffffffull) fail(IG_E_INVALID_ARG, "enumerate: more than 2^32 rows");
     const uint64_t blocks = (n + kTile - 1) / kTile;
     const uint64_t n_tiles = blocks * (blocks + 1) / 2;
-    const uint64_t pairs = (uint64_t)n * (n - 1) / 2;
+    const uint64_t my_tiles = src.list ? 0 : (n_tiles > src.tile_begin ? (n_tiles - src.tile_begin + src.tile_step - 1) / src.tile_step : 0);
+    const uint64_t pairs = src.list ? src.n_list : (uint64_t)n * (n - 1) / 2 / src.tile_step;
     const int stride = (int)(k | 1);
     const size_t smem = (size_t)kLocalSlots * 8 + 2 * (size_t)kTile * stride * 8;
     if (smem > 200 * 1024) fail(IG_E_INVALID_ARG, "enumerate: rows wider than the shared-memory tile (K > 200)");
@@ -411,7 +420,8 @@ void enumerate_rows(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, uint32_
     // (x4) and rerun if the table fills.  Results never depend on capacity.
     uint64_t guess = (uint64_t)(4.0 * std::pow((double)(pairs + n), 0.8)) + 2 * n + 1024;
     uint64_t cap = next_pow2(std::max<uint64_t>(guess, 1u << 16));
-    const uint64_t max_cap = next_pow2(2 * (pairs + n) + 1024);
+    const uint64_t bound = src.list ? src.n_list : std::min<uint64_t>(my_tiles * (uint64_t)kTile * kTile, pairs * src.tile_step + n);
+    const uint64_t max_cap = next_pow2(2 * bound + 1024);
     if (cap > max_cap) cap = max_cap;
     int retries = 0;
     std::vector<DevBuf> level_reps;  // per level: reps
@@ -429,10 +439,15 @@ void enumerate_rows(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, uint32_
             const uint64_t lcap = level == 0 ? cap : next_pow2(4 * n_pending + 1024);
             const uint64_t ovf_cap = level == 0 ? std::max<uint64_t>(1u << 20, cap / 64) : n_pending + 1;
             Table T = tm.make(ctx, lcap, ovf_cap, 0x2545f4914f6cdd1dull * (uint64_t)(level + 1));
-            if (level == 0) {
-                const unsigned grid = (unsigned)std::min<uint64_t>(n_tiles, (uint64_t)ctx.sm_count * 16);
-                IGB_LAUNCH(ctx, pair_enum, grid, kPairThreads, smem, d_rows, (uint32_t)n, (int)k, stride, n_tiles,
-                           T, 0ull);
+            if (level == 0 && src.list) {
+                if (src.n_list)
+                    IGB_LAUNCH(ctx, pair_insert_list, grid_for(ctx, src.n_list, 256), 256, 0, d_rows, (int)k, src.list,
+                               src.n_list, T);
+            } else if (level == 0) {
+                const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(my_tiles, (uint64_t)ctx.sm_count * 16));
+                if (my_tiles)
+                    IGB_LAUNCH(ctx, pair_enum, grid, kPairThreads, smem, d_rows, (uint32_t)n, (int)k, stride, n_tiles,
+                               T, src.tile_begin, src.tile_step);
             } else {
                 IGB_LAUNCH(ctx, pair_insert_list, grid_for(ctx, n_pending, 256), 256, 0, d_rows, (int)k,
                            pending.as<uint2>(), n_pending, T);
@@ -460,14 +475,13 @@ void enumerate_rows(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, uint32_
     }
     uint64_t total = 0;
     for (auto c : level_counts) total += c;
-    out.buf.alloc(total * k * 8, ctx.stream);
-    out.n = total;
+    reps_out.alloc(std::max<uint64_t>(total, 1) * sizeof(uint2), ctx.stream);
     uint64_t off = 0;
     for (size_t l = 0; l < level_reps.size(); ++l) {
         const uint64_t c = level_counts[l];
         if (c)
-            IGB_LAUNCH(ctx, materialize, grid_for(ctx, c * k, 256), 256, 0, d_rows, (int)k,
-                       level_reps[l].as<uint2>(), c, out.data() + off * k);
+            IGB_CUDA(cudaMemcpyAsync(reps_out.as<uint2>() + off, level_reps[l].p, c * sizeof(uint2),
+                                     cudaMemcpyDeviceToDevice, ctx.stream));
         off += c;
     }
     if (stats) {
@@ -477,9 +491,51 @@ void enumerate_rows(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, uint32_
         stats->levels = (int)level_reps.size();
         stats->collisions = collisions_total;
     }
+    return total;
 }
 
+namespace {
+// Owner of a candidate = its content fingerprint (unseeded, identical on every
+// rank because the distinct canonical rows are) mod world.
+__global__ void owner_of(const int64_t* __restrict__ X, int k, const uint2* __restrict__ reps, uint64_t n, int world,
+                         uint32_t* __restrict__ owner, unsigned long long* __restrict__ counts) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint2 p = reps[i];
+        const int64_t* a = X + (size_t)p.x * k;
+        const int64_t* b = X + (size_t)p.y * k;
+        Fp fp;
+        for (int w = 0; w < k; ++w) fp.add((uint64_t)(a[w] & b[w]));
+        const uint32_t o = (uint32_t)((fp.final(k) >> 32) % (uint64_t)world);
+        owner[i] = o;
+        atomicAdd(counts + o, 1ull);
+    }
+}
+
+__global__ void scatter_owner(const uint2* __restrict__ reps, const uint32_t* __restrict__ owner, uint64_t n,
+                              unsigned long long* __restrict__ cursor, uint2* __restrict__ send) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        send[atomicAdd(cursor + owner[i], 1ull)] = reps[i];
+}
 }  // namespace
+
+void bucket_by_owner(Ctx& ctx, const int64_t* d_rows, size_t k, const uint2* d_reps, uint64_t count, int world,
+                     DevBuf& send, std::vector<uint64_t>& counts) {
+    counts.assign(world, 0);
+    send.alloc(std::max<uint64_t>(count, 1) * sizeof(uint2), ctx.stream);
+    if (count == 0) return;
+    DevBuf owner(count * 4, ctx.stream), cnt(world * 8, ctx.stream), cur(world * 8, ctx.stream);
+    IGB_CUDA(cudaMemsetAsync(cnt.p, 0, world * 8, ctx.stream));
+    IGB_LAUNCH(ctx, owner_of, grid_for(ctx, count, 256), 256, 0, d_rows, (int)k, d_reps, count, world,
+               owner.as<uint32_t>(), cnt.as<unsigned long long>());
+    IGB_CUDA(cudaMemcpyAsync(counts.data(), cnt.p, world * 8, cudaMemcpyDeviceToHost, ctx.stream));
+    IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+    std::vector<uint64_t> start(world, 0);
+    for (int r = 1; r < world; ++r) start[r] = start[r - 1] + counts[r - 1];
+    IGB_CUDA(cudaMemcpyAsync(cur.p, start.data(), world * 8, cudaMemcpyHostToDevice, ctx.stream));
+    IGB_LAUNCH(ctx, scatter_owner, grid_for(ctx, count, 256), 256, 0, d_reps, owner.as<uint32_t>(), count,
+               cur.as<unsigned long long>(), send.as<uint2>());
+    IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+}
 
 int score_dev(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const int64_t* d_support, int64_t* d_score) {
     if (np == 0) return IG_OK;

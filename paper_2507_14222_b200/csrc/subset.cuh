@@ -2,6 +2,8 @@
 // mining kernels (mine.cu).  Device pointers throughout; k = words per row.
 #pragma once
 
+#include <vector>
+
 #include "ig_internal.cuh"
 
 namespace igb {
@@ -34,6 +36,25 @@ struct EnumStats {
 };
 void enumerate_dev(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, uint32_t L, DevRows& out,
                    EnumStats* stats);
+
+// Which pairs of the (distinct, canonical) rows to insert: the tiles
+// tile_begin, tile_begin + tile_step, ... of the u <= v triangle, or an explicit
+// list of (u, v) row pairs (multi-GPU owner phase).
+struct PairSource {
+    uint64_t tile_begin = 0, tile_step = 1;
+    const uint2* list = nullptr;
+    uint64_t n_list = 0;
+};
+// Exact dedup of the non-empty pair intersections of `src`: one representative
+// (u, v) per distinct content -> reps_out; returns the count.
+uint64_t dedup_pairs(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, const PairSource& src, DevBuf& reps_out,
+                     EnumStats* stats);
+void materialize_pairs(Ctx& ctx, const int64_t* d_rows, size_t k, const uint2* d_reps, uint64_t count, uint32_t L,
+                       DevRows& out);
+// Multi-GPU: route representatives to their owner rank (fingerprint of the
+// content mod world).  send gets the records grouped by destination; counts[world].
+void bucket_by_owner(Ctx& ctx, const int64_t* d_rows, size_t k, const uint2* d_reps, uint64_t count, int world,
+                     DevBuf& send, std::vector<uint64_t>& counts);
 
 // score[p] = support[p] * popcount(p)^2 with overflow flag (mine.hpp:46-48).
 // Returns IG_OK / IG_E_OVERFLOW.
