@@ -208,8 +208,21 @@ def run_b200(args):
     dA = torch.empty(n_test, dtype=torch.int64, device="cuda")
     dN = torch.empty(n_test, dtype=torch.int64, device="cuda")
 
+    if world > 1:
+        from paper_2507_14222_b200 import sharded
+        ex = sharded.TorchExchange()
+
     def step_resident():
         enc = api.encode_training(dev_tr, ctx)
+        if world > 1:
+            # pair tiles round-robin, candidates to fingerprint owners (NCCL all-to-all),
+            # owner-local support/coverage, partial evidence all-reduced.
+            res = sharded.fit_distributed(ctx, enc, rank, world, ex)
+            tenc = api.encode_rows(dev_te, enc, ctx)
+            a, n = sharded.evidence_distributed(res, tenc, ex)
+            dA.copy_(a)
+            dN.copy_(n)
+            return enc, res.model, tenc
         model = api.fit_encoded(enc)
         tenc = api.encode_rows(dev_te, enc, ctx)
         model.evidence_device(tenc.device_rows(2), n_test, dA.data_ptr(), dN.data_ptr())
@@ -217,6 +230,11 @@ def run_b200(args):
 
     def step_e2e():
         enc = api.encode_training(cols_tr, ctx)
+        if world > 1:
+            res = sharded.fit_distributed(ctx, enc, rank, world, ex)
+            tenc = api.encode_rows(cols_te, enc, ctx)
+            a, n = sharded.evidence_distributed(res, tenc, ex)
+            return res.model, a.cpu().numpy(), n.cpu().numpy()
         model = api.fit_encoded(enc)
         tenc = api.encode_rows(cols_te, enc, ctx)
         A, N = model.evidence_encoded(tenc)
@@ -310,7 +328,8 @@ def run_b200(args):
     line = {"metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-            "config": workload_config(args, n_train, n_test, {"parallelism": f"replicas{world}" if world > 1 else "1gpu",
+            "config": workload_config(args, n_train, n_test, {"parallelism": (f"sharded{world}: pair tiles round-robin, NCCL all-to-all to fingerprint owners, "
+                                                                              "all-reduce of partial evidence") if world > 1 else "1gpu",
                                                               "L": tenc.logical_len, "K": K,
                                                               "candidates": [model.count(0, 0), model.count(1, 0)],
                                                               "pure": P}),
