@@ -223,6 +223,10 @@ __global__ void invert_rank(const uint16_t* __restrict__ byrank, uint32_t L, uin
     for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < L; r += gridDim.x * blockDim.x) rank[byrank[r]] = (uint16_t)r;
 }
 
+__global__ void minus_one(uint32_t* __restrict__ v, size_t n) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) v[i] -= 1;
+}
+
 enum Mode : int { kMatch = 0, kSupport = 1, kCover = 2, kMatchChecked = 3 };
 
 // Warp per pattern over the CSR token lists.
@@ -408,13 +412,189 @@ __global__ void vertical_work(const uint32_t* __restrict__ tok_off, const uint16
     if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
 }
 
+// ------------------------------------------------------------------ grouped scan
+// Patterns sharing their two rarest tokens (t1, t2) share the word list
+// S = {(w, post[t1][w] & post[t2][w]) != 0}: it is built once per group (warp per
+// group over the non-zero words of t1) and every pattern of the group walks S
+// instead of all non-zero words of t1, ANDing only its remaining tokens.  At
+// C3 ~1M patterns fall into ~35k groups, so most of the (t1, t2) work is shared.
+constexpr uint32_t kNoTok = 0xffffu;
+
+__global__ void group_keys(const uint32_t* __restrict__ tok_off, const uint16_t* __restrict__ toks, size_t np,
+                           uint32_t* __restrict__ key, uint32_t* __restrict__ idx) {
+    for (size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += (size_t)gridDim.x * blockDim.x) {
+        const uint32_t o = tok_off[p], m = tok_off[p + 1] - o;
+        const uint32_t t1 = m >= 1 ? toks[o] : kNoTok, t2 = m >= 2 ? toks[o + 1] : kNoTok;
+        key[p] = (t1 << 16) | t2;
+        idx[p] = (uint32_t)p;
+    }
+}
+
+__global__ void group_heads(const uint32_t* __restrict__ key, size_t np, uint8_t* __restrict__ head,
+                            uint32_t* __restrict__ head32) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < np; i += (size_t)gridDim.x * blockDim.x) {
+        const uint8_t h = (i == 0 || key[i] != key[i - 1]) ? 1 : 0;
+        head[i] = h;
+        head32[i] = h;
+    }
+}
+
+// upper bound of each group's list: non-zero words of t1 (all words without t1)
+__global__ void group_bound(const uint32_t* __restrict__ gkey, size_t G, const uint32_t* __restrict__ nz_off,
+                            size_t W, unsigned long long* __restrict__ ub) {
+    for (size_t g = (size_t)blockIdx.x * blockDim.x + threadIdx.x; g < G; g += (size_t)gridDim.x * blockDim.x) {
+        const uint32_t t1 = gkey[g] >> 16;
+        ub[g] = t1 == kNoTok ? (unsigned long long)W : (unsigned long long)(nz_off[t1 + 1] - nz_off[t1]);
+    }
+}
+
+// Warp per group: S = non-zero (w, post[t1][w] & post[t2][w]).
+__global__ void group_lists(const uint32_t* __restrict__ gkey, size_t G, const unsigned long long* __restrict__ dense,
+                            size_t W, size_t n_rows, const uint32_t* __restrict__ nz_off,
+                            const uint32_t* __restrict__ nz_idx, const unsigned long long* __restrict__ goff,
+                            uint32_t* __restrict__ glen, uint32_t* __restrict__ ew, unsigned long long* __restrict__ em) {
+    const int lane = threadIdx.x & 31;
+    const size_t warps = ((size_t)gridDim.x * blockDim.x) >> 5;
+    for (size_t g = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < G; g += warps) {
+        const uint32_t t1 = gkey[g] >> 16, t2 = gkey[g] & 0xffffu;
+        const uint32_t beg = t1 == kNoTok ? 0u : nz_off[t1];
+        const uint32_t end = t1 == kNoTok ? (uint32_t)W : nz_off[t1 + 1];
+        const unsigned long long base = goff[g];
+        uint32_t cnt = 0;
+        for (uint32_t j0 = beg; j0 < end; j0 += 32) {
+            const uint32_t j = j0 + lane;
+            unsigned long long m = 0;
+            uint32_t w = 0;
+            if (j < end) {
+                if (t1 == kNoTok) {
+                    w = j;
+                    const size_t lo = (size_t)w * 64;
+                    m = n_rows - lo >= 64 ? ~0ull : ((1ull << (n_rows - lo)) - 1ull);
+                } else {
+                    w = nz_idx[j];
+                    m = dense[(size_t)t1 * W + w];
+                    if (t2 != kNoTok) m &= dense[(size_t)t2 * W + w];
+                }
+            }
+            const uint32_t bal = __ballot_sync(kFull, m != 0ull);
+            if (m) {
+                const uint32_t pos = cnt + __popc(bal & ((1u << lane) - 1u));
+                ew[base + pos] = w;
+                em[base + pos] = m;
+            }
+            cnt += __popc(bal);
+        }
+        if (lane == 0) glen[g] = cnt;
+    }
+}
+
+// Warp per pattern (in group order): walk the group's list, AND tokens 3.., then
+// match / support / cover as posting_scan.
+template <int MODE>
+__global__ void __launch_bounds__(256)
+grouped_scan(const unsigned long long* __restrict__ dense, size_t W, size_t n_rows,
+             const uint32_t* __restrict__ tok_off, const uint16_t* __restrict__ toks, size_t np,
+             const uint32_t* __restrict__ order, const uint32_t* __restrict__ gid,
+             const unsigned long long* __restrict__ goff, const uint32_t* __restrict__ glen,
+             const uint32_t* __restrict__ ew, const unsigned long long* __restrict__ em,
+             const int64_t* __restrict__ scores, unsigned long long* __restrict__ acc,
+             int64_t* __restrict__ support_out, uint8_t* __restrict__ cover_out, int* __restrict__ flags) {
+    const int lane = threadIdx.x & 31;
+    const size_t warps = ((size_t)gridDim.x * blockDim.x) >> 5;
+    bool ovf = false;
+    for (size_t i = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < np; i += warps) {
+        const uint32_t p = order[i];
+        const uint32_t g = gid[i];
+        const uint32_t o = tok_off[p];
+        const uint32_t m = tok_off[p + 1] - o;
+        const uint32_t tl = lane < m ? (uint32_t)toks[o + lane] : 0u;
+        const unsigned long long base = goff[g];
+        const uint32_t len = glen[g];
+        unsigned long long s = 0;
+        if (MODE == kMatch || MODE == kMatchChecked) s = (unsigned long long)scores[p];
+        uint32_t cnt = 0;
+        bool hit = false;
+        const uint32_t Wu = (uint32_t)W;
+        for (uint32_t j0 = 0; j0 < len; j0 += 32) {
+            const uint32_t j = j0 + lane;
+            const uint32_t w = j < len ? ew[base + j] : 0u;
+            unsigned long long mw = j < len ? em[base + j] : 0ull;
+            const unsigned long long* col = dense + w;
+            for (uint32_t t = 2; t < m; t += 4) {
+                if (!__any_sync(kFull, mw != 0ull)) break;
+                uint32_t tk[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t ii = min(t + u, m - 1);
+                    tk[u] = ii < 32 ? __shfl_sync(kFull, tl, ii) : (uint32_t)toks[o + ii];
+                }
+                if (mw) {
+                    const unsigned long long a = col[tk[0] * Wu], b = col[tk[1] * Wu];
+                    const unsigned long long c = col[tk[2] * Wu], d = col[tk[3] * Wu];
+                    mw &= (a & b) & (c & d);
+                }
+            }
+            if (MODE == kSupport) {
+                cnt += __popcll(mw);
+            } else if (MODE == kCover) {
+                if (__any_sync(kFull, mw != 0ull)) {
+                    hit = true;
+                    break;
+                }
+            } else {
+                unsigned long long* row = acc + (size_t)w * 64;
+                while (mw) {
+                    const int b = __ffsll((long long)mw) - 1;
+                    mw &= mw - 1;
+                    if (MODE == kMatchChecked) {
+                        const unsigned long long old = atomicAdd(row + b, s);
+                        if (old + s > (unsigned long long)INT64_MAX) ovf = true;
+                    } else {
+                        atomicAdd(row + b, s);
+                    }
+                }
+            }
+        }
+        if (MODE == kSupport) {
+            for (int o2 = 16; o2; o2 >>= 1) cnt += __shfl_xor_sync(kFull, cnt, o2);
+            if (lane == 0) support_out[p] = (int64_t)cnt;
+        } else if (MODE == kCover) {
+            if (lane == 0) cover_out[p] = hit ? 1 : 0;
+        }
+    }
+    if (MODE == kMatchChecked && ovf) atomicOr(flags, 1);
+}
+
+// diagnostics: word-ANDs of the grouped algorithm without early exit
+//   Σ_groups ub(g) * min(2, |t1,t2|) + Σ_patterns glen(g(p)) * max(0, m_p - 2)
+__global__ void grouped_work(const uint32_t* __restrict__ tok_off, size_t np, const uint32_t* __restrict__ order,
+                             const uint32_t* __restrict__ gid, const uint32_t* __restrict__ glen,
+                             unsigned long long* __restrict__ out) {
+    unsigned long long acc = 0;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < np; i += (size_t)gridDim.x * blockDim.x) {
+        const uint32_t p = order[i];
+        const uint32_t m = tok_off[p + 1] - tok_off[p];
+        if (m > 2) acc += (unsigned long long)glen[gid[i]] * (m - 2);
+    }
+    for (int s = 16; s; s >>= 1) acc += __shfl_xor_sync(kFull, acc, s);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
+}
+
+__global__ void group_work(const uint32_t* __restrict__ gkey, const unsigned long long* __restrict__ ub, size_t G,
+                           unsigned long long* __restrict__ out) {
+    unsigned long long acc = 0;
+    for (size_t g = (size_t)blockIdx.x * blockDim.x + threadIdx.x; g < G; g += (size_t)gridDim.x * blockDim.x)
+        acc += ub[g] * (((gkey[g] & 0xffffu) != kNoTok) ? 2ull : 1ull);
+    for (int s = 16; s; s >>= 1) acc += __shfl_xor_sync(kFull, acc, s);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
+}
+
 template <int MODE>
 void launch_scan(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Postings& P, const int64_t* scores,
                  unsigned long long* acc, int64_t* support, uint8_t* cover, int* flags) {
     if (np == 0) return;
     PatternTokens T;
     pattern_tokens(ctx, d_pat, np, k, P, T);
-    const size_t blocks = std::min<size_t>((np + 7) / 8, (size_t)ctx.sm_count * 64);
     const bool diag = ctx.diag && (MODE == kMatch || MODE == kMatchChecked);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (diag) {
@@ -422,15 +602,65 @@ void launch_scan(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Post
         IGB_CUDA(cudaEventCreate(&e1));
         IGB_CUDA(cudaEventRecord(e0, ctx.stream));
     }
-    IGB_LAUNCH(ctx, posting_scan<MODE>, (unsigned)blocks, 256, 0, P.dense.as<unsigned long long>(), P.W,
-               P.nz_off.as<uint32_t>(), P.nz_idx.as<uint32_t>(), P.n, T.off.as<uint32_t>(), T.toks.as<uint16_t>(), np,
+    // group patterns by their two rarest tokens
+    DevBuf key(np * 4, ctx.stream), key2(np * 4, ctx.stream), idx(np * 4, ctx.stream), order(np * 4, ctx.stream);
+    IGB_LAUNCH(ctx, group_keys, grid_for(ctx, np, 256), 256, 0, T.off.as<uint32_t>(), T.toks.as<uint16_t>(), np,
+               key.as<uint32_t>(), idx.as<uint32_t>());
+    size_t tb = 0;
+    IGB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, key.as<uint32_t>(), key2.as<uint32_t>(), idx.as<uint32_t>(),
+                                             order.as<uint32_t>(), (int64_t)np, 0, 32, ctx.stream));
+    DevBuf temp(tb, ctx.stream);
+    IGB_CUDA(cub::DeviceRadixSort::SortPairs(temp.p, tb, key.as<uint32_t>(), key2.as<uint32_t>(), idx.as<uint32_t>(),
+                                             order.as<uint32_t>(), (int64_t)np, 0, 32, ctx.stream));
+    DevBuf head(np, ctx.stream), head32(np * 4, ctx.stream), gid(np * 4, ctx.stream), gkey(np * 4, ctx.stream),
+        nsel(8, ctx.stream);
+    IGB_LAUNCH(ctx, group_heads, grid_for(ctx, np, 256), 256, 0, key2.as<uint32_t>(), np, head.as<uint8_t>(),
+               head32.as<uint32_t>());
+    size_t tb2 = 0, tb3 = 0;
+    IGB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb2, head32.as<uint32_t>(), gid.as<uint32_t>(), (int64_t)np,
+                                           ctx.stream));
+    IGB_CUDA(cub::DeviceSelect::Flagged(nullptr, tb3, key2.as<uint32_t>(), head.as<uint8_t>(), gkey.as<uint32_t>(),
+                                        nsel.as<int64_t>(), (int64_t)np, ctx.stream));
+    DevBuf temp2(std::max(tb2, tb3), ctx.stream);
+    IGB_CUDA(cub::DeviceScan::InclusiveSum(temp2.p, tb2, head32.as<uint32_t>(), gid.as<uint32_t>(), (int64_t)np,
+                                           ctx.stream));
+    IGB_CUDA(cub::DeviceSelect::Flagged(temp2.p, tb3, key2.as<uint32_t>(), head.as<uint8_t>(), gkey.as<uint32_t>(),
+                                        nsel.as<int64_t>(), (int64_t)np, ctx.stream));
+    int64_t G = 0;
+    IGB_CUDA(cudaMemcpyAsync(&G, nsel.p, 8, cudaMemcpyDeviceToHost, ctx.stream));
+    IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+    // gid = inclusive count of heads -> 1-based; shift to 0-based in the scan kernel below
+    DevBuf ub((G + 1) * 8, ctx.stream), goff((G + 1) * 8, ctx.stream), glen(G * 4 + 4, ctx.stream);
+    IGB_LAUNCH(ctx, group_bound, grid_for(ctx, (size_t)G, 256), 256, 0, gkey.as<uint32_t>(), (size_t)G,
+               P.nz_off.as<uint32_t>(), P.W, ub.as<unsigned long long>());
+    IGB_CUDA(cudaMemsetAsync(ub.as<unsigned long long>() + G, 0, 8, ctx.stream));
+    size_t tb4 = 0;
+    IGB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb4, ub.as<unsigned long long>(), goff.as<unsigned long long>(),
+                                           (int64_t)G + 1, ctx.stream));
+    DevBuf temp4(tb4, ctx.stream);
+    IGB_CUDA(cub::DeviceScan::ExclusiveSum(temp4.p, tb4, ub.as<unsigned long long>(), goff.as<unsigned long long>(),
+                                           (int64_t)G + 1, ctx.stream));
+    unsigned long long E = 0;
+    IGB_CUDA(cudaMemcpyAsync(&E, goff.as<unsigned long long>() + G, 8, cudaMemcpyDeviceToHost, ctx.stream));
+    IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+    DevBuf ew(std::max<unsigned long long>(E, 1) * 4, ctx.stream), em(std::max<unsigned long long>(E, 1) * 8, ctx.stream);
+    IGB_LAUNCH(ctx, group_lists, grid_for(ctx, (size_t)G * 32, 256), 256, 0, gkey.as<uint32_t>(), (size_t)G,
+               P.dense.as<unsigned long long>(), P.W, P.n, P.nz_off.as<uint32_t>(), P.nz_idx.as<uint32_t>(),
+               goff.as<unsigned long long>(), glen.as<uint32_t>(), ew.as<uint32_t>(), em.as<unsigned long long>());
+    IGB_LAUNCH(ctx, minus_one, grid_for(ctx, np, 256), 256, 0, gid.as<uint32_t>(), np);
+    const size_t blocks = std::min<size_t>((np + 7) / 8, (size_t)ctx.sm_count * 64);
+    IGB_LAUNCH(ctx, grouped_scan<MODE>, (unsigned)blocks, 256, 0, P.dense.as<unsigned long long>(), P.W, P.n,
+               T.off.as<uint32_t>(), T.toks.as<uint16_t>(), np, order.as<uint32_t>(), gid.as<uint32_t>(),
+               goff.as<unsigned long long>(), glen.as<uint32_t>(), ew.as<uint32_t>(), em.as<unsigned long long>(),
                scores, acc, support, cover, flags);
     if (diag) {
         IGB_CUDA(cudaEventRecord(e1, ctx.stream));
         DevBuf w(8, ctx.stream);
         IGB_CUDA(cudaMemsetAsync(w.p, 0, 8, ctx.stream));
-        IGB_LAUNCH(ctx, vertical_work, grid_for(ctx, np, 256), 256, 0, T.off.as<uint32_t>(), T.toks.as<uint16_t>(),
-                   P.nz_off.as<uint32_t>(), np, w.as<unsigned long long>());
+        IGB_LAUNCH(ctx, grouped_work, grid_for(ctx, np, 256), 256, 0, T.off.as<uint32_t>(), np, order.as<uint32_t>(),
+                   gid.as<uint32_t>(), glen.as<uint32_t>(), w.as<unsigned long long>());
+        IGB_LAUNCH(ctx, group_work, grid_for(ctx, (size_t)G, 256), 256, 0, gkey.as<uint32_t>(),
+                   ub.as<unsigned long long>(), (size_t)G, w.as<unsigned long long>());
         unsigned long long hw = 0;
         IGB_CUDA(cudaMemcpyAsync(&hw, w.p, 8, cudaMemcpyDeviceToHost, ctx.stream));
         IGB_CUDA(cudaStreamSynchronize(ctx.stream));
