@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(HERE, "libig_b200.so")
+SO_PATH = os.environ.get("IG_B200_LIB") or os.path.join(HERE, "libig_b200.so")  # override: experiments only
 
 
 class NativeMissing(ImportError):

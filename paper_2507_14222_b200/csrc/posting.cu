@@ -488,6 +488,50 @@ __global__ void group_lists(const uint32_t* __restrict__ gkey, size_t G, const u
     }
 }
 
+// Warp-cooperative scatter of the set bits of every lane's (word w, mask mw):
+// bit q of the warp's concatenated hits goes to lane q % 32, which finds its
+// source lane by binary search over the shuffled prefix counts and the bit with
+// __fns, so the REDs are spread evenly over the lanes instead of each lane
+// walking its own mask (the masks are very uneven).  Call with all 32 lanes.
+template <bool CHECKED>
+__device__ __forceinline__ void warp_scatter_hits(uint32_t w, unsigned long long mw, unsigned long long s,
+                                                  unsigned long long* __restrict__ acc, bool& ovf) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t lo = (uint32_t)mw, hi = (uint32_t)(mw >> 32);
+    const uint32_t c = __popc(lo) + __popc(hi);
+    uint32_t incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const uint32_t excl = incl - c;
+    const uint32_t total = __shfl_sync(kFull, incl, 31);
+    for (uint32_t q0 = 0; q0 < total; q0 += 32) {
+        const uint32_t q = q0 + lane;
+        int L = 0;
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+            const uint32_t e = __shfl_sync(kFull, excl, L + step);
+            if (e <= q) L += step;
+        }
+        const uint32_t r = q - __shfl_sync(kFull, excl, L);
+        const uint32_t slo = __shfl_sync(kFull, lo, L), shi = __shfl_sync(kFull, hi, L);
+        const uint32_t sw = __shfl_sync(kFull, w, L);
+        if (q < total) {
+            const uint32_t plo = __popc(slo);
+            const uint32_t bit = r < plo ? __fns(slo, 0, (int)r + 1) : 32u + __fns(shi, 0, (int)(r - plo) + 1);
+            unsigned long long* dst = acc + (size_t)sw * 64 + bit;
+            if (CHECKED) {
+                const unsigned long long old = atomicAdd(dst, s);
+                if (old + s > (unsigned long long)INT64_MAX) ovf = true;
+            } else {
+                atomicAdd(dst, s);
+            }
+        }
+    }
+}
+
 // Warp per pattern (in group order): walk the group's list, AND tokens 3.., then
 // match / support / cover as posting_scan.
 template <int MODE>
@@ -542,17 +586,7 @@ grouped_scan(const unsigned long long* __restrict__ dense, size_t W, size_t n_ro
                     break;
                 }
             } else {
-                unsigned long long* row = acc + (size_t)w * 64;
-                while (mw) {
-                    const int b = __ffsll((long long)mw) - 1;
-                    mw &= mw - 1;
-                    if (MODE == kMatchChecked) {
-                        const unsigned long long old = atomicAdd(row + b, s);
-                        if (old + s > (unsigned long long)INT64_MAX) ovf = true;
-                    } else {
-                        atomicAdd(row + b, s);
-                    }
-                }
+                warp_scatter_hits<MODE == kMatchChecked>(w, mw, s, acc, ovf);
             }
         }
         if (MODE == kSupport) {

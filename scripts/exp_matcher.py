@@ -16,9 +16,10 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
         a.record(st); r.model.evidence_device(r.test.device_rows(2), n, dA.data_ptr(), dN.data_ptr()); b.record(st)
         torch.cuda.synchronize(); ts.append(a.elapsed_time(b))
     ok = bool((dA.cpu().numpy() == r.A).all() and (dN.cpu().numpy() == r.N).all())
-    print(json.dumps({"env": {k: v for k, v in os.environ.items() if k.startswith("IG_")}, "ms": ts, "same_as_first": ok}))
+    ctx.set_diagnostics(True); r.model.evidence_device(r.test.device_rows(2), n, dA.data_ptr(), dN.data_ptr()); dm = ctx.diag_match()
+    print(json.dumps({"env": {k: v[-30:] for k, v in os.environ.items() if k.startswith("IG_")}, "ms": ts, "diag": dm, "same_as_first": ok}))
     sys.exit(0)
-for env in ({}, {"IG_EXP_NOHITS": "1"}, {"IG_MATCHER": "tiled"}):
+for env in ({}, {"IG_B200_LIB": os.path.join(os.path.dirname(os.path.abspath(__file__)), "libig_b200_nohits.so")}):
     e = dict(os.environ); e.update(env)
     out = subprocess.run([sys.executable, __file__, "child"], env=e, capture_output=True, text=True)
     print(out.stdout.strip() or out.stderr[-2000:], flush=True)
