@@ -28,7 +28,6 @@ namespace igb {
 
 namespace {
 
-constexpr int kTile = 64;
 constexpr int kPairThreads = 256;
 constexpr uint64_t kRepInit = 0ull;  // slot.y = ((u << 32) | v) + 1 once written; all-zero slot = empty
 
@@ -126,30 +125,31 @@ __device__ __forceinline__ void tile_of(uint64_t t, uint32_t& bi, uint32_t& bj) 
 constexpr int kLocalSlots = 4096;
 constexpr int kLocalProbes = 64;
 
+template <int TILE>
 __global__ void __launch_bounds__(kPairThreads)
 pair_enum(const int64_t* __restrict__ X, uint32_t n, int k, int stride, uint64_t n_tiles, Table T,
           uint64_t tile_begin, uint64_t tile_step) {
     extern __shared__ int64_t sm[];
     unsigned long long* local = reinterpret_cast<unsigned long long*>(sm);  // kLocalSlots
     int64_t* sI = sm + kLocalSlots;
-    int64_t* sJ = sI + (size_t)kTile * stride;
+    int64_t* sJ = sI + (size_t)TILE * stride;
     for (uint64_t it = blockIdx.x;; it += gridDim.x) {
         const uint64_t t = tile_begin + it * tile_step;  // this rank's tiles: begin, begin + step, ...
         if (t >= n_tiles) break;
         if (*(volatile int*)T.fail) return;
         uint32_t bi, bj;
         tile_of(t, bi, bj);
-        const uint32_t i0 = bi * kTile, j0 = bj * kTile;
+        const uint32_t i0 = bi * TILE, j0 = bj * TILE;
         __syncthreads();
-        for (int q = threadIdx.x; q < kTile * k; q += kPairThreads) {
+        for (int q = threadIdx.x; q < TILE * k; q += kPairThreads) {
             const int r = q / k, w = q % k;
             sI[r * stride + w] = (i0 + r < n) ? X[(size_t)(i0 + r) * k + w] : 0;
             sJ[r * stride + w] = (j0 + r < n) ? X[(size_t)(j0 + r) * k + w] : 0;
         }
         for (int q = threadIdx.x; q < kLocalSlots; q += kPairThreads) local[q] = 0ull;
         __syncthreads();
-        for (int q = threadIdx.x; q < kTile * kTile; q += kPairThreads) {
-            const int r = q / kTile, c = q % kTile;
+        for (int q = threadIdx.x; q < TILE * TILE; q += kPairThreads) {
+            const int r = q / TILE, c = q % TILE;
             const uint32_t u = i0 + r, v = j0 + c;
             if (u >= n || v >= n || u > v) continue;
             const int64_t* a = sI + r * stride;
@@ -175,8 +175,8 @@ pair_enum(const int64_t* __restrict__ X, uint32_t n, int k, int stride, uint64_t
                 }
                 if ((cur >> 12) != (entry >> 12)) continue;
                 const int q2 = (int)(cur & 0xfffu);
-                const int64_t* a2 = sI + (q2 / kTile) * stride;
-                const int64_t* b2 = sJ + (q2 % kTile) * stride;
+                const int64_t* a2 = sI + (q2 / TILE) * stride;
+                const int64_t* b2 = sJ + (q2 % TILE) * stride;
                 bool same = true;
                 for (int w = 0; w < k && same; ++w) same = ((a2[w] & b2[w]) == (a[w] & b[w]));
                 if (same) {
@@ -407,20 +407,27 @@ uint64_t dedup_pairs(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, const 
     reps_out.alloc(8, ctx.stream);
     if (n == 0) return 0;
     if (n > 0xffffffffull) fail(IG_E_INVALID_ARG, "enumerate: more than 2^32 rows");
-    const uint64_t blocks = (n + kTile - 1) / kTile;
+    const int stride = (int)(k | 1);
+    int tile_rows = 64;
+    while (tile_rows > 16 && (size_t)kLocalSlots * 8 + 2 * (size_t)tile_rows * stride * 8 > 200 * 1024) tile_rows /= 2;
+    const uint64_t blocks = (n + tile_rows - 1) / tile_rows;
     const uint64_t n_tiles = blocks * (blocks + 1) / 2;
     const uint64_t my_tiles = src.list ? 0 : (n_tiles > src.tile_begin ? (n_tiles - src.tile_begin + src.tile_step - 1) / src.tile_step : 0);
     const uint64_t pairs = src.list ? src.n_list : (uint64_t)n * (n - 1) / 2 / src.tile_step;
-    const int stride = (int)(k | 1);
-    const size_t smem = (size_t)kLocalSlots * 8 + 2 * (size_t)kTile * stride * 8;
-    if (smem > 200 * 1024) fail(IG_E_INVALID_ARG, "enumerate: rows wider than the shared-memory tile (K > 200)");
-    IGB_CUDA(cudaFuncSetAttribute(pair_enum, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    // 64-row tiles; narrower tiles for wide rows (CICIDS shape, K up to ~750) so
+    // both row blocks still fit in shared memory
+    const int tile = tile_rows;
+    const size_t smem = (size_t)kLocalSlots * 8 + 2 * (size_t)tile * stride * 8;
+    if (smem > 200 * 1024) fail(IG_E_INVALID_ARG, "enumerate: rows wider than the shared-memory tile (K > 750)");
+    IGB_CUDA(cudaFuncSetAttribute(pair_enum<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    IGB_CUDA(cudaFuncSetAttribute(pair_enum<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    IGB_CUDA(cudaFuncSetAttribute(pair_enum<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
 
     // Initial capacity from a sub-linear guess of the distinct count; doubled
     // (x4) and rerun if the table fills.  Results never depend on capacity.
     uint64_t guess = (uint64_t)(4.0 * std::pow((double)(pairs + n), 0.8)) + 2 * n + 1024;
     uint64_t cap = next_pow2(std::max<uint64_t>(guess, 1u << 16));
-    const uint64_t bound = src.list ? src.n_list : std::min<uint64_t>(my_tiles * (uint64_t)kTile * kTile, pairs * src.tile_step + n);
+    const uint64_t bound = src.list ? src.n_list : std::min<uint64_t>(my_tiles * (uint64_t)tile * tile, pairs * src.tile_step + n);
     const uint64_t max_cap = next_pow2(2 * bound + 1024);
     if (cap > max_cap) cap = max_cap;
     int retries = 0;
@@ -445,9 +452,17 @@ uint64_t dedup_pairs(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, const 
                                src.n_list, T);
             } else if (level == 0) {
                 const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(my_tiles, (uint64_t)ctx.sm_count * 16));
-                if (my_tiles)
-                    IGB_LAUNCH(ctx, pair_enum, grid, kPairThreads, smem, d_rows, (uint32_t)n, (int)k, stride, n_tiles,
-                               T, src.tile_begin, src.tile_step);
+                if (my_tiles) {
+                    if (tile == 64)
+                        IGB_LAUNCH(ctx, pair_enum<64>, grid, kPairThreads, smem, d_rows, (uint32_t)n, (int)k, stride,
+                                   n_tiles, T, src.tile_begin, src.tile_step);
+                    else if (tile == 32)
+                        IGB_LAUNCH(ctx, pair_enum<32>, grid, kPairThreads, smem, d_rows, (uint32_t)n, (int)k, stride,
+                                   n_tiles, T, src.tile_begin, src.tile_step);
+                    else
+                        IGB_LAUNCH(ctx, pair_enum<16>, grid, kPairThreads, smem, d_rows, (uint32_t)n, (int)k, stride,
+                                   n_tiles, T, src.tile_begin, src.tile_step);
+                }
             } else {
                 IGB_LAUNCH(ctx, pair_insert_list, grid_for(ctx, n_pending, 256), 256, 0, d_rows, (int)k,
                            pending.as<uint2>(), n_pending, T);

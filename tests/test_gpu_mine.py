@@ -65,7 +65,7 @@ def test_degenerate_classes(api):
     assert api.enumerate_candidates(api.PackedMatrix(z, L)).patterns.rows == 0
 
 
-@pytest.mark.parametrize("n,L,dens", [(600, 96, 0.6), (2500, 300, 0.93), (1500, 1000, 0.985)])
+@pytest.mark.parametrize("n,L,dens", [(600, 96, 0.6), (2500, 300, 0.93), (1500, 1000, 0.985), (300, 12000, 0.9985), (200, 40000, 0.9996)])
 def test_fit_vs_oracle_random(api, n, L, dens):
     rng = np.random.default_rng(n + L)
     Xa = random_rows(rng, n, L, dens)
