@@ -532,6 +532,55 @@ __device__ __forceinline__ void warp_scatter_hits(uint32_t w, unsigned long long
     }
 }
 
+// Difference-array form of the same scatter (unchecked matcher): each run of
+// consecutive matching rows in a posting word adds +s at its first row and -s
+// after its last row; an inclusive scan over rows afterwards yields the sums.
+// Rows are in canonical order, so matches come in runs (~4 rows per run at C3)
+// and the RED count drops accordingly.  Exact: every partial prefix is a sum of
+// non-negative contributions <= the final value.
+__device__ __forceinline__ void warp_scatter_runs(uint32_t w, unsigned long long mw, long long s,
+                                                  unsigned long long* __restrict__ diff) {
+    const int lane = threadIdx.x & 31;
+    const unsigned long long starts = mw & ~(mw << 1), ends = mw & ~(mw >> 1);
+    const uint32_t s_lo = (uint32_t)starts, s_hi = (uint32_t)(starts >> 32);
+    const uint32_t e_lo = (uint32_t)ends, e_hi = (uint32_t)(ends >> 32);
+    const uint32_t ns = __popc(s_lo) + __popc(s_hi);
+    const uint32_t c = 2 * ns;  // as many ends as starts
+    uint32_t incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const uint32_t excl = incl - c;
+    const uint32_t total = __shfl_sync(kFull, incl, 31);
+    for (uint32_t q0 = 0; q0 < total; q0 += 32) {
+        const uint32_t q = q0 + lane;
+        int L = 0;
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+            const uint32_t e = __shfl_sync(kFull, excl, L + step);
+            if (e <= q) L += step;
+        }
+        uint32_t r = q - __shfl_sync(kFull, excl, L);
+        const uint32_t nsL = __shfl_sync(kFull, ns, L);
+        const bool is_end = r >= nsL;
+        if (is_end) r -= nsL;
+        // every lane takes part in every shuffle; select afterwards
+        const uint32_t xs_lo = __shfl_sync(kFull, s_lo, L), xs_hi = __shfl_sync(kFull, s_hi, L);
+        const uint32_t xe_lo = __shfl_sync(kFull, e_lo, L), xe_hi = __shfl_sync(kFull, e_hi, L);
+        const uint32_t mlo = is_end ? xe_lo : xs_lo;
+        const uint32_t mhi = is_end ? xe_hi : xs_hi;
+        const uint32_t sw = __shfl_sync(kFull, w, L);
+        if (q < total) {
+            const uint32_t plo = __popc(mlo);
+            const uint32_t bit = r < plo ? __fns(mlo, 0, (int)r + 1) : 32u + __fns(mhi, 0, (int)(r - plo) + 1);
+            const size_t row = (size_t)sw * 64 + bit + (is_end ? 1 : 0);
+            atomicAdd(diff + row, (unsigned long long)(is_end ? -s : s));
+        }
+    }
+}
+
 // Warp per pattern (in group order): walk the group's list, AND tokens 3.., then
 // match / support / cover as posting_scan.
 template <int MODE>
@@ -586,7 +635,10 @@ grouped_scan(const unsigned long long* __restrict__ dense, size_t W, size_t n_ro
                     break;
                 }
             } else {
-                warp_scatter_hits<MODE == kMatchChecked>(w, mw, s, acc, ovf);
+                if (MODE == kMatch)
+                    warp_scatter_runs(w, mw, (long long)s, acc);  // acc is a difference array
+                else
+                    warp_scatter_hits<true>(w, mw, s, acc, ovf);
             }
         }
         if (MODE == kSupport) {
@@ -795,23 +847,29 @@ void posting_match(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const in
                    int64_t* d_out, int* d_overflow, bool sum_fits) {
     const size_t n = std::max<size_t>(P.n, 1);
     if (P.group.p == nullptr && P.perm.p == nullptr && P.n_src != P.n) fail(IG_E_CUDA, "posting_match: bad postings");
-    // sum_fits: Σ scores <= INT64_MAX, so no evidence sum can overflow and the
-    // accumulation needs no returned value (fire-and-forget RED).
-    auto run = [&](unsigned long long* acc) {
-        if (sum_fits)
-            launch_scan<kMatch>(ctx, d_pat, np, k, P, d_scores, acc, nullptr, nullptr, d_overflow);
-        else
-            launch_scan<kMatchChecked>(ctx, d_pat, np, k, P, d_scores, acc, nullptr, nullptr, d_overflow);
-    };
+    // sum_fits: Σ scores <= INT64_MAX, so no evidence sum can overflow: run-based
+    // difference array + scan (fire-and-forget REDs).  Otherwise per-match
+    // checked atomics.
+    DevBuf acc((n + 64 + 1) * 8, ctx.stream);
+    IGB_CUDA(cudaMemsetAsync(acc.p, 0, (n + 64 + 1) * 8, ctx.stream));
+    if (sum_fits) {
+        launch_scan<kMatch>(ctx, d_pat, np, k, P, d_scores, acc.as<unsigned long long>(), nullptr, nullptr,
+                            d_overflow);
+        size_t tb = 0;
+        IGB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, acc.as<unsigned long long>(), acc.as<unsigned long long>(),
+                                               (int64_t)n, ctx.stream));
+        DevBuf temp(tb, ctx.stream);
+        IGB_CUDA(cub::DeviceScan::InclusiveSum(temp.p, tb, acc.as<unsigned long long>(), acc.as<unsigned long long>(),
+                                               (int64_t)n, ctx.stream));
+    } else {
+        launch_scan<kMatchChecked>(ctx, d_pat, np, k, P, d_scores, acc.as<unsigned long long>(), nullptr, nullptr,
+                                   d_overflow);
+    }
     if (!P.perm.p) {
-        IGB_CUDA(cudaMemsetAsync(d_out, 0, n * 8, ctx.stream));
-        run(reinterpret_cast<unsigned long long*>(d_out));
+        IGB_CUDA(cudaMemcpyAsync(d_out, acc.p, std::max<size_t>(P.n, 1) * 8, cudaMemcpyDeviceToDevice, ctx.stream));
         return;
     }
-    // accumulate in the postings' (canonical) row order, then scatter back
-    DevBuf acc(n * 8, ctx.stream);
-    IGB_CUDA(cudaMemsetAsync(acc.p, 0, n * 8, ctx.stream));
-    run(acc.as<unsigned long long>());
+    // accumulated in the postings' (canonical) row order: scatter back to source rows
     IGB_LAUNCH(ctx, scatter_u64, grid_for(ctx, P.n_src, 256), 256, 0, acc.as<unsigned long long>(),
                P.perm.as<uint32_t>(), P.group.as<uint32_t>(), P.n_src, d_out);
 }
