@@ -115,9 +115,16 @@ void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m, bool enumerate 
     const size_t k = igb::words_for(L);
     Timer tm(ctx.stream);
     tm.mark();  // 0
-    for (int c = 0; c < 2 && enumerate; ++c) {
+    // canonical order of each class's rows, shared by enumeration (distinct rows)
+    // and the class postings
+    DevBuf perm[2];
+    for (int c = 0; c < 2; ++c) {
         if (X[c].n == 0) fail(IG_E_DATA, "enumerate_candidates: empty class");
-        igb::enumerate_dev(ctx, X[c].p, X[c].n, k, L, m.cand[c].rows, &m.stats[c]);
+        perm[c].alloc(X[c].n * 4, ctx.stream);
+        igb::sort_rows_canonical(ctx, X[c].p, X[c].n, k, perm[c].as<uint32_t>());
+    }
+    for (int c = 0; c < 2 && enumerate; ++c) {
+        igb::enumerate_dev(ctx, X[c].p, X[c].n, k, L, m.cand[c].rows, &m.stats[c], perm[c].as<uint32_t>());
         m.cand[c].pairs = m.stats[c].pairs;
         m.cand[c].ordered = false;
     }
@@ -126,7 +133,8 @@ void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m, bool enumerate 
     const bool vertical = igb::postings_supported(L, std::max(X[0].n, X[1].n));
     igb::Postings PX[2];
     if (vertical)
-        for (int c = 0; c < 2; ++c) igb::build_postings(ctx, X[c].p, X[c].n, k, L, PX[c]);
+        for (int c = 0; c < 2; ++c)
+            igb::build_postings(ctx, X[c].p, X[c].n, k, L, PX[c], true, false, perm[c].as<uint32_t>());
     for (int c = 0; c < 2; ++c) {
         ig_candidates& C = m.cand[c];
         const size_t np = C.rows.n;
@@ -586,6 +594,17 @@ int ig_columns_build(const ig_table* t, const ig_schema* s, int with_labels, ig_
     return guard(nullptr, [&] {
         auto c = std::make_unique<ig_columns>();
         igb::build_columns(*t, *s, with_labels != 0, *c);
+        // Page-lock the typed arrays once so every encode's H2D runs at full PCIe/C2C
+        // speed; best effort (no GPU here -> plain pageable copies).
+        auto pin = [&](void* p, size_t bytes) {
+            if (bytes && cudaHostRegister(p, bytes, cudaHostRegisterDefault) == cudaSuccess)
+                c->pinned.push_back(p);
+            else
+                cudaGetLastError();
+        };
+        pin(c->values.data(), c->values.size() * 8);
+        pin(c->cat.data(), c->cat.size() * 4);
+        pin(c->is_attack.data(), c->is_attack.size());
         *out = c.release();
     });
 }
@@ -596,7 +615,11 @@ size_t ig_columns_rows(const ig_columns* c) { return c ? c->n_rows : 0; }
 size_t ig_columns_bytes(const ig_columns* c) {
     return c ? c->values.size() * 8 + c->cat.size() * 4 + c->is_attack.size() : 0;
 }
-void ig_columns_free(ig_columns* c) { delete c; }
+void ig_columns_free(ig_columns* c) {
+    if (!c) return;
+    for (void* p : c->pinned) cudaHostUnregister(p);
+    delete c;
+}
 
 int ig_encode_training(ig_ctx* ctx, const ig_columns* cols, ig_encoding** out) {
     *out = nullptr;

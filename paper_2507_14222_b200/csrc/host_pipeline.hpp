@@ -56,6 +56,7 @@ struct ig_columns {
     // owned with a cudaFree deleter; null until uploaded.
     std::shared_ptr<void> d_values, d_cat, d_attack;
     int device = -1;
+    std::vector<void*> pinned;  // arrays page-locked with cudaHostRegister (ig_columns_build)
 };
 
 namespace igb {

@@ -379,9 +379,9 @@ void canonical_order(Ctx& ctx, DevRows& rows, DevBuf* a, DevBuf* b) {
 // (canonical order, which also groups similar rows into the same tiles) equals
 // B^c over all rows with up to quadratically fewer pairs.
 void enumerate_dev(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, uint32_t L, DevRows& out,
-                   EnumStats* stats) {
+                   EnumStats* stats, const uint32_t* d_perm) {
     DevBuf U;
-    const size_t m = distinct_rows(ctx, d_rows, n, k, U);
+    const size_t m = distinct_rows(ctx, d_rows, n, k, U, d_perm);
     PairSource src;  // every tile of the triangle
     DevBuf reps;
     const uint64_t c = dedup_pairs(ctx, U.as<int64_t>(), m, k, src, reps, stats);

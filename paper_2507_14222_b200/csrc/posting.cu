@@ -176,6 +176,7 @@ __global__ void pattern_token_fill(const int64_t* __restrict__ pat, size_t np, i
 // its inverse, re-indexing a pattern's bits by rank and reading them back in
 // bit order lists its tokens rarest first with no per-pattern sort: O(|b| + K).
 constexpr int kRankWords = 64;
+template <int KW>
 __global__ void pattern_token_fill_rank(const int64_t* __restrict__ pat, size_t np, int k,
                                         const uint16_t* __restrict__ grank, const uint16_t* __restrict__ gbyrank,
                                         uint32_t L, const uint32_t* __restrict__ off, uint16_t* __restrict__ toks) {
@@ -188,19 +189,24 @@ __global__ void pattern_token_fill_rank(const int64_t* __restrict__ pat, size_t 
     }
     __syncthreads();
     for (size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += (size_t)gridDim.x * blockDim.x) {
-        uint64_t rb[kRankWords];
-        for (int w = 0; w < k; ++w) rb[w] = 0;
+        uint64_t rb[KW];  // rank-space bitmap, kept in registers (static indices only)
+#pragma unroll
+        for (int q = 0; q < KW; ++q) rb[q] = 0;
         for (int w = 0; w < k; ++w) {
             uint64_t x = (uint64_t)pat[p * k + w];
             while (x) {
                 const int b = __ffsll((long long)x) - 1;
                 x &= x - 1;
                 const uint32_t r = rank[w * 64 + b];
-                rb[r >> 6] |= 1ull << (r & 63);
+                const uint64_t bit = 1ull << (r & 63);
+                const uint32_t rq = r >> 6;
+#pragma unroll
+                for (int q = 0; q < KW; ++q) rb[q] |= (rq == (uint32_t)q) ? bit : 0ull;
             }
         }
         uint32_t o = off[p];
-        for (int q = 0; q < k; ++q) {
+#pragma unroll
+        for (int q = 0; q < KW; ++q) {
             uint64_t y = rb[q];
             while (y) {
                 const int b = __ffsll((long long)y) - 1;
@@ -383,10 +389,21 @@ void pattern_tokens(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const P
                                                  tok.as<uint16_t>(), byrank.as<uint16_t>(), (int64_t)L, 0, 64, ctx.stream));
         IGB_LAUNCH(ctx, invert_rank, grid_for(ctx, L, 256), 256, 0, byrank.as<uint16_t>(), L, rank.as<uint16_t>());
         const size_t smem = (size_t)L * 4;
-        if (smem > 48 * 1024)
-            IGB_CUDA(cudaFuncSetAttribute(pattern_token_fill_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        IGB_LAUNCH(ctx, pattern_token_fill_rank, grid_for(ctx, np, 128), 128, smem, d_pat, np, (int)k,
-                   rank.as<uint16_t>(), byrank.as<uint16_t>(), L, T.off.as<uint32_t>(), T.toks.as<uint16_t>());
+#define IGB_FILL_RANK(KW)                                                                                          \
+    {                                                                                                              \
+        if (smem > 48 * 1024)                                                                                      \
+            IGB_CUDA(cudaFuncSetAttribute(pattern_token_fill_rank<KW>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                          (int)smem));                                                             \
+        IGB_LAUNCH(ctx, pattern_token_fill_rank<KW>, grid_for(ctx, np, 128), 128, smem, d_pat, np, (int)k,         \
+                   rank.as<uint16_t>(), byrank.as<uint16_t>(), L, T.off.as<uint32_t>(), T.toks.as<uint16_t>());   \
+    }
+        if (k <= 16)
+            IGB_FILL_RANK(16)
+        else if (k <= 32)
+            IGB_FILL_RANK(32)
+        else
+            IGB_FILL_RANK(64)
+#undef IGB_FILL_RANK
         return;
     }
     const size_t smem = (size_t)P.L * 4;
@@ -765,7 +782,7 @@ void launch_scan(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Post
 bool postings_supported(uint32_t L, size_t n) { return words_for(L) * 64 < 65535 && n < 0xffffffffull; }
 
 void build_postings(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, uint32_t /*logical_len*/, Postings& P,
-                    bool canonical, bool distinct) {
+                    bool canonical, bool distinct, const uint32_t* d_perm) {
     const uint32_t L = (uint32_t)(64 * k);  // every bit position, padding included
     P.L = L;
     P.n_src = n;
@@ -774,7 +791,10 @@ void build_postings(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, uint32_
     P.rep.release();
     if ((canonical || distinct) && n > 1) {
         P.perm.alloc(n * 4, ctx.stream);
-        sort_rows_canonical(ctx, d_rows, n, k, P.perm.as<uint32_t>());
+        if (d_perm)
+            IGB_CUDA(cudaMemcpyAsync(P.perm.p, d_perm, n * 4, cudaMemcpyDeviceToDevice, ctx.stream));
+        else
+            sort_rows_canonical(ctx, d_rows, n, k, P.perm.as<uint32_t>());
     }
     size_t nd = n;
     const uint32_t* rows_of = P.perm.as<uint32_t>();  // posting row -> source row

@@ -27,7 +27,7 @@ bool postings_supported(uint32_t L, size_t n);
 // distinct: one posting row per distinct row (for coverage / evidence, where
 // multiplicity does not matter or is restored by `group`); never for support.
 void build_postings(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, uint32_t L, Postings& P,
-                    bool canonical = true, bool distinct = false);
+                    bool canonical = true, bool distinct = false, const uint32_t* d_perm = nullptr);
 void posting_support(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Postings& P, int64_t* d_support);
 void posting_cover(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Postings& P, uint8_t* d_mask);
 // d_out[source row] (P.n int64) is zeroed and accumulated; requires all scores >= 0.

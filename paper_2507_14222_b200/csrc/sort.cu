@@ -291,13 +291,16 @@ void sort_rows_canonical(Ctx& ctx, const int64_t* d_words, size_t n, size_t k, u
     if (cur != d_perm) IGB_CUDA(cudaMemcpyAsync(d_perm, cur, n * 4, cudaMemcpyDeviceToDevice, ctx.stream));
 }
 
-size_t distinct_rows(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, DevBuf& out) {
+size_t distinct_rows(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, DevBuf& out, const uint32_t* d_perm) {
     if (n == 0) {
         out.alloc(8, ctx.stream);
         return 0;
     }
     DevBuf perm(n * 4, ctx.stream), head(n, ctx.stream), rep(n * 4, ctx.stream), nsel(8, ctx.stream);
-    sort_rows_canonical(ctx, d_rows, n, k, perm.as<uint32_t>());
+    if (d_perm)
+        IGB_CUDA(cudaMemcpyAsync(perm.p, d_perm, n * 4, cudaMemcpyDeviceToDevice, ctx.stream));
+    else
+        sort_rows_canonical(ctx, d_rows, n, k, perm.as<uint32_t>());
     IGB_LAUNCH(ctx, row_heads_k, grid_for(ctx, n, 256), 256, 0, d_rows, perm.as<uint32_t>(), n, (int)k,
                head.as<uint8_t>());
     size_t tb = 0;

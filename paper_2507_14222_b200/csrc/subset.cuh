@@ -35,7 +35,7 @@ struct EnumStats {
     uint64_t collisions = 0;  // inserts that met an equal fingerprint of different content
 };
 void enumerate_dev(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, uint32_t L, DevRows& out,
-                   EnumStats* stats);
+                   EnumStats* stats, const uint32_t* d_perm = nullptr);
 
 // Which pairs of the (distinct, canonical) rows to insert: the tiles
 // tile_begin, tile_begin + tile_step, ... of the u <= v triangle, or an explicit
