@@ -8,7 +8,9 @@
 #include <chrono>
 #include <cstring>
 #include <memory>
+#include <exception>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "encode.cuh"
@@ -105,85 +107,140 @@ struct Timer {
     }
 };
 
+// Run fn(ctx, cls) for the two classes concurrently: class 0 on the calling
+// thread and the context stream, class 1 on a second host thread and the
+// context's auxiliary stream (ordered after everything already queued on the
+// main stream; the main stream waits for it afterwards).  The classes are
+// independent within each phase, so their host-side syncs overlap with the
+// other class's kernels.
+constexpr size_t kConcurrentRows = 40000;        // training rows (C3: 14,851; C4: 118,813)
+constexpr size_t kConcurrentPatterns = 8u << 20; // pure patterns (C3: 2.2 M; C4: 32 M)
+
+template <class F>
+void for_both_classes(igb::Ctx& ctx, F&& fn, bool concurrent = true) {
+    if (!concurrent) {
+        fn(ctx, 0);
+        fn(ctx, 1);
+        return;
+    }
+    cudaEvent_t fork, join;
+    IGB_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    IGB_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+    IGB_CUDA(cudaEventRecord(fork, ctx.stream));
+    IGB_CUDA(cudaStreamWaitEvent(ctx.aux, fork, 0));
+    igb::Ctx c1 = ctx;
+    c1.stream = ctx.aux;
+    c1.launches = 0;
+    c1.diag_match_ms = 0;
+    c1.diag_match_words = 0;
+    c1.diag_match_launches = 0;
+    std::exception_ptr e0, e1;
+    std::thread th([&] {
+        try {
+            IGB_CUDA(cudaSetDevice(ctx.device));
+            fn(c1, 1);
+        } catch (...) {
+            e1 = std::current_exception();
+        }
+    });
+    try {
+        fn(ctx, 0);
+    } catch (...) {
+        e0 = std::current_exception();
+    }
+    th.join();
+    cudaEventRecord(join, c1.stream);
+    cudaStreamWaitEvent(ctx.stream, join, 0);
+    cudaEventDestroy(fork);
+    cudaEventDestroy(join);
+    ctx.launches += c1.launches;
+    ctx.diag_match_ms += c1.diag_match_ms;
+    ctx.diag_match_words += c1.diag_match_words;
+    ctx.diag_match_launches += c1.diag_match_launches;
+    if (e0) std::rethrow_exception(e0);
+    if (e1) std::rethrow_exception(e1);
+}
+
 // The mining half of cmd_train: for both classes enumerate →
-// support → score → total; canonical order; reject_covered against
-// the opposite class.
+// support → score → total, reject_covered against the opposite
+// class, canonical order.
 // enumerate = false: m.cand[c].rows already hold the candidates (multi-GPU
 // owner shard); only support -> score -> purify -> order run.
 void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m, bool enumerate = true) {
     m.L = L;
     const size_t k = igb::words_for(L);
+    for (int c = 0; c < 2; ++c)
+        if (X[c].n == 0) fail(IG_E_DATA, "enumerate_candidates: empty class");
     Timer tm(ctx.stream);
     tm.mark();  // 0
-    // canonical order of each class's rows, shared by enumeration (distinct rows)
-    // and the class postings
-    DevBuf perm[2];
-    for (int c = 0; c < 2; ++c) {
-        if (X[c].n == 0) fail(IG_E_DATA, "enumerate_candidates: empty class");
-        perm[c].alloc(X[c].n * 4, ctx.stream);
-        igb::sort_rows_canonical(ctx, X[c].p, X[c].n, k, perm[c].as<uint32_t>());
-    }
-    for (int c = 0; c < 2 && enumerate; ++c) {
-        igb::enumerate_dev(ctx, X[c].p, X[c].n, k, L, m.cand[c].rows, &m.stats[c], perm[c].as<uint32_t>());
-        m.cand[c].pairs = m.stats[c].pairs;
-        m.cand[c].ordered = false;
-    }
-    tm.mark();  // 1
-    // Row postings of each class, shared by support (own class) and coverage (opposite class).
     const bool vertical = igb::postings_supported(L, std::max(X[0].n, X[1].n));
+    // Small fits are launch/sync bound: overlap the classes.  Large ones fill the
+    // GPU with each class alone, and concurrent multi-GB allocations on two
+    // streams only fragment the memory pool, so they run one after the other.
+    const bool concurrent = X[0].n + X[1].n <= kConcurrentRows;
+    DevBuf perm[2];
     igb::Postings PX[2];
-    if (vertical)
-        for (int c = 0; c < 2; ++c)
-            igb::build_postings(ctx, X[c].p, X[c].n, k, L, PX[c], true, false, perm[c].as<uint32_t>());
-    for (int c = 0; c < 2; ++c) {
+    // phase A (per class): canonical row order (shared by enumeration and the
+    // postings), candidates, postings, support, score, checked total
+    for_both_classes(ctx, [&](igb::Ctx& cx, int c) {
+        perm[c].alloc(X[c].n * 4, cx.stream);
+        igb::sort_rows_canonical(cx, X[c].p, X[c].n, k, perm[c].as<uint32_t>());
+        if (enumerate) {
+            igb::enumerate_dev(cx, X[c].p, X[c].n, k, L, m.cand[c].rows, &m.stats[c], perm[c].as<uint32_t>());
+            m.cand[c].pairs = m.stats[c].pairs;
+            m.cand[c].ordered = false;
+        }
+        if (vertical) igb::build_postings(cx, X[c].p, X[c].n, k, L, PX[c], true, false, perm[c].as<uint32_t>());
         ig_candidates& C = m.cand[c];
         const size_t np = C.rows.n;
-        C.support.alloc(std::max<size_t>(np, 1) * 8, ctx.stream);
-        C.score.alloc(std::max<size_t>(np, 1) * 8, ctx.stream);
+        C.support.alloc(std::max<size_t>(np, 1) * 8, cx.stream);
+        C.score.alloc(std::max<size_t>(np, 1) * 8, cx.stream);
         if (vertical)
-            igb::posting_support(ctx, C.rows.data(), np, k, PX[c], C.support.as<int64_t>());
+            igb::posting_support(cx, C.rows.data(), np, k, PX[c], C.support.as<int64_t>());
         else
-            igb::count_support_dev(ctx, C.rows.data(), np, X[c].p, X[c].n, k, C.support.as<int64_t>());
-        if (igb::score_dev(ctx, C.rows.data(), np, k, C.support.as<int64_t>(), C.score.as<int64_t>()) != IG_OK)
+            igb::count_support_dev(cx, C.rows.data(), np, X[c].p, X[c].n, k, C.support.as<int64_t>());
+        if (igb::score_dev(cx, C.rows.data(), np, k, C.support.as<int64_t>(), C.score.as<int64_t>()) != IG_OK)
             fail(IG_E_OVERFLOW, "pattern score overflows int64");
         int64_t total = 0;
-        if (igb::total_score_dev(ctx, C.score.as<int64_t>(), np, &total) != IG_OK)
+        if (igb::total_score_dev(cx, C.score.as<int64_t>(), np, &total) != IG_OK)
             fail(IG_E_OVERFLOW, "total score overflows int64");
         m.partial_total[c] = (uint64_t)total;
         C.has_support = C.has_score = true;
-    }
-    tm.mark();  // 2
-    for (int c = 0; c < 2; ++c) {
+    }, concurrent);
+    tm.mark();  // 1
+    // phase B (per class): reject_covered against the other class's postings,
+    // compaction, canonical order of the pure dictionary (the model output; the
+    // candidate sets B^c are ordered on first copy-out)
+    for_both_classes(ctx, [&](igb::Ctx& cx, int c) {
         ig_candidates& C = m.cand[c];
         const size_t np = C.rows.n;
-        DevBuf mask(std::max<size_t>(np, 1), ctx.stream);
+        DevBuf mask(std::max<size_t>(np, 1), cx.stream);
         if (vertical && X[1 - c].n > 0)
-            igb::posting_cover(ctx, C.rows.data(), np, k, PX[1 - c], mask.as<uint8_t>());
+            igb::posting_cover(cx, C.rows.data(), np, k, PX[1 - c], mask.as<uint8_t>());
         else
-            igb::coverage_any_dev(ctx, C.rows.data(), np, X[1 - c].p, X[1 - c].n, k, mask.as<uint8_t>());
+            igb::coverage_any_dev(cx, C.rows.data(), np, X[1 - c].p, X[1 - c].n, k, mask.as<uint8_t>());
         ig_candidates& P = m.pure[c];
         P.rows.k = k;
         P.rows.L = L;
-        P.rows.buf.alloc(std::max<size_t>(np * k, 1) * 8, ctx.stream);
-        P.support.alloc(std::max<size_t>(np, 1) * 8, ctx.stream);
-        P.score.alloc(std::max<size_t>(np, 1) * 8, ctx.stream);
-        P.rows.n = igb::compact_unflagged(ctx, C.rows.data(), C.support.as<int64_t>(), C.score.as<int64_t>(),
+        P.rows.buf.alloc(std::max<size_t>(np * k, 1) * 8, cx.stream);
+        P.support.alloc(std::max<size_t>(np, 1) * 8, cx.stream);
+        P.score.alloc(std::max<size_t>(np, 1) * 8, cx.stream);
+        P.rows.n = igb::compact_unflagged(cx, C.rows.data(), C.support.as<int64_t>(), C.score.as<int64_t>(),
                                           mask.as<uint8_t>(), np, k, P.rows.data(), P.support.as<int64_t>(),
                                           P.score.as<int64_t>());
         P.has_support = P.has_score = true;
-    }
-    tm.mark();  // 3
-    // Canonical order of the pure dictionaries (the model output).  The full
-    // candidate sets B^c are ordered on first copy-out (ig_model_copy which=0).
-    for (int c = 0; c < 2; ++c) igb::canonical_order(ctx, m.pure[c].rows, &m.pure[c].support, &m.pure[c].score);
-    tm.mark();  // 4
+        igb::canonical_order(cx, P.rows, &P.support, &P.score);
+        IGB_CUDA(cudaStreamSynchronize(cx.stream));
+    }, concurrent);
+    tm.mark();  // 2
     IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+    IGB_CUDA(cudaStreamSynchronize(ctx.aux));
     m.ms[0] = 0;
-    m.ms[1] = tm.ms(0, 1);
-    m.ms[2] = tm.ms(1, 2);
-    m.ms[3] = tm.ms(2, 3);
-    m.ms[4] = tm.ms(3, 4);
-    m.ms[5] = tm.ms(0, 4);
+    m.ms[1] = tm.ms(0, 1);  // enumerate + support + score (both classes, concurrent)
+    m.ms[2] = 0;
+    m.ms[3] = tm.ms(1, 2);  // purify + order
+    m.ms[4] = 0;
+    m.ms[5] = tm.ms(0, 2);
     for (int c = 0; c < 2; ++c) {
         for (ig_candidates* C : {&m.cand[c], &m.pure[c]}) {
             C->rows.buf.persist();
@@ -226,12 +283,12 @@ void evidence_impl(igb::Ctx& ctx, const ig_model& m, const int64_t* d_tests, siz
         igb::build_postings(ctx, d_tests, nt, k, L, PT, true, true);
         DevBuf flag(sizeof(int), ctx.stream);
         IGB_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), ctx.stream));
-        for (int c = 0; c < 2; ++c) {
+        for_both_classes(ctx, [&](igb::Ctx& cx, int c) {
             const ig_candidates& P = m.pure[c];
             // the fit checked Σ candidate scores <= INT64_MAX (total_score); pure ⊆ candidates
-            igb::posting_match(ctx, P.rows.data(), P.rows.n, k, P.score.as<int64_t>(), PT, c == 0 ? d_A : d_N,
+            igb::posting_match(cx, P.rows.data(), P.rows.n, k, P.score.as<int64_t>(), PT, c == 0 ? d_A : d_N,
                                flag.as<int>(), true);
-        }
+        }, m.pure[0].rows.n + m.pure[1].rows.n <= kConcurrentPatterns);
         int h = 0;
         IGB_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
         IGB_CUDA(cudaStreamSynchronize(ctx.stream));
@@ -267,6 +324,7 @@ int ig_ctx_create(int device, ig_ctx** out) {
     c->device = device;
     int st = guard(c.get(), [&] {
         IGB_CUDA(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
+        IGB_CUDA(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
         c->stream = c->own;
         cudaDeviceProp prop;
         IGB_CUDA(cudaGetDeviceProperties(&prop, device));
@@ -289,9 +347,10 @@ int ig_ctx_create(int device, ig_ctx** out) {
 void ig_ctx_destroy(ig_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
-    if (ctx->own) {
-        cudaStreamSynchronize(ctx->own);
-        cudaStreamDestroy(ctx->own);
+    for (cudaStream_t st : {ctx->own, ctx->aux}) {
+        if (!st) continue;
+        cudaStreamSynchronize(st);
+        cudaStreamDestroy(st);
     }
     delete ctx;
 }

@@ -86,6 +86,7 @@ struct Ctx {
     int device = 0;
     cudaStream_t own = nullptr;
     cudaStream_t stream = nullptr;
+    cudaStream_t aux = nullptr;  // second class's stream (for_both_classes)
     std::string err;
     uint64_t launches = 0;
     int sm_count = 148;
