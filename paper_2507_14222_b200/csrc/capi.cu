@@ -214,11 +214,13 @@ void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m, bool enumerate 
     for_both_classes(ctx, [&](igb::Ctx& cx, int c) {
         ig_candidates& C = m.cand[c];
         const size_t np = C.rows.n;
+        igb::Trace tr(cx, "purify", c);
         DevBuf mask(std::max<size_t>(np, 1), cx.stream);
         if (vertical && X[1 - c].n > 0)
             igb::posting_cover(cx, C.rows.data(), np, k, PX[1 - c], mask.as<uint8_t>());
         else
             igb::coverage_any_dev(cx, C.rows.data(), np, X[1 - c].p, X[1 - c].n, k, mask.as<uint8_t>());
+        tr.mark("cover");
         ig_candidates& P = m.pure[c];
         P.rows.k = k;
         P.rows.L = L;
@@ -229,8 +231,10 @@ void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m, bool enumerate 
                                           mask.as<uint8_t>(), np, k, P.rows.data(), P.support.as<int64_t>(),
                                           P.score.as<int64_t>());
         P.has_support = P.has_score = true;
+        tr.mark("compact");
         igb::canonical_order(cx, P.rows, &P.support, &P.score);
         IGB_CUDA(cudaStreamSynchronize(cx.stream));
+        tr.mark("order");
     }, concurrent);
     tm.mark();  // 2
     IGB_CUDA(cudaStreamSynchronize(ctx.stream));

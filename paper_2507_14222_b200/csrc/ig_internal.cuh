@@ -5,6 +5,8 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
+#include <ctime>
 #include <string>
 #include <utility>
 #include <vector>
@@ -96,6 +98,34 @@ struct Ctx {
     double diag_match_ms = 0;      // CUDA-event time of the matcher kernels
     uint64_t diag_match_words = 0; // posting word-ANDs of the matcher (Σ_p |b_p| * nnz(rarest token))
     uint64_t diag_match_launches = 0;
+};
+
+// IG_TRACE=1: per-operation wall times on stderr (synchronises the stream at
+// every mark; diagnostics only).
+struct Trace {
+    const Ctx& ctx;
+    const char* what;
+    int cls;
+    bool on;
+    double t0;
+    static double now() {
+        timespec ts;
+        clock_gettime(CLOCK_MONOTONIC, &ts);
+        return ts.tv_sec + ts.tv_nsec * 1e-9;
+    }
+    Trace(const Ctx& c, const char* w, int cl) : ctx(c), what(w), cls(cl), on(getenv("IG_TRACE") != nullptr), t0(0) {
+        if (on) {
+            cudaStreamSynchronize(ctx.stream);
+            t0 = now();
+        }
+    }
+    void mark(const char* step) {
+        if (!on) return;
+        cudaStreamSynchronize(ctx.stream);
+        const double t = now();
+        fprintf(stderr, "[ig trace] %s class %d %s %.3f ms\n", what, cls, step, (t - t0) * 1e3);
+        t0 = t;
+    }
 };
 
 inline size_t words_for(uint32_t L) { return (static_cast<size_t>(L) + 63) / 64; }
