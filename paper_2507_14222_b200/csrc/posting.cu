@@ -189,24 +189,19 @@ __global__ void pattern_token_fill_rank(const int64_t* __restrict__ pat, size_t 
     }
     __syncthreads();
     for (size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += (size_t)gridDim.x * blockDim.x) {
-        uint64_t rb[KW];  // rank-space bitmap, kept in registers (static indices only)
-#pragma unroll
-        for (int q = 0; q < KW; ++q) rb[q] = 0;
+        uint64_t rb[KW];  // rank-space bitmap (local memory: dynamic indices)
+        for (int q = 0; q < k; ++q) rb[q] = 0;
         for (int w = 0; w < k; ++w) {
             uint64_t x = (uint64_t)pat[p * k + w];
             while (x) {
                 const int b = __ffsll((long long)x) - 1;
                 x &= x - 1;
                 const uint32_t r = rank[w * 64 + b];
-                const uint64_t bit = 1ull << (r & 63);
-                const uint32_t rq = r >> 6;
-#pragma unroll
-                for (int q = 0; q < KW; ++q) rb[q] |= (rq == (uint32_t)q) ? bit : 0ull;
+                rb[r >> 6] |= 1ull << (r & 63);
             }
         }
         uint32_t o = off[p];
-#pragma unroll
-        for (int q = 0; q < KW; ++q) {
+        for (int q = 0; q < k; ++q) {
             uint64_t y = rb[q];
             while (y) {
                 const int b = __ffsll((long long)y) - 1;
@@ -630,19 +625,25 @@ grouped_scan(const unsigned long long* __restrict__ dense, size_t W, size_t n_ro
             const uint32_t w = j < len ? ew[base + j] : 0u;
             unsigned long long mw = j < len ? em[base + j] : 0ull;
             const unsigned long long* col = dense + w;
-            for (uint32_t t = 2; t < m; t += 4) {
+            // tokens 2..31 come from the lanes' registers (no branch per token);
+            // the rare tail past 32 tokens is read from memory
+            const uint32_t m32 = min(m, 32u);
+            for (uint32_t t = 2; t < m32; t += 4) {
                 if (!__any_sync(kFull, mw != 0ull)) break;
-                uint32_t tk[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const uint32_t ii = min(t + u, m - 1);
-                    tk[u] = ii < 32 ? __shfl_sync(kFull, tl, ii) : (uint32_t)toks[o + ii];
-                }
+                const uint32_t t0 = __shfl_sync(kFull, tl, t);
+                const uint32_t t1 = __shfl_sync(kFull, tl, min(t + 1, m32 - 1));
+                const uint32_t t2 = __shfl_sync(kFull, tl, min(t + 2, m32 - 1));
+                const uint32_t t3 = __shfl_sync(kFull, tl, min(t + 3, m32 - 1));
                 if (mw) {
-                    const unsigned long long a = col[tk[0] * Wu], b = col[tk[1] * Wu];
-                    const unsigned long long c = col[tk[2] * Wu], d = col[tk[3] * Wu];
+                    const unsigned long long a = col[t0 * Wu], b = col[t1 * Wu];
+                    const unsigned long long c = col[t2 * Wu], d = col[t3 * Wu];
                     mw &= (a & b) & (c & d);
                 }
+            }
+            for (uint32_t t = 32; t < m; ++t) {
+                if (!__any_sync(kFull, mw != 0ull)) break;
+                const uint32_t tt = toks[o + t];
+                if (mw) mw &= col[tt * Wu];
             }
             if (MODE == kSupport) {
                 cnt += __popcll(mw);
@@ -652,10 +653,12 @@ grouped_scan(const unsigned long long* __restrict__ dense, size_t W, size_t n_ro
                     break;
                 }
             } else {
-                if (MODE == kMatch)
-                    warp_scatter_runs(w, mw, (long long)s, acc);  // acc is a difference array
-                else
-                    warp_scatter_hits<true>(w, mw, s, acc, ovf);
+                if (__any_sync(kFull, mw != 0ull)) {
+                    if (MODE == kMatch)
+                        warp_scatter_runs(w, mw, (long long)s, acc);  // acc is a difference array
+                    else
+                        warp_scatter_hits<true>(w, mw, s, acc, ovf);
+                }
             }
         }
         if (MODE == kSupport) {
