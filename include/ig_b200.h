@@ -207,6 +207,26 @@ int ig_fit_encoded(ig_ctx* ctx, const ig_encoding* train, const ig_kernel_config
 int ig_evidence_encoded(ig_ctx* ctx, const ig_model* m, const ig_encoding* tests, int64_t* A,
                         int64_t* N);
 
+/* ---------------------------------------------------------------- archive / explain
+ * SURVEY.md §8(f) ranks 1-2.  ModelArchive: schema
+ * text with exact hex-float statistics + vocabulary in bit order + the pure
+ * dictionaries; an encoding rebuilt from (schema, vocabulary) tokenises test
+ * rows exactly like the training encoding.                                  */
+/* *len = text size; copies min(cap-1, len) bytes + NUL when buf is given. */
+int ig_schema_to_text(const ig_schema* s, char* buf, size_t cap, size_t* len);
+int ig_schema_from_text(const char* text, ig_schema** out);
+/* vocab: '\n'-terminated tokens in bit order (ig_encoding_vocabulary). */
+int ig_encoding_from_vocabulary(const ig_schema* s, const char* vocab, ig_encoding** out);
+/* Pure dictionaries (canonical order) -> model usable by ig_evidence* / ig_explain. */
+int ig_model_from_dictionaries(ig_ctx* ctx, uint32_t logical_len, const int64_t* words_attack,
+                               const int64_t* supports_attack, const int64_t* scores_attack, size_t n_attack,
+                               const int64_t* words_normal, const int64_t* supports_normal,
+                               const int64_t* scores_normal, size_t n_normal, ig_model** out);
+/* explain: indices into P^cls (ascending) of the patterns
+ * contained in one test row; *n_found may exceed cap (call again larger). */
+int ig_explain(ig_ctx* ctx, const ig_model* m, int cls, const int64_t* row, uint32_t logical_len, uint32_t* idx,
+               size_t cap, size_t* n_found);
+
 /* ---------------------------------------------------------------- multi-GPU
  * SURVEY.md §8(e).  One shard per rank (one process per GPU); training rows
  * are replicated (every rank runs ig_encode_training on the same columns).

@@ -97,6 +97,11 @@ SIGNATURES = [
     ("ig_encoding_removed_rows", C.c_int, [vp, pu64]),
     ("ig_encoding_free", None, [vp]),
     ("ig_fit_encoded", C.c_int, [vp, vp, C.POINTER(KernelConfigC), C.POINTER(vp)]),
+    ("ig_schema_to_text", C.c_int, [vp, C.c_char_p, sz, C.POINTER(sz)]),
+    ("ig_schema_from_text", C.c_int, [C.c_char_p, C.POINTER(vp)]),
+    ("ig_encoding_from_vocabulary", C.c_int, [vp, C.c_char_p, C.POINTER(vp)]),
+    ("ig_model_from_dictionaries", C.c_int, [vp, u32, p64, p64, p64, sz, p64, p64, p64, sz, C.POINTER(vp)]),
+    ("ig_explain", C.c_int, [vp, vp, C.c_int, p64, u32, C.POINTER(C.c_uint32), sz, C.POINTER(sz)]),
     ("ig_shard_create", C.c_int, [vp, vp, C.c_int, C.c_int, C.POINTER(KernelConfigC), C.POINTER(vp)]),
     ("ig_shard_enumerate", C.c_int, [vp, vp, C.c_int, pu64, C.POINTER(vp)]),
     ("ig_shard_receive", C.c_int, [vp, vp, C.c_int, vp, C.c_uint64]),

@@ -618,3 +618,164 @@ def train_and_score(csv: bytes, label_column: str = "label", decimals: int = 1, 
     tenc = encode_rows(Columns(te, schema, False), enc, ctx)
     A, Nv = model.evidence_encoded(tenc)
     return RunResult(model, enc, tenc, A, Nv)
+
+
+# ---------------------------------------------------------------- archive / explain
+ARCHIVE_MAGIC = "ig-b200-archive 1"
+
+
+def _esc(s: str) -> str:
+    out = []
+    for ch in s:
+        o = ord(ch)
+        out.append(f"\\x{o:02x}" if ch == "\\" or o < 0x20 else ch)
+    return "".join(out)
+
+
+def _unesc(s: str) -> str:
+    out, i = [], 0
+    while i < len(s):
+        if s[i] == "\\" and s[i + 1:i + 2] == "x":
+            out.append(chr(int(s[i + 2:i + 4], 16)))
+            i += 4
+        else:
+            out.append(s[i])
+            i += 1
+    return "".join(out)
+
+
+def schema_to_text(schema: Schema) -> str:
+    n = C.c_size_t()
+    st = lib.ig_schema_to_text(schema.handle, None, 0, C.byref(n))
+    if st:
+        _raise(st)
+    buf = C.create_string_buffer(n.value + 1)
+    lib.ig_schema_to_text(schema.handle, buf, n.value + 1, C.byref(n))
+    return buf.raw[:n.value].decode("utf-8", errors="surrogateescape")
+
+
+def schema_from_text(text: str) -> Schema:
+    h = C.c_void_p()
+    st = lib.ig_schema_from_text(text.encode("utf-8", errors="surrogateescape"), C.byref(h))
+    if st:
+        _raise(st)
+    ncols = int(text.split("columns ", 1)[1].split("\n", 1)[0])
+    return Schema(h, ncols)
+
+
+def encoding_from_vocabulary(schema: Schema, vocabulary: list[str], ctx: Optional[Context] = None) -> Encoding:
+    """The vocabulary lookup of a training encoding, rebuilt for test-time encode_rows."""
+    ctx = ctx or default_context()
+    blob = "".join(t + "\n" for t in vocabulary).encode("utf-8", errors="surrogateescape")
+    h = C.c_void_p()
+    st = lib.ig_encoding_from_vocabulary(schema.handle, blob, C.byref(h))
+    if st:
+        _raise(st)
+    return Encoding(ctx, h)
+
+
+def model_from_dictionaries(L: int, attack: Dictionary, normal: Dictionary, ctx: Optional[Context] = None) -> Model:
+    ctx = ctx or default_context()
+    arrs = []
+    for d in (attack, normal):
+        w = _words(d.words, L)
+        s = np.ascontiguousarray(d.supports, np.int64)
+        sc = np.ascontiguousarray(d.scores, np.int64)
+        arrs.append((w, s, sc))
+    h = C.c_void_p()
+    (wa, sa, ca), (wn, sn, cn) = arrs
+    ctx.check(lib.ig_model_from_dictionaries(ctx.handle, L, _p64(wa), _p64(sa), _p64(ca), wa.shape[0], _p64(wn),
+                                             _p64(sn), _p64(cn), wn.shape[0], C.byref(h)))
+    m = Model(ctx, h)
+    m._keep = arrs
+    return m
+
+
+def explain(model: Model, row, cls: int) -> np.ndarray:
+    """indices (ascending, into the pure dictionary of `cls`) of
+    the patterns contained in one packed test row."""
+    r = np.ascontiguousarray(row, np.int64).reshape(-1)
+    cap = 1024
+    while True:
+        idx = np.zeros(cap, np.uint32)
+        n = C.c_size_t()
+        model.ctx.check(lib.ig_explain(model.ctx.handle, model.handle, cls, _p64(r), model.logical_len,
+                                       idx.ctypes.data_as(C.POINTER(C.c_uint32)), cap, C.byref(n)))
+        if n.value <= cap:
+            return idx[:n.value].copy()
+        cap = n.value
+
+
+def explain_row(model: Model, row, vocabulary: list[str], dictionaries=None) -> dict:
+    """Human-readable evidence of one row: matched pure patterns per class with
+    their tokens, support and score; the score totals equal A and N."""
+    dictionaries = dictionaries or [model.dictionary(0, 1), model.dictionary(1, 1)]
+    out = {}
+    for cls, name in ((0, "attack"), (1, "normal")):
+        d = dictionaries[cls]
+        items = []
+        for i in explain(model, row, cls).tolist():
+            words = d.words[i].view(np.uint64)
+            toks = [vocabulary[w * 64 + b] for w in range(words.shape[0]) for b in range(64)
+                    if (int(words[w]) >> b) & 1]
+            items.append({"tokens": toks, "support": int(d.supports[i]), "score": int(d.scores[i])})
+        out[name] = items
+        out["A" if cls == 0 else "N"] = sum(x["score"] for x in items)
+    return out
+
+
+def save_model(model: Model, schema: Schema, vocabulary: list[str], r: float = 0.568) -> bytes:
+    """ModelArchive: stable-ordered text, canonical pattern
+    order, packed words base-64; save -> load -> save is byte-identical."""
+    import base64
+    lines = [ARCHIVE_MAGIC, f"r {float(r).hex()}", "stats_mode batch", "[schema]"]
+    lines += schema_to_text(schema).rstrip("\n").split("\n")
+    lines.append(f"[vocabulary] {len(vocabulary)}")
+    lines += [_esc(t) for t in vocabulary]
+    k = (model.logical_len + 63) // 64
+    for cls, name in ((0, "attack"), (1, "normal")):
+        d = model.dictionary(cls, 1)
+        lines.append(f"[dictionary {name}] {d.words.shape[0]} {k}")
+        for tag, a in (("words", d.words), ("supports", d.supports), ("scores", d.scores)):
+            lines.append(tag + " " + base64.b64encode(np.ascontiguousarray(a, "<i8").tobytes()).decode())
+    lines.append("[end]")
+    return ("\n".join(lines) + "\n").encode("utf-8", errors="surrogateescape")
+
+
+@dataclass
+class LoadedModel:
+    model: Model
+    schema: Schema
+    vocabulary: list
+    encoding: Encoding
+    r: float
+
+
+def load_model(data: bytes, ctx: Optional[Context] = None) -> LoadedModel:
+    import base64
+    ctx = ctx or default_context()
+    lines = data.decode("utf-8", errors="surrogateescape").split("\n")
+    if lines[0] != ARCHIVE_MAGIC:
+        raise DataError("not an ig-b200 archive")
+    r = float.fromhex(lines[1].split(" ", 1)[1])
+    i = lines.index("[schema]") + 1
+    j = next(t for t in range(i, len(lines)) if lines[t].startswith("[vocabulary]"))
+    schema = schema_from_text("\n".join(lines[i:j]) + "\n")
+    nv = int(lines[j].split(" ")[1])
+    vocab = [_unesc(t) for t in lines[j + 1:j + 1 + nv]]
+    L = len(vocab)
+    pos = j + 1 + nv
+    dicts = []
+    for _ in range(2):
+        _, rest = lines[pos].split("] ", 1)
+        n, k = (int(x) for x in rest.split())
+        vals = {}
+        for t in range(3):
+            tag, b64 = lines[pos + 1 + t].split(" ", 1)
+            vals[tag] = np.frombuffer(base64.b64decode(b64), "<i8").astype(np.int64)
+        dicts.append(Dictionary(vals["words"].reshape(n, k) if n else np.zeros((0, k), np.int64),
+                                vals["supports"], vals["scores"]))
+        pos += 4
+    model = model_from_dictionaries(L, dicts[0], dicts[1], ctx)
+    enc = encoding_from_vocabulary(schema, vocab, ctx)
+    return LoadedModel(model, schema, vocab, enc, r)

@@ -32,6 +32,7 @@ struct ig_candidates {
 
 struct ig_model {
     uint32_t L = 0;
+    bool sum_fits = true;  // Σ scores of each dictionary <= INT64_MAX (fit: checked on the candidates)
     uint64_t partial_total[2] = {0, 0};  // Σ candidate scores per class (checked)
     ig_candidates cand[2];
     ig_candidates pure[2];
@@ -291,7 +292,7 @@ void evidence_impl(igb::Ctx& ctx, const ig_model& m, const int64_t* d_tests, siz
             const ig_candidates& P = m.pure[c];
             // the fit checked Σ candidate scores <= INT64_MAX (total_score); pure ⊆ candidates
             igb::posting_match(cx, P.rows.data(), P.rows.n, k, P.score.as<int64_t>(), PT, c == 0 ? d_A : d_N,
-                               flag.as<int>(), true);
+                               flag.as<int>(), m.sum_fits);
         }, m.pure[0].rows.n + m.pure[1].rows.n <= kConcurrentPatterns);
         int h = 0;
         IGB_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
@@ -842,5 +843,98 @@ int ig_shard_finish(ig_ctx* ctx, ig_shard* s, uint64_t* partial_totals) {
 const ig_model* ig_shard_model(const ig_shard* s) { return s ? &s->model : nullptr; }
 
 void ig_shard_free(ig_shard* s) { delete s; }
+
+
+// ------------------------------------------------------------------ archive / explain
+int ig_schema_to_text(const ig_schema* s, char* buf, size_t cap, size_t* len) {
+    return guard(nullptr, [&] {
+        const std::string t = igb::schema_to_text(*s);
+        *len = t.size();
+        if (buf && cap) {
+            const size_t n = std::min(cap - 1, t.size());
+            std::memcpy(buf, t.data(), n);
+            buf[n] = '\0';
+        }
+    });
+}
+
+int ig_schema_from_text(const char* text, ig_schema** out) {
+    *out = nullptr;
+    return guard(nullptr, [&] {
+        auto s = std::make_unique<ig_schema>();
+        igb::schema_from_text(text, *s);
+        *out = s.release();
+    });
+}
+
+int ig_encoding_from_vocabulary(const ig_schema* s, const char* vocab_blob, ig_encoding** out) {
+    *out = nullptr;
+    return guard(nullptr, [&] {
+        std::vector<std::string> toks;
+        std::string cur;
+        for (const char* p = vocab_blob; *p; ++p) {
+            if (*p == '\n') {
+                toks.push_back(cur);
+                cur.clear();
+            } else {
+                cur += *p;
+            }
+        }
+        if (!cur.empty()) toks.push_back(cur);
+        auto e = std::make_unique<ig_encoding>();
+        igb::encoding_from_vocab(*s, toks, *e);
+        *out = e.release();
+    });
+}
+
+int ig_model_from_dictionaries(ig_ctx* ctx, uint32_t L, const int64_t* wa, const int64_t* sa, const int64_t* ca,
+                               size_t na, const int64_t* wn, const int64_t* sn, const int64_t* cn, size_t nn,
+                               ig_model** out) {
+    *out = nullptr;
+    return guard(ctx, [&] {
+        auto m = std::make_unique<ig_model>();
+        m->L = L;
+        const int64_t* W[2] = {wa, wn};
+        const int64_t* S[2] = {sa, sn};
+        const int64_t* C[2] = {ca, cn};
+        const size_t Nn[2] = {na, nn};
+        const size_t k = igb::words_for(L);
+        for (int c = 0; c < 2; ++c) {
+            ig_candidates& P = m->pure[c];
+            upload_rows(*ctx, W[c], Nn[c], L, P.rows);
+            P.support.alloc(std::max<size_t>(Nn[c], 1) * 8, ctx->stream);
+            P.score.alloc(std::max<size_t>(Nn[c], 1) * 8, ctx->stream);
+            if (Nn[c]) {
+                IGB_CUDA(cudaMemcpyAsync(P.support.p, S[c], Nn[c] * 8, cudaMemcpyHostToDevice, ctx->stream));
+                IGB_CUDA(cudaMemcpyAsync(P.score.p, C[c], Nn[c] * 8, cudaMemcpyHostToDevice, ctx->stream));
+            }
+            P.has_support = P.has_score = true;
+            P.rows.buf.persist();
+            P.support.persist();
+            P.score.persist();
+            bool neg = false;
+            __int128 tot = 0;
+            for (size_t i = 0; i < Nn[c]; ++i) {
+                neg |= C[c][i] < 0;
+                tot += C[c][i];
+            }
+            if (neg || tot > (__int128)INT64_MAX) m->sum_fits = false;  // evidence then uses checked sums
+            m->cand[c].rows.k = k;
+            m->cand[c].rows.L = L;
+        }
+        IGB_CUDA(cudaStreamSynchronize(ctx->stream));
+        *out = m.release();
+    });
+}
+
+int ig_explain(ig_ctx* ctx, const ig_model* m, int cls, const int64_t* row, uint32_t L, uint32_t* idx, size_t cap,
+               size_t* n_found) {
+    return guard(ctx, [&] {
+        if (cls < 0 || cls > 1) fail(IG_E_INVALID_ARG, "class must be 0 (attack) or 1 (normal)");
+        if (L != m->L) fail(IG_E_INVALID_ARG, "explain: logical length mismatch");
+        const ig_candidates& P = m->pure[cls];
+        *n_found = igb::explain_dev(*ctx, P.rows.data(), P.rows.n, P.rows.k, row, idx, cap);
+    });
+}
 
 }  // extern "C"

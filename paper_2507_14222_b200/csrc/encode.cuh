@@ -27,4 +27,10 @@ namespace igb {
 void encode_training_dev(Ctx& ctx, const ig_columns& c, ig_encoding& e);
 void upload_columns(Ctx& ctx, ig_columns& c);
 void encode_rows_dev(Ctx& ctx, const ig_columns& c, const ig_encoding& train, ig_encoding& e);
+// archive.cu
+std::string schema_to_text(const ig_schema& s);
+void schema_from_text(const std::string& text, ig_schema& s);
+void encoding_from_vocab(const ig_schema& s, const std::vector<std::string>& tokens, ig_encoding& e);
+size_t explain_dev(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const int64_t* h_row, uint32_t* h_idx,
+                   size_t cap);
 }  // namespace igb

@@ -147,3 +147,16 @@ def test_normal_stats_examples():
     mu, sg = api.fit_normal_stats([40, 50, 60])
     assert mu == 50.0 and abs(sg - 8.16496580927726) < 1e-12
     assert api.fit_normal_stats([0, 0, 0]) == (0.0, 0.0)
+
+
+def test_schema_text_round_trip():
+    """Archive schema section: exact hex-float statistics and escaped names."""
+    from paper_2507_14222_b200 import api
+    t = api.read_csv(b'a b,"x\ny",lab\\el\n0.1,p,normal\n0.2,"q,r",neptune\n0.3,,normal\n')
+    s = api.infer_schema(t, "lab\\el", decimals=3, normal_values=["normal"])
+    txt = api.schema_to_text(s)
+    s2 = api.schema_from_text(txt)
+    assert api.schema_to_text(s2) == txt
+    for j in range(3):
+        assert s.column(j) == s2.column(j)
+    assert s2.label_index == 2
