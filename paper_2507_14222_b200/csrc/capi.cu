@@ -184,14 +184,18 @@ void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m, bool enumerate 
     // phase A (per class): canonical row order (shared by enumeration and the
     // postings), candidates, postings, support, score, checked total
     for_both_classes(ctx, [&](igb::Ctx& cx, int c) {
+        igb::Trace tr(cx, "fitA", c);
         perm[c].alloc(X[c].n * 4, cx.stream);
         igb::sort_rows_canonical(cx, X[c].p, X[c].n, k, perm[c].as<uint32_t>());
+        tr.mark("sort_rows");
         if (enumerate) {
             igb::enumerate_dev(cx, X[c].p, X[c].n, k, L, m.cand[c].rows, &m.stats[c], perm[c].as<uint32_t>());
             m.cand[c].pairs = m.stats[c].pairs;
             m.cand[c].ordered = false;
         }
+        tr.mark("enumerate");
         if (vertical) igb::build_postings(cx, X[c].p, X[c].n, k, L, PX[c], true, false, perm[c].as<uint32_t>());
+        tr.mark("postings");
         ig_candidates& C = m.cand[c];
         const size_t np = C.rows.n;
         C.support.alloc(std::max<size_t>(np, 1) * 8, cx.stream);
@@ -200,6 +204,7 @@ void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m, bool enumerate 
             igb::posting_support(cx, C.rows.data(), np, k, PX[c], C.support.as<int64_t>());
         else
             igb::count_support_dev(cx, C.rows.data(), np, X[c].p, X[c].n, k, C.support.as<int64_t>());
+        tr.mark("support");
         if (igb::score_dev(cx, C.rows.data(), np, k, C.support.as<int64_t>(), C.score.as<int64_t>()) != IG_OK)
             fail(IG_E_OVERFLOW, "pattern score overflows int64");
         int64_t total = 0;
@@ -207,6 +212,7 @@ void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m, bool enumerate 
             fail(IG_E_OVERFLOW, "total score overflows int64");
         m.partial_total[c] = (uint64_t)total;
         C.has_support = C.has_score = true;
+        tr.mark("score+total");
     }, concurrent);
     tm.mark();  // 1
     // phase B (per class): reject_covered against the other class's postings,
@@ -284,15 +290,19 @@ void evidence_impl(igb::Ctx& ctx, const ig_model& m, const int64_t* d_tests, siz
     // Fit scores are support * size^2 >= 0, so the vertical matcher applies;
     // test-row postings are built once and shared by both dictionaries.
     if (igb::postings_supported(L, nt)) {
+        igb::Trace tr(ctx, "evidence", -1);
         igb::Postings PT;
         igb::build_postings(ctx, d_tests, nt, k, L, PT, true, true);
+        tr.mark("test_postings");
         DevBuf flag(sizeof(int), ctx.stream);
         IGB_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), ctx.stream));
         for_both_classes(ctx, [&](igb::Ctx& cx, int c) {
             const ig_candidates& P = m.pure[c];
             // the fit checked Σ candidate scores <= INT64_MAX (total_score); pure ⊆ candidates
+            igb::Trace trc(cx, "evidence", c);
             igb::posting_match(cx, P.rows.data(), P.rows.n, k, P.score.as<int64_t>(), PT, c == 0 ? d_A : d_N,
                                flag.as<int>(), m.sum_fits);
+            trc.mark("match");
         }, m.pure[0].rows.n + m.pure[1].rows.n <= kConcurrentPatterns);
         int h = 0;
         IGB_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
@@ -340,6 +350,18 @@ int ig_ctx_create(int device, ig_ctx** out) {
         IGB_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
         uint64_t thr = UINT64_MAX;
         IGB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+        // Map the working set once: growing the pool later (new physical pages)
+        // costs ~100 ms per first-time allocation pattern inside a fit.
+        size_t free_b = 0, total_b = 0;
+        IGB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        size_t reserve = std::min<size_t>(free_b / 4, size_t{24} << 30);
+        if (const char* e = getenv("IG_POOL_RESERVE_GB")) reserve = (size_t)(atof(e) * (1ull << 30));
+        if (reserve) {
+            void* p = nullptr;
+            if (cudaMallocAsync(&p, reserve, c->own) == cudaSuccess) cudaFreeAsync(p, c->own);
+            cudaGetLastError();
+            IGB_CUDA(cudaStreamSynchronize(c->own));
+        }
     });
     if (st != IG_OK) {
         g_err = c->err;
