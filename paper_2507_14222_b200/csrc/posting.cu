@@ -654,10 +654,23 @@ grouped_scan(const unsigned long long* __restrict__ dense, size_t W, size_t n_ro
                 }
             } else {
                 if (__any_sync(kFull, mw != 0ull)) {
-                    if (MODE == kMatch)
-                        warp_scatter_runs(w, mw, (long long)s, acc);  // acc is a difference array
-                    else
+                    if (MODE == kMatch) {
+                        // difference array: +s at each run start, -s after each run end
+                        unsigned long long st = mw & ~(mw << 1), en = mw & ~(mw >> 1);
+                        unsigned long long* row = acc + (size_t)w * 64;
+                        while (st) {
+                            const int b = __ffsll((long long)st) - 1;
+                            st &= st - 1;
+                            atomicAdd(row + b, s);
+                        }
+                        while (en) {
+                            const int b = __ffsll((long long)en) - 1;
+                            en &= en - 1;
+                            atomicAdd(row + b + 1, (unsigned long long)(-(long long)s));
+                        }
+                    } else {
                         warp_scatter_hits<true>(w, mw, s, acc, ovf);
+                    }
                 }
             }
         }
