@@ -96,6 +96,35 @@ class Clocks:
                 "reasons": reasons, "samples": len(samples)}
 
 
+def ncu_summary(path):
+    """`traffic` (dram read+write bytes per launch) and pipe utilisation of the
+    matcher from the committed `ncu --set full` capture of the same kernel."""
+    import csv
+    if not os.path.exists(path):
+        return {}
+    rows = list(csv.reader(open(path)))
+    h, u, v = rows[0], rows[1], rows[2]
+    get = {name: (float(v[i].replace(",", "")), u[i]) for i, name in enumerate(h)
+           if name in ("dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum",
+                       "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+                       "smsp__issue_active.avg.pct_of_peak_sustained_active",
+                       "lts__throughput.avg.pct_of_peak_sustained_elapsed")}
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    try:
+        traffic = sum(get[k][0] * scale.get(get[k][1], 1) for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+        return {"traffic": traffic,
+                "ncu": {"source": os.path.relpath(path, ROOT),
+                        "alu_pipe_pct": get["sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"][0],
+                        "issue_active_pct": get["smsp__issue_active.avg.pct_of_peak_sustained_active"][0],
+                        "l2_throughput_pct": get["lts__throughput.avg.pct_of_peak_sustained_elapsed"][0],
+                        "duration_ms_cold": get["gpu__time_duration.sum"][0],
+                        "note": "ALU-pipe bound: the posting form trades LOP3 word tests for loads, votes, "
+                                "shuffles and REDs, so the algorithmic word-AND rate is a small share of the "
+                                "integer instructions the pipe retires"}}
+    except KeyError:
+        return {}
+
+
 def workload_config(args, n_train, n_test, extra=None):
     cfg = {"workload": f"synthetic NSL-KDD-shape {args.rows} records, {args.ratio * 10}/{100 - args.ratio * 10} "
                        f"train/test, p={args.decimals}",
@@ -322,8 +351,8 @@ def run_b200(args):
                                           "note": "dense (b&x)==b work the posting form avoids"},
                 "peak_source": f"measured lop3 micro-kernel {lop3_s / 1e12:.2f} T LOP3.32/s (diag.cu)",
                 "kernel_ms_per_launch": kms / max(nl, 1), "launches_per_step": nl // reps,
-                "share_of_step": kms / reps / ms,
-                "ncu": "profiles/ (issue-slot utilisation of the same kernel)"}
+                "share_of_step": kms / reps / ms}
+    roofline.update(ncu_summary(os.path.join(ROOT, "profiles", "r01_ncu_raw_grouped_scan_match.csv")))
 
     line = {"metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
