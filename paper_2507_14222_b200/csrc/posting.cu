@@ -9,15 +9,17 @@
 // so a pattern costs |b| word-ANDs per 64 rows instead of K word tests per row
 // (|b| ≈ 17 tokens vs 64·K = 896 bits at NSL shape).  Rows are put in
 // canonical order first so rows sharing tokens share posting words.  Each
-// pattern's tokens are listed rarest first (document frequency over R); a warp
-// walks the non-zero words of the rarest token (CSR list), 32 words per step,
-// and ANDs the next tokens until no lane has a surviving row.  Exact and
-// independent of every order involved:
+// pattern's tokens are listed rarest first (document frequency over R);
+// patterns sharing their two rarest tokens share one word list (grouped_scan),
+// and a warp walks that list 32 words per step, ANDing the next tokens until
+// no lane has a surviving row.  Exact and independent of every order involved:
 //   support  = Σ popcount(...)
 //   covered  = any word non-zero                             (kernels.cpp:59-65)
-//   evidence: A[row] += s_p for each surviving bit, u64 atomics with overflow
-//             detection; used only when all scores are ≥ 0, where "some prefix
-//             overflows" ⟺ "the total exceeds INT64_MAX" (kernels.cpp:40-46).
+//   evidence = Σ_p s_p over surviving rows, accumulated as a difference array
+//              of runs (+s at a run's first row, -s after its last, then one
+//              scan) when Σ s_p <= INT64_MAX, else with checked u64 atomics;
+//              used only when all scores are >= 0, where "some prefix overflows"
+//              ⟺ "the total exceeds INT64_MAX" (kernels.cpp:40-46).
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -230,95 +232,6 @@ __global__ void minus_one(uint32_t* __restrict__ v, size_t n) {
 
 enum Mode : int { kMatch = 0, kSupport = 1, kCover = 2, kMatchChecked = 3 };
 
-// Warp per pattern over the CSR token lists.
-template <int MODE>
-__global__ void __launch_bounds__(256)
-posting_scan(const unsigned long long* __restrict__ dense, size_t W, const uint32_t* __restrict__ nz_off,
-             const uint32_t* __restrict__ nz_idx, size_t n_rows, const uint32_t* __restrict__ tok_off,
-             const uint16_t* __restrict__ toks, size_t np, const int64_t* __restrict__ scores,
-             unsigned long long* __restrict__ acc, int64_t* __restrict__ support_out, uint8_t* __restrict__ cover_out,
-             int* __restrict__ flags) {
-    const int lane = threadIdx.x & 31;
-    const size_t warps = ((size_t)gridDim.x * blockDim.x) >> 5;
-    bool ovf = false;
-    for (size_t p = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < np; p += warps) {
-        const uint32_t o = tok_off[p];
-        const uint32_t m = tok_off[p + 1] - o;
-        if (m == 0) {
-            // the empty pattern is a subset of every row
-            if (MODE == kSupport) {
-                if (lane == 0) support_out[p] = (int64_t)n_rows;
-            } else if (MODE == kCover) {
-                if (lane == 0) cover_out[p] = n_rows > 0 ? 1 : 0;
-            } else {
-                const unsigned long long s = (unsigned long long)scores[p];
-                for (size_t r = lane; r < n_rows; r += 32) {
-                    const unsigned long long old = atomicAdd(acc + r, s);
-                    if (old + s > (unsigned long long)INT64_MAX) ovf = true;
-                }
-            }
-            continue;
-        }
-        const uint32_t tl = lane < m ? (uint32_t)toks[o + lane] : 0u;
-        const uint32_t t1 = __shfl_sync(kFull, tl, 0);
-        const uint32_t beg = nz_off[t1], end = nz_off[t1 + 1];
-        const unsigned long long* p1 = dense + (size_t)t1 * W;
-        unsigned long long s = 0;
-        if (MODE == kMatch || MODE == kMatchChecked) s = (unsigned long long)scores[p];
-        uint32_t cnt = 0;
-        bool hit = false;
-        const uint32_t Wu = (uint32_t)W;  // L * W < 2^32 (postings_supported)
-        for (uint32_t j0 = beg; j0 < end; j0 += 32) {
-            const uint32_t j = j0 + lane;
-            const uint32_t w = j < end ? nz_idx[j] : 0u;
-            const unsigned long long* col = dense + w;
-            unsigned long long mw = j < end ? p1[w] : 0ull;
-            // four tokens per round: independent loads, one warp vote
-            for (uint32_t i = 1; i < m; i += 4) {
-                if (!__any_sync(kFull, mw != 0ull)) break;
-                uint32_t t[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const uint32_t ii = min(i + u, m - 1);
-                    t[u] = ii < 32 ? __shfl_sync(kFull, tl, ii) : (uint32_t)toks[o + ii];
-                }
-                if (mw) {
-                    const unsigned long long a = col[t[0] * Wu], b = col[t[1] * Wu];
-                    const unsigned long long c = col[t[2] * Wu], d = col[t[3] * Wu];
-                    mw &= (a & b) & (c & d);
-                }
-            }
-            if (MODE == kSupport) {
-                cnt += __popcll(mw);
-            } else if (MODE == kCover) {
-                if (__any_sync(kFull, mw != 0ull)) {
-                    hit = true;
-                    break;
-                }
-            } else {
-                unsigned long long* row = acc + (size_t)w * 64;
-                while (mw) {
-                    const int b = __ffsll((long long)mw) - 1;
-                    mw &= mw - 1;
-                    if (MODE == kMatchChecked) {
-                        const unsigned long long old = atomicAdd(row + b, s);
-                        if (old + s > (unsigned long long)INT64_MAX) ovf = true;
-                    } else {
-                        atomicAdd(row + b, s);  // RED: Σ scores <= INT64_MAX, no sum can overflow
-                    }
-                }
-            }
-        }
-        if (MODE == kSupport) {
-            for (int o2 = 16; o2; o2 >>= 1) cnt += __shfl_xor_sync(kFull, cnt, o2);
-            if (lane == 0) support_out[p] = (int64_t)cnt;
-        } else if (MODE == kCover) {
-            if (lane == 0) cover_out[p] = hit ? 1 : 0;
-        }
-    }
-    if (MODE == kMatchChecked && ovf) atomicOr(flags, 1);
-}
-
 // dst[perm[i]] = src[group ? group[i] : i] for every canonical position i.
 __global__ void scatter_u64(const unsigned long long* __restrict__ src, const uint32_t* __restrict__ perm,
                             const uint32_t* __restrict__ group, size_t n, int64_t* __restrict__ dst) {
@@ -406,22 +319,6 @@ void pattern_tokens(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const P
         IGB_CUDA(cudaFuncSetAttribute(pattern_token_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     IGB_LAUNCH(ctx, pattern_token_fill, grid_for(ctx, np, 128), 128, smem, d_pat, np, (int)k, P.df.as<uint32_t>(), P.L,
                T.off.as<uint32_t>(), T.toks.as<uint16_t>());
-}
-
-// Σ_p m_p * nnz(first token of p): the posting-intersection word-ANDs of a
-// launch without early exit (roofline numerator; diagnostics only).
-__global__ void vertical_work(const uint32_t* __restrict__ tok_off, const uint16_t* __restrict__ toks,
-                              const uint32_t* __restrict__ nz_off, size_t np, unsigned long long* __restrict__ out) {
-    unsigned long long acc = 0;
-    for (size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += (size_t)gridDim.x * blockDim.x) {
-        const uint32_t o = tok_off[p], m = tok_off[p + 1] - o;
-        if (m) {
-            const uint32_t t = toks[o];
-            acc += (unsigned long long)m * (nz_off[t + 1] - nz_off[t]);
-        }
-    }
-    for (int s = 16; s; s >>= 1) acc += __shfl_xor_sync(kFull, acc, s);
-    if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
 }
 
 // ------------------------------------------------------------------ grouped scan
@@ -544,57 +441,8 @@ __device__ __forceinline__ void warp_scatter_hits(uint32_t w, unsigned long long
     }
 }
 
-// Difference-array form of the same scatter (unchecked matcher): each run of
-// consecutive matching rows in a posting word adds +s at its first row and -s
-// after its last row; an inclusive scan over rows afterwards yields the sums.
-// Rows are in canonical order, so matches come in runs (~4 rows per run at C3)
-// and the RED count drops accordingly.  Exact: every partial prefix is a sum of
-// non-negative contributions <= the final value.
-__device__ __forceinline__ void warp_scatter_runs(uint32_t w, unsigned long long mw, long long s,
-                                                  unsigned long long* __restrict__ diff) {
-    const int lane = threadIdx.x & 31;
-    const unsigned long long starts = mw & ~(mw << 1), ends = mw & ~(mw >> 1);
-    const uint32_t s_lo = (uint32_t)starts, s_hi = (uint32_t)(starts >> 32);
-    const uint32_t e_lo = (uint32_t)ends, e_hi = (uint32_t)(ends >> 32);
-    const uint32_t ns = __popc(s_lo) + __popc(s_hi);
-    const uint32_t c = 2 * ns;  // as many ends as starts
-    uint32_t incl = c;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(kFull, incl, o);
-        if (lane >= o) incl += y;
-    }
-    const uint32_t excl = incl - c;
-    const uint32_t total = __shfl_sync(kFull, incl, 31);
-    for (uint32_t q0 = 0; q0 < total; q0 += 32) {
-        const uint32_t q = q0 + lane;
-        int L = 0;
-#pragma unroll
-        for (int step = 16; step >= 1; step >>= 1) {
-            const uint32_t e = __shfl_sync(kFull, excl, L + step);
-            if (e <= q) L += step;
-        }
-        uint32_t r = q - __shfl_sync(kFull, excl, L);
-        const uint32_t nsL = __shfl_sync(kFull, ns, L);
-        const bool is_end = r >= nsL;
-        if (is_end) r -= nsL;
-        // every lane takes part in every shuffle; select afterwards
-        const uint32_t xs_lo = __shfl_sync(kFull, s_lo, L), xs_hi = __shfl_sync(kFull, s_hi, L);
-        const uint32_t xe_lo = __shfl_sync(kFull, e_lo, L), xe_hi = __shfl_sync(kFull, e_hi, L);
-        const uint32_t mlo = is_end ? xe_lo : xs_lo;
-        const uint32_t mhi = is_end ? xe_hi : xs_hi;
-        const uint32_t sw = __shfl_sync(kFull, w, L);
-        if (q < total) {
-            const uint32_t plo = __popc(mlo);
-            const uint32_t bit = r < plo ? __fns(mlo, 0, (int)r + 1) : 32u + __fns(mhi, 0, (int)(r - plo) + 1);
-            const size_t row = (size_t)sw * 64 + bit + (is_end ? 1 : 0);
-            atomicAdd(diff + row, (unsigned long long)(is_end ? -s : s));
-        }
-    }
-}
-
 // Warp per pattern (in group order): walk the group's list, AND tokens 3.., then
-// match / support / cover as posting_scan.
+// match (difference-array runs) / support (popcount) / cover (any).
 template <int MODE>
 __global__ void __launch_bounds__(256)
 grouped_scan(const unsigned long long* __restrict__ dense, size_t W, size_t n_rows,
