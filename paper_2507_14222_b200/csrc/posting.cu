@@ -443,6 +443,18 @@ __device__ __forceinline__ void warp_scatter_hits(uint32_t w, unsigned long long
 
 // Warp per pattern (in group order): walk the group's list, AND tokens 3.., then
 // match (difference-array runs) / support (popcount) / cover (any).
+//
+// ld_tok: posting word of token t at the lane's column, col + t * (W * 8)
+// bytes, the address formed by one IMAD.WIDE.U32 on the FMA pipe (the
+// multiplier is a runtime value, so it is not strength-reduced into the
+// 64-bit add + LEA pair that would land on the ALU pipe this kernel saturates).
+__device__ __forceinline__ unsigned long long ld_tok(const unsigned long long* col, uint32_t t, uint32_t wbytes) {
+    unsigned long long v;
+    asm("{\n\t.reg .u64 a;\n\tmad.wide.u32 a, %1, %2, %3;\n\tld.global.nc.u64 %0, [a];\n\t}"
+        : "=l"(v) : "r"(t), "r"(wbytes), "l"(col));
+    return v;
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(256)
 grouped_scan(const unsigned long long* __restrict__ dense, size_t W, size_t n_rows,
@@ -460,33 +472,34 @@ grouped_scan(const unsigned long long* __restrict__ dense, size_t W, size_t n_ro
         const uint32_t g = gid[i];
         const uint32_t o = tok_off[p];
         const uint32_t m = tok_off[p + 1] - o;
-        const uint32_t tl = lane < m ? (uint32_t)toks[o + lane] : 0u;
+        const uint32_t Wu = (uint32_t)W, wb = Wu * 8u;
+        // lane l holds token l (l < m); lanes past the pattern repeat token 0,
+        // whose posting already contains every surviving word of the group
+        // list, so ANDing it again is a no-op
+        const uint32_t t0 = m ? (uint32_t)toks[o] : 0u;
+        const uint32_t toff = lane < m ? (uint32_t)toks[o + lane] : t0;
         const unsigned long long base = goff[g];
         const uint32_t len = glen[g];
         unsigned long long s = 0;
         if (MODE == kMatch || MODE == kMatchChecked) s = (unsigned long long)scores[p];
         uint32_t cnt = 0;
         bool hit = false;
-        const uint32_t Wu = (uint32_t)W;
         for (uint32_t j0 = 0; j0 < len; j0 += 32) {
             const uint32_t j = j0 + lane;
             const uint32_t w = j < len ? ew[base + j] : 0u;
             unsigned long long mw = j < len ? em[base + j] : 0ull;
             const unsigned long long* col = dense + w;
-            // tokens 2..31 come from the lanes' registers (no branch per token);
-            // the rare tail past 32 tokens is read from memory
-            const uint32_t m32 = min(m, 32u);
-            for (uint32_t t = 2; t < m32; t += 4) {
-                if (!__any_sync(kFull, mw != 0ull)) break;
-                const uint32_t t0 = __shfl_sync(kFull, tl, t);
-                const uint32_t t1 = __shfl_sync(kFull, tl, min(t + 1, m32 - 1));
-                const uint32_t t2 = __shfl_sync(kFull, tl, min(t + 2, m32 - 1));
-                const uint32_t t3 = __shfl_sync(kFull, tl, min(t + 3, m32 - 1));
-                if (mw) {
-                    const unsigned long long a = col[t0 * Wu], b = col[t1 * Wu];
-                    const unsigned long long c = col[t2 * Wu], d = col[t3 * Wu];
-                    mw &= (a & b) & (c & d);
-                }
+            // tokens 2..31 from the lanes' registers, four per round, with
+            // compile-time shuffle lanes (lanes 32/33 of the last round wrap
+            // to tokens 0/1: no-ops); the rare tail past 32 is read from memory
+#pragma unroll
+            for (int t = 2; t < 32; t += 4) {
+                if ((uint32_t)t >= m) break;
+                const bool live = mw != 0ull;
+                if (!__any_sync(kFull, live)) break;
+                const uint32_t o0 = __shfl_sync(kFull, toff, t), o1 = __shfl_sync(kFull, toff, (t + 1) & 31);
+                const uint32_t o2 = __shfl_sync(kFull, toff, (t + 2) & 31), o3 = __shfl_sync(kFull, toff, (t + 3) & 31);
+                if (live) mw &= (ld_tok(col, o0, wb) & ld_tok(col, o1, wb)) & (ld_tok(col, o2, wb) & ld_tok(col, o3, wb));
             }
             for (uint32_t t = 32; t < m; ++t) {
                 if (!__any_sync(kFull, mw != 0ull)) break;
@@ -504,17 +517,17 @@ grouped_scan(const unsigned long long* __restrict__ dense, size_t W, size_t n_ro
                 if (__any_sync(kFull, mw != 0ull)) {
                     if (MODE == kMatch) {
                         // difference array: +s at each run start, -s after each run end
+                        // every run has one start and one end: one loop retires both;
+                        // ctz(x) = popc(~x & (x - 1)) avoids the 64-bit find-first sequence
                         unsigned long long st = mw & ~(mw << 1), en = mw & ~(mw >> 1);
                         unsigned long long* row = acc + (size_t)w * 64;
                         while (st) {
-                            const int b = __ffsll((long long)st) - 1;
-                            st &= st - 1;
-                            atomicAdd(row + b, s);
-                        }
-                        while (en) {
-                            const int b = __ffsll((long long)en) - 1;
-                            en &= en - 1;
-                            atomicAdd(row + b + 1, (unsigned long long)(-(long long)s));
+                            __builtin_assume(en != 0ull);
+                            const unsigned long long st1 = st - 1, en1 = en - 1;
+                            atomicAdd(row + __popcll(~st & st1), s);
+                            atomicAdd(row + 1 + __popcll(~en & en1), 0ull - s);
+                            st &= st1;
+                            en &= en1;
                         }
                     } else {
                         warp_scatter_hits<true>(w, mw, s, acc, ovf);
@@ -643,7 +656,10 @@ void launch_scan(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Post
 
 }  // namespace
 
-bool postings_supported(uint32_t L, size_t n) { return words_for(L) * 64 < 65535 && n < 0xffffffffull; }
+bool postings_supported(uint32_t L, size_t n) {
+    // token ids fit u16 (and W * 8 fits u32)
+    return words_for(L) * 64 < 65535 && n < 0xffffffffull;
+}
 
 void build_postings(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, uint32_t /*logical_len*/, Postings& P,
                     bool canonical, bool distinct, const uint32_t* d_perm) {
