@@ -149,6 +149,10 @@ pair_enum(const int64_t* __restrict__ X, uint32_t n, int k, int stride, uint64_t
         for (int q = threadIdx.x; q < kLocalSlots; q += kPairThreads) local[q] = 0ull;
         __syncthreads();
         for (int q = threadIdx.x; q < TILE * TILE; q += kPairThreads) {
+            // every lane runs the same trip count: re-converge the warp each
+            // pair so the AND + fingerprint work runs on full warps (lanes
+            // otherwise drift apart after the data-dependent probe paths)
+            __syncwarp();
             const int r = q / TILE, c = q % TILE;
             const uint32_t u = i0 + r, v = j0 + c;
             if (u >= n || v >= n || u > v) continue;
