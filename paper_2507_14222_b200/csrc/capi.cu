@@ -119,7 +119,8 @@ constexpr size_t kConcurrentPatterns = 8u << 20; // pure patterns (C3: 2.2 M; C4
 
 template <class F>
 void for_both_classes(igb::Ctx& ctx, F&& fn, bool concurrent = true) {
-    if (!concurrent) {
+    static const bool serial = getenv("IG_SERIAL_CLASSES") != nullptr;  // profiling: one class at a time
+    if (!concurrent || serial) {
         fn(ctx, 0);
         fn(ctx, 1);
         return;

@@ -150,19 +150,19 @@ __device__ __forceinline__ uint64_t mix64(uint64_t h) {
     return h;
 }
 
-// Streaming fingerprint of a K-word candidate: word-position dependent so that
-// permuted words do not collide; finalised with fmix64.  A fingerprint is only
-// a bucket hint — every equality is confirmed on the full words.
+// Fingerprint of a K-word candidate: NH over per-word keys (the UMAC inner
+// hash), sum_w (lo_w + klo_w) * (hi_w + khi_w) mod 2^64 with 32-bit halves —
+// one IMAD.WIDE per word — finalised with fmix64.  For rows of equal length
+// and uniform keys two distinct rows collide with probability <= 2^-32; a new
+// key set per collision level separates any pair that collided.  A fingerprint
+// is only a bucket hint: every equality is confirmed on the full words.
 struct Fp {
-    uint64_t h = 0x9e3779b97f4a7c15ull;
-    __device__ __forceinline__ void add(uint64_t w) {
-        h ^= w * 0x87c37b91114253d5ull;
-        h = (h << 31) | (h >> 33);
-        h *= 0x4cf5ad432745937full;
-        h += 0x52dce729ull;
+    uint64_t acc = 0;
+    __device__ __forceinline__ void add(uint64_t w, uint64_t key) {
+        acc += (uint64_t)((uint32_t)w + (uint32_t)key) * (uint64_t)((uint32_t)(w >> 32) + (uint32_t)(key >> 32));
     }
     __device__ __forceinline__ uint64_t final(uint32_t k) const {
-        uint64_t f = mix64(h ^ k);
+        uint64_t f = mix64(acc + k);
         return f ? f : 1ull;  // 0 marks an empty hash slot
     }
 };

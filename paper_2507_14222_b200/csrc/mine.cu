@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "ig_internal.cuh"
 #include "subset.cuh"
@@ -43,6 +44,8 @@ struct Table {
     unsigned long long* collisions;
     int* fail;  // bit0 table full, bit1 overflow list full
     uint64_t seed;
+    const unsigned long long* keys;  // K fingerprint keys of this level (derived from seed)
+    uint64_t fp_mask;                // ~0; narrowed only by the IG_TEST_FP_BITS collision test knob
 };
 
 __device__ __forceinline__ ulonglong2 cas128(ulonglong2* addr, ulonglong2 cmp, ulonglong2 val) {
@@ -57,6 +60,12 @@ __device__ __forceinline__ ulonglong2 cas128(ulonglong2* addr, ulonglong2 cmp, u
         : "l"(cmp.x), "l"(cmp.y), "l"(val.x), "l"(val.y), "l"(addr)
         : "memory");
     return old;
+}
+
+// Per-word fingerprint keys of one hash level (splitmix64 stream of the seed).
+constexpr uint64_t kOwnerSeed = 0x6a09e667f3bcc909ull;
+__global__ void fp_keys(uint64_t seed, int k, unsigned long long* __restrict__ keys) {
+    for (int w = threadIdx.x; w < k; w += blockDim.x) keys[w] = mix64(seed + 0x9e3779b97f4a7c15ull * (uint64_t)(w + 1));
 }
 
 __device__ __forceinline__ uint64_t ld_volatile(const unsigned long long* p) {
@@ -163,10 +172,10 @@ pair_enum(const int64_t* __restrict__ X, uint32_t n, int k, int stride, uint64_t
             for (int w = 0; w < k; ++w) {
                 const uint64_t x = (uint64_t)(a[w] & b[w]);
                 nz |= x;
-                fp.add(x);
+                fp.add(x, __ldg(T.keys + w));
             }
             if (!nz) continue;  // SPEC.md:338 empty intersections dropped at the source
-            const uint64_t f = fp.final(k);
+            const uint64_t f = (fp.final(k) & T.fp_mask) | 1ull;
             // local entry: 51-bit tag (never zero) | 12-bit pair index within the tile
             const unsigned long long entry = ((((f >> 13) | (1ull << 50))) << 12) | (unsigned)q;
             bool dup = false;
@@ -203,9 +212,8 @@ __global__ void pair_insert_list(const int64_t* __restrict__ X, int k, const uin
         const int64_t* a = X + (size_t)p.x * k;
         const int64_t* b = X + (size_t)p.y * k;
         Fp fp;
-        fp.h ^= T.seed;
-        for (int w = 0; w < k; ++w) fp.add((uint64_t)(__ldg(a + w) & __ldg(b + w)));
-        table_insert(T, X, k, p.x, p.y, fp.final(k),
+        for (int w = 0; w < k; ++w) fp.add((uint64_t)(__ldg(a + w) & __ldg(b + w)), __ldg(T.keys + w));
+        table_insert(T, X, k, p.x, p.y, (fp.final(k) & T.fp_mask) | 1ull,
                      [&](int w) { return __ldg(a + w) & __ldg(b + w); });
     }
 }
@@ -293,8 +301,10 @@ unsigned grid_for(const Ctx& ctx, size_t work, int threads) {
 }
 
 struct TableMem {
-    DevBuf slots, reps, ovf, ctr;  // ctr: count, ovf_count, collisions, fail
-    Table make(Ctx& ctx, uint64_t cap, uint64_t ovf_cap, uint64_t seed) {
+    DevBuf slots, reps, ovf, ctr, keys;  // ctr: count, ovf_count, collisions, fail
+    Table make(Ctx& ctx, uint64_t cap, uint64_t ovf_cap, uint64_t seed, size_t k) {
+        keys.alloc(std::max<size_t>(k, 1) * 8, ctx.stream);
+        IGB_LAUNCH(ctx, fp_keys, 1, 256, 0, seed, (int)k, keys.as<unsigned long long>());
         slots.alloc(cap * sizeof(ulonglong2), ctx.stream);
         IGB_CUDA(cudaMemsetAsync(slots.p, 0, cap * sizeof(ulonglong2), ctx.stream));  // empty slot = {0, 0}
         const uint64_t limit = cap / 4 * 3;
@@ -314,6 +324,12 @@ struct TableMem {
         T.collisions = ctr.as<unsigned long long>() + 2;
         T.fail = reinterpret_cast<int*>(ctr.as<unsigned long long>() + 3);
         T.seed = seed;
+        T.keys = keys.as<unsigned long long>();
+        T.fp_mask = ~0ull;
+        if (const char* e = std::getenv("IG_TEST_FP_BITS")) {  // test knob: force fingerprint collisions
+            const int bits = std::atoi(e);
+            if (bits > 0 && bits < 64) T.fp_mask = (1ull << bits) - 1;
+        }
         return T;
     }
 };
@@ -449,7 +465,7 @@ uint64_t dedup_pairs(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, const 
             TableMem tm;
             const uint64_t lcap = level == 0 ? cap : next_pow2(4 * n_pending + 1024);
             const uint64_t ovf_cap = level == 0 ? std::max<uint64_t>(1u << 20, cap / 64) : n_pending + 1;
-            Table T = tm.make(ctx, lcap, ovf_cap, 0x2545f4914f6cdd1dull * (uint64_t)(level + 1));
+            Table T = tm.make(ctx, lcap, ovf_cap, 0x2545f4914f6cdd1dull * (uint64_t)(level + 1), k);
             if (level == 0 && src.list) {
                 if (src.n_list)
                     IGB_LAUNCH(ctx, pair_insert_list, grid_for(ctx, src.n_list, 256), 256, 0, d_rows, (int)k, src.list,
@@ -517,13 +533,14 @@ namespace {
 // Owner of a candidate = its content fingerprint (unseeded, identical on every
 // rank because the distinct canonical rows are) mod world.
 __global__ void owner_of(const int64_t* __restrict__ X, int k, const uint2* __restrict__ reps, uint64_t n, int world,
-                         uint32_t* __restrict__ owner, unsigned long long* __restrict__ counts) {
+                         const unsigned long long* __restrict__ keys, uint32_t* __restrict__ owner,
+                         unsigned long long* __restrict__ counts) {
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint2 p = reps[i];
         const int64_t* a = X + (size_t)p.x * k;
         const int64_t* b = X + (size_t)p.y * k;
         Fp fp;
-        for (int w = 0; w < k; ++w) fp.add((uint64_t)(a[w] & b[w]));
+        for (int w = 0; w < k; ++w) fp.add((uint64_t)(a[w] & b[w]), keys[w]);
         const uint32_t o = (uint32_t)((fp.final(k) >> 32) % (uint64_t)world);
         owner[i] = o;
         atomicAdd(counts + o, 1ull);
@@ -544,8 +561,10 @@ void bucket_by_owner(Ctx& ctx, const int64_t* d_rows, size_t k, const uint2* d_r
     if (count == 0) return;
     DevBuf owner(count * 4, ctx.stream), cnt(world * 8, ctx.stream), cur(world * 8, ctx.stream);
     IGB_CUDA(cudaMemsetAsync(cnt.p, 0, world * 8, ctx.stream));
+    DevBuf keys(std::max<size_t>(k, 1) * 8, ctx.stream);
+    IGB_LAUNCH(ctx, fp_keys, 1, 256, 0, kOwnerSeed, (int)k, keys.as<unsigned long long>());
     IGB_LAUNCH(ctx, owner_of, grid_for(ctx, count, 256), 256, 0, d_rows, (int)k, d_reps, count, world,
-               owner.as<uint32_t>(), cnt.as<unsigned long long>());
+               keys.as<unsigned long long>(), owner.as<uint32_t>(), cnt.as<unsigned long long>());
     IGB_CUDA(cudaMemcpyAsync(counts.data(), cnt.p, world * 8, cudaMemcpyDeviceToHost, ctx.stream));
     IGB_CUDA(cudaStreamSynchronize(ctx.stream));
     std::vector<uint64_t> start(world, 0);

@@ -573,8 +573,10 @@ template <int MODE>
 void launch_scan(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Postings& P, const int64_t* scores,
                  unsigned long long* acc, int64_t* support, uint8_t* cover, int* flags) {
     if (np == 0) return;
+    Trace tr(ctx, MODE == kSupport ? "scan:support" : MODE == kCover ? "scan:cover" : "scan:match", -1);
     PatternTokens T;
     pattern_tokens(ctx, d_pat, np, k, P, T);
+    tr.mark("token_lists");
     const bool diag = ctx.diag && (MODE == kMatch || MODE == kMatchChecked);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (diag) {
@@ -623,16 +625,19 @@ void launch_scan(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Post
     unsigned long long E = 0;
     IGB_CUDA(cudaMemcpyAsync(&E, goff.as<unsigned long long>() + G, 8, cudaMemcpyDeviceToHost, ctx.stream));
     IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+    tr.mark("group_sort");
     DevBuf ew(std::max<unsigned long long>(E, 1) * 4, ctx.stream), em(std::max<unsigned long long>(E, 1) * 8, ctx.stream);
     IGB_LAUNCH(ctx, group_lists, grid_for(ctx, (size_t)G * 32, 256), 256, 0, gkey.as<uint32_t>(), (size_t)G,
                P.dense.as<unsigned long long>(), P.W, P.n, P.nz_off.as<uint32_t>(), P.nz_idx.as<uint32_t>(),
                goff.as<unsigned long long>(), glen.as<uint32_t>(), ew.as<uint32_t>(), em.as<unsigned long long>());
     IGB_LAUNCH(ctx, minus_one, grid_for(ctx, np, 256), 256, 0, gid.as<uint32_t>(), np);
+    tr.mark("group_lists");
     const size_t blocks = std::min<size_t>((np + 7) / 8, (size_t)ctx.sm_count * 64);
     IGB_LAUNCH(ctx, grouped_scan<MODE>, (unsigned)blocks, 256, 0, P.dense.as<unsigned long long>(), P.W, P.n,
                T.off.as<uint32_t>(), T.toks.as<uint16_t>(), np, order.as<uint32_t>(), gid.as<uint32_t>(),
                goff.as<unsigned long long>(), glen.as<uint32_t>(), ew.as<uint32_t>(), em.as<unsigned long long>(),
                scores, acc, support, cover, flags);
+    tr.mark("grouped_scan");
     if (diag) {
         IGB_CUDA(cudaEventRecord(e1, ctx.stream));
         DevBuf w(8, ctx.stream);

@@ -58,22 +58,29 @@ __global__ void column_insert(const int64_t* __restrict__ words, size_t n, int k
         ulonglong2* T = tables + (size_t)w * slots;
         uint32_t s = (uint32_t)(mix64(v) & (slots - 1));
         for (uint32_t probe = 0;; ++probe, s = (s + 1) & (slots - 1)) {
-            if (probe >= slots || counts[w] >= slots / 2) {
+            if (probe >= slots) {
                 atomicOr(full, 1);
                 return;
             }
-            unsigned long long tag = ldv(&T[s].y);
-            if (tag == 0) {
+            // plain (L1-cacheable) reads: popular values would otherwise hammer
+            // one L2 line per column.  A slot changes once, {0,0} -> {v,1}, by
+            // a 128-bit CAS, so a stale read can only show it empty (the CAS
+            // below then returns the real content) and a non-zero tag always
+            // comes with its value.
+            ulonglong2 e;  // one 16-byte load (value and tag from the same snapshot)
+            asm("ld.global.v2.u64 {%0, %1}, [%2];" : "=l"(e.x), "=l"(e.y) : "l"(T + s));
+            if (e.y == 0) {
                 const ulonglong2 old = cas128(T + s, make_ulonglong2(0ull, 0ull), make_ulonglong2(v, 1ull));
                 if (old.y == 0) {
-                    atomicAdd(counts + w, 1u);
+                    // load check only on the (rare) insert path: past half load the
+                    // host retries with a larger table
+                    if (atomicAdd(counts + w, 1u) + 1 >= slots / 2) atomicOr(full, 1);
                     break;
                 }
                 if (old.x == v) break;
                 continue;
             }
-            unsigned long long x = ldv(&T[s].x);
-            if (x == v) break;
+            if (e.x == v) break;
         }
     }
 }
@@ -170,6 +177,51 @@ __global__ void gather_rows_u32(const int64_t* __restrict__ src, const uint32_t*
         dst[q] = src[(size_t)idx[q / k] * k + q % k];
 }
 
+// Small sets (n <= kSmallSort): exact stable rank by counting, one launch.
+// rank(i) = #{j : row_j < row_i} + #{j < i : row_j == row_i}; thread i keeps its
+// row in registers and streams 128-row chunks of the j range through shared
+// memory (warp-broadcast reads).  blockIdx.y splits the j range so that even a
+// few thousand rows fill every SM; partial counts meet in rank[] by atomics.
+constexpr uint32_t kSmallSort = 10240;
+constexpr int kRankChunk = 128;
+template <int KMAX>
+__global__ void __launch_bounds__(kRankChunk)
+rank_by_count(const int64_t* __restrict__ rows, uint32_t n, int k, uint32_t j_per_split, uint32_t* __restrict__ rank) {
+    __shared__ unsigned long long sj[kRankChunk * KMAX];
+    const uint32_t i = blockIdx.x * kRankChunk + threadIdx.x;
+    unsigned long long r[KMAX];
+#pragma unroll
+    for (int w = 0; w < KMAX; ++w) r[w] = (i < n && w < k) ? (unsigned long long)rows[(size_t)i * k + w] : 0ull;
+    const uint32_t jb = blockIdx.y * j_per_split, je = min(n, jb + j_per_split);
+    uint32_t cnt = 0;
+    for (uint32_t j0 = jb; j0 < je; j0 += kRankChunk) {
+        const uint32_t m = min((uint32_t)kRankChunk, je - j0);
+        __syncthreads();
+        for (uint32_t q = threadIdx.x; q < m * (uint32_t)k; q += kRankChunk)
+            sj[(q / k) * KMAX + q % k] = (unsigned long long)rows[(size_t)j0 * k + q];
+        __syncthreads();
+        for (uint32_t jj = 0; jj < m; ++jj) {
+            const unsigned long long* b = sj + jj * KMAX;
+            int cmp = 0;  // -1: row_j < row_i, 1: row_j > row_i
+#pragma unroll
+            for (int w = 0; w < KMAX; ++w) {
+                if (w >= k) break;
+                const unsigned long long x = b[w];
+                if (x != r[w]) {
+                    cmp = x < r[w] ? -1 : 1;
+                    break;
+                }
+            }
+            cnt += (cmp < 0 || (cmp == 0 && j0 + jj < i)) ? 1u : 0u;
+        }
+    }
+    if (i < n) atomicAdd(rank + i, cnt);
+}
+
+__global__ void perm_from_rank(const uint32_t* __restrict__ rank, uint32_t n, uint32_t* __restrict__ perm) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) perm[rank[i]] = i;
+}
+
 uint32_t next_pow2_u32(uint64_t x) {
     uint64_t p = 1;
     while (p < x) p <<= 1;
@@ -182,6 +234,27 @@ void sort_rows_canonical(Ctx& ctx, const int64_t* d_words, size_t n, size_t k, u
     if (n == 0) return;
     if (n == 1 || k == 0) {
         IGB_LAUNCH(ctx, iota32, 1, 32, 0, d_perm, n);
+        return;
+    }
+    Trace tr(ctx, "sort_rows", -1);
+    if (n <= kSmallSort && k <= 32) {
+        DevBuf rank(n * 4, ctx.stream);
+        IGB_CUDA(cudaMemsetAsync(rank.p, 0, n * 4, ctx.stream));
+        const uint32_t bx = (uint32_t)((n + kRankChunk - 1) / kRankChunk);
+        // split j so that bx * by covers ~4 CTAs per SM, in whole chunks
+        uint32_t by = std::max<uint32_t>(1, (uint32_t)(4 * ctx.sm_count) / bx);
+        uint32_t per = (uint32_t)((n + by - 1) / by);
+        per = (per + kRankChunk - 1) / kRankChunk * kRankChunk;
+        by = (uint32_t)((n + per - 1) / per);
+        const dim3 grid(bx, by);
+        if (k <= 16)
+            IGB_LAUNCH(ctx, rank_by_count<16>, grid, kRankChunk, 0, d_words, (uint32_t)n, (int)k, per,
+                       rank.as<uint32_t>());
+        else
+            IGB_LAUNCH(ctx, rank_by_count<32>, grid, kRankChunk, 0, d_words, (uint32_t)n, (int)k, per,
+                       rank.as<uint32_t>());
+        IGB_LAUNCH(ctx, perm_from_rank, grid_for(ctx, n, 256), 256, 0, rank.as<uint32_t>(), (uint32_t)n, d_perm);
+        tr.mark("rank_by_count");
         return;
     }
     // Per-column hash sets; start small (columns usually hold a few thousand
@@ -232,6 +305,7 @@ void sort_rows_canonical(Ctx& ctx, const int64_t* d_words, size_t n, size_t k, u
         sort_rows_canonical_lsd(ctx, d_words, n, k, d_perm);
         return;
     }
+    tr.mark("column_hash");
     // Rank the distinct values of every column.
     uint64_t m = 0;
     for (size_t w = 0; w < k; ++w) m += hc[w];
@@ -262,6 +336,7 @@ void sort_rows_canonical(Ctx& ctx, const int64_t* d_words, size_t n, size_t k, u
     IGB_CUDA(cudaMemcpyAsync(cstart.p, hstart.data(), (k + 1) * 4, cudaMemcpyHostToDevice, ctx.stream));
     IGB_LAUNCH(ctx, write_ranks, grid_for(ctx, m, 256), 256, 0, where.as<uint32_t>(), m, slots,
                cstart.as<unsigned int>(), tables.as<ulonglong2>());
+    tr.mark("column_ranks");
     // Packed keys and LSD over the key words (least significant word first).
     DevBuf dfields(k * sizeof(Field), ctx.stream), keys((size_t)n_keys * n * 8, ctx.stream);
     IGB_CUDA(cudaMemcpyAsync(dfields.p, fields.data(), k * sizeof(Field), cudaMemcpyHostToDevice, ctx.stream));
@@ -289,6 +364,12 @@ void sort_rows_canonical(Ctx& ctx, const int64_t* d_words, size_t n, size_t k, u
         std::swap(cur, alt);
     }
     if (cur != d_perm) IGB_CUDA(cudaMemcpyAsync(d_perm, cur, n * 4, cudaMemcpyDeviceToDevice, ctx.stream));
+    if (tr.on) {
+        int bits = 0;
+        for (int b : used_bits) bits += b;
+        fprintf(stderr, "[ig trace] sort_rows n=%zu k=%zu keys=%d bits=%d\n", n, k, n_keys, bits);
+    }
+    tr.mark("lsd");
 }
 
 size_t distinct_rows(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, DevBuf& out, const uint32_t* d_perm) {

@@ -90,3 +90,23 @@ def test_progress_callback(api):
     seen = []
     cs = api.enumerate_candidates(api.PackedMatrix(X, 64), progress=lambda d, t, f: seen.append((d, t, f)))
     assert seen and seen[-1] == (100 * 99 // 2, 100 * 99 // 2, cs.patterns.rows)
+
+
+@pytest.mark.parametrize("bits", [10, 16])
+def test_forced_fingerprint_collisions_stay_exact(api, monkeypatch, bits):
+    """Fingerprints narrowed to `bits` bits (test knob) make most distinct
+    candidates collide: the tile-local and device-wide tables must still keep
+    exactly the distinct contents, through as many collision levels as needed."""
+    monkeypatch.setenv("IG_TEST_FP_BITS", str(bits))
+    rng = np.random.default_rng(bits)
+    L = 200
+    Xa = random_rows(rng, 150, L, 0.8)
+    Xn = random_rows(rng, 130, L, 0.8)
+    ref = oracle.fit(Xa, Xn)
+    m = api.fit(Xa, Xn, L)
+    for c in range(2):
+        for which, want in ((0, ref.candidates[c]), (1, ref.pure[c])):
+            d = m.dictionary(c, which)
+            assert which == 1 or len(want.words) > (8 << bits if bits == 10 else 4000)
+            assert np.array_equal(d.words, want.words), (c, which)
+            assert np.array_equal(d.supports, want.supports), (c, which)
