@@ -36,6 +36,11 @@ struct ig_model {
     uint64_t partial_total[2] = {0, 0};  // Σ candidate scores per class (checked)
     ig_candidates cand[2];
     ig_candidates pure[2];
+    // scan index of each pure dictionary (token lists ranked by the training
+    // rows' frequencies, grouped by rarest pair), built by fit; evidence reuses
+    // it for every test batch.  Absent for models assembled from dictionaries.
+    igb::PatternIndex pidx[2];
+    bool has_pidx = false;
     double ms[6] = {0, 0, 0, 0, 0, 0};
     igb::EnumStats stats[2];
 };
@@ -182,8 +187,8 @@ void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m, bool enumerate 
     const bool concurrent = X[0].n + X[1].n <= kConcurrentRows;
     DevBuf perm[2];
     igb::Postings PX[2];
-    // phase A (per class): canonical row order (shared by enumeration and the
-    // postings), candidates, postings, support, score, checked total
+    // phase A1 (per class): canonical row order (shared by enumeration and the
+    // postings), candidates, postings
     for_both_classes(ctx, [&](igb::Ctx& cx, int c) {
         igb::Trace tr(cx, "fitA", c);
         perm[c].alloc(X[c].n * 4, cx.stream);
@@ -197,14 +202,26 @@ void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m, bool enumerate 
         tr.mark("enumerate");
         if (vertical) igb::build_postings(cx, X[c].p, X[c].n, k, L, PX[c], true, false, perm[c].as<uint32_t>());
         tr.mark("postings");
+    }, concurrent);
+    // one token rank space for every scan of this fit: frequencies over all
+    // training rows.  Each candidate set gets one index (token lists + groups)
+    // shared by its support and coverage scans; the pure subset inherits it.
+    igb::RankSpace R;
+    igb::PatternIndex CI[2];
+    if (vertical) igb::combined_rank_space(ctx, PX[0], PX[1], R);
+    // phase A2 (per class): candidate index, support, score, checked total
+    for_both_classes(ctx, [&](igb::Ctx& cx, int c) {
+        igb::Trace tr(cx, "fitA", c);
         ig_candidates& C = m.cand[c];
         const size_t np = C.rows.n;
         C.support.alloc(std::max<size_t>(np, 1) * 8, cx.stream);
         C.score.alloc(std::max<size_t>(np, 1) * 8, cx.stream);
-        if (vertical)
-            igb::posting_support(cx, C.rows.data(), np, k, PX[c], C.support.as<int64_t>());
-        else
+        if (vertical) {
+            igb::build_pattern_index(cx, C.rows.data(), np, k, R, CI[c]);
+            igb::posting_support(cx, C.rows.data(), np, k, PX[c], C.support.as<int64_t>(), &CI[c]);
+        } else {
             igb::count_support_dev(cx, C.rows.data(), np, X[c].p, X[c].n, k, C.support.as<int64_t>());
+        }
         tr.mark("support");
         if (igb::score_dev(cx, C.rows.data(), np, k, C.support.as<int64_t>(), C.score.as<int64_t>()) != IG_OK)
             fail(IG_E_OVERFLOW, "pattern score overflows int64");
@@ -225,7 +242,7 @@ void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m, bool enumerate 
         igb::Trace tr(cx, "purify", c);
         DevBuf mask(std::max<size_t>(np, 1), cx.stream);
         if (vertical && X[1 - c].n > 0)
-            igb::posting_cover(cx, C.rows.data(), np, k, PX[1 - c], mask.as<uint8_t>());
+            igb::posting_cover(cx, C.rows.data(), np, k, PX[1 - c], mask.as<uint8_t>(), &CI[c]);
         else
             igb::coverage_any_dev(cx, C.rows.data(), np, X[1 - c].p, X[1 - c].n, k, mask.as<uint8_t>());
         tr.mark("cover");
@@ -235,15 +252,29 @@ void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m, bool enumerate 
         P.rows.buf.alloc(std::max<size_t>(np * k, 1) * 8, cx.stream);
         P.support.alloc(std::max<size_t>(np, 1) * 8, cx.stream);
         P.score.alloc(std::max<size_t>(np, 1) * 8, cx.stream);
+        DevBuf kept;  // pure (compacted) position -> candidate index
         P.rows.n = igb::compact_unflagged(cx, C.rows.data(), C.support.as<int64_t>(), C.score.as<int64_t>(),
                                           mask.as<uint8_t>(), np, k, P.rows.data(), P.support.as<int64_t>(),
-                                          P.score.as<int64_t>());
+                                          P.score.as<int64_t>(), vertical ? &kept : nullptr);
         P.has_support = P.has_score = true;
         tr.mark("compact");
-        igb::canonical_order(cx, P.rows, &P.support, &P.score);
-        IGB_CUDA(cudaStreamSynchronize(cx.stream));
+        DevBuf order;  // canonical position -> compacted position
+        igb::canonical_order(cx, P.rows, &P.support, &P.score, vertical ? &order : nullptr);
         tr.mark("order");
+        if (vertical) {
+            // the pure dictionary's scan index = the candidates' restricted to it
+            const size_t n = P.rows.n;
+            DevBuf src(std::max<size_t>(n, 1) * 4, cx.stream);
+            igb::compose_u32(cx, kept.as<uint32_t>(), order.p ? order.as<uint32_t>() : nullptr, n,
+                             src.as<uint32_t>());
+            igb::subset_pattern_index(cx, CI[c], src.as<uint32_t>(), n, m.pidx[c]);
+            for (DevBuf* b : {&m.pidx[c].off, &m.pidx[c].toks, &m.pidx[c].order, &m.pidx[c].gid, &m.pidx[c].gkey})
+                b->persist();
+            tr.mark("pure_index");
+        }
+        IGB_CUDA(cudaStreamSynchronize(cx.stream));
     }, concurrent);
+    m.has_pidx = vertical;
     tm.mark();  // 2
     IGB_CUDA(cudaStreamSynchronize(ctx.stream));
     IGB_CUDA(cudaStreamSynchronize(ctx.aux));
@@ -302,7 +333,7 @@ void evidence_impl(igb::Ctx& ctx, const ig_model& m, const int64_t* d_tests, siz
             // the fit checked Σ candidate scores <= INT64_MAX (total_score); pure ⊆ candidates
             igb::Trace trc(cx, "evidence", c);
             igb::posting_match(cx, P.rows.data(), P.rows.n, k, P.score.as<int64_t>(), PT, c == 0 ? d_A : d_N,
-                               flag.as<int>(), m.sum_fits);
+                               flag.as<int>(), m.sum_fits, m.has_pidx ? &m.pidx[c] : nullptr);
             trc.mark("match");
         }, m.pure[0].rows.n + m.pure[1].rows.n <= kConcurrentPatterns);
         int h = 0;

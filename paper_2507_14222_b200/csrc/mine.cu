@@ -378,7 +378,7 @@ void gather_rows(Ctx& ctx, const int64_t* d_src, const uint32_t* d_perm, size_t 
     IGB_LAUNCH(ctx, gather_rows_k, grid_for(ctx, n * k, 256), 256, 0, d_src, d_perm, n, (int)k, d_dst);
 }
 
-void canonical_order(Ctx& ctx, DevRows& rows, DevBuf* a, DevBuf* b) {
+void canonical_order(Ctx& ctx, DevRows& rows, DevBuf* a, DevBuf* b, DevBuf* o_perm) {
     const size_t n = rows.n, k = rows.k;
     if (n < 2) return;
     DevBuf perm(n * 4, ctx.stream);
@@ -393,6 +393,17 @@ void canonical_order(Ctx& ctx, DevRows& rows, DevBuf* a, DevBuf* b) {
                    t.as<int64_t>());
         *pay = std::move(t);
     }
+    if (o_perm) *o_perm = std::move(perm);
+}
+
+__global__ void compose_k(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b, size_t n,
+                          uint32_t* __restrict__ out) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        out[i] = a[b ? b[i] : i];
+}
+
+void compose_u32(Ctx& ctx, const uint32_t* a, const uint32_t* b, size_t n, uint32_t* out) {
+    if (n) IGB_LAUNCH(ctx, compose_k, grid_for(ctx, n, 256), 256, 0, a, b, n, out);
 }
 
 // Identical rows give identical intersections, so B^c over the distinct rows
@@ -620,7 +631,7 @@ __global__ void compact_rows_k(const int64_t* __restrict__ src, const uint32_t* 
 
 size_t compact_unflagged(Ctx& ctx, const int64_t* d_words, const int64_t* d_sup, const int64_t* d_sc,
                          const uint8_t* d_flag, size_t n, size_t k, int64_t* o_words, int64_t* o_sup,
-                         int64_t* o_sc) {
+                         int64_t* o_sc, DevBuf* o_idx) {
     if (n == 0) return 0;
     DevBuf keep(n, ctx.stream), idx(n * 4, ctx.stream), nsel(8, ctx.stream), iota(n * 4, ctx.stream);
     IGB_LAUNCH(ctx, flag_to_keep, grid_for(ctx, n, 256), 256, 0, d_flag, n, keep.as<uint8_t>());
@@ -640,6 +651,7 @@ size_t compact_unflagged(Ctx& ctx, const int64_t* d_words, const int64_t* d_sup,
         if (d_sup) IGB_LAUNCH(ctx, gather_i64, grid_for(ctx, m, 256), 256, 0, d_sup, idx.as<uint32_t>(), (size_t)m, o_sup);
         if (d_sc) IGB_LAUNCH(ctx, gather_i64, grid_for(ctx, m, 256), 256, 0, d_sc, idx.as<uint32_t>(), (size_t)m, o_sc);
     }
+    if (o_idx) *o_idx = std::move(idx);
     return (size_t)m;
 }
 

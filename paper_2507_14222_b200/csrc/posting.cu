@@ -263,63 +263,58 @@ __global__ void fix_group(const uint32_t* __restrict__ head, size_t n, uint32_t*
         group[i] = group[i] + head[i] - 1;
 }
 
-// CSR token lists of `np` patterns ordered by the document frequency of P.
-struct PatternTokens {
-    DevBuf off, toks;
-};
-
-void pattern_tokens(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Postings& P, PatternTokens& T) {
-    DevBuf cnt((np + 1) * 4, ctx.stream);
-    T.off.alloc((np + 1) * 4, ctx.stream);
-    IGB_LAUNCH(ctx, pattern_token_count, grid_for(ctx, np, 256), 256, 0, d_pat, np, (int)k, cnt.as<uint32_t>());
-    IGB_CUDA(cudaMemsetAsync(cnt.as<uint32_t>() + np, 0, 4, ctx.stream));
-    size_t tb = 0;
-    IGB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.as<uint32_t>(), T.off.as<uint32_t>(), (int64_t)np + 1,
-                                           ctx.stream));
-    DevBuf temp(tb, ctx.stream);
-    IGB_CUDA(cub::DeviceScan::ExclusiveSum(temp.p, tb, cnt.as<uint32_t>(), T.off.as<uint32_t>(), (int64_t)np + 1,
-                                           ctx.stream));
-    uint32_t total = 0;
-    IGB_CUDA(cudaMemcpyAsync(&total, T.off.as<uint32_t>() + np, 4, cudaMemcpyDeviceToHost, ctx.stream));
-    IGB_CUDA(cudaStreamSynchronize(ctx.stream));
-    T.toks.alloc(std::max<size_t>(total, 1) * 2, ctx.stream);
-    if (k <= kRankWords) {
-        const uint32_t L = P.L;
-        DevBuf key(L * 8, ctx.stream), key2(L * 8, ctx.stream), tok(L * 2, ctx.stream), byrank(L * 2, ctx.stream),
-            rank(L * 2, ctx.stream);
-        IGB_LAUNCH(ctx, rank_keys, grid_for(ctx, L, 256), 256, 0, P.df.as<uint32_t>(), L, key.as<unsigned long long>(),
-                   tok.as<uint16_t>());
-        size_t tb2 = 0;
-        IGB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb2, key.as<unsigned long long>(), key2.as<unsigned long long>(),
-                                                 tok.as<uint16_t>(), byrank.as<uint16_t>(), (int64_t)L, 0, 64, ctx.stream));
-        DevBuf temp2(tb2, ctx.stream);
-        IGB_CUDA(cub::DeviceRadixSort::SortPairs(temp2.p, tb2, key.as<unsigned long long>(), key2.as<unsigned long long>(),
-                                                 tok.as<uint16_t>(), byrank.as<uint16_t>(), (int64_t)L, 0, 64, ctx.stream));
-        IGB_LAUNCH(ctx, invert_rank, grid_for(ctx, L, 256), 256, 0, byrank.as<uint16_t>(), L, rank.as<uint16_t>());
-        const size_t smem = (size_t)L * 4;
-#define IGB_FILL_RANK(KW)                                                                                          \
-    {                                                                                                              \
-        if (smem > 48 * 1024)                                                                                      \
-            IGB_CUDA(cudaFuncSetAttribute(pattern_token_fill_rank<KW>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                          (int)smem));                                                             \
-        IGB_LAUNCH(ctx, pattern_token_fill_rank<KW>, grid_for(ctx, np, 128), 128, smem, d_pat, np, (int)k,         \
-                   rank.as<uint16_t>(), byrank.as<uint16_t>(), L, T.off.as<uint32_t>(), T.toks.as<uint16_t>());   \
-    }
-        if (k <= 16)
-            IGB_FILL_RANK(16)
-        else if (k <= 32)
-            IGB_FILL_RANK(32)
-        else
-            IGB_FILL_RANK(64)
-#undef IGB_FILL_RANK
-        return;
-    }
-    const size_t smem = (size_t)P.L * 4;
-    if (smem > 48 * 1024)
-        IGB_CUDA(cudaFuncSetAttribute(pattern_token_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    IGB_LAUNCH(ctx, pattern_token_fill, grid_for(ctx, np, 128), 128, smem, d_pat, np, (int)k, P.df.as<uint32_t>(), P.L,
-               T.off.as<uint32_t>(), T.toks.as<uint16_t>());
+// Pattern-index helper kernels (host functions below, outside this namespace).
+__global__ void add_u32(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b, uint32_t n,
+                        uint32_t* __restrict__ out) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = a[i] + b[i];
 }
+
+// subset index: token counts of the chosen source patterns
+__global__ void sub_count(const uint32_t* __restrict__ src_off, const uint32_t* __restrict__ src_of, size_t n,
+                          uint32_t* __restrict__ cnt) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        const uint32_t s = src_of[i];
+        cnt[i] = src_off[s + 1] - src_off[s];
+    }
+}
+
+__global__ void sub_copy(const uint32_t* __restrict__ src_off, const uint16_t* __restrict__ src_toks,
+                         const uint32_t* __restrict__ src_of, size_t n, const uint32_t* __restrict__ off,
+                         uint16_t* __restrict__ toks) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        const uint32_t s = src_of[i], b = src_off[s], m = src_off[s + 1] - b, o = off[i];
+        for (uint32_t t = 0; t < m; ++t) toks[o + t] = src_toks[b + t];
+    }
+}
+
+__global__ void fill_u32(uint32_t* __restrict__ p, size_t n, uint32_t v) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] = v;
+}
+
+__global__ void scatter_pos(const uint32_t* __restrict__ src_of, size_t n, uint32_t* __restrict__ inv) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        inv[src_of[i]] = (uint32_t)i;
+}
+
+// walk the source's group order, keeping the chosen patterns (their new index)
+// and their old group id
+__global__ void map_order(const uint32_t* __restrict__ order, const uint32_t* __restrict__ gid, size_t n,
+                          const uint32_t* __restrict__ inv, uint32_t* __restrict__ val, uint32_t* __restrict__ og,
+                          uint8_t* __restrict__ keep) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        const uint32_t p = inv[order[i]];
+        val[i] = p;
+        og[i] = gid[i];
+        keep[i] = p != 0xffffffffu ? 1 : 0;
+    }
+}
+
+__global__ void gather_u32(const uint32_t* __restrict__ src, const uint32_t* __restrict__ idx, size_t n,
+                           uint32_t* __restrict__ dst) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        dst[i] = src[idx[i]];
+}
+
 
 // ------------------------------------------------------------------ grouped scan
 // Patterns sharing their two rarest tokens (t1, t2) share the word list
@@ -570,13 +565,19 @@ __global__ void group_work(const uint32_t* __restrict__ gkey, const unsigned lon
 }
 
 template <int MODE>
-void launch_scan(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Postings& P, const int64_t* scores,
-                 unsigned long long* acc, int64_t* support, uint8_t* cover, int* flags) {
+void launch_scan(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Postings& P, const PatternIndex* I,
+                 const int64_t* scores, unsigned long long* acc, int64_t* support, uint8_t* cover, int* flags) {
     if (np == 0) return;
     Trace tr(ctx, MODE == kSupport ? "scan:support" : MODE == kCover ? "scan:cover" : "scan:match", -1);
-    PatternTokens T;
-    pattern_tokens(ctx, d_pat, np, k, P, T);
-    tr.mark("token_lists");
+    PatternIndex local;
+    if (!I) {  // no shared index: rank the tokens by this postings' document frequency
+        RankSpace R;
+        make_rank_space(ctx, P.df.as<uint32_t>(), P.L, R);
+        build_pattern_index(ctx, d_pat, np, k, R, local);
+        I = &local;
+        tr.mark("pattern_index");
+    }
+    if (I->np != np) fail(IG_E_CUDA, "pattern index does not match the pattern set");
     const bool diag = ctx.diag && (MODE == kMatch || MODE == kMatchChecked);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (diag) {
@@ -584,37 +585,12 @@ void launch_scan(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Post
         IGB_CUDA(cudaEventCreate(&e1));
         IGB_CUDA(cudaEventRecord(e0, ctx.stream));
     }
-    // group patterns by their two rarest tokens
-    DevBuf key(np * 4, ctx.stream), key2(np * 4, ctx.stream), idx(np * 4, ctx.stream), order(np * 4, ctx.stream);
-    IGB_LAUNCH(ctx, group_keys, grid_for(ctx, np, 256), 256, 0, T.off.as<uint32_t>(), T.toks.as<uint16_t>(), np,
-               key.as<uint32_t>(), idx.as<uint32_t>());
-    size_t tb = 0;
-    IGB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, key.as<uint32_t>(), key2.as<uint32_t>(), idx.as<uint32_t>(),
-                                             order.as<uint32_t>(), (int64_t)np, 0, 32, ctx.stream));
-    DevBuf temp(tb, ctx.stream);
-    IGB_CUDA(cub::DeviceRadixSort::SortPairs(temp.p, tb, key.as<uint32_t>(), key2.as<uint32_t>(), idx.as<uint32_t>(),
-                                             order.as<uint32_t>(), (int64_t)np, 0, 32, ctx.stream));
-    DevBuf head(np, ctx.stream), head32(np * 4, ctx.stream), gid(np * 4, ctx.stream), gkey(np * 4, ctx.stream),
-        nsel(8, ctx.stream);
-    IGB_LAUNCH(ctx, group_heads, grid_for(ctx, np, 256), 256, 0, key2.as<uint32_t>(), np, head.as<uint8_t>(),
-               head32.as<uint32_t>());
-    size_t tb2 = 0, tb3 = 0;
-    IGB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb2, head32.as<uint32_t>(), gid.as<uint32_t>(), (int64_t)np,
-                                           ctx.stream));
-    IGB_CUDA(cub::DeviceSelect::Flagged(nullptr, tb3, key2.as<uint32_t>(), head.as<uint8_t>(), gkey.as<uint32_t>(),
-                                        nsel.as<int64_t>(), (int64_t)np, ctx.stream));
-    DevBuf temp2(std::max(tb2, tb3), ctx.stream);
-    IGB_CUDA(cub::DeviceScan::InclusiveSum(temp2.p, tb2, head32.as<uint32_t>(), gid.as<uint32_t>(), (int64_t)np,
-                                           ctx.stream));
-    IGB_CUDA(cub::DeviceSelect::Flagged(temp2.p, tb3, key2.as<uint32_t>(), head.as<uint8_t>(), gkey.as<uint32_t>(),
-                                        nsel.as<int64_t>(), (int64_t)np, ctx.stream));
-    int64_t G = 0;
-    IGB_CUDA(cudaMemcpyAsync(&G, nsel.p, 8, cudaMemcpyDeviceToHost, ctx.stream));
-    IGB_CUDA(cudaStreamSynchronize(ctx.stream));
-    // gid = inclusive count of heads -> 1-based; shift to 0-based in the scan kernel below
+    const size_t G = I->G;
+    // every group's word list S = non-zero (w, post[t1][w] & post[t2][w]) in P
     DevBuf ub((G + 1) * 8, ctx.stream), goff((G + 1) * 8, ctx.stream), glen(G * 4 + 4, ctx.stream);
-    IGB_LAUNCH(ctx, group_bound, grid_for(ctx, (size_t)G, 256), 256, 0, gkey.as<uint32_t>(), (size_t)G,
-               P.nz_off.as<uint32_t>(), P.W, ub.as<unsigned long long>());
+    if (G)
+        IGB_LAUNCH(ctx, group_bound, grid_for(ctx, G, 256), 256, 0, I->gkey.as<uint32_t>(), G,
+                   P.nz_off.as<uint32_t>(), P.W, ub.as<unsigned long long>());
     IGB_CUDA(cudaMemsetAsync(ub.as<unsigned long long>() + G, 0, 8, ctx.stream));
     size_t tb4 = 0;
     IGB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb4, ub.as<unsigned long long>(), goff.as<unsigned long long>(),
@@ -625,16 +601,15 @@ void launch_scan(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Post
     unsigned long long E = 0;
     IGB_CUDA(cudaMemcpyAsync(&E, goff.as<unsigned long long>() + G, 8, cudaMemcpyDeviceToHost, ctx.stream));
     IGB_CUDA(cudaStreamSynchronize(ctx.stream));
-    tr.mark("group_sort");
     DevBuf ew(std::max<unsigned long long>(E, 1) * 4, ctx.stream), em(std::max<unsigned long long>(E, 1) * 8, ctx.stream);
-    IGB_LAUNCH(ctx, group_lists, grid_for(ctx, (size_t)G * 32, 256), 256, 0, gkey.as<uint32_t>(), (size_t)G,
-               P.dense.as<unsigned long long>(), P.W, P.n, P.nz_off.as<uint32_t>(), P.nz_idx.as<uint32_t>(),
-               goff.as<unsigned long long>(), glen.as<uint32_t>(), ew.as<uint32_t>(), em.as<unsigned long long>());
-    IGB_LAUNCH(ctx, minus_one, grid_for(ctx, np, 256), 256, 0, gid.as<uint32_t>(), np);
+    if (G)
+        IGB_LAUNCH(ctx, group_lists, grid_for(ctx, G * 32, 256), 256, 0, I->gkey.as<uint32_t>(), G,
+                   P.dense.as<unsigned long long>(), P.W, P.n, P.nz_off.as<uint32_t>(), P.nz_idx.as<uint32_t>(),
+                   goff.as<unsigned long long>(), glen.as<uint32_t>(), ew.as<uint32_t>(), em.as<unsigned long long>());
     tr.mark("group_lists");
     const size_t blocks = std::min<size_t>((np + 7) / 8, (size_t)ctx.sm_count * 64);
     IGB_LAUNCH(ctx, grouped_scan<MODE>, (unsigned)blocks, 256, 0, P.dense.as<unsigned long long>(), P.W, P.n,
-               T.off.as<uint32_t>(), T.toks.as<uint16_t>(), np, order.as<uint32_t>(), gid.as<uint32_t>(),
+               I->off.as<uint32_t>(), I->toks.as<uint16_t>(), np, I->order.as<uint32_t>(), I->gid.as<uint32_t>(),
                goff.as<unsigned long long>(), glen.as<uint32_t>(), ew.as<uint32_t>(), em.as<unsigned long long>(),
                scores, acc, support, cover, flags);
     tr.mark("grouped_scan");
@@ -642,10 +617,11 @@ void launch_scan(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Post
         IGB_CUDA(cudaEventRecord(e1, ctx.stream));
         DevBuf w(8, ctx.stream);
         IGB_CUDA(cudaMemsetAsync(w.p, 0, 8, ctx.stream));
-        IGB_LAUNCH(ctx, grouped_work, grid_for(ctx, np, 256), 256, 0, T.off.as<uint32_t>(), np, order.as<uint32_t>(),
-                   gid.as<uint32_t>(), glen.as<uint32_t>(), w.as<unsigned long long>());
-        IGB_LAUNCH(ctx, group_work, grid_for(ctx, (size_t)G, 256), 256, 0, gkey.as<uint32_t>(),
-                   ub.as<unsigned long long>(), (size_t)G, w.as<unsigned long long>());
+        IGB_LAUNCH(ctx, grouped_work, grid_for(ctx, np, 256), 256, 0, I->off.as<uint32_t>(), np,
+                   I->order.as<uint32_t>(), I->gid.as<uint32_t>(), glen.as<uint32_t>(), w.as<unsigned long long>());
+        if (G)
+            IGB_LAUNCH(ctx, group_work, grid_for(ctx, G, 256), 256, 0, I->gkey.as<uint32_t>(),
+                       ub.as<unsigned long long>(), G, w.as<unsigned long long>());
         unsigned long long hw = 0;
         IGB_CUDA(cudaMemcpyAsync(&hw, w.p, 8, cudaMemcpyDeviceToHost, ctx.stream));
         IGB_CUDA(cudaStreamSynchronize(ctx.stream));
@@ -660,6 +636,166 @@ void launch_scan(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Post
 }
 
 }  // namespace
+
+// ------------------------------------------------------------------ pattern index
+void make_rank_space(Ctx& ctx, const uint32_t* d_df, uint32_t L, RankSpace& R) {
+    R.L = L;
+    R.df.alloc((size_t)L * 4, ctx.stream);
+    IGB_CUDA(cudaMemcpyAsync(R.df.p, d_df, (size_t)L * 4, cudaMemcpyDeviceToDevice, ctx.stream));
+    R.rank.alloc((size_t)L * 2, ctx.stream);
+    R.byrank.alloc((size_t)L * 2, ctx.stream);
+    DevBuf key((size_t)L * 8, ctx.stream), key2((size_t)L * 8, ctx.stream), tok((size_t)L * 2, ctx.stream);
+    IGB_LAUNCH(ctx, rank_keys, grid_for(ctx, L, 256), 256, 0, d_df, L, key.as<unsigned long long>(),
+               tok.as<uint16_t>());
+    size_t tb = 0;
+    IGB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, key.as<unsigned long long>(), key2.as<unsigned long long>(),
+                                             tok.as<uint16_t>(), R.byrank.as<uint16_t>(), (int64_t)L, 0, 64, ctx.stream));
+    DevBuf temp(tb, ctx.stream);
+    IGB_CUDA(cub::DeviceRadixSort::SortPairs(temp.p, tb, key.as<unsigned long long>(), key2.as<unsigned long long>(),
+                                             tok.as<uint16_t>(), R.byrank.as<uint16_t>(), (int64_t)L, 0, 64, ctx.stream));
+    IGB_LAUNCH(ctx, invert_rank, grid_for(ctx, L, 256), 256, 0, R.byrank.as<uint16_t>(), L, R.rank.as<uint16_t>());
+}
+
+void combined_rank_space(Ctx& ctx, const Postings& A, const Postings& B, RankSpace& R) {
+    if (A.L != B.L) fail(IG_E_CUDA, "combined_rank_space: postings of different widths");
+    DevBuf df((size_t)A.L * 4, ctx.stream);
+    IGB_LAUNCH(ctx, add_u32, grid_for(ctx, A.L, 256), 256, 0, A.df.as<uint32_t>(), B.df.as<uint32_t>(), A.L,
+               df.as<uint32_t>());
+    make_rank_space(ctx, df.as<uint32_t>(), A.L, R);
+}
+
+void build_pattern_index(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const RankSpace& R, PatternIndex& I) {
+    Trace tr(ctx, "pattern_index", -1);
+    I.np = np;
+    I.G = 0;
+    I.off.alloc((np + 1) * 4, ctx.stream);
+    I.order.alloc(std::max<size_t>(np, 1) * 4, ctx.stream);
+    I.gid.alloc(std::max<size_t>(np, 1) * 4, ctx.stream);
+    I.gkey.alloc(std::max<size_t>(np, 1) * 4, ctx.stream);
+    // CSR token lists, rarest first in R
+    DevBuf cnt((np + 1) * 4, ctx.stream);
+    if (np)
+        IGB_LAUNCH(ctx, pattern_token_count, grid_for(ctx, np, 256), 256, 0, d_pat, np, (int)k, cnt.as<uint32_t>());
+    IGB_CUDA(cudaMemsetAsync(cnt.as<uint32_t>() + np, 0, 4, ctx.stream));
+    size_t tb = 0;
+    IGB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.as<uint32_t>(), I.off.as<uint32_t>(), (int64_t)np + 1,
+                                           ctx.stream));
+    DevBuf temp(tb, ctx.stream);
+    IGB_CUDA(cub::DeviceScan::ExclusiveSum(temp.p, tb, cnt.as<uint32_t>(), I.off.as<uint32_t>(), (int64_t)np + 1,
+                                           ctx.stream));
+    uint32_t total = 0;
+    IGB_CUDA(cudaMemcpyAsync(&total, I.off.as<uint32_t>() + np, 4, cudaMemcpyDeviceToHost, ctx.stream));
+    IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+    I.toks.alloc(std::max<size_t>(total, 1) * 2, ctx.stream);
+    if (np == 0) return;
+    const uint32_t L = R.L;
+    if (k <= kRankWords) {
+        const size_t smem = (size_t)L * 4;
+#define IGB_FILL_RANK(KW)                                                                                          \
+    {                                                                                                              \
+        if (smem > 48 * 1024)                                                                                      \
+            IGB_CUDA(cudaFuncSetAttribute(pattern_token_fill_rank<KW>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                          (int)smem));                                                             \
+        IGB_LAUNCH(ctx, pattern_token_fill_rank<KW>, grid_for(ctx, np, 128), 128, smem, d_pat, np, (int)k,         \
+                   R.rank.as<uint16_t>(), R.byrank.as<uint16_t>(), L, I.off.as<uint32_t>(), I.toks.as<uint16_t>()); \
+    }
+        if (k <= 16)
+            IGB_FILL_RANK(16)
+        else if (k <= 32)
+            IGB_FILL_RANK(32)
+        else
+            IGB_FILL_RANK(64)
+#undef IGB_FILL_RANK
+    } else {
+        const size_t smem = (size_t)L * 4;
+        if (smem > 48 * 1024)
+            IGB_CUDA(cudaFuncSetAttribute(pattern_token_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        IGB_LAUNCH(ctx, pattern_token_fill, grid_for(ctx, np, 128), 128, smem, d_pat, np, (int)k,
+                   R.df.as<uint32_t>(), L, I.off.as<uint32_t>(), I.toks.as<uint16_t>());
+    }
+    tr.mark("token_lists");
+    // group patterns by their two rarest tokens
+    DevBuf key(np * 4, ctx.stream), key2(np * 4, ctx.stream), idx(np * 4, ctx.stream);
+    IGB_LAUNCH(ctx, group_keys, grid_for(ctx, np, 256), 256, 0, I.off.as<uint32_t>(), I.toks.as<uint16_t>(), np,
+               key.as<uint32_t>(), idx.as<uint32_t>());
+    size_t tb1 = 0;
+    IGB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb1, key.as<uint32_t>(), key2.as<uint32_t>(), idx.as<uint32_t>(),
+                                             I.order.as<uint32_t>(), (int64_t)np, 0, 32, ctx.stream));
+    DevBuf temp1(tb1, ctx.stream);
+    IGB_CUDA(cub::DeviceRadixSort::SortPairs(temp1.p, tb1, key.as<uint32_t>(), key2.as<uint32_t>(), idx.as<uint32_t>(),
+                                             I.order.as<uint32_t>(), (int64_t)np, 0, 32, ctx.stream));
+    group_ids(ctx, key2.as<uint32_t>(), np, I);
+    tr.mark("group_sort");
+}
+
+// gid (0-based, per sorted position) and gkey (per group) from the sorted keys
+void group_ids(Ctx& ctx, const uint32_t* d_sorted_key, size_t np, PatternIndex& I) {
+    DevBuf head(np, ctx.stream), head32(np * 4, ctx.stream), nsel(8, ctx.stream);
+    IGB_LAUNCH(ctx, group_heads, grid_for(ctx, np, 256), 256, 0, d_sorted_key, np, head.as<uint8_t>(),
+               head32.as<uint32_t>());
+    size_t tb2 = 0, tb3 = 0;
+    IGB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb2, head32.as<uint32_t>(), I.gid.as<uint32_t>(), (int64_t)np,
+                                           ctx.stream));
+    IGB_CUDA(cub::DeviceSelect::Flagged(nullptr, tb3, d_sorted_key, head.as<uint8_t>(), I.gkey.as<uint32_t>(),
+                                        nsel.as<int64_t>(), (int64_t)np, ctx.stream));
+    DevBuf temp2(std::max(tb2, tb3), ctx.stream);
+    IGB_CUDA(cub::DeviceScan::InclusiveSum(temp2.p, tb2, head32.as<uint32_t>(), I.gid.as<uint32_t>(), (int64_t)np,
+                                           ctx.stream));
+    IGB_CUDA(cub::DeviceSelect::Flagged(temp2.p, tb3, d_sorted_key, head.as<uint8_t>(), I.gkey.as<uint32_t>(),
+                                        nsel.as<int64_t>(), (int64_t)np, ctx.stream));
+    IGB_LAUNCH(ctx, minus_one, grid_for(ctx, np, 256), 256, 0, I.gid.as<uint32_t>(), np);
+    int64_t G = 0;
+    IGB_CUDA(cudaMemcpyAsync(&G, nsel.p, 8, cudaMemcpyDeviceToHost, ctx.stream));
+    IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+    I.G = (size_t)G;
+}
+
+void subset_pattern_index(Ctx& ctx, const PatternIndex& S, const uint32_t* d_src_of, size_t n, PatternIndex& I) {
+    I.np = n;
+    I.G = 0;
+    I.off.alloc((n + 1) * 4, ctx.stream);
+    I.order.alloc(std::max<size_t>(n, 1) * 4, ctx.stream);
+    I.gid.alloc(std::max<size_t>(n, 1) * 4, ctx.stream);
+    I.gkey.alloc(std::max<size_t>(n, 1) * 4, ctx.stream);
+    DevBuf cnt((n + 1) * 4, ctx.stream);
+    if (n)
+        IGB_LAUNCH(ctx, sub_count, grid_for(ctx, n, 256), 256, 0, S.off.as<uint32_t>(), d_src_of, n,
+                   cnt.as<uint32_t>());
+    IGB_CUDA(cudaMemsetAsync(cnt.as<uint32_t>() + n, 0, 4, ctx.stream));
+    size_t tb = 0;
+    IGB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.as<uint32_t>(), I.off.as<uint32_t>(), (int64_t)n + 1,
+                                           ctx.stream));
+    DevBuf temp(tb, ctx.stream);
+    IGB_CUDA(cub::DeviceScan::ExclusiveSum(temp.p, tb, cnt.as<uint32_t>(), I.off.as<uint32_t>(), (int64_t)n + 1,
+                                           ctx.stream));
+    uint32_t total = 0;
+    IGB_CUDA(cudaMemcpyAsync(&total, I.off.as<uint32_t>() + n, 4, cudaMemcpyDeviceToHost, ctx.stream));
+    IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+    I.toks.alloc(std::max<size_t>(total, 1) * 2, ctx.stream);
+    if (n == 0) return;
+    IGB_LAUNCH(ctx, sub_copy, grid_for(ctx, n, 256), 256, 0, S.off.as<uint32_t>(), S.toks.as<uint16_t>(), d_src_of, n,
+               I.off.as<uint32_t>(), I.toks.as<uint16_t>());
+    // the source's group order restricted to the subset keeps its key order
+    const size_t ns = S.np;
+    DevBuf inv(ns * 4, ctx.stream), val(ns * 4, ctx.stream), og(ns * 4, ctx.stream), keep(ns, ctx.stream),
+        og2(std::max<size_t>(n, 1) * 4, ctx.stream), key(std::max<size_t>(n, 1) * 4, ctx.stream), nsel(8, ctx.stream);
+    IGB_LAUNCH(ctx, fill_u32, grid_for(ctx, ns, 256), 256, 0, inv.as<uint32_t>(), ns, 0xffffffffu);
+    IGB_LAUNCH(ctx, scatter_pos, grid_for(ctx, n, 256), 256, 0, d_src_of, n, inv.as<uint32_t>());
+    IGB_LAUNCH(ctx, map_order, grid_for(ctx, ns, 256), 256, 0, S.order.as<uint32_t>(), S.gid.as<uint32_t>(), ns,
+               inv.as<uint32_t>(), val.as<uint32_t>(), og.as<uint32_t>(), keep.as<uint8_t>());
+    size_t tb1 = 0;
+    IGB_CUDA(cub::DeviceSelect::Flagged(nullptr, tb1, val.as<uint32_t>(), keep.as<uint8_t>(), I.order.as<uint32_t>(),
+                                        nsel.as<int64_t>(), (int64_t)ns, ctx.stream));
+    DevBuf temp1(tb1, ctx.stream);
+    IGB_CUDA(cub::DeviceSelect::Flagged(temp1.p, tb1, val.as<uint32_t>(), keep.as<uint8_t>(), I.order.as<uint32_t>(),
+                                        nsel.as<int64_t>(), (int64_t)ns, ctx.stream));
+    IGB_CUDA(cub::DeviceSelect::Flagged(temp1.p, tb1, og.as<uint32_t>(), keep.as<uint8_t>(), og2.as<uint32_t>(),
+                                        nsel.as<int64_t>(), (int64_t)ns, ctx.stream));
+    // group key of every kept position = the source group's key
+    IGB_LAUNCH(ctx, gather_u32, grid_for(ctx, n, 256), 256, 0, S.gkey.as<uint32_t>(), og2.as<uint32_t>(), n,
+               key.as<uint32_t>());
+    group_ids(ctx, key.as<uint32_t>(), n, I);
+}
 
 bool postings_supported(uint32_t L, size_t n) {
     // token ids fit u16 (and W * 8 fits u32)
@@ -740,16 +876,18 @@ void build_postings(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, uint32_
                P.W, P.nz_off.as<uint32_t>(), P.nz_idx.as<uint32_t>());
 }
 
-void posting_support(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Postings& P, int64_t* d_support) {
-    launch_scan<kSupport>(ctx, d_pat, np, k, P, nullptr, nullptr, d_support, nullptr, nullptr);
+void posting_support(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Postings& P, int64_t* d_support,
+                     const PatternIndex* I) {
+    launch_scan<kSupport>(ctx, d_pat, np, k, P, I, nullptr, nullptr, d_support, nullptr, nullptr);
 }
 
-void posting_cover(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Postings& P, uint8_t* d_mask) {
-    launch_scan<kCover>(ctx, d_pat, np, k, P, nullptr, nullptr, nullptr, d_mask, nullptr);
+void posting_cover(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Postings& P, uint8_t* d_mask,
+                   const PatternIndex* I) {
+    launch_scan<kCover>(ctx, d_pat, np, k, P, I, nullptr, nullptr, nullptr, d_mask, nullptr);
 }
 
 void posting_match(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const int64_t* d_scores, const Postings& P,
-                   int64_t* d_out, int* d_overflow, bool sum_fits) {
+                   int64_t* d_out, int* d_overflow, bool sum_fits, const PatternIndex* I) {
     const size_t n = std::max<size_t>(P.n, 1);
     if (P.group.p == nullptr && P.perm.p == nullptr && P.n_src != P.n) fail(IG_E_CUDA, "posting_match: bad postings");
     // sum_fits: Σ scores <= INT64_MAX, so no evidence sum can overflow: run-based
@@ -758,7 +896,7 @@ void posting_match(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const in
     DevBuf acc((n + 64 + 1) * 8, ctx.stream);
     IGB_CUDA(cudaMemsetAsync(acc.p, 0, (n + 64 + 1) * 8, ctx.stream));
     if (sum_fits) {
-        launch_scan<kMatch>(ctx, d_pat, np, k, P, d_scores, acc.as<unsigned long long>(), nullptr, nullptr,
+        launch_scan<kMatch>(ctx, d_pat, np, k, P, I, d_scores, acc.as<unsigned long long>(), nullptr, nullptr,
                             d_overflow);
         size_t tb = 0;
         IGB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, acc.as<unsigned long long>(), acc.as<unsigned long long>(),
@@ -767,7 +905,7 @@ void posting_match(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const in
         IGB_CUDA(cub::DeviceScan::InclusiveSum(temp.p, tb, acc.as<unsigned long long>(), acc.as<unsigned long long>(),
                                                (int64_t)n, ctx.stream));
     } else {
-        launch_scan<kMatchChecked>(ctx, d_pat, np, k, P, d_scores, acc.as<unsigned long long>(), nullptr, nullptr,
+        launch_scan<kMatchChecked>(ctx, d_pat, np, k, P, I, d_scores, acc.as<unsigned long long>(), nullptr, nullptr,
                                    d_overflow);
     }
     if (!P.perm.p) {

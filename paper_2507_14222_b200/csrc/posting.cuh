@@ -22,17 +22,50 @@ struct Postings {
     DevBuf rep;          // posting row -> source row (distinct builds only)
 };
 
+// Token rank space: tokens ordered by (document frequency, id), rarest first.
+struct RankSpace {
+    uint32_t L = 0;
+    DevBuf df;      // L u32
+    DevBuf rank;    // L u16: token -> rank
+    DevBuf byrank;  // L u16: rank -> token
+};
+
+// A pattern set's scan index, independent of the postings it is scanned
+// against: CSR token lists (rarest first in a rank space) and the patterns
+// grouped by their two rarest tokens (t1, t2).
+struct PatternIndex {
+    size_t np = 0;   // patterns
+    size_t G = 0;    // groups
+    DevBuf off;      // np+1 u32: token list offsets
+    DevBuf toks;     // u16 tokens
+    DevBuf order;    // np u32: patterns in group-key order
+    DevBuf gid;      // np u32: group of each ordered position
+    DevBuf gkey;     // G u32: (t1 << 16) | t2
+};
+
+void make_rank_space(Ctx& ctx, const uint32_t* d_df, uint32_t L, RankSpace& R);
+// df = A.df + B.df (postings of the two training classes)
+void combined_rank_space(Ctx& ctx, const Postings& A, const Postings& B, RankSpace& R);
+void build_pattern_index(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const RankSpace& R, PatternIndex& I);
+void group_ids(Ctx& ctx, const uint32_t* d_sorted_key, size_t np, PatternIndex& I);
+// index of the patterns S.pattern[d_src_of[i]], i < n (a subset, e.g. the pure
+// patterns among the candidates), without re-ranking or re-sorting
+void subset_pattern_index(Ctx& ctx, const PatternIndex& S, const uint32_t* d_src_of, size_t n, PatternIndex& I);
+
 bool postings_supported(uint32_t L, size_t n);
 // canonical: index rows in words::less order (clusters rows that share tokens).
 // distinct: one posting row per distinct row (for coverage / evidence, where
 // multiplicity does not matter or is restored by `group`); never for support.
 void build_postings(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, uint32_t L, Postings& P,
                     bool canonical = true, bool distinct = false, const uint32_t* d_perm = nullptr);
-void posting_support(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Postings& P, int64_t* d_support);
-void posting_cover(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Postings& P, uint8_t* d_mask);
+// I: the patterns' scan index (nullptr: built here, ranked by P's frequencies)
+void posting_support(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Postings& P, int64_t* d_support,
+                     const PatternIndex* I = nullptr);
+void posting_cover(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Postings& P, uint8_t* d_mask,
+                   const PatternIndex* I = nullptr);
 // d_out[source row] (P.n int64) is zeroed and accumulated; requires all scores >= 0.
 // sum_fits: caller proved Σ scores <= INT64_MAX (no overflow check needed).
 void posting_match(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const int64_t* d_scores, const Postings& P,
-                   int64_t* d_out, int* d_overflow, bool sum_fits);
+                   int64_t* d_out, int* d_overflow, bool sum_fits, const PatternIndex* I = nullptr);
 
 }  // namespace igb

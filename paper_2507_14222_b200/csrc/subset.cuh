@@ -66,9 +66,12 @@ int total_score_dev(Ctx& ctx, const int64_t* d_score, size_t np, int64_t* total)
 // Keep rows whose flag is 0 (stable), with their supports/scores.
 size_t compact_unflagged(Ctx& ctx, const int64_t* d_words, const int64_t* d_sup, const int64_t* d_sc,
                          const uint8_t* d_flag, size_t n, size_t k, int64_t* o_words, int64_t* o_sup,
-                         int64_t* o_sc);
+                         int64_t* o_sc, DevBuf* o_idx = nullptr);  // o_idx: kept position -> source index
 
 // Reorder rows (+ optional per-row int64 payloads) into canonical words::less order.
-void canonical_order(Ctx& ctx, DevRows& rows, DevBuf* a, DevBuf* b);
+// o_perm (optional): canonical position -> previous position (left empty when n < 2).
+void canonical_order(Ctx& ctx, DevRows& rows, DevBuf* a, DevBuf* b, DevBuf* o_perm = nullptr);
+// out[i] = a[b ? b[i] : i]
+void compose_u32(Ctx& ctx, const uint32_t* a, const uint32_t* b, size_t n, uint32_t* out);
 
 }  // namespace igb
