@@ -215,9 +215,9 @@ __global__ void pattern_token_fill_rank(const int64_t* __restrict__ pat, size_t 
 }
 
 __global__ void rank_keys(const uint32_t* __restrict__ df, uint32_t L, unsigned long long* __restrict__ key,
-                          uint16_t* __restrict__ tok) {
+                          uint16_t* __restrict__ tok, bool descending) {
     for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < L; t += gridDim.x * blockDim.x) {
-        key[t] = ((unsigned long long)df[t] << 16) | t;
+        key[t] = ((unsigned long long)(descending ? 0xffffffffu - df[t] : df[t]) << 16) | t;
         tok[t] = (uint16_t)t;
     }
 }
@@ -638,7 +638,7 @@ void launch_scan(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Post
 }  // namespace
 
 // ------------------------------------------------------------------ pattern index
-void make_rank_space(Ctx& ctx, const uint32_t* d_df, uint32_t L, RankSpace& R) {
+void make_rank_space(Ctx& ctx, const uint32_t* d_df, uint32_t L, RankSpace& R, bool descending) {
     R.L = L;
     R.df.alloc((size_t)L * 4, ctx.stream);
     IGB_CUDA(cudaMemcpyAsync(R.df.p, d_df, (size_t)L * 4, cudaMemcpyDeviceToDevice, ctx.stream));
@@ -646,7 +646,7 @@ void make_rank_space(Ctx& ctx, const uint32_t* d_df, uint32_t L, RankSpace& R) {
     R.byrank.alloc((size_t)L * 2, ctx.stream);
     DevBuf key((size_t)L * 8, ctx.stream), key2((size_t)L * 8, ctx.stream), tok((size_t)L * 2, ctx.stream);
     IGB_LAUNCH(ctx, rank_keys, grid_for(ctx, L, 256), 256, 0, d_df, L, key.as<unsigned long long>(),
-               tok.as<uint16_t>());
+               tok.as<uint16_t>(), descending);
     size_t tb = 0;
     IGB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, key.as<unsigned long long>(), key2.as<unsigned long long>(),
                                              tok.as<uint16_t>(), R.byrank.as<uint16_t>(), (int64_t)L, 0, 64, ctx.stream));
@@ -751,6 +751,7 @@ void group_ids(Ctx& ctx, const uint32_t* d_sorted_key, size_t np, PatternIndex& 
 }
 
 void subset_pattern_index(Ctx& ctx, const PatternIndex& S, const uint32_t* d_src_of, size_t n, PatternIndex& I) {
+    Trace tr(ctx, "subset_index", -1);
     I.np = n;
     I.G = 0;
     I.off.alloc((n + 1) * 4, ctx.stream);
@@ -775,6 +776,7 @@ void subset_pattern_index(Ctx& ctx, const PatternIndex& S, const uint32_t* d_src
     if (n == 0) return;
     IGB_LAUNCH(ctx, sub_copy, grid_for(ctx, n, 256), 256, 0, S.off.as<uint32_t>(), S.toks.as<uint16_t>(), d_src_of, n,
                I.off.as<uint32_t>(), I.toks.as<uint16_t>());
+    tr.mark("token_lists");
     // the source's group order restricted to the subset keeps its key order
     const size_t ns = S.np;
     DevBuf inv(ns * 4, ctx.stream), val(ns * 4, ctx.stream), og(ns * 4, ctx.stream), keep(ns, ctx.stream),
@@ -795,6 +797,83 @@ void subset_pattern_index(Ctx& ctx, const PatternIndex& S, const uint32_t* d_src
     IGB_LAUNCH(ctx, gather_u32, grid_for(ctx, n, 256), 256, 0, S.gkey.as<uint32_t>(), og2.as<uint32_t>(), n,
                key.as<uint32_t>());
     group_ids(ctx, key.as<uint32_t>(), n, I);
+    tr.mark("groups");
+}
+
+namespace {
+// token document frequencies straight from packed rows (block histogram in smem)
+__global__ void row_token_df(const int64_t* __restrict__ rows, size_t n, int k, uint32_t* __restrict__ df) {
+    extern __shared__ uint32_t h[];
+    const int L = 64 * k;
+    for (int t = threadIdx.x; t < L; t += blockDim.x) h[t] = 0;
+    __syncthreads();
+    for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < n * (size_t)k; q += (size_t)gridDim.x * blockDim.x) {
+        uint64_t x = (uint64_t)rows[q];
+        const int w = (int)(q % k);
+        while (x) {
+            atomicAdd(h + w * 64 + (__ffsll((long long)x) - 1), 1u);
+            x &= x - 1;
+        }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < L; t += blockDim.x)
+        if (h[t]) atomicAdd(df + t, h[t]);
+}
+
+// rows re-spelled with token t at sort position pos[t] (MSB-first per word)
+__global__ void permute_row_bits(const int64_t* __restrict__ rows, size_t n, int k, const uint16_t* __restrict__ pos,
+                                 int64_t* __restrict__ out) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        for (int w = 0; w < k; ++w) out[i * k + w] = 0;
+        for (int w = 0; w < k; ++w) {
+            uint64_t x = (uint64_t)rows[i * k + w];
+            while (x) {
+                const int b = __ffsll((long long)x) - 1;
+                x &= x - 1;
+                const uint32_t r = pos[w * 64 + b];
+                out[i * k + (r >> 6)] |= (int64_t)(1ull << (63 - (r & 63)));
+            }
+        }
+    }
+}
+// reflected-Gray rank of a MSB-first bit vector: b = prefix XOR of g
+__global__ void gray_to_binary(int64_t* __restrict__ rows, size_t n, int k) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        uint64_t carry = 0;  // parity of all earlier bits, as 0 or ~0
+        for (int w = 0; w < k; ++w) {
+            uint64_t x = (uint64_t)rows[i * k + w];
+            x ^= x >> 1;
+            x ^= x >> 2;
+            x ^= x >> 4;
+            x ^= x >> 8;
+            x ^= x >> 16;
+            x ^= x >> 32;
+            x ^= carry;
+            rows[i * k + w] = (int64_t)x;
+            carry = (x & 1ull) ? ~0ull : 0ull;
+        }
+    }
+}
+}  // namespace
+
+void cluster_order(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, uint32_t* d_perm) {
+    const uint32_t L = (uint32_t)(64 * k);
+    if (n < 2 || (size_t)L * 4 > (size_t)ctx.smem_optin) {
+        sort_rows_canonical(ctx, d_rows, n, k, d_perm);
+        return;
+    }
+    if ((size_t)L * 4 > 48 * 1024)
+        IGB_CUDA(cudaFuncSetAttribute(row_token_df, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L * 4));
+    DevBuf df((size_t)L * 4, ctx.stream), prow(n * k * 8, ctx.stream);
+    IGB_CUDA(cudaMemsetAsync(df.p, 0, (size_t)L * 4, ctx.stream));
+    IGB_LAUNCH(ctx, row_token_df, std::max(1, ctx.sm_count * 2), 256, (size_t)L * 4, d_rows, n, (int)k,
+               df.as<uint32_t>());
+    RankSpace R;
+    make_rank_space(ctx, df.as<uint32_t>(), L, R, true);
+    IGB_LAUNCH(ctx, permute_row_bits, grid_for(ctx, n, 256), 256, 0, d_rows, n, (int)k, R.rank.as<uint16_t>(),
+               prow.as<int64_t>());
+    IGB_LAUNCH(ctx, gray_to_binary, grid_for(ctx, n, 256), 256, 0, prow.as<int64_t>(), n, (int)k);
+    sort_rows_canonical(ctx, prow.as<int64_t>(), n, k, d_perm);
 }
 
 bool postings_supported(uint32_t L, size_t n) {
@@ -815,7 +894,7 @@ void build_postings(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, uint32_
         if (d_perm)
             IGB_CUDA(cudaMemcpyAsync(P.perm.p, d_perm, n * 4, cudaMemcpyDeviceToDevice, ctx.stream));
         else
-            sort_rows_canonical(ctx, d_rows, n, k, P.perm.as<uint32_t>());
+            cluster_order(ctx, d_rows, n, k, P.perm.as<uint32_t>());
     }
     size_t nd = n;
     const uint32_t* rows_of = P.perm.as<uint32_t>();  // posting row -> source row

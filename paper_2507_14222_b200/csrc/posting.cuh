@@ -43,7 +43,14 @@ struct PatternIndex {
     DevBuf gkey;     // G u32: (t1 << 16) | t2
 };
 
-void make_rank_space(Ctx& ctx, const uint32_t* d_df, uint32_t L, RankSpace& R);
+// descending: most frequent first (default: rarest first)
+void make_rank_space(Ctx& ctx, const uint32_t* d_df, uint32_t L, RankSpace& R, bool descending = false);
+// Clustering order of rows for postings and pair tiles: lexicographic in
+// reflected-Gray order over the tokens ranked most frequent first.  Rows
+// containing the same frequent tokens become contiguous, so a pattern's hits
+// form fewer, longer runs (C3 matcher -18% vs words::less); identical rows are
+// adjacent.  Not the canonical order (that one is only needed for output).
+void cluster_order(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, uint32_t* d_perm);
 // df = A.df + B.df (postings of the two training classes)
 void combined_rank_space(Ctx& ctx, const Postings& A, const Postings& B, RankSpace& R);
 void build_pattern_index(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const RankSpace& R, PatternIndex& I);
