@@ -328,7 +328,7 @@ def run_b200(args):
     h2d = cols_tr.nbytes + cols_te.nbytes
     d2h = 2 * n_test * 8
 
-    # ---- roofline of the dominant kernel: the matcher (kernel 6, posting_scan<kMatch>)
+    # ---- roofline of the dominant kernel: the matcher (kernel 6, grouped_scan<kMatch>)
     P = [model.count(0, 1), model.count(1, 1)]
     K = (tenc.logical_len + 63) // 64
     ctx.set_diagnostics(True)
@@ -341,7 +341,7 @@ def run_b200(args):
     peak_words = lop3_s / 2 / 1e9   # a 64-bit word AND = 2 LOP3.32
     achieved = words / (kms * 1e-3) / 1e9
     horiz = (P[0] + P[1]) * n_test * K * reps
-    roofline = {"bound": "int", "kernel": "posting_scan<kMatch> (matcher, kernel 6)", "achieved": achieved,
+    roofline = {"bound": "int", "kernel": "grouped_scan<kMatch> (matcher, kernel 6)", "achieved": achieved,
                 "peak": peak_words, "unit": "Gword/s", "frac": achieved / peak_words, "traffic": None,
                 "algorithmic_work": (f"posting-list intersection: sum over pure patterns of |b| x nnz-words(rarest "
                                      f"token) = {words // reps} 64-bit word-ANDs per evidence call "

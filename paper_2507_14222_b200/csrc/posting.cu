@@ -278,12 +278,15 @@ __global__ void sub_count(const uint32_t* __restrict__ src_off, const uint32_t* 
     }
 }
 
+// warp per pattern: coalesced token copies
 __global__ void sub_copy(const uint32_t* __restrict__ src_off, const uint16_t* __restrict__ src_toks,
                          const uint32_t* __restrict__ src_of, size_t n, const uint32_t* __restrict__ off,
                          uint16_t* __restrict__ toks) {
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    for (size_t i = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n;
+         i += ((size_t)gridDim.x * blockDim.x) >> 5) {
         const uint32_t s = src_of[i], b = src_off[s], m = src_off[s + 1] - b, o = off[i];
-        for (uint32_t t = 0; t < m; ++t) toks[o + t] = src_toks[b + t];
+        for (uint32_t t = lane; t < m; t += 32) toks[o + t] = src_toks[b + t];
     }
 }
 
@@ -774,7 +777,7 @@ void subset_pattern_index(Ctx& ctx, const PatternIndex& S, const uint32_t* d_src
     IGB_CUDA(cudaStreamSynchronize(ctx.stream));
     I.toks.alloc(std::max<size_t>(total, 1) * 2, ctx.stream);
     if (n == 0) return;
-    IGB_LAUNCH(ctx, sub_copy, grid_for(ctx, n, 256), 256, 0, S.off.as<uint32_t>(), S.toks.as<uint16_t>(), d_src_of, n,
+    IGB_LAUNCH(ctx, sub_copy, grid_for(ctx, n * 32, 256), 256, 0, S.off.as<uint32_t>(), S.toks.as<uint16_t>(), d_src_of, n,
                I.off.as<uint32_t>(), I.toks.as<uint16_t>());
     tr.mark("token_lists");
     // the source's group order restricted to the subset keeps its key order
