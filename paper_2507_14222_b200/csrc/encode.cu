@@ -146,41 +146,45 @@ __global__ void pack_cells(const int64_t* __restrict__ codes, size_t n, int n_fe
 }
 
 // Run heads of the canonically sorted rows: head[i] = rows differ from i-1.
-__global__ void run_heads(const int64_t* __restrict__ rows, const uint32_t* __restrict__ perm, size_t n, int k,
-                          uint32_t* __restrict__ head) {
+
+
+
+// Anti-contradiction grouping without sorting: every row joins the hash slot
+// of its exact content (open addressing; a slot holds the first row's index + 1,
+// equality is checked on all K words), and ORs its class into the slot.
+__global__ void group_insert(const int64_t* __restrict__ rows, size_t n, int k, unsigned int* __restrict__ slot_row,
+                             uint32_t mask, const uint8_t* __restrict__ attack, unsigned int* __restrict__ slot_cls,
+                             uint32_t* __restrict__ grp) {
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-        uint32_t h = 1;
-        if (i > 0) {
-            const int64_t* a = rows + (size_t)perm[i] * k;
-            const int64_t* b = rows + (size_t)perm[i - 1] * k;
-            h = 0;
-            for (int w = 0; w < k; ++w)
-                if (a[w] != b[w]) {
-                    h = 1;
-                    break;
-                }
+        const int64_t* a = rows + i * k;
+        uint64_t h = 0x9e3779b97f4a7c15ull;
+        for (int w = 0; w < k; ++w) h = mix64(h ^ (uint64_t)a[w]);
+        uint32_t s = (uint32_t)h & mask;
+        for (;; s = (s + 1) & mask) {
+            unsigned int cur = slot_row[s];
+            if (cur == 0u) {
+                cur = atomicCAS(slot_row + s, 0u, (unsigned int)i + 1u);
+                if (cur == 0u) break;  // first row of this content
+            }
+            const int64_t* b = rows + (size_t)(cur - 1u) * k;
+            bool same = true;
+            for (int w = 0; w < k && same; ++w) same = a[w] == b[w];
+            if (same) break;
         }
-        head[i] = h;
+        grp[i] = s;
+        atomicOr(slot_cls + s, attack[i] ? 1u : 2u);
     }
 }
 
-__global__ void run_classes(const uint32_t* __restrict__ run_id, const uint32_t* __restrict__ perm,
-                            const uint8_t* __restrict__ attack, size_t n, uint32_t* __restrict__ run_cls) {
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
-        atomicOr(run_cls + run_id[i] - 1, attack[perm[i]] ? 1u : 2u);
-}
-
-// Per source row: keep flags per class and the contradiction flag.
-__global__ void row_flags(const uint32_t* __restrict__ run_id, const uint32_t* __restrict__ perm,
-                          const uint32_t* __restrict__ run_cls, const uint8_t* __restrict__ attack, size_t n,
-                          uint8_t* __restrict__ keep_a, uint8_t* __restrict__ keep_n, uint8_t* __restrict__ removed) {
+__global__ void group_flags(const uint32_t* __restrict__ grp, const unsigned int* __restrict__ slot_cls,
+                            const uint8_t* __restrict__ attack, size_t n, uint8_t* __restrict__ keep_a,
+                            uint8_t* __restrict__ keep_n, uint8_t* __restrict__ removed) {
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-        const uint32_t src = perm[i];
-        const bool contra = run_cls[run_id[i] - 1] == 3u;
-        const bool a = attack[src] != 0;
-        keep_a[src] = (!contra && a) ? 1 : 0;
-        keep_n[src] = (!contra && !a) ? 1 : 0;
-        removed[src] = contra ? 1 : 0;
+        const bool contra = slot_cls[grp[i]] == 3u;
+        const bool a = attack[i] != 0;
+        keep_a[i] = (!contra && a) ? 1 : 0;
+        keep_n[i] = (!contra && !a) ? 1 : 0;
+        removed[i] = contra ? 1 : 0;
     }
 }
 
@@ -403,21 +407,16 @@ void encode_training_dev(Ctx& ctx, const ig_columns& c, ig_encoding& e) {
     size_t n_att = 0;
     for (uint8_t a : c.is_attack) n_att += a;
     if (n_att == 0 || n_att == n) fail(IG_E_DATA, "training data must contain both attack and normal instances");
-    DevBuf perm(n * 4, ctx.stream), head(n * 4, ctx.stream), rid(n * 4, ctx.stream), rcls(n * 4, ctx.stream);
-    sort_rows_canonical(ctx, all.data(), n, k, perm.as<uint32_t>());
-    IGB_LAUNCH(ctx, run_heads, grid_for(ctx, n, 256), 256, 0, all.data(), perm.as<uint32_t>(), n, (int)k,
-               head.as<uint32_t>());
-    size_t tb = 0;
-    IGB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, head.as<uint32_t>(), rid.as<uint32_t>(), (int64_t)n, ctx.stream));
-    DevBuf temp(tb, ctx.stream);
-    IGB_CUDA(cub::DeviceScan::InclusiveSum(temp.p, tb, head.as<uint32_t>(), rid.as<uint32_t>(), (int64_t)n, ctx.stream));
-    IGB_CUDA(cudaMemsetAsync(rcls.p, 0, n * 4, ctx.stream));
-    IGB_LAUNCH(ctx, run_classes, grid_for(ctx, n, 256), 256, 0, rid.as<uint32_t>(), perm.as<uint32_t>(),
-               d.attack_ptr, n, rcls.as<uint32_t>());
+    uint32_t slots = 1024;
+    while (slots < 2 * n) slots <<= 1;
+    DevBuf slot_row((size_t)slots * 4, ctx.stream), slot_cls((size_t)slots * 4, ctx.stream), grp(n * 4, ctx.stream);
+    IGB_CUDA(cudaMemsetAsync(slot_row.p, 0, (size_t)slots * 4, ctx.stream));
+    IGB_CUDA(cudaMemsetAsync(slot_cls.p, 0, (size_t)slots * 4, ctx.stream));
+    IGB_LAUNCH(ctx, group_insert, grid_for(ctx, n, 256), 256, 0, all.data(), n, (int)k, slot_row.as<unsigned int>(),
+               slots - 1, d.attack_ptr, slot_cls.as<unsigned int>(), grp.as<uint32_t>());
     DevBuf keep_a(n, ctx.stream), keep_n(n, ctx.stream), removed(n, ctx.stream);
-    IGB_LAUNCH(ctx, row_flags, grid_for(ctx, n, 256), 256, 0, rid.as<uint32_t>(), perm.as<uint32_t>(),
-               rcls.as<uint32_t>(), d.attack_ptr, n, keep_a.as<uint8_t>(), keep_n.as<uint8_t>(),
-               removed.as<uint8_t>());
+    IGB_LAUNCH(ctx, group_flags, grid_for(ctx, n, 256), 256, 0, grp.as<uint32_t>(), slot_cls.as<unsigned int>(),
+               d.attack_ptr, n, keep_a.as<uint8_t>(), keep_n.as<uint8_t>(), removed.as<uint8_t>());
     DevBuf idx_a, idx_n, idx_r;
     const size_t na = select_flagged(ctx, keep_a.as<uint8_t>(), n, idx_a);
     const size_t nn = select_flagged(ctx, keep_n.as<uint8_t>(), n, idx_n);
