@@ -44,9 +44,6 @@ __device__ __forceinline__ ulonglong2 cas128(ulonglong2* addr, ulonglong2 cmp, u
     return old;
 }
 
-__device__ __forceinline__ unsigned long long ldv(const unsigned long long* p) {
-    return *reinterpret_cast<const volatile unsigned long long*>(p);
-}
 
 // slot = {value, tag}; tag 0 = empty, 1 = present, 2 + rank after ranking.
 __global__ void column_insert(const int64_t* __restrict__ words, size_t n, int k, ulonglong2* __restrict__ tables,
@@ -113,6 +110,40 @@ __global__ void write_ranks(const uint32_t* __restrict__ where, size_t m, uint32
         const uint32_t w = q / slots;
         tables[q].y = 2ull + (i - col_start[w]);
     }
+}
+
+// Small columns (every column <= kRankSmall distinct values): per-column
+// segments of the distinct values, then each value's rank = #smaller values
+// of its column, counted against the column staged in shared memory.
+constexpr uint32_t kRankSmall = 4096;
+__global__ void column_collect_seg(const ulonglong2* __restrict__ tables, int k, uint32_t slots,
+                                   unsigned int* __restrict__ cursor, unsigned long long* __restrict__ vals,
+                                   uint32_t* __restrict__ where) {
+    const size_t total = (size_t)k * slots;
+    for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += (size_t)gridDim.x * blockDim.x) {
+        const ulonglong2 e = tables[q];
+        if (e.y != 0) {
+            const unsigned int o = atomicAdd(cursor + q / slots, 1u);
+            vals[o] = e.x;
+            where[o] = (uint32_t)q;
+        }
+    }
+}
+
+__global__ void column_rank_small(const unsigned long long* __restrict__ vals, const uint32_t* __restrict__ where,
+                                  const unsigned int* __restrict__ cstart, ulonglong2* __restrict__ tables) {
+    __shared__ unsigned long long sv[kRankSmall];
+    const int w = blockIdx.x;
+    const uint32_t b = cstart[w], d = cstart[w + 1] - b;
+    const uint32_t i = blockIdx.y * blockDim.x + threadIdx.x;
+    if (blockIdx.y * blockDim.x >= d) return;  // whole block past this column (uniform)
+    for (uint32_t j = threadIdx.x; j < d; j += blockDim.x) sv[j] = vals[b + j];
+    __syncthreads();
+    if (i >= d) return;
+    const unsigned long long v = sv[i];
+    uint32_t r = 0;
+    for (uint32_t j = 0; j < d; ++j) r += sv[j] < v ? 1u : 0u;
+    tables[where[b + i]].y = 2ull + r;
 }
 
 struct Field {
@@ -308,34 +339,52 @@ void sort_rows_canonical(Ctx& ctx, const int64_t* d_words, size_t n, size_t k, u
     tr.mark("column_hash");
     // Rank the distinct values of every column.
     uint64_t m = 0;
-    for (size_t w = 0; w < k; ++w) m += hc[w];
-    DevBuf vals(m * 8, ctx.stream), vals2(m * 8, ctx.stream), where(m * 4, ctx.stream), where2(m * 4, ctx.stream),
-        col(m * 4, ctx.stream), col2(m * 4, ctx.stream), nout(4, ctx.stream), cstart((k + 1) * 4, ctx.stream);
-    IGB_CUDA(cudaMemsetAsync(nout.p, 0, 4, ctx.stream));
-    IGB_LAUNCH(ctx, column_collect, grid_for(ctx, (size_t)k * slots, 256), 256, 0, tables.as<ulonglong2>(), (int)k,
-               slots, vals.as<unsigned long long>(), where.as<uint32_t>(), nout.as<unsigned int>());
-    size_t tb1 = 0, tb2 = 0;
-    IGB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb1, vals.as<unsigned long long>(),
-                                             vals2.as<unsigned long long>(), where.as<uint32_t>(),
-                                             where2.as<uint32_t>(), (int64_t)m, 0, 64, ctx.stream));
-    IGB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb2, col.as<uint32_t>(), col2.as<uint32_t>(),
-                                             where2.as<uint32_t>(), where.as<uint32_t>(), (int64_t)m, 0, 32,
-                                             ctx.stream));
-    DevBuf temp(std::max(tb1, tb2), ctx.stream);
-    IGB_CUDA(cub::DeviceRadixSort::SortPairs(temp.p, tb1, vals.as<unsigned long long>(),
-                                             vals2.as<unsigned long long>(), where.as<uint32_t>(),
-                                             where2.as<uint32_t>(), (int64_t)m, 0, 64, ctx.stream));
-    IGB_LAUNCH(ctx, column_of, grid_for(ctx, m, 256), 256, 0, where2.as<uint32_t>(), m, slots, col.as<uint32_t>());
-    int cbits = 1;
-    while ((1ull << cbits) < k) ++cbits;
-    IGB_CUDA(cub::DeviceRadixSort::SortPairs(temp.p, tb2, col.as<uint32_t>(), col2.as<uint32_t>(),
-                                             where2.as<uint32_t>(), where.as<uint32_t>(), (int64_t)m, 0, cbits,
-                                             ctx.stream));
-    std::vector<unsigned int> hstart(k + 1, 0);
-    for (size_t w = 0; w < k; ++w) hstart[w + 1] = hstart[w] + hc[w];
-    IGB_CUDA(cudaMemcpyAsync(cstart.p, hstart.data(), (k + 1) * 4, cudaMemcpyHostToDevice, ctx.stream));
-    IGB_LAUNCH(ctx, write_ranks, grid_for(ctx, m, 256), 256, 0, where.as<uint32_t>(), m, slots,
-               cstart.as<unsigned int>(), tables.as<ulonglong2>());
+    uint32_t dmax = 0;
+    for (size_t w = 0; w < k; ++w) {
+        m += hc[w];
+        dmax = std::max<uint32_t>(dmax, hc[w]);
+    }
+    if (dmax <= kRankSmall) {
+        std::vector<unsigned int> hs(k + 1, 0);
+        for (size_t w = 0; w < k; ++w) hs[w + 1] = hs[w] + hc[w];
+        DevBuf vals(m * 8, ctx.stream), where(m * 4, ctx.stream), cstart((k + 1) * 4, ctx.stream),
+            cursor((k + 1) * 4, ctx.stream);
+        IGB_CUDA(cudaMemcpyAsync(cstart.p, hs.data(), (k + 1) * 4, cudaMemcpyHostToDevice, ctx.stream));
+        IGB_CUDA(cudaMemcpyAsync(cursor.p, cstart.p, (k + 1) * 4, cudaMemcpyDeviceToDevice, ctx.stream));
+        IGB_LAUNCH(ctx, column_collect_seg, grid_for(ctx, (size_t)k * slots, 256), 256, 0, tables.as<ulonglong2>(),
+                   (int)k, slots, cursor.as<unsigned int>(), vals.as<unsigned long long>(), where.as<uint32_t>());
+        const dim3 grid((unsigned)k, (dmax + 255) / 256);
+        IGB_LAUNCH(ctx, column_rank_small, grid, 256, 0, vals.as<unsigned long long>(), where.as<uint32_t>(),
+                   cstart.as<unsigned int>(), tables.as<ulonglong2>());
+    } else {
+        DevBuf vals(m * 8, ctx.stream), vals2(m * 8, ctx.stream), where(m * 4, ctx.stream), where2(m * 4, ctx.stream),
+            col(m * 4, ctx.stream), col2(m * 4, ctx.stream), nout(4, ctx.stream), cstart((k + 1) * 4, ctx.stream);
+        IGB_CUDA(cudaMemsetAsync(nout.p, 0, 4, ctx.stream));
+        IGB_LAUNCH(ctx, column_collect, grid_for(ctx, (size_t)k * slots, 256), 256, 0, tables.as<ulonglong2>(), (int)k,
+                   slots, vals.as<unsigned long long>(), where.as<uint32_t>(), nout.as<unsigned int>());
+        size_t tb1 = 0, tb2 = 0;
+        IGB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb1, vals.as<unsigned long long>(),
+                                                 vals2.as<unsigned long long>(), where.as<uint32_t>(),
+                                                 where2.as<uint32_t>(), (int64_t)m, 0, 64, ctx.stream));
+        IGB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb2, col.as<uint32_t>(), col2.as<uint32_t>(),
+                                                 where2.as<uint32_t>(), where.as<uint32_t>(), (int64_t)m, 0, 32,
+                                                 ctx.stream));
+        DevBuf temp(std::max(tb1, tb2), ctx.stream);
+        IGB_CUDA(cub::DeviceRadixSort::SortPairs(temp.p, tb1, vals.as<unsigned long long>(),
+                                                 vals2.as<unsigned long long>(), where.as<uint32_t>(),
+                                                 where2.as<uint32_t>(), (int64_t)m, 0, 64, ctx.stream));
+        IGB_LAUNCH(ctx, column_of, grid_for(ctx, m, 256), 256, 0, where2.as<uint32_t>(), m, slots, col.as<uint32_t>());
+        int cbits = 1;
+        while ((1ull << cbits) < k) ++cbits;
+        IGB_CUDA(cub::DeviceRadixSort::SortPairs(temp.p, tb2, col.as<uint32_t>(), col2.as<uint32_t>(),
+                                                 where2.as<uint32_t>(), where.as<uint32_t>(), (int64_t)m, 0, cbits,
+                                                 ctx.stream));
+        std::vector<unsigned int> hstart(k + 1, 0);
+        for (size_t w = 0; w < k; ++w) hstart[w + 1] = hstart[w] + hc[w];
+        IGB_CUDA(cudaMemcpyAsync(cstart.p, hstart.data(), (k + 1) * 4, cudaMemcpyHostToDevice, ctx.stream));
+        IGB_LAUNCH(ctx, write_ranks, grid_for(ctx, m, 256), 256, 0, where.as<uint32_t>(), m, slots,
+                   cstart.as<unsigned int>(), tables.as<ulonglong2>());
+    }
     tr.mark("column_ranks");
     // Packed keys and LSD over the key words (least significant word first).
     DevBuf dfields(k * sizeof(Field), ctx.stream), keys((size_t)n_keys * n * 8, ctx.stream);
