@@ -268,7 +268,8 @@ void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m, bool enumerate 
             igb::compose_u32(cx, kept.as<uint32_t>(), order.p ? order.as<uint32_t>() : nullptr, n,
                              src.as<uint32_t>());
             igb::subset_pattern_index(cx, CI[c], src.as<uint32_t>(), n, m.pidx[c]);
-            for (DevBuf* b : {&m.pidx[c].off, &m.pidx[c].toks, &m.pidx[c].order, &m.pidx[c].gid, &m.pidx[c].gkey})
+            for (DevBuf* b : {&m.pidx[c].beg, &m.pidx[c].len, m.pidx[c].toks.get(), &m.pidx[c].order, &m.pidx[c].gid,
+                              &m.pidx[c].gkey})
                 b->persist();
             tr.mark("pure_index");
         }

@@ -269,24 +269,14 @@ __global__ void add_u32(const uint32_t* __restrict__ a, const uint32_t* __restri
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = a[i] + b[i];
 }
 
-// subset index: token counts of the chosen source patterns
-__global__ void sub_count(const uint32_t* __restrict__ src_off, const uint32_t* __restrict__ src_of, size_t n,
-                          uint32_t* __restrict__ cnt) {
+// subset index: the chosen source patterns' token-list extents
+__global__ void sub_lists(const uint32_t* __restrict__ src_beg, const uint32_t* __restrict__ src_len,
+                          const uint32_t* __restrict__ src_of, size_t n, uint32_t* __restrict__ beg,
+                          uint32_t* __restrict__ len) {
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
         const uint32_t s = src_of[i];
-        cnt[i] = src_off[s + 1] - src_off[s];
-    }
-}
-
-// warp per pattern: coalesced token copies
-__global__ void sub_copy(const uint32_t* __restrict__ src_off, const uint16_t* __restrict__ src_toks,
-                         const uint32_t* __restrict__ src_of, size_t n, const uint32_t* __restrict__ off,
-                         uint16_t* __restrict__ toks) {
-    const int lane = threadIdx.x & 31;
-    for (size_t i = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n;
-         i += ((size_t)gridDim.x * blockDim.x) >> 5) {
-        const uint32_t s = src_of[i], b = src_off[s], m = src_off[s + 1] - b, o = off[i];
-        for (uint32_t t = lane; t < m; t += 32) toks[o + t] = src_toks[b + t];
+        beg[i] = src_beg[s];
+        len[i] = src_len[s];
     }
 }
 
@@ -327,10 +317,11 @@ __global__ void gather_u32(const uint32_t* __restrict__ src, const uint32_t* __r
 // C3 ~1M patterns fall into ~35k groups, so most of the (t1, t2) work is shared.
 constexpr uint32_t kNoTok = 0xffffu;
 
-__global__ void group_keys(const uint32_t* __restrict__ tok_off, const uint16_t* __restrict__ toks, size_t np,
+__global__ void group_keys(const uint32_t* __restrict__ tok_beg, const uint32_t* __restrict__ tok_len,
+                           const uint16_t* __restrict__ toks, size_t np,
                            uint32_t* __restrict__ key, uint32_t* __restrict__ idx) {
     for (size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += (size_t)gridDim.x * blockDim.x) {
-        const uint32_t o = tok_off[p], m = tok_off[p + 1] - o;
+        const uint32_t o = tok_beg[p], m = tok_len[p];
         const uint32_t t1 = m >= 1 ? toks[o] : kNoTok, t2 = m >= 2 ? toks[o + 1] : kNoTok;
         key[p] = (t1 << 16) | t2;
         idx[p] = (uint32_t)p;
@@ -456,7 +447,8 @@ __device__ __forceinline__ unsigned long long ld_tok(const unsigned long long* c
 template <int MODE>
 __global__ void __launch_bounds__(256)
 grouped_scan(const unsigned long long* __restrict__ dense, size_t W, size_t n_rows,
-             const uint32_t* __restrict__ tok_off, const uint16_t* __restrict__ toks, size_t np,
+             const uint32_t* __restrict__ tok_beg, const uint32_t* __restrict__ tok_len,
+             const uint16_t* __restrict__ toks, size_t np,
              const uint32_t* __restrict__ order, const uint32_t* __restrict__ gid,
              const unsigned long long* __restrict__ goff, const uint32_t* __restrict__ glen,
              const uint32_t* __restrict__ ew, const unsigned long long* __restrict__ em,
@@ -468,8 +460,8 @@ grouped_scan(const unsigned long long* __restrict__ dense, size_t W, size_t n_ro
     for (size_t i = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < np; i += warps) {
         const uint32_t p = order[i];
         const uint32_t g = gid[i];
-        const uint32_t o = tok_off[p];
-        const uint32_t m = tok_off[p + 1] - o;
+        const uint32_t o = tok_beg[p];
+        const uint32_t m = tok_len[p];
         const uint32_t Wu = (uint32_t)W, wb = Wu * 8u;
         // lane l holds token l (l < m); lanes past the pattern repeat token 0,
         // whose posting already contains every surviving word of the group
@@ -545,13 +537,13 @@ grouped_scan(const unsigned long long* __restrict__ dense, size_t W, size_t n_ro
 
 // diagnostics: word-ANDs of the grouped algorithm without early exit
 //   Σ_groups ub(g) * min(2, |t1,t2|) + Σ_patterns glen(g(p)) * max(0, m_p - 2)
-__global__ void grouped_work(const uint32_t* __restrict__ tok_off, size_t np, const uint32_t* __restrict__ order,
+__global__ void grouped_work(const uint32_t* __restrict__ tok_len, size_t np, const uint32_t* __restrict__ order,
                              const uint32_t* __restrict__ gid, const uint32_t* __restrict__ glen,
                              unsigned long long* __restrict__ out) {
     unsigned long long acc = 0;
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < np; i += (size_t)gridDim.x * blockDim.x) {
         const uint32_t p = order[i];
-        const uint32_t m = tok_off[p + 1] - tok_off[p];
+        const uint32_t m = tok_len[p];
         if (m > 2) acc += (unsigned long long)glen[gid[i]] * (m - 2);
     }
     for (int s = 16; s; s >>= 1) acc += __shfl_xor_sync(kFull, acc, s);
@@ -612,7 +604,8 @@ void launch_scan(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Post
     tr.mark("group_lists");
     const size_t blocks = std::min<size_t>((np + 7) / 8, (size_t)ctx.sm_count * 64);
     IGB_LAUNCH(ctx, grouped_scan<MODE>, (unsigned)blocks, 256, 0, P.dense.as<unsigned long long>(), P.W, P.n,
-               I->off.as<uint32_t>(), I->toks.as<uint16_t>(), np, I->order.as<uint32_t>(), I->gid.as<uint32_t>(),
+               I->beg.as<uint32_t>(), I->len.as<uint32_t>(), I->toks->as<uint16_t>(), np, I->order.as<uint32_t>(),
+               I->gid.as<uint32_t>(),
                goff.as<unsigned long long>(), glen.as<uint32_t>(), ew.as<uint32_t>(), em.as<unsigned long long>(),
                scores, acc, support, cover, flags);
     tr.mark("grouped_scan");
@@ -620,7 +613,7 @@ void launch_scan(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Post
         IGB_CUDA(cudaEventRecord(e1, ctx.stream));
         DevBuf w(8, ctx.stream);
         IGB_CUDA(cudaMemsetAsync(w.p, 0, 8, ctx.stream));
-        IGB_LAUNCH(ctx, grouped_work, grid_for(ctx, np, 256), 256, 0, I->off.as<uint32_t>(), np,
+        IGB_LAUNCH(ctx, grouped_work, grid_for(ctx, np, 256), 256, 0, I->len.as<uint32_t>(), np,
                    I->order.as<uint32_t>(), I->gid.as<uint32_t>(), glen.as<uint32_t>(), w.as<unsigned long long>());
         if (G)
             IGB_LAUNCH(ctx, group_work, grid_for(ctx, G, 256), 256, 0, I->gkey.as<uint32_t>(),
@@ -671,25 +664,26 @@ void build_pattern_index(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, co
     Trace tr(ctx, "pattern_index", -1);
     I.np = np;
     I.G = 0;
-    I.off.alloc((np + 1) * 4, ctx.stream);
+    I.beg.alloc((np + 1) * 4, ctx.stream);  // CSR offsets (np + 1)
+    I.len.alloc((np + 1) * 4, ctx.stream);
     I.order.alloc(std::max<size_t>(np, 1) * 4, ctx.stream);
     I.gid.alloc(std::max<size_t>(np, 1) * 4, ctx.stream);
     I.gkey.alloc(std::max<size_t>(np, 1) * 4, ctx.stream);
     // CSR token lists, rarest first in R
-    DevBuf cnt((np + 1) * 4, ctx.stream);
     if (np)
-        IGB_LAUNCH(ctx, pattern_token_count, grid_for(ctx, np, 256), 256, 0, d_pat, np, (int)k, cnt.as<uint32_t>());
-    IGB_CUDA(cudaMemsetAsync(cnt.as<uint32_t>() + np, 0, 4, ctx.stream));
+        IGB_LAUNCH(ctx, pattern_token_count, grid_for(ctx, np, 256), 256, 0, d_pat, np, (int)k, I.len.as<uint32_t>());
+    IGB_CUDA(cudaMemsetAsync(I.len.as<uint32_t>() + np, 0, 4, ctx.stream));
     size_t tb = 0;
-    IGB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.as<uint32_t>(), I.off.as<uint32_t>(), (int64_t)np + 1,
+    IGB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, I.len.as<uint32_t>(), I.beg.as<uint32_t>(), (int64_t)np + 1,
                                            ctx.stream));
     DevBuf temp(tb, ctx.stream);
-    IGB_CUDA(cub::DeviceScan::ExclusiveSum(temp.p, tb, cnt.as<uint32_t>(), I.off.as<uint32_t>(), (int64_t)np + 1,
+    IGB_CUDA(cub::DeviceScan::ExclusiveSum(temp.p, tb, I.len.as<uint32_t>(), I.beg.as<uint32_t>(), (int64_t)np + 1,
                                            ctx.stream));
     uint32_t total = 0;
-    IGB_CUDA(cudaMemcpyAsync(&total, I.off.as<uint32_t>() + np, 4, cudaMemcpyDeviceToHost, ctx.stream));
+    IGB_CUDA(cudaMemcpyAsync(&total, I.beg.as<uint32_t>() + np, 4, cudaMemcpyDeviceToHost, ctx.stream));
     IGB_CUDA(cudaStreamSynchronize(ctx.stream));
-    I.toks.alloc(std::max<size_t>(total, 1) * 2, ctx.stream);
+    I.toks = std::make_shared<DevBuf>();
+    I.toks->alloc(std::max<size_t>(total, 1) * 2, ctx.stream);
     if (np == 0) return;
     const uint32_t L = R.L;
     if (k <= kRankWords) {
@@ -700,7 +694,7 @@ void build_pattern_index(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, co
             IGB_CUDA(cudaFuncSetAttribute(pattern_token_fill_rank<KW>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                           (int)smem));                                                             \
         IGB_LAUNCH(ctx, pattern_token_fill_rank<KW>, grid_for(ctx, np, 128), 128, smem, d_pat, np, (int)k,         \
-                   R.rank.as<uint16_t>(), R.byrank.as<uint16_t>(), L, I.off.as<uint32_t>(), I.toks.as<uint16_t>()); \
+                   R.rank.as<uint16_t>(), R.byrank.as<uint16_t>(), L, I.beg.as<uint32_t>(), I.toks->as<uint16_t>()); \
     }
         if (k <= 16)
             IGB_FILL_RANK(16)
@@ -714,12 +708,13 @@ void build_pattern_index(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, co
         if (smem > 48 * 1024)
             IGB_CUDA(cudaFuncSetAttribute(pattern_token_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         IGB_LAUNCH(ctx, pattern_token_fill, grid_for(ctx, np, 128), 128, smem, d_pat, np, (int)k,
-                   R.df.as<uint32_t>(), L, I.off.as<uint32_t>(), I.toks.as<uint16_t>());
+                   R.df.as<uint32_t>(), L, I.beg.as<uint32_t>(), I.toks->as<uint16_t>());
     }
     tr.mark("token_lists");
     // group patterns by their two rarest tokens
     DevBuf key(np * 4, ctx.stream), key2(np * 4, ctx.stream), idx(np * 4, ctx.stream);
-    IGB_LAUNCH(ctx, group_keys, grid_for(ctx, np, 256), 256, 0, I.off.as<uint32_t>(), I.toks.as<uint16_t>(), np,
+    IGB_LAUNCH(ctx, group_keys, grid_for(ctx, np, 256), 256, 0, I.beg.as<uint32_t>(), I.len.as<uint32_t>(),
+               I.toks->as<uint16_t>(), np,
                key.as<uint32_t>(), idx.as<uint32_t>());
     size_t tb1 = 0;
     IGB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb1, key.as<uint32_t>(), key2.as<uint32_t>(), idx.as<uint32_t>(),
@@ -757,28 +752,15 @@ void subset_pattern_index(Ctx& ctx, const PatternIndex& S, const uint32_t* d_src
     Trace tr(ctx, "subset_index", -1);
     I.np = n;
     I.G = 0;
-    I.off.alloc((n + 1) * 4, ctx.stream);
+    I.beg.alloc(std::max<size_t>(n, 1) * 4, ctx.stream);
+    I.len.alloc(std::max<size_t>(n, 1) * 4, ctx.stream);
     I.order.alloc(std::max<size_t>(n, 1) * 4, ctx.stream);
     I.gid.alloc(std::max<size_t>(n, 1) * 4, ctx.stream);
     I.gkey.alloc(std::max<size_t>(n, 1) * 4, ctx.stream);
-    DevBuf cnt((n + 1) * 4, ctx.stream);
-    if (n)
-        IGB_LAUNCH(ctx, sub_count, grid_for(ctx, n, 256), 256, 0, S.off.as<uint32_t>(), d_src_of, n,
-                   cnt.as<uint32_t>());
-    IGB_CUDA(cudaMemsetAsync(cnt.as<uint32_t>() + n, 0, 4, ctx.stream));
-    size_t tb = 0;
-    IGB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.as<uint32_t>(), I.off.as<uint32_t>(), (int64_t)n + 1,
-                                           ctx.stream));
-    DevBuf temp(tb, ctx.stream);
-    IGB_CUDA(cub::DeviceScan::ExclusiveSum(temp.p, tb, cnt.as<uint32_t>(), I.off.as<uint32_t>(), (int64_t)n + 1,
-                                           ctx.stream));
-    uint32_t total = 0;
-    IGB_CUDA(cudaMemcpyAsync(&total, I.off.as<uint32_t>() + n, 4, cudaMemcpyDeviceToHost, ctx.stream));
-    IGB_CUDA(cudaStreamSynchronize(ctx.stream));
-    I.toks.alloc(std::max<size_t>(total, 1) * 2, ctx.stream);
+    I.toks = S.toks;  // token lists are shared with the source index, not copied
     if (n == 0) return;
-    IGB_LAUNCH(ctx, sub_copy, grid_for(ctx, n * 32, 256), 256, 0, S.off.as<uint32_t>(), S.toks.as<uint16_t>(), d_src_of, n,
-               I.off.as<uint32_t>(), I.toks.as<uint16_t>());
+    IGB_LAUNCH(ctx, sub_lists, grid_for(ctx, n, 256), 256, 0, S.beg.as<uint32_t>(), S.len.as<uint32_t>(), d_src_of, n,
+               I.beg.as<uint32_t>(), I.len.as<uint32_t>());
     tr.mark("token_lists");
     // the source's group order restricted to the subset keeps its key order
     const size_t ns = S.np;

@@ -1,6 +1,8 @@
 // posting.cuh — posting-bitmap (vertical) subset tests; see posting.cu.
 #pragma once
 
+#include <memory>
+
 #include "ig_internal.cuh"
 
 namespace igb {
@@ -36,8 +38,9 @@ struct RankSpace {
 struct PatternIndex {
     size_t np = 0;   // patterns
     size_t G = 0;    // groups
-    DevBuf off;      // np+1 u32: token list offsets
-    DevBuf toks;     // u16 tokens
+    DevBuf beg;      // np u32: start of each pattern's token list in *toks
+    DevBuf len;      // np u32: its length
+    std::shared_ptr<DevBuf> toks;  // u16 tokens (shared by subset indexes)
     DevBuf order;    // np u32: patterns in group-key order
     DevBuf gid;      // np u32: group of each ordered position
     DevBuf gkey;     // G u32: (t1 << 16) | t2
