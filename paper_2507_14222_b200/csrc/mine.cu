@@ -142,6 +142,8 @@ pair_enum(const int64_t* __restrict__ X, uint32_t n, int k, int stride, uint64_t
     unsigned long long* local = reinterpret_cast<unsigned long long*>(sm);  // kLocalSlots
     int64_t* sI = sm + kLocalSlots;
     int64_t* sJ = sI + (size_t)TILE * stride;
+    unsigned long long* sKey = reinterpret_cast<unsigned long long*>(sJ + (size_t)TILE * stride);  // k fingerprint keys
+    for (int w = threadIdx.x; w < k; w += kPairThreads) sKey[w] = T.keys[w];
     for (uint64_t it = blockIdx.x;; it += gridDim.x) {
         const uint64_t t = tile_begin + it * tile_step;  // this rank's tiles: begin, begin + step, ...
         if (t >= n_tiles) break;
@@ -172,7 +174,7 @@ pair_enum(const int64_t* __restrict__ X, uint32_t n, int k, int stride, uint64_t
             for (int w = 0; w < k; ++w) {
                 const uint64_t x = (uint64_t)(a[w] & b[w]);
                 nz |= x;
-                fp.add(x, __ldg(T.keys + w));
+                fp.add(x, sKey[w]);
             }
             if (!nz) continue;  // SPEC.md:338 empty intersections dropped at the source
             const uint64_t f = (fp.final(k) & T.fp_mask) | 1ull;
@@ -440,7 +442,7 @@ uint64_t dedup_pairs(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, const 
     if (n > 0xffffffffull) fail(IG_E_INVALID_ARG, "enumerate: more than 2^32 rows");
     const int stride = (int)(k | 1);
     int tile_rows = 64;
-    while (tile_rows > 16 && (size_t)kLocalSlots * 8 + 2 * (size_t)tile_rows * stride * 8 > 200 * 1024) tile_rows /= 2;
+    while (tile_rows > 16 && (size_t)kLocalSlots * 8 + 2 * (size_t)tile_rows * stride * 8 + k * 8 > 200 * 1024) tile_rows /= 2;
     const uint64_t blocks = (n + tile_rows - 1) / tile_rows;
     const uint64_t n_tiles = blocks * (blocks + 1) / 2;
     const uint64_t my_tiles = src.list ? 0 : (n_tiles > src.tile_begin ? (n_tiles - src.tile_begin + src.tile_step - 1) / src.tile_step : 0);
@@ -448,8 +450,8 @@ uint64_t dedup_pairs(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, const 
     // 64-row tiles; narrower tiles for wide rows (CICIDS shape, K up to ~750) so
     // both row blocks still fit in shared memory
     const int tile = tile_rows;
-    const size_t smem = (size_t)kLocalSlots * 8 + 2 * (size_t)tile * stride * 8;
-    if (smem > 200 * 1024) fail(IG_E_INVALID_ARG, "enumerate: rows wider than the shared-memory tile (K > 750)");
+    const size_t smem = (size_t)kLocalSlots * 8 + 2 * (size_t)tile * stride * 8 + k * 8;
+    if (smem > 200 * 1024) fail(IG_E_INVALID_ARG, "enumerate: rows wider than the shared-memory tile (K > 700)");
     IGB_CUDA(cudaFuncSetAttribute(pair_enum<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     IGB_CUDA(cudaFuncSetAttribute(pair_enum<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     IGB_CUDA(cudaFuncSetAttribute(pair_enum<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
