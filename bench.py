@@ -259,6 +259,7 @@ def run_b200(args):
 
     def step_e2e():
         enc = api.encode_training(cols_tr, ctx)
+        cols_te.prefetch(ctx)  # test columns' H2D (copy stream) overlaps the fit
         if world > 1:
             res = sharded.fit_distributed(ctx, enc, rank, world, ex)
             tenc = api.encode_rows(cols_te, enc, ctx)

@@ -181,6 +181,10 @@ int ig_columns_build(const ig_table* t, const ig_schema* s, int with_labels, ig_
 /* Keep a copy of the columns resident on the context's device; later encodes
  * of these columns read HBM instead of host memory (bench `value` leg). */
 int ig_columns_upload(ig_ctx* ctx, ig_columns* c);
+/* Start the host->device copy of the columns on the context's copy stream and
+ * return at once; the next encode of these columns waits for it (one-shot).
+ * Lets a caller overlap the test columns' transfer with the fit. */
+int ig_columns_prefetch(ig_ctx* ctx, ig_columns* c);
 size_t ig_columns_rows(const ig_columns* c);
 size_t ig_columns_bytes(const ig_columns* c);
 void ig_columns_free(ig_columns* c);

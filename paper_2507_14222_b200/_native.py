@@ -83,6 +83,7 @@ SIGNATURES = [
     ("ig_schema_free", None, [vp]),
     ("ig_columns_build", C.c_int, [vp, vp, C.c_int, C.POINTER(vp)]),
     ("ig_columns_upload", C.c_int, [vp, vp]),
+    ("ig_columns_prefetch", C.c_int, [vp, vp]),
     ("ig_columns_rows", sz, [vp]),
     ("ig_columns_bytes", sz, [vp]),
     ("ig_columns_free", None, [vp]),

@@ -458,6 +458,12 @@ class Columns:
         ctx.check(lib.ig_columns_upload(ctx.handle, self.handle))
         return self
 
+    def prefetch(self, ctx: Optional[Context] = None) -> "Columns":
+        """Start the H2D copy now (copy stream); the next encode of these columns uses it."""
+        ctx = ctx or default_context()
+        ctx.check(lib.ig_columns_prefetch(ctx.handle, self.handle))
+        return self
+
     @property
     def rows(self) -> int:
         return int(lib.ig_columns_rows(self.handle))

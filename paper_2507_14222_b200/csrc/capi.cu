@@ -373,6 +373,7 @@ int ig_ctx_create(int device, ig_ctx** out) {
     int st = guard(c.get(), [&] {
         IGB_CUDA(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
         IGB_CUDA(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+        IGB_CUDA(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
         c->stream = c->own;
         cudaDeviceProp prop;
         IGB_CUDA(cudaGetDeviceProperties(&prop, device));
@@ -407,7 +408,7 @@ int ig_ctx_create(int device, ig_ctx** out) {
 void ig_ctx_destroy(ig_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
-    for (cudaStream_t st : {ctx->own, ctx->aux}) {
+    for (cudaStream_t st : {ctx->own, ctx->aux, ctx->copy}) {
         if (!st) continue;
         cudaStreamSynchronize(st);
         cudaStreamDestroy(st);
@@ -730,12 +731,17 @@ int ig_columns_build(const ig_table* t, const ig_schema* s, int with_labels, ig_
 int ig_columns_upload(ig_ctx* ctx, ig_columns* c) {
     return guard(ctx, [&] { igb::upload_columns(*ctx, *c); });
 }
+int ig_columns_prefetch(ig_ctx* ctx, ig_columns* c) {
+    if (!ctx || !c) return IG_E_INVALID_ARG;
+    return guard(ctx, [&] { igb::prefetch_columns(*ctx, *c); });
+}
 size_t ig_columns_rows(const ig_columns* c) { return c ? c->n_rows : 0; }
 size_t ig_columns_bytes(const ig_columns* c) {
     return c ? c->values.size() * 8 + c->cat.size() * 4 + c->is_attack.size() : 0;
 }
 void ig_columns_free(ig_columns* c) {
     if (!c) return;
+    igb::drop_prefetch(*c);
     for (void* p : c->pinned) cudaHostUnregister(p);
     delete c;
 }

@@ -225,6 +225,17 @@ struct DeviceCols {
 };
 
 // H2D of the parsed columns + kernel (1a): per-cell codes.
+namespace {
+struct PrefetchCols {
+    DevBuf values, cat, attack;
+    cudaEvent_t ready = nullptr;
+    int device = -1;
+    ~PrefetchCols() {
+        if (ready) cudaEventDestroy(ready);
+    }
+};
+}  // namespace
+
 void upload_and_code(Ctx& ctx, const ig_columns& c, DeviceCols& d) {
     d.n = c.n_rows;
     std::vector<ColDesc> desc;
@@ -244,7 +255,20 @@ void upload_and_code(Ctx& ctx, const ig_columns& c, DeviceCols& d) {
                                  ctx.stream));
     const double* vals;
     const int32_t* cats;
-    if (c.d_values && c.device == ctx.device) {
+    auto* pf = static_cast<PrefetchCols*>(c.prefetch.get());
+    if (pf && pf->device == ctx.device) {
+        // a prefetch is in flight: order after it, then own its buffers
+        // (freed on this stream once the encode kernels are done)
+        IGB_CUDA(cudaStreamWaitEvent(ctx.stream, pf->ready, 0));
+        d.values = std::move(pf->values);
+        d.cat = std::move(pf->cat);
+        d.attack = std::move(pf->attack);
+        d.values.s = d.cat.s = d.attack.s = ctx.stream;
+        c.prefetch.reset();
+        vals = d.values.as<double>();
+        cats = d.cat.as<int32_t>();
+        d.attack_ptr = d.attack.as<uint8_t>();
+    } else if (c.d_values && c.device == ctx.device) {
         // resident columns (ig_columns_upload): no host traffic
         vals = static_cast<const double*>(c.d_values.get());
         cats = static_cast<const int32_t*>(c.d_cat.get());
@@ -317,6 +341,29 @@ void pack_with(Ctx& ctx, const ig_encoding& e, const DeviceCols& d,
 }
 
 }  // namespace
+
+void prefetch_columns(Ctx& ctx, ig_columns& c) {
+    auto pf = std::make_shared<PrefetchCols>();
+    pf->device = ctx.device;
+    pf->values.alloc(std::max<size_t>(c.values.size(), 1) * 8, ctx.copy);
+    pf->cat.alloc(std::max<size_t>(c.cat.size(), 1) * 4, ctx.copy);
+    pf->attack.alloc(std::max<size_t>(c.is_attack.size(), 1), ctx.copy);
+    if (!c.values.empty())
+        IGB_CUDA(cudaMemcpyAsync(pf->values.p, c.values.data(), c.values.size() * 8, cudaMemcpyHostToDevice, ctx.copy));
+    if (!c.cat.empty())
+        IGB_CUDA(cudaMemcpyAsync(pf->cat.p, c.cat.data(), c.cat.size() * 4, cudaMemcpyHostToDevice, ctx.copy));
+    if (!c.is_attack.empty())
+        IGB_CUDA(cudaMemcpyAsync(pf->attack.p, c.is_attack.data(), c.is_attack.size(), cudaMemcpyHostToDevice,
+                                 ctx.copy));
+    IGB_CUDA(cudaEventCreateWithFlags(&pf->ready, cudaEventDisableTiming));
+    IGB_CUDA(cudaEventRecord(pf->ready, ctx.copy));
+    c.prefetch = pf;
+}
+
+void drop_prefetch(ig_columns& c) {
+    if (auto* pf = static_cast<PrefetchCols*>(c.prefetch.get())) cudaEventSynchronize(pf->ready);
+    c.prefetch.reset();
+}
 
 void encode_training_dev(Ctx& ctx, const ig_columns& c, ig_encoding& e) {
     if (c.is_attack.size() != c.n_rows) fail(IG_E_INVALID_ARG, "encode_training: columns built without labels");

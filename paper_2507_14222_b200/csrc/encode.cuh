@@ -26,6 +26,9 @@ struct ig_encoding {
 namespace igb {
 void encode_training_dev(Ctx& ctx, const ig_columns& c, ig_encoding& e);
 void upload_columns(Ctx& ctx, ig_columns& c);
+void prefetch_columns(Ctx& ctx, ig_columns& c);
+// wait for an unconsumed prefetch (its host source is about to go away) and drop it
+void drop_prefetch(ig_columns& c);
 void encode_rows_dev(Ctx& ctx, const ig_columns& c, const ig_encoding& train, ig_encoding& e);
 // archive.cu
 std::string schema_to_text(const ig_schema& s);

@@ -57,6 +57,9 @@ struct ig_columns {
     std::shared_ptr<void> d_values, d_cat, d_attack;
     int device = -1;
     std::vector<void*> pinned;  // arrays page-locked with cudaHostRegister (ig_columns_build)
+    // In-flight copy started by ig_columns_prefetch (opaque, see encode.cu);
+    // consumed by the next encode of these columns.
+    mutable std::shared_ptr<void> prefetch;
 };
 
 namespace igb {

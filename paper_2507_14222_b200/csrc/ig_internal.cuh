@@ -89,6 +89,7 @@ struct Ctx {
     cudaStream_t own = nullptr;
     cudaStream_t stream = nullptr;
     cudaStream_t aux = nullptr;  // second class's stream (for_both_classes)
+    cudaStream_t copy = nullptr; // host->device prefetches (ig_columns_prefetch)
     std::string err;
     uint64_t launches = 0;
     int sm_count = 148;

@@ -116,6 +116,14 @@ __global__ void write_ranks(const uint32_t* __restrict__ where, size_t m, uint32
 // segments of the distinct values, then each value's rank = #smaller values
 // of its column, counted against the column staged in shared memory.
 constexpr uint32_t kRankSmall = 4096;
+constexpr int kParamCols = 64;  // small per-column tables travel as kernel parameters
+struct Starts {
+    unsigned int v[kParamCols + 1];
+};
+
+__global__ void init_cursor(Starts st, int k, unsigned int* __restrict__ cursor) {
+    for (int w = threadIdx.x; w <= k; w += blockDim.x) cursor[w] = st.v[w];
+}
 __global__ void column_collect_seg(const ulonglong2* __restrict__ tables, int k, uint32_t slots,
                                    unsigned int* __restrict__ cursor, unsigned long long* __restrict__ vals,
                                    uint32_t* __restrict__ where) {
@@ -131,10 +139,10 @@ __global__ void column_collect_seg(const ulonglong2* __restrict__ tables, int k,
 }
 
 __global__ void column_rank_small(const unsigned long long* __restrict__ vals, const uint32_t* __restrict__ where,
-                                  const unsigned int* __restrict__ cstart, ulonglong2* __restrict__ tables) {
+                                  Starts st, ulonglong2* __restrict__ tables) {
     __shared__ unsigned long long sv[kRankSmall];
     const int w = blockIdx.x;
-    const uint32_t b = cstart[w], d = cstart[w + 1] - b;
+    const uint32_t b = st.v[w], d = st.v[w + 1] - b;
     const uint32_t i = blockIdx.y * blockDim.x + threadIdx.x;
     if (blockIdx.y * blockDim.x >= d) return;  // whole block past this column (uniform)
     for (uint32_t j = threadIdx.x; j < d; j += blockDim.x) sv[j] = vals[b + j];
@@ -150,10 +158,13 @@ struct Field {
     int key;    // packed key word
     int shift;  // bit position of the field's LSB inside that key word
 };
+struct FieldTable {
+    Field f[kParamCols];
+};
 
 // Packed keys, MSB-first by word: keys[j][i] for key word j of row i.
 __global__ void pack_keys(const int64_t* __restrict__ words, size_t n, int k, const ulonglong2* __restrict__ tables,
-                          uint32_t slots, const Field* __restrict__ fields, int n_keys,
+                          uint32_t slots, const Field* __restrict__ fields, FieldTable ft, int n_keys,
                           unsigned long long* __restrict__ keys) {
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
         unsigned long long acc[8];
@@ -164,7 +175,7 @@ __global__ void pack_keys(const int64_t* __restrict__ words, size_t n, int k, co
             uint32_t s = (uint32_t)(mix64(v) & (slots - 1));
             while (T[s].x != v || T[s].y == 0) s = (s + 1) & (slots - 1);
             const unsigned long long r = T[s].y - 2;
-            const Field f = fields[w];
+            const Field f = fields ? fields[w] : ft.f[w];
 #pragma unroll
             for (int j = 0; j < 8; ++j)
                 if (j == f.key) acc[j] |= r << f.shift;
@@ -344,18 +355,18 @@ void sort_rows_canonical(Ctx& ctx, const int64_t* d_words, size_t n, size_t k, u
         m += hc[w];
         dmax = std::max<uint32_t>(dmax, hc[w]);
     }
-    if (dmax <= kRankSmall) {
-        std::vector<unsigned int> hs(k + 1, 0);
-        for (size_t w = 0; w < k; ++w) hs[w + 1] = hs[w] + hc[w];
-        DevBuf vals(m * 8, ctx.stream), where(m * 4, ctx.stream), cstart((k + 1) * 4, ctx.stream),
-            cursor((k + 1) * 4, ctx.stream);
-        IGB_CUDA(cudaMemcpyAsync(cstart.p, hs.data(), (k + 1) * 4, cudaMemcpyHostToDevice, ctx.stream));
-        IGB_CUDA(cudaMemcpyAsync(cursor.p, cstart.p, (k + 1) * 4, cudaMemcpyDeviceToDevice, ctx.stream));
+    if (dmax <= kRankSmall && k <= (size_t)kParamCols) {
+        // no host->device copies here: they would queue behind a caller's
+        // bulk prefetch on the copy engine
+        Starts st{};
+        for (size_t w = 0; w < k; ++w) st.v[w + 1] = st.v[w] + hc[w];
+        DevBuf vals(m * 8, ctx.stream), where(m * 4, ctx.stream), cursor((k + 1) * 4, ctx.stream);
+        IGB_LAUNCH(ctx, init_cursor, 1, 128, 0, st, (int)k, cursor.as<unsigned int>());
         IGB_LAUNCH(ctx, column_collect_seg, grid_for(ctx, (size_t)k * slots, 256), 256, 0, tables.as<ulonglong2>(),
                    (int)k, slots, cursor.as<unsigned int>(), vals.as<unsigned long long>(), where.as<uint32_t>());
         const dim3 grid((unsigned)k, (dmax + 255) / 256);
-        IGB_LAUNCH(ctx, column_rank_small, grid, 256, 0, vals.as<unsigned long long>(), where.as<uint32_t>(),
-                   cstart.as<unsigned int>(), tables.as<ulonglong2>());
+        IGB_LAUNCH(ctx, column_rank_small, grid, 256, 0, vals.as<unsigned long long>(), where.as<uint32_t>(), st,
+                   tables.as<ulonglong2>());
     } else {
         DevBuf vals(m * 8, ctx.stream), vals2(m * 8, ctx.stream), where(m * 4, ctx.stream), where2(m * 4, ctx.stream),
             col(m * 4, ctx.stream), col2(m * 4, ctx.stream), nout(4, ctx.stream), cstart((k + 1) * 4, ctx.stream);
@@ -387,10 +398,16 @@ void sort_rows_canonical(Ctx& ctx, const int64_t* d_words, size_t n, size_t k, u
     }
     tr.mark("column_ranks");
     // Packed keys and LSD over the key words (least significant word first).
-    DevBuf dfields(k * sizeof(Field), ctx.stream), keys((size_t)n_keys * n * 8, ctx.stream);
-    IGB_CUDA(cudaMemcpyAsync(dfields.p, fields.data(), k * sizeof(Field), cudaMemcpyHostToDevice, ctx.stream));
+    DevBuf dfields, keys((size_t)n_keys * n * 8, ctx.stream);
+    FieldTable ft{};
+    if (k <= (size_t)kParamCols) {
+        for (size_t w = 0; w < k; ++w) ft.f[w] = fields[w];
+    } else {
+        dfields.alloc(k * sizeof(Field), ctx.stream);
+        IGB_CUDA(cudaMemcpyAsync(dfields.p, fields.data(), k * sizeof(Field), cudaMemcpyHostToDevice, ctx.stream));
+    }
     IGB_LAUNCH(ctx, pack_keys, grid_for(ctx, n, 128), 128, 0, d_words, n, (int)k, tables.as<ulonglong2>(), slots,
-               dfields.as<Field>(), n_keys, keys.as<unsigned long long>());
+               dfields.p ? dfields.as<Field>() : nullptr, ft, n_keys, keys.as<unsigned long long>());
     DevBuf k1(n * 8, ctx.stream), k2(n * 8, ctx.stream), p2(n * 4, ctx.stream);
     IGB_LAUNCH(ctx, iota32, grid_for(ctx, n, 256), 256, 0, d_perm, n);
     size_t tb3 = 0;

@@ -110,3 +110,31 @@ def test_nsl_fit_vs_oracle(api, rows, ratio_k, test_sample):
     A = oracle.fused_score(ref.pure[0].words, ref.pure[0].scores, T[idx])
     N = oracle.fused_score(ref.pure[1].words, ref.pure[1].scores, T[idx])
     assert np.array_equal(r.A[idx], A) and np.array_equal(r.N[idx], N)
+
+
+def test_prefetched_columns_encode_identically(api, golden_dir):
+    """ig_columns_prefetch: the copy-stream transfer feeds the next encode with
+    the same bytes as the synchronous path (and is consumed once)."""
+    g = json.load(open(os.path.join(golden_dir, "nsl_c1.json")))
+    csv = synth.nsl_csv(g["rows"], seed=g["seed"])
+    table = api.read_csv(csv)
+    ntr = g["ratio_k"] * table.rows // 10
+    tr, te = table.slice(0, ntr), table.slice(ntr, table.rows)
+    schema = api.infer_schema(tr, "label", decimals=g["decimals"])
+    ctr, cte = api.Columns(tr, schema, True), api.Columns(te, schema, False)
+    ctx = api.default_context()
+    want = api.encode_training(ctr, ctx)
+    ctr.prefetch(ctx)
+    got = api.encode_training(ctr, ctx)
+    assert got.vocabulary == want.vocabulary
+    for c in range(2):
+        assert np.array_equal(got.matrix(c), want.matrix(c))
+    t_want = api.encode_rows(cte, want, ctx).matrix(2)
+    cte.prefetch(ctx)
+    t_got = api.encode_rows(cte, want, ctx).matrix(2)
+    assert np.array_equal(t_got, t_want)
+    assert np.array_equal(api.encode_rows(cte, want, ctx).matrix(2), t_want)  # prefetch consumed
+    assert _digest(t_want) == _digest(api.train_and_score(csv, decimals=g["decimals"],
+                                                          ratio_k=g["ratio_k"]).test.matrix(2))
+    cte.prefetch(ctx)  # dropped unconsumed when the columns are freed
+    del cte
