@@ -10,9 +10,10 @@ from paper_2507_14222_b200 import synth
 pytestmark = pytest.mark.gpu
 
 
-def test_cicids_shape_fit_and_evidence():
+@pytest.mark.parametrize("rows", [6000, 14000])
+def test_cicids_shape_fit_and_evidence(rows):
     from paper_2507_14222_b200 import api
-    csv = synth.cicids_csv(6000, seed=3)
+    csv = synth.cicids_csv(rows, seed=3)
     r = api.train_and_score(csv, label_column="Label", normal_values=["BENIGN"], decimals=2, ratio_k=8)
     L = r.train.logical_len
     assert (L + 63) // 64 >= 64  # wide rows
