@@ -302,6 +302,12 @@ __global__ void map_order(const uint32_t* __restrict__ order, const uint32_t* __
     }
 }
 
+__global__ void gather_u64k(const unsigned long long* __restrict__ src, const uint32_t* __restrict__ idx, size_t n,
+                            unsigned long long* __restrict__ dst) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        dst[i] = src[idx[i]];
+}
+
 __global__ void gather_u32(const uint32_t* __restrict__ src, const uint32_t* __restrict__ idx, size_t n,
                            uint32_t* __restrict__ dst) {
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
@@ -317,23 +323,75 @@ __global__ void gather_u32(const uint32_t* __restrict__ src, const uint32_t* __r
 // C3 ~1M patterns fall into ~35k groups, so most of the (t1, t2) work is shared.
 constexpr uint32_t kNoTok = 0xffffu;
 
+// group key of a pattern: its three rarest tokens (t1, t2, t3), kNoTok when absent
 __global__ void group_keys(const uint32_t* __restrict__ tok_beg, const uint32_t* __restrict__ tok_len,
                            const uint16_t* __restrict__ toks, size_t np,
-                           uint32_t* __restrict__ key, uint32_t* __restrict__ idx) {
+                           unsigned long long* __restrict__ key, uint32_t* __restrict__ idx) {
     for (size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += (size_t)gridDim.x * blockDim.x) {
         const uint32_t o = tok_beg[p], m = tok_len[p];
-        const uint32_t t1 = m >= 1 ? toks[o] : kNoTok, t2 = m >= 2 ? toks[o + 1] : kNoTok;
-        key[p] = (t1 << 16) | t2;
+        const unsigned long long t1 = m >= 1 ? toks[o] : kNoTok, t2 = m >= 2 ? toks[o + 1] : kNoTok,
+                                 t3 = m >= 3 ? toks[o + 2] : kNoTok;
+        key[p] = (t1 << 32) | (t2 << 16) | t3;
         idx[p] = (uint32_t)p;
     }
 }
 
-__global__ void group_heads(const uint32_t* __restrict__ key, size_t np, uint8_t* __restrict__ head,
+template <class K>
+__global__ void group_heads(const K* __restrict__ key, size_t np, uint8_t* __restrict__ head,
                             uint32_t* __restrict__ head32) {
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < np; i += (size_t)gridDim.x * blockDim.x) {
         const uint8_t h = (i == 0 || key[i] != key[i - 1]) ? 1 : 0;
         head[i] = h;
         head32[i] = h;
+    }
+}
+
+// parent (t1, t2) key of every (t1, t2, t3) group
+__global__ void parent_keys(const unsigned long long* __restrict__ gkey, size_t G, uint32_t* __restrict__ pk) {
+    for (size_t g = (size_t)blockIdx.x * blockDim.x + threadIdx.x; g < G; g += (size_t)gridDim.x * blockDim.x)
+        pk[g] = (uint32_t)(gkey[g] >> 16);
+}
+
+// upper bound of a 3-group's list: its parent's list length
+__global__ void child_bound(const uint32_t* __restrict__ pid, size_t G, const uint32_t* __restrict__ plen,
+                            unsigned long long* __restrict__ ub) {
+    for (size_t g = (size_t)blockIdx.x * blockDim.x + threadIdx.x; g < G; g += (size_t)gridDim.x * blockDim.x)
+        ub[g] = plen[pid[g]];
+}
+
+// Warp per (t1, t2, t3) group: its parent (t1, t2) list filtered by post[t3].
+__global__ void child_lists(const unsigned long long* __restrict__ gkey, const uint32_t* __restrict__ pid, size_t G,
+                            const unsigned long long* __restrict__ dense, size_t W,
+                            const unsigned long long* __restrict__ poff, const uint32_t* __restrict__ plen,
+                            const uint32_t* __restrict__ pw, const unsigned long long* __restrict__ pm,
+                            const unsigned long long* __restrict__ goff, uint32_t* __restrict__ glen,
+                            uint32_t* __restrict__ ew, unsigned long long* __restrict__ em) {
+    const int lane = threadIdx.x & 31;
+    const size_t warps = ((size_t)gridDim.x * blockDim.x) >> 5;
+    for (size_t g = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < G; g += warps) {
+        const uint32_t t3 = (uint32_t)(gkey[g] & 0xffffu);
+        const uint32_t par = pid[g];
+        const unsigned long long pb = poff[par], base = goff[g];
+        const uint32_t len = plen[par];
+        uint32_t cnt = 0;
+        for (uint32_t j0 = 0; j0 < len; j0 += 32) {
+            const uint32_t j = j0 + lane;
+            uint32_t w = 0;
+            unsigned long long m = 0;
+            if (j < len) {
+                w = pw[pb + j];
+                m = pm[pb + j];
+                if (t3 != kNoTok) m &= dense[(size_t)t3 * W + w];
+            }
+            const uint32_t bal = __ballot_sync(kFull, m != 0ull);
+            if (m) {
+                const uint32_t pos = cnt + __popc(bal & ((1u << lane) - 1u));
+                ew[base + pos] = w;
+                em[base + pos] = m;
+            }
+            cnt += __popc(bal);
+        }
+        if (lane == 0) glen[g] = cnt;
     }
 }
 
@@ -479,11 +537,12 @@ grouped_scan(const unsigned long long* __restrict__ dense, size_t W, size_t n_ro
             const uint32_t w = j < len ? ew[base + j] : 0u;
             unsigned long long mw = j < len ? em[base + j] : 0ull;
             const unsigned long long* col = dense + w;
-            // tokens 2..31 from the lanes' registers, four per round, with
-            // compile-time shuffle lanes (lanes 32/33 of the last round wrap
-            // to tokens 0/1: no-ops); the rare tail past 32 is read from memory
+            // tokens 3..31 from the lanes' registers (0..2 are the group key,
+            // already applied in the list), four per round, with compile-time
+            // shuffle lanes (lanes 32..34 of the last round wrap to tokens
+            // 0..2: no-ops); the rare tail past 32 is read from memory
 #pragma unroll
-            for (int t = 2; t < 32; t += 4) {
+            for (int t = 3; t < 32; t += 4) {
                 if ((uint32_t)t >= m) break;
                 const bool live = mw != 0ull;
                 if (!__any_sync(kFull, live)) break;
@@ -544,17 +603,17 @@ __global__ void grouped_work(const uint32_t* __restrict__ tok_len, size_t np, co
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < np; i += (size_t)gridDim.x * blockDim.x) {
         const uint32_t p = order[i];
         const uint32_t m = tok_len[p];
-        if (m > 2) acc += (unsigned long long)glen[gid[i]] * (m - 2);
+        if (m > 3) acc += (unsigned long long)glen[gid[i]] * (m - 3);
     }
     for (int s = 16; s; s >>= 1) acc += __shfl_xor_sync(kFull, acc, s);
     if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
 }
 
-__global__ void group_work(const uint32_t* __restrict__ gkey, const unsigned long long* __restrict__ ub, size_t G,
+__global__ void group_work(const uint32_t* __restrict__ pkey, const unsigned long long* __restrict__ ub, size_t G,
                            unsigned long long* __restrict__ out) {
     unsigned long long acc = 0;
     for (size_t g = (size_t)blockIdx.x * blockDim.x + threadIdx.x; g < G; g += (size_t)gridDim.x * blockDim.x)
-        acc += ub[g] * (((gkey[g] & 0xffffu) != kNoTok) ? 2ull : 1ull);
+        acc += ub[g] * (((pkey[g] & 0xffffu) != kNoTok) ? 2ull : 1ull);
     for (int s = 16; s; s >>= 1) acc += __shfl_xor_sync(kFull, acc, s);
     if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
 }
@@ -580,27 +639,44 @@ void launch_scan(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Post
         IGB_CUDA(cudaEventCreate(&e1));
         IGB_CUDA(cudaEventRecord(e0, ctx.stream));
     }
-    const size_t G = I->G;
-    // every group's word list S = non-zero (w, post[t1][w] & post[t2][w]) in P
-    DevBuf ub((G + 1) * 8, ctx.stream), goff((G + 1) * 8, ctx.stream), glen(G * 4 + 4, ctx.stream);
-    if (G)
-        IGB_LAUNCH(ctx, group_bound, grid_for(ctx, G, 256), 256, 0, I->gkey.as<uint32_t>(), G,
+    const size_t G = I->G, G2 = I->G2;
+    // parent (t1, t2) lists S2 = non-zero (w, post[t1][w] & post[t2][w]) in P,
+    // then each (t1, t2, t3) group's list S = S2 filtered by post[t3]
+    DevBuf ub((G2 + 1) * 8, ctx.stream), poff((G2 + 1) * 8, ctx.stream), plen(G2 * 4 + 4, ctx.stream);
+    if (G2)
+        IGB_LAUNCH(ctx, group_bound, grid_for(ctx, G2, 256), 256, 0, I->pkey.as<uint32_t>(), G2,
                    P.nz_off.as<uint32_t>(), P.W, ub.as<unsigned long long>());
-    IGB_CUDA(cudaMemsetAsync(ub.as<unsigned long long>() + G, 0, 8, ctx.stream));
+    IGB_CUDA(cudaMemsetAsync(ub.as<unsigned long long>() + G2, 0, 8, ctx.stream));
     size_t tb4 = 0;
-    IGB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb4, ub.as<unsigned long long>(), goff.as<unsigned long long>(),
-                                           (int64_t)G + 1, ctx.stream));
+    IGB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb4, ub.as<unsigned long long>(), poff.as<unsigned long long>(),
+                                           (int64_t)std::max(G, G2) + 1, ctx.stream));
     DevBuf temp4(tb4, ctx.stream);
-    IGB_CUDA(cub::DeviceScan::ExclusiveSum(temp4.p, tb4, ub.as<unsigned long long>(), goff.as<unsigned long long>(),
+    IGB_CUDA(cub::DeviceScan::ExclusiveSum(temp4.p, tb4, ub.as<unsigned long long>(), poff.as<unsigned long long>(),
+                                           (int64_t)G2 + 1, ctx.stream));
+    unsigned long long E2 = 0;
+    IGB_CUDA(cudaMemcpyAsync(&E2, poff.as<unsigned long long>() + G2, 8, cudaMemcpyDeviceToHost, ctx.stream));
+    IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+    DevBuf pw(std::max<unsigned long long>(E2, 1) * 4, ctx.stream), pm(std::max<unsigned long long>(E2, 1) * 8, ctx.stream);
+    if (G2)
+        IGB_LAUNCH(ctx, group_lists, grid_for(ctx, G2 * 32, 256), 256, 0, I->pkey.as<uint32_t>(), G2,
+                   P.dense.as<unsigned long long>(), P.W, P.n, P.nz_off.as<uint32_t>(), P.nz_idx.as<uint32_t>(),
+                   poff.as<unsigned long long>(), plen.as<uint32_t>(), pw.as<uint32_t>(), pm.as<unsigned long long>());
+    DevBuf ub3((G + 1) * 8, ctx.stream), goff((G + 1) * 8, ctx.stream), glen(G * 4 + 4, ctx.stream);
+    if (G)
+        IGB_LAUNCH(ctx, child_bound, grid_for(ctx, G, 256), 256, 0, I->pid.as<uint32_t>(), G, plen.as<uint32_t>(),
+                   ub3.as<unsigned long long>());
+    IGB_CUDA(cudaMemsetAsync(ub3.as<unsigned long long>() + G, 0, 8, ctx.stream));
+    IGB_CUDA(cub::DeviceScan::ExclusiveSum(temp4.p, tb4, ub3.as<unsigned long long>(), goff.as<unsigned long long>(),
                                            (int64_t)G + 1, ctx.stream));
     unsigned long long E = 0;
     IGB_CUDA(cudaMemcpyAsync(&E, goff.as<unsigned long long>() + G, 8, cudaMemcpyDeviceToHost, ctx.stream));
     IGB_CUDA(cudaStreamSynchronize(ctx.stream));
     DevBuf ew(std::max<unsigned long long>(E, 1) * 4, ctx.stream), em(std::max<unsigned long long>(E, 1) * 8, ctx.stream);
     if (G)
-        IGB_LAUNCH(ctx, group_lists, grid_for(ctx, G * 32, 256), 256, 0, I->gkey.as<uint32_t>(), G,
-                   P.dense.as<unsigned long long>(), P.W, P.n, P.nz_off.as<uint32_t>(), P.nz_idx.as<uint32_t>(),
-                   goff.as<unsigned long long>(), glen.as<uint32_t>(), ew.as<uint32_t>(), em.as<unsigned long long>());
+        IGB_LAUNCH(ctx, child_lists, grid_for(ctx, G * 32, 256), 256, 0, I->gkey.as<unsigned long long>(),
+                   I->pid.as<uint32_t>(), G, P.dense.as<unsigned long long>(), P.W, poff.as<unsigned long long>(),
+                   plen.as<uint32_t>(), pw.as<uint32_t>(), pm.as<unsigned long long>(), goff.as<unsigned long long>(),
+                   glen.as<uint32_t>(), ew.as<uint32_t>(), em.as<unsigned long long>());
     tr.mark("group_lists");
     const size_t blocks = std::min<size_t>((np + 7) / 8, (size_t)ctx.sm_count * 64);
     IGB_LAUNCH(ctx, grouped_scan<MODE>, (unsigned)blocks, 256, 0, P.dense.as<unsigned long long>(), P.W, P.n,
@@ -615,9 +691,9 @@ void launch_scan(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Post
         IGB_CUDA(cudaMemsetAsync(w.p, 0, 8, ctx.stream));
         IGB_LAUNCH(ctx, grouped_work, grid_for(ctx, np, 256), 256, 0, I->len.as<uint32_t>(), np,
                    I->order.as<uint32_t>(), I->gid.as<uint32_t>(), glen.as<uint32_t>(), w.as<unsigned long long>());
-        if (G)
-            IGB_LAUNCH(ctx, group_work, grid_for(ctx, G, 256), 256, 0, I->gkey.as<uint32_t>(),
-                       ub.as<unsigned long long>(), G, w.as<unsigned long long>());
+        if (G2)
+            IGB_LAUNCH(ctx, group_work, grid_for(ctx, G2, 256), 256, 0, I->pkey.as<uint32_t>(),
+                       ub.as<unsigned long long>(), G2, w.as<unsigned long long>());
         unsigned long long hw = 0;
         IGB_CUDA(cudaMemcpyAsync(&hw, w.p, 8, cudaMemcpyDeviceToHost, ctx.stream));
         IGB_CUDA(cudaStreamSynchronize(ctx.stream));
@@ -668,7 +744,7 @@ void build_pattern_index(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, co
     I.len.alloc((np + 1) * 4, ctx.stream);
     I.order.alloc(std::max<size_t>(np, 1) * 4, ctx.stream);
     I.gid.alloc(std::max<size_t>(np, 1) * 4, ctx.stream);
-    I.gkey.alloc(std::max<size_t>(np, 1) * 4, ctx.stream);
+    I.gkey.alloc(std::max<size_t>(np, 1) * 8, ctx.stream);
     // CSR token lists, rarest first in R
     if (np)
         IGB_LAUNCH(ctx, pattern_token_count, grid_for(ctx, np, 256), 256, 0, d_pat, np, (int)k, I.len.as<uint32_t>());
@@ -711,41 +787,69 @@ void build_pattern_index(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, co
                    R.df.as<uint32_t>(), L, I.beg.as<uint32_t>(), I.toks->as<uint16_t>());
     }
     tr.mark("token_lists");
-    // group patterns by their two rarest tokens
-    DevBuf key(np * 4, ctx.stream), key2(np * 4, ctx.stream), idx(np * 4, ctx.stream);
+    // group patterns by their three rarest tokens
+    DevBuf key(np * 8, ctx.stream), key2(np * 8, ctx.stream), idx(np * 4, ctx.stream);
     IGB_LAUNCH(ctx, group_keys, grid_for(ctx, np, 256), 256, 0, I.beg.as<uint32_t>(), I.len.as<uint32_t>(),
-               I.toks->as<uint16_t>(), np,
-               key.as<uint32_t>(), idx.as<uint32_t>());
+               I.toks->as<uint16_t>(), np, key.as<unsigned long long>(), idx.as<uint32_t>());
     size_t tb1 = 0;
-    IGB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb1, key.as<uint32_t>(), key2.as<uint32_t>(), idx.as<uint32_t>(),
-                                             I.order.as<uint32_t>(), (int64_t)np, 0, 32, ctx.stream));
+    IGB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb1, key.as<unsigned long long>(), key2.as<unsigned long long>(),
+                                             idx.as<uint32_t>(), I.order.as<uint32_t>(), (int64_t)np, 0, 48,
+                                             ctx.stream));
     DevBuf temp1(tb1, ctx.stream);
-    IGB_CUDA(cub::DeviceRadixSort::SortPairs(temp1.p, tb1, key.as<uint32_t>(), key2.as<uint32_t>(), idx.as<uint32_t>(),
-                                             I.order.as<uint32_t>(), (int64_t)np, 0, 32, ctx.stream));
-    group_ids(ctx, key2.as<uint32_t>(), np, I);
+    IGB_CUDA(cub::DeviceRadixSort::SortPairs(temp1.p, tb1, key.as<unsigned long long>(), key2.as<unsigned long long>(),
+                                             idx.as<uint32_t>(), I.order.as<uint32_t>(), (int64_t)np, 0, 48,
+                                             ctx.stream));
+    group_ids(ctx, key2.as<unsigned long long>(), np, I);
     tr.mark("group_sort");
 }
 
-// gid (0-based, per sorted position) and gkey (per group) from the sorted keys
-void group_ids(Ctx& ctx, const uint32_t* d_sorted_key, size_t np, PatternIndex& I) {
+// gid (0-based, per sorted position) and gkey (per group) from the sorted keys,
+// then the (t1, t2) parent of every group (pid, pkey)
+void group_ids(Ctx& ctx, const unsigned long long* d_sorted_key, size_t np, PatternIndex& I) {
     DevBuf head(np, ctx.stream), head32(np * 4, ctx.stream), nsel(8, ctx.stream);
-    IGB_LAUNCH(ctx, group_heads, grid_for(ctx, np, 256), 256, 0, d_sorted_key, np, head.as<uint8_t>(),
-               head32.as<uint32_t>());
+    IGB_LAUNCH(ctx, group_heads<unsigned long long>, grid_for(ctx, np, 256), 256, 0, d_sorted_key, np,
+               head.as<uint8_t>(), head32.as<uint32_t>());
     size_t tb2 = 0, tb3 = 0;
     IGB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb2, head32.as<uint32_t>(), I.gid.as<uint32_t>(), (int64_t)np,
                                            ctx.stream));
-    IGB_CUDA(cub::DeviceSelect::Flagged(nullptr, tb3, d_sorted_key, head.as<uint8_t>(), I.gkey.as<uint32_t>(),
-                                        nsel.as<int64_t>(), (int64_t)np, ctx.stream));
+    IGB_CUDA(cub::DeviceSelect::Flagged(nullptr, tb3, d_sorted_key, head.as<uint8_t>(),
+                                        I.gkey.as<unsigned long long>(), nsel.as<int64_t>(), (int64_t)np, ctx.stream));
     DevBuf temp2(std::max(tb2, tb3), ctx.stream);
     IGB_CUDA(cub::DeviceScan::InclusiveSum(temp2.p, tb2, head32.as<uint32_t>(), I.gid.as<uint32_t>(), (int64_t)np,
                                            ctx.stream));
-    IGB_CUDA(cub::DeviceSelect::Flagged(temp2.p, tb3, d_sorted_key, head.as<uint8_t>(), I.gkey.as<uint32_t>(),
-                                        nsel.as<int64_t>(), (int64_t)np, ctx.stream));
+    IGB_CUDA(cub::DeviceSelect::Flagged(temp2.p, tb3, d_sorted_key, head.as<uint8_t>(),
+                                        I.gkey.as<unsigned long long>(), nsel.as<int64_t>(), (int64_t)np, ctx.stream));
     IGB_LAUNCH(ctx, minus_one, grid_for(ctx, np, 256), 256, 0, I.gid.as<uint32_t>(), np);
     int64_t G = 0;
     IGB_CUDA(cudaMemcpyAsync(&G, nsel.p, 8, cudaMemcpyDeviceToHost, ctx.stream));
     IGB_CUDA(cudaStreamSynchronize(ctx.stream));
     I.G = (size_t)G;
+    // parents: the groups are sorted by (t1, t2, t3), so equal (t1, t2) are adjacent
+    const size_t Gs = std::max<size_t>(I.G, 1);
+    I.pid.alloc(Gs * 4, ctx.stream);
+    I.pkey.alloc(Gs * 4, ctx.stream);
+    I.G2 = 0;
+    if (!G) return;
+    DevBuf pk(Gs * 4, ctx.stream), ph(Gs, ctx.stream), ph32(Gs * 4, ctx.stream);
+    IGB_LAUNCH(ctx, parent_keys, grid_for(ctx, I.G, 256), 256, 0, I.gkey.as<unsigned long long>(), I.G,
+               pk.as<uint32_t>());
+    IGB_LAUNCH(ctx, group_heads<uint32_t>, grid_for(ctx, I.G, 256), 256, 0, pk.as<uint32_t>(), I.G, ph.as<uint8_t>(),
+               ph32.as<uint32_t>());
+    size_t tb4 = 0, tb5 = 0;
+    IGB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb4, ph32.as<uint32_t>(), I.pid.as<uint32_t>(), (int64_t)I.G,
+                                           ctx.stream));
+    IGB_CUDA(cub::DeviceSelect::Flagged(nullptr, tb5, pk.as<uint32_t>(), ph.as<uint8_t>(), I.pkey.as<uint32_t>(),
+                                        nsel.as<int64_t>(), (int64_t)I.G, ctx.stream));
+    DevBuf temp3(std::max(tb4, tb5), ctx.stream);
+    IGB_CUDA(cub::DeviceScan::InclusiveSum(temp3.p, tb4, ph32.as<uint32_t>(), I.pid.as<uint32_t>(), (int64_t)I.G,
+                                           ctx.stream));
+    IGB_CUDA(cub::DeviceSelect::Flagged(temp3.p, tb5, pk.as<uint32_t>(), ph.as<uint8_t>(), I.pkey.as<uint32_t>(),
+                                        nsel.as<int64_t>(), (int64_t)I.G, ctx.stream));
+    IGB_LAUNCH(ctx, minus_one, grid_for(ctx, I.G, 256), 256, 0, I.pid.as<uint32_t>(), I.G);
+    int64_t G2 = 0;
+    IGB_CUDA(cudaMemcpyAsync(&G2, nsel.p, 8, cudaMemcpyDeviceToHost, ctx.stream));
+    IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+    I.G2 = (size_t)G2;
 }
 
 void subset_pattern_index(Ctx& ctx, const PatternIndex& S, const uint32_t* d_src_of, size_t n, PatternIndex& I) {
@@ -756,7 +860,7 @@ void subset_pattern_index(Ctx& ctx, const PatternIndex& S, const uint32_t* d_src
     I.len.alloc(std::max<size_t>(n, 1) * 4, ctx.stream);
     I.order.alloc(std::max<size_t>(n, 1) * 4, ctx.stream);
     I.gid.alloc(std::max<size_t>(n, 1) * 4, ctx.stream);
-    I.gkey.alloc(std::max<size_t>(n, 1) * 4, ctx.stream);
+    I.gkey.alloc(std::max<size_t>(n, 1) * 8, ctx.stream);
     I.toks = S.toks;  // token lists are shared with the source index, not copied
     if (n == 0) return;
     IGB_LAUNCH(ctx, sub_lists, grid_for(ctx, n, 256), 256, 0, S.beg.as<uint32_t>(), S.len.as<uint32_t>(), d_src_of, n,
@@ -765,7 +869,7 @@ void subset_pattern_index(Ctx& ctx, const PatternIndex& S, const uint32_t* d_src
     // the source's group order restricted to the subset keeps its key order
     const size_t ns = S.np;
     DevBuf inv(ns * 4, ctx.stream), val(ns * 4, ctx.stream), og(ns * 4, ctx.stream), keep(ns, ctx.stream),
-        og2(std::max<size_t>(n, 1) * 4, ctx.stream), key(std::max<size_t>(n, 1) * 4, ctx.stream), nsel(8, ctx.stream);
+        og2(std::max<size_t>(n, 1) * 4, ctx.stream), key(std::max<size_t>(n, 1) * 8, ctx.stream), nsel(8, ctx.stream);
     IGB_LAUNCH(ctx, fill_u32, grid_for(ctx, ns, 256), 256, 0, inv.as<uint32_t>(), ns, 0xffffffffu);
     IGB_LAUNCH(ctx, scatter_pos, grid_for(ctx, n, 256), 256, 0, d_src_of, n, inv.as<uint32_t>());
     IGB_LAUNCH(ctx, map_order, grid_for(ctx, ns, 256), 256, 0, S.order.as<uint32_t>(), S.gid.as<uint32_t>(), ns,
@@ -779,9 +883,9 @@ void subset_pattern_index(Ctx& ctx, const PatternIndex& S, const uint32_t* d_src
     IGB_CUDA(cub::DeviceSelect::Flagged(temp1.p, tb1, og.as<uint32_t>(), keep.as<uint8_t>(), og2.as<uint32_t>(),
                                         nsel.as<int64_t>(), (int64_t)ns, ctx.stream));
     // group key of every kept position = the source group's key
-    IGB_LAUNCH(ctx, gather_u32, grid_for(ctx, n, 256), 256, 0, S.gkey.as<uint32_t>(), og2.as<uint32_t>(), n,
-               key.as<uint32_t>());
-    group_ids(ctx, key.as<uint32_t>(), n, I);
+    IGB_LAUNCH(ctx, gather_u64k, grid_for(ctx, n, 256), 256, 0, S.gkey.as<unsigned long long>(), og2.as<uint32_t>(), n,
+               key.as<unsigned long long>());
+    group_ids(ctx, key.as<unsigned long long>(), n, I);
     tr.mark("groups");
 }
 

@@ -34,7 +34,7 @@ struct RankSpace {
 
 // A pattern set's scan index, independent of the postings it is scanned
 // against: CSR token lists (rarest first in a rank space) and the patterns
-// grouped by their two rarest tokens (t1, t2).
+// grouped by their three rarest tokens (t1, t2, t3) under (t1, t2) parents.
 struct PatternIndex {
     size_t np = 0;   // patterns
     size_t G = 0;    // groups
@@ -43,7 +43,10 @@ struct PatternIndex {
     std::shared_ptr<DevBuf> toks;  // u16 tokens (shared by subset indexes)
     DevBuf order;    // np u32: patterns in group-key order
     DevBuf gid;      // np u32: group of each ordered position
-    DevBuf gkey;     // G u32: (t1 << 16) | t2
+    DevBuf gkey;     // G u64: (t1 << 32) | (t2 << 16) | t3
+    size_t G2 = 0;   // parent groups (t1, t2)
+    DevBuf pid;      // G u32: parent of each group
+    DevBuf pkey;     // G2 u32: (t1 << 16) | t2
 };
 
 // descending: most frequent first (default: rarest first)
@@ -57,7 +60,7 @@ void cluster_order(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, uint32_t
 // df = A.df + B.df (postings of the two training classes)
 void combined_rank_space(Ctx& ctx, const Postings& A, const Postings& B, RankSpace& R);
 void build_pattern_index(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const RankSpace& R, PatternIndex& I);
-void group_ids(Ctx& ctx, const uint32_t* d_sorted_key, size_t np, PatternIndex& I);
+void group_ids(Ctx& ctx, const unsigned long long* d_sorted_key, size_t np, PatternIndex& I);
 // index of the patterns S.pattern[d_src_of[i]], i < n (a subset, e.g. the pure
 // patterns among the candidates), without re-ranking or re-sorting
 void subset_pattern_index(Ctx& ctx, const PatternIndex& S, const uint32_t* d_src_of, size_t n, PatternIndex& I);
