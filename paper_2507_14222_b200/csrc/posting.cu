@@ -323,16 +323,30 @@ __global__ void gather_u32(const uint32_t* __restrict__ src, const uint32_t* __r
 // C3 ~1M patterns fall into ~35k groups, so most of the (t1, t2) work is shared.
 constexpr uint32_t kNoTok = 0xffffu;
 
-// group key of a pattern: its three rarest tokens (t1, t2, t3), kNoTok when absent
+// group key of a pattern: its three rarest tokens (t1, t2, t3), absent = all
+// ones, packed in b bits each (3b-bit radix sort); expand_keys restores the
+// (t1 << 32) | (t2 << 16) | t3 form with kNoTok, which sorts identically
 __global__ void group_keys(const uint32_t* __restrict__ tok_beg, const uint32_t* __restrict__ tok_len,
-                           const uint16_t* __restrict__ toks, size_t np,
+                           const uint16_t* __restrict__ toks, size_t np, int b,
                            unsigned long long* __restrict__ key, uint32_t* __restrict__ idx) {
+    const unsigned long long none = (1ull << b) - 1ull;
     for (size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += (size_t)gridDim.x * blockDim.x) {
         const uint32_t o = tok_beg[p], m = tok_len[p];
-        const unsigned long long t1 = m >= 1 ? toks[o] : kNoTok, t2 = m >= 2 ? toks[o + 1] : kNoTok,
-                                 t3 = m >= 3 ? toks[o + 2] : kNoTok;
-        key[p] = (t1 << 32) | (t2 << 16) | t3;
+        const unsigned long long t1 = m >= 1 ? toks[o] : none, t2 = m >= 2 ? toks[o + 1] : none,
+                                 t3 = m >= 3 ? toks[o + 2] : none;
+        key[p] = (t1 << (2 * b)) | (t2 << b) | t3;
         idx[p] = (uint32_t)p;
+    }
+}
+
+__global__ void expand_keys(unsigned long long* __restrict__ key, size_t n, int b) {
+    const unsigned long long none = (1ull << b) - 1ull;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        const unsigned long long x = key[i];
+        unsigned long long t[3] = {(x >> (2 * b)) & none, (x >> b) & none, x & none};
+        for (auto& v : t)
+            if (v == none) v = kNoTok;
+        key[i] = (t[0] << 32) | (t[1] << 16) | t[2];
     }
 }
 
@@ -788,17 +802,20 @@ void build_pattern_index(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, co
     }
     tr.mark("token_lists");
     // group patterns by their three rarest tokens
+    int b = 1;
+    while ((1u << b) <= L) ++b;  // token ids < L < 2^b - 1 stays free for "absent"
     DevBuf key(np * 8, ctx.stream), key2(np * 8, ctx.stream), idx(np * 4, ctx.stream);
     IGB_LAUNCH(ctx, group_keys, grid_for(ctx, np, 256), 256, 0, I.beg.as<uint32_t>(), I.len.as<uint32_t>(),
-               I.toks->as<uint16_t>(), np, key.as<unsigned long long>(), idx.as<uint32_t>());
+               I.toks->as<uint16_t>(), np, b, key.as<unsigned long long>(), idx.as<uint32_t>());
     size_t tb1 = 0;
     IGB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb1, key.as<unsigned long long>(), key2.as<unsigned long long>(),
-                                             idx.as<uint32_t>(), I.order.as<uint32_t>(), (int64_t)np, 0, 48,
+                                             idx.as<uint32_t>(), I.order.as<uint32_t>(), (int64_t)np, 0, 3 * b,
                                              ctx.stream));
     DevBuf temp1(tb1, ctx.stream);
     IGB_CUDA(cub::DeviceRadixSort::SortPairs(temp1.p, tb1, key.as<unsigned long long>(), key2.as<unsigned long long>(),
-                                             idx.as<uint32_t>(), I.order.as<uint32_t>(), (int64_t)np, 0, 48,
+                                             idx.as<uint32_t>(), I.order.as<uint32_t>(), (int64_t)np, 0, 3 * b,
                                              ctx.stream));
+    IGB_LAUNCH(ctx, expand_keys, grid_for(ctx, np, 256), 256, 0, key2.as<unsigned long long>(), np, b);
     group_ids(ctx, key2.as<unsigned long long>(), np, I);
     tr.mark("group_sort");
 }
