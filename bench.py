@@ -208,7 +208,16 @@ def run_b200(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    # IG_BENCH_FORCE_SHARDED=1 (under torchrun) runs the sharded NCCL path even
+    # at world size 1: a plumbing check of the N>1 code on a single GPU
+    sharded_mode = world > 1 or os.environ.get("IG_BENCH_FORCE_SHARDED") == "1"
+    out = sys.stdout
+    if sharded_mode:
+        # NCCL prints its banner on stdout at communicator creation: send fd 1
+        # to stderr for the whole run and write the JSON line to the saved fd
+        out = os.fdopen(os.dup(1), "w")
+        sys.stdout.flush()
+        os.dup2(2, 1)
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
@@ -238,13 +247,13 @@ def run_b200(args):
     dA = torch.empty(n_test, dtype=torch.int64, device="cuda")
     dN = torch.empty(n_test, dtype=torch.int64, device="cuda")
 
-    if world > 1:
+    if sharded_mode:
         from paper_2507_14222_b200 import sharded
         ex = sharded.TorchExchange()
 
     def step_resident():
         enc = api.encode_training(dev_tr, ctx)
-        if world > 1:
+        if sharded_mode:
             # pair tiles round-robin, candidates to fingerprint owners (NCCL all-to-all),
             # owner-local support/coverage, partial evidence all-reduced.
             res = sharded.fit_distributed(ctx, enc, rank, world, ex)
@@ -261,7 +270,7 @@ def run_b200(args):
     def step_e2e():
         enc = api.encode_training(cols_tr, ctx)
         cols_te.prefetch(ctx)  # test columns' H2D (copy stream) overlaps the fit
-        if world > 1:
+        if sharded_mode:
             res = sharded.fit_distributed(ctx, enc, rank, world, ex)
             tenc = api.encode_rows(cols_te, enc, ctx)
             a, n = sharded.evidence_distributed(res, tenc, ex)
@@ -367,7 +376,7 @@ def run_b200(args):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": workload_config(args, n_train, n_test, {"parallelism": (f"sharded{world}: pair tiles round-robin, NCCL all-to-all to fingerprint owners, "
-                                                                              "all-reduce of partial evidence") if world > 1 else "1gpu",
+                                                                              "all-reduce of partial evidence") if sharded_mode else "1gpu",
                                                               **cfg_extra}),
             "phases_ms": {"fit": phases, "step_median": ms, "steps": step_ms},
             "host_prep_s": host_prep, "gen_s": t_gen,
@@ -376,7 +385,7 @@ def run_b200(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_reference(csv, args, args.cpu_sample_tests)
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        print(json.dumps(line), file=out, flush=True)
     if dist is not None:
         dist.destroy_process_group()
 

@@ -80,6 +80,7 @@ __device__ void table_insert(const Table& T, const int64_t* __restrict__ X, int 
     const uint64_t rep = (((uint64_t)u << 32) | v) + 1;
     uint64_t s = (fp ^ T.seed) & T.mask;
     for (uint64_t probes = 0; probes <= T.mask; ++probes, s = (s + 1) & T.mask) {
+        if ((probes & 63) == 63 && *(volatile int*)T.fail) return;  // long probe into a full table
         ulonglong2* slot = T.slots + s;
         ulonglong2 cur;
         cur.x = ld_volatile(&slot->x);
@@ -210,6 +211,7 @@ __global__ void pair_insert_list(const int64_t* __restrict__ X, int k, const uin
                                  size_t n_list, Table T) {
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_list;
          i += (size_t)gridDim.x * blockDim.x) {
+        if (*(volatile int*)T.fail) return;  // table full: the host retries with a larger one
         const uint2 p = list[i];
         const int64_t* a = X + (size_t)p.x * k;
         const int64_t* b = X + (size_t)p.y * k;
@@ -458,7 +460,10 @@ uint64_t dedup_pairs(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, const 
 
     // Initial capacity from a sub-linear guess of the distinct count; doubled
     // (x4) and rerun if the table fills.  Results never depend on capacity.
-    uint64_t guess = (uint64_t)(4.0 * std::pow((double)(pairs + n), 0.8)) + 2 * n + 1024;
+    // a list source (received records) is already deduplicated per sender:
+    // nearly every record is distinct
+    uint64_t guess = src.list ? 2 * src.n_list + 1024
+                              : (uint64_t)(4.0 * std::pow((double)(pairs + n), 0.8)) + 2 * n + 1024;
     uint64_t cap = next_pow2(std::max<uint64_t>(guess, 1u << 16));
     const uint64_t bound = src.list ? src.n_list : std::min<uint64_t>(my_tiles * (uint64_t)tile * tile, pairs * src.tile_step + n);
     const uint64_t max_cap = next_pow2(2 * bound + 1024);

@@ -33,7 +33,12 @@ class _CudaArray:
 
 
 class _ShardModel(Model):
-    """The owned dictionaries of a shard (memory owned by the shard)."""
+    """The owned dictionaries of a shard (memory owned by the shard, which this
+    view keeps alive)."""
+
+    def __init__(self, ctx: Context, handle, owner: "Shard"):
+        super().__init__(ctx, handle)
+        self._owner = owner
 
     def __del__(self):
         self.handle = None
@@ -71,7 +76,7 @@ class Shard:
 
     @property
     def model(self) -> Model:
-        return _ShardModel(self.ctx, lib.ig_shard_model(self.handle))
+        return _ShardModel(self.ctx, lib.ig_shard_model(self.handle), self)
 
     def partial_evidence(self, tenc: Encoding):
         """A/N of the owned dictionaries only (int64 device tensors)."""

@@ -55,3 +55,23 @@ def test_emulated_world_matches_single_device(mods, rows, ratio):
             A += a
             N += n
         assert np.array_equal(A.cpu().numpy(), A1) and np.array_equal(N.cpu().numpy(), N1), world
+
+
+def test_shard_model_outlives_its_shard_handle(mods):
+    """A shard's model view keeps the shard alive (the bench keeps only the model)."""
+    import gc
+    api, sharded = mods
+    csv = synth.nsl_csv(2500, seed=78)
+    ctx = api.default_context()
+    table = api.read_csv(csv)
+    ntr = 8 * table.rows // 10
+    tr, te = table.slice(0, ntr), table.slice(ntr, table.rows)
+    schema = api.infer_schema(tr, "label", decimals=1)
+    enc = api.encode_training(api.Columns(tr, schema, True), ctx)
+    tenc = api.encode_rows(api.Columns(te, schema, False), enc, ctx)
+    single = api.fit_encoded(enc)
+    model = sharded.fit_emulated(ctx, enc, 1)[0].model  # the shard list is dropped here
+    gc.collect()
+    A, N = model.evidence_encoded(tenc)
+    A1, N1 = single.evidence_encoded(tenc)
+    assert np.array_equal(A, A1) and np.array_equal(N, N1)
