@@ -222,6 +222,24 @@ __global__ void rank_keys(const uint32_t* __restrict__ df, uint32_t L, unsigned 
     }
 }
 
+// Small token universes (L <= kRankCount): rank by counting against the keys
+// staged in shared memory — one launch instead of a radix sort's passes.
+constexpr uint32_t kRankCount = 4096;
+__global__ void rank_by_key_count(const uint32_t* __restrict__ df, uint32_t L, bool descending,
+                                  uint16_t* __restrict__ rank, uint16_t* __restrict__ byrank) {
+    __shared__ unsigned long long key[kRankCount];
+    for (uint32_t t = threadIdx.x; t < L; t += blockDim.x)
+        key[t] = ((unsigned long long)(descending ? 0xffffffffu - df[t] : df[t]) << 16) | t;
+    __syncthreads();
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < L; t += gridDim.x * blockDim.x) {
+        const unsigned long long k = key[t];
+        uint32_t r = 0;
+        for (uint32_t j = 0; j < L; ++j) r += key[j] < k ? 1u : 0u;
+        rank[t] = (uint16_t)r;
+        byrank[r] = (uint16_t)t;
+    }
+}
+
 __global__ void invert_rank(const uint16_t* __restrict__ byrank, uint32_t L, uint16_t* __restrict__ rank) {
     for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < L; r += gridDim.x * blockDim.x) rank[byrank[r]] = (uint16_t)r;
 }
@@ -730,6 +748,11 @@ void make_rank_space(Ctx& ctx, const uint32_t* d_df, uint32_t L, RankSpace& R, b
     IGB_CUDA(cudaMemcpyAsync(R.df.p, d_df, (size_t)L * 4, cudaMemcpyDeviceToDevice, ctx.stream));
     R.rank.alloc((size_t)L * 2, ctx.stream);
     R.byrank.alloc((size_t)L * 2, ctx.stream);
+    if (L <= kRankCount) {
+        IGB_LAUNCH(ctx, rank_by_key_count, (L + 255) / 256, 256, 0, d_df, L, descending, R.rank.as<uint16_t>(),
+                   R.byrank.as<uint16_t>());
+        return;
+    }
     DevBuf key((size_t)L * 8, ctx.stream), key2((size_t)L * 8, ctx.stream), tok((size_t)L * 2, ctx.stream);
     IGB_LAUNCH(ctx, rank_keys, grid_for(ctx, L, 256), 256, 0, d_df, L, key.as<unsigned long long>(),
                tok.as<uint16_t>(), descending);

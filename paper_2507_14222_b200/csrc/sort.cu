@@ -224,7 +224,7 @@ __global__ void gather_rows_u32(const int64_t* __restrict__ src, const uint32_t*
 // row in registers and streams 128-row chunks of the j range through shared
 // memory (warp-broadcast reads).  blockIdx.y splits the j range so that even a
 // few thousand rows fill every SM; partial counts meet in rank[] by atomics.
-constexpr uint32_t kSmallSort = 10240;
+constexpr uint32_t kSmallSort = 24576;
 constexpr int kRankChunk = 128;
 template <int KMAX>
 __global__ void __launch_bounds__(kRankChunk)
@@ -264,6 +264,32 @@ __global__ void perm_from_rank(const uint32_t* __restrict__ rank, uint32_t n, ui
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) perm[rank[i]] = i;
 }
 
+__global__ void keys_to_rows(const unsigned long long* __restrict__ keys, size_t n, int n_keys,
+                             int64_t* __restrict__ rows) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        for (int j = 0; j < n_keys; ++j) rows[i * n_keys + j] = (int64_t)keys[(size_t)j * n + i];
+}
+
+// perm = stable canonical order of n rows of k words (k <= 32) by counting
+void count_sort_rows(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, uint32_t* d_perm) {
+    DevBuf rank(n * 4, ctx.stream);
+    IGB_CUDA(cudaMemsetAsync(rank.p, 0, n * 4, ctx.stream));
+    const uint32_t bx = (uint32_t)((n + kRankChunk - 1) / kRankChunk);
+    // split j so that bx * by covers ~4 CTAs per SM, in whole chunks
+    uint32_t by = std::max<uint32_t>(1, (uint32_t)(4 * ctx.sm_count) / bx);
+    uint32_t per = (uint32_t)((n + by - 1) / by);
+    per = (per + kRankChunk - 1) / kRankChunk * kRankChunk;
+    by = (uint32_t)((n + per - 1) / per);
+    const dim3 grid(bx, by);
+    if (k <= 8)
+        IGB_LAUNCH(ctx, rank_by_count<8>, grid, kRankChunk, 0, d_rows, (uint32_t)n, (int)k, per, rank.as<uint32_t>());
+    else if (k <= 16)
+        IGB_LAUNCH(ctx, rank_by_count<16>, grid, kRankChunk, 0, d_rows, (uint32_t)n, (int)k, per, rank.as<uint32_t>());
+    else
+        IGB_LAUNCH(ctx, rank_by_count<32>, grid, kRankChunk, 0, d_rows, (uint32_t)n, (int)k, per, rank.as<uint32_t>());
+    IGB_LAUNCH(ctx, perm_from_rank, grid_for(ctx, n, 256), 256, 0, rank.as<uint32_t>(), (uint32_t)n, d_perm);
+}
+
 uint32_t next_pow2_u32(uint64_t x) {
     uint64_t p = 1;
     while (p < x) p <<= 1;
@@ -279,26 +305,6 @@ void sort_rows_canonical(Ctx& ctx, const int64_t* d_words, size_t n, size_t k, u
         return;
     }
     Trace tr(ctx, "sort_rows", -1);
-    if (n <= kSmallSort && k <= 32) {
-        DevBuf rank(n * 4, ctx.stream);
-        IGB_CUDA(cudaMemsetAsync(rank.p, 0, n * 4, ctx.stream));
-        const uint32_t bx = (uint32_t)((n + kRankChunk - 1) / kRankChunk);
-        // split j so that bx * by covers ~4 CTAs per SM, in whole chunks
-        uint32_t by = std::max<uint32_t>(1, (uint32_t)(4 * ctx.sm_count) / bx);
-        uint32_t per = (uint32_t)((n + by - 1) / by);
-        per = (per + kRankChunk - 1) / kRankChunk * kRankChunk;
-        by = (uint32_t)((n + per - 1) / per);
-        const dim3 grid(bx, by);
-        if (k <= 16)
-            IGB_LAUNCH(ctx, rank_by_count<16>, grid, kRankChunk, 0, d_words, (uint32_t)n, (int)k, per,
-                       rank.as<uint32_t>());
-        else
-            IGB_LAUNCH(ctx, rank_by_count<32>, grid, kRankChunk, 0, d_words, (uint32_t)n, (int)k, per,
-                       rank.as<uint32_t>());
-        IGB_LAUNCH(ctx, perm_from_rank, grid_for(ctx, n, 256), 256, 0, rank.as<uint32_t>(), (uint32_t)n, d_perm);
-        tr.mark("rank_by_count");
-        return;
-    }
     // Per-column hash sets; start small (columns usually hold a few thousand
     // distinct words) and grow x16 when a column passes half load.
     uint32_t slots = next_pow2_u32(std::min<uint64_t>(2 * n + 16, 1ull << 16));
@@ -408,6 +414,16 @@ void sort_rows_canonical(Ctx& ctx, const int64_t* d_words, size_t n, size_t k, u
     }
     IGB_LAUNCH(ctx, pack_keys, grid_for(ctx, n, 128), 128, 0, d_words, n, (int)k, tables.as<ulonglong2>(), slots,
                dfields.p ? dfields.as<Field>() : nullptr, ft, n_keys, keys.as<unsigned long long>());
+    if (n <= kSmallSort) {
+        // few rows: rank by counting on the packed keys (<= 8 words, most
+        // comparisons end at the first) instead of ~B/8 launch-bound radix passes
+        DevBuf krows(n * n_keys * 8, ctx.stream);
+        IGB_LAUNCH(ctx, keys_to_rows, grid_for(ctx, n, 256), 256, 0, keys.as<unsigned long long>(), n, n_keys,
+                   krows.as<int64_t>());
+        count_sort_rows(ctx, krows.as<int64_t>(), n, (size_t)n_keys, d_perm);
+        tr.mark("count_keys");
+        return;
+    }
     DevBuf k1(n * 8, ctx.stream), k2(n * 8, ctx.stream), p2(n * 4, ctx.stream);
     IGB_LAUNCH(ctx, iota32, grid_for(ctx, n, 256), 256, 0, d_perm, n);
     size_t tb3 = 0;
