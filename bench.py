@@ -262,9 +262,11 @@ def run_b200(args):
             dA.copy_(a)
             dN.copy_(n)
             return enc, res.model, tenc
-        model = api.fit_encoded(enc)
+        # the test rows are packed and indexed in the background (index stream)
+        # while the fit runs
         tenc = api.encode_rows(dev_te, enc, ctx)
-        model.evidence_device(tenc.device_rows(2), n_test, dA.data_ptr(), dN.data_ptr())
+        model = api.fit_encoded(enc)
+        model.evidence_encoded_device(tenc, dA.data_ptr(), dN.data_ptr())
         return enc, model, tenc
 
     def step_e2e():
@@ -275,8 +277,8 @@ def run_b200(args):
             tenc = api.encode_rows(cols_te, enc, ctx)
             a, n = sharded.evidence_distributed(res, tenc, ex)
             return res.model, a.cpu().numpy(), n.cpu().numpy()
+        tenc = api.encode_rows(cols_te, enc, ctx)  # from the prefetch: background pack + index
         model = api.fit_encoded(enc)
-        tenc = api.encode_rows(cols_te, enc, ctx)
         A, N = model.evidence_encoded(tenc)
         return model, A, N
 

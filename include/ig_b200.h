@@ -210,6 +210,13 @@ void ig_encoding_free(ig_encoding* e);
 int ig_fit_encoded(ig_ctx* ctx, const ig_encoding* train, const ig_kernel_config* cfg, ig_model** out);
 int ig_evidence_encoded(ig_ctx* ctx, const ig_model* m, const ig_encoding* tests, int64_t* A,
                         int64_t* N);
+/* Same with device outputs d_A / d_N (int64[rows]), ordered on the context
+ * stream.  A test encoding made by ig_encode_rows from resident or prefetched
+ * columns is packed and indexed (row postings) in the background on the
+ * context's index stream, overlapping a fit issued meanwhile; evidence and every
+ * accessor wait for it. */
+int ig_evidence_encoded_device(ig_ctx* ctx, const ig_model* m, const ig_encoding* tests, int64_t* d_A,
+                               int64_t* d_N);
 
 /* ---------------------------------------------------------------- archive / explain
  * SURVEY.md §8(f) ranks 1-2.  ModelArchive: schema

@@ -110,6 +110,7 @@ SIGNATURES = [
     ("ig_shard_model", vp, [vp]),
     ("ig_shard_free", None, [vp]),
     ("ig_evidence_encoded", C.c_int, [vp, vp, vp, p64, p64]),
+    ("ig_evidence_encoded_device", C.c_int, [vp, vp, vp, vp, vp]),
 ]
 
 for _name, _res, _args in SIGNATURES:

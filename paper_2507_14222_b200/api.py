@@ -331,6 +331,11 @@ class Model:
         self.ctx.check(lib.ig_evidence_device(self.ctx.handle, self.handle, C.c_void_p(d_tests_ptr), n_tests,
                                               self.logical_len, C.c_void_p(d_A_ptr), C.c_void_p(d_N_ptr)))
 
+    def evidence_encoded_device(self, enc: "Encoding", d_A_ptr: int, d_N_ptr: int) -> None:
+        """evidence of a test encoding into device int64 buffers (ordered on the context stream)."""
+        self.ctx.check(lib.ig_evidence_encoded_device(self.ctx.handle, self.handle, enc.handle,
+                                                      C.c_void_p(d_A_ptr), C.c_void_p(d_N_ptr)))
+
     def evidence_encoded(self, enc: "Encoding") -> tuple[np.ndarray, np.ndarray]:
         n = enc.rows(2)
         A = np.zeros(n, np.int64)

@@ -45,6 +45,33 @@ struct ig_model {
     igb::EnumStats stats[2];
 };
 
+// Background index of a test encoding: its rows are packed on the context's
+// index stream (rows_ready) and a host thread builds their postings there
+// (done), so a fit issued meanwhile on the other streams overlaps both.
+struct RowIndexJob {
+    std::thread th;
+    igb::Postings P;
+    bool has_postings = false;
+    cudaEvent_t rows_ready = nullptr, done = nullptr;
+    std::exception_ptr err;
+    uint64_t launches = 0;
+    bool joined = false;
+    // join the builder (rethrows its error); launches are added to `ctx` once
+    void wait(igb::Ctx* ctx) {
+        if (!joined) {
+            if (th.joinable()) th.join();
+            joined = true;
+            if (ctx) ctx->launches += launches;
+        }
+        if (err) std::rethrow_exception(err);
+    }
+    ~RowIndexJob() {
+        if (th.joinable()) th.join();
+        if (rows_ready) cudaEventDestroy(rows_ready);
+        if (done) cudaEventDestroy(done);
+    }
+};
+
 namespace {
 
 thread_local std::string g_err;
@@ -317,15 +344,16 @@ void copy_out(igb::Ctx& ctx, ig_candidates& c, int64_t* words, int64_t* sup, int
 }
 
 void evidence_impl(igb::Ctx& ctx, const ig_model& m, const int64_t* d_tests, size_t nt, uint32_t L, int64_t* d_A,
-                   int64_t* d_N) {
+                   int64_t* d_N, const igb::Postings* pre = nullptr) {
     if (L != m.L) fail(IG_E_INVALID_ARG, "fused_score: logical length mismatch");
     const size_t k = igb::words_for(L);
     // Fit scores are support * size^2 >= 0, so the vertical matcher applies;
     // test-row postings are built once and shared by both dictionaries.
     if (igb::postings_supported(L, nt)) {
         igb::Trace tr(ctx, "evidence", -1);
-        igb::Postings PT;
-        igb::build_postings(ctx, d_tests, nt, k, L, PT, true, true);
+        igb::Postings own;
+        if (!pre) igb::build_postings(ctx, d_tests, nt, k, L, own, true, true);
+        const igb::Postings& PT = pre ? *pre : own;
         tr.mark("test_postings");
         DevBuf flag(sizeof(int), ctx.stream);
         IGB_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), ctx.stream));
@@ -338,8 +366,7 @@ void evidence_impl(igb::Ctx& ctx, const ig_model& m, const int64_t* d_tests, siz
             trc.mark("match");
         }, m.pure[0].rows.n + m.pure[1].rows.n <= kConcurrentPatterns);
         int h = 0;
-        IGB_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
-        IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+        igb::read_back(ctx, &h, flag.p, sizeof(int));
         if (h) fail(IG_E_OVERFLOW, "evidence score sum overflows int64");
         return;
     }
@@ -374,6 +401,7 @@ int ig_ctx_create(int device, ig_ctx** out) {
         IGB_CUDA(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
         IGB_CUDA(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
         IGB_CUDA(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+        IGB_CUDA(cudaStreamCreateWithFlags(&c->index, cudaStreamNonBlocking));
         c->stream = c->own;
         cudaDeviceProp prop;
         IGB_CUDA(cudaGetDeviceProperties(&prop, device));
@@ -408,7 +436,7 @@ int ig_ctx_create(int device, ig_ctx** out) {
 void ig_ctx_destroy(ig_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
-    for (cudaStream_t st : {ctx->own, ctx->aux, ctx->copy}) {
+    for (cudaStream_t st : {ctx->own, ctx->aux, ctx->copy, ctx->index}) {
         if (!st) continue;
         cudaStreamSynchronize(st);
         cudaStreamDestroy(st);
@@ -761,11 +789,53 @@ int ig_encode_rows(ig_ctx* ctx, const ig_columns* cols, const ig_encoding* train
     *out = nullptr;
     return guard(ctx, [&] {
         auto e = std::make_unique<ig_encoding>();
-        igb::encode_rows_dev(*ctx, *cols, *train, *e);
+        auto job = std::make_shared<RowIndexJob>();
+        IGB_CUDA(cudaEventCreateWithFlags(&job->rows_ready, cudaEventDisableTiming));
+        IGB_CUDA(cudaEventCreateWithFlags(&job->done, cudaEventDisableTiming));
+        // the index stream runs after everything already queued on the context stream
+        IGB_CUDA(cudaEventRecord(job->rows_ready, ctx->stream));
+        IGB_CUDA(cudaStreamWaitEvent(ctx->index, job->rows_ready, 0));
+        igb::Ctx cx = *ctx;
+        cx.stream = ctx->index;
+        cx.launches = 0;
+        igb::encode_rows_dev(cx, *cols, *train, *e, /*queue_only=*/true);
+        ctx->launches += cx.launches;
         e->all.buf.persist();
+        IGB_CUDA(cudaEventRecord(job->rows_ready, ctx->index));
+        const size_t n = e->all.n, k = e->all.k;
+        const uint32_t L = e->L;
+        if (n && igb::postings_supported(L, n)) {
+            job->has_postings = true;
+            cx.launches = 0;
+            const int64_t* rows = e->all.data();
+            RowIndexJob* j = job.get();
+            job->th = std::thread([j, cx, rows, n, k, L]() mutable {
+                try {
+                    IGB_CUDA(cudaSetDevice(cx.device));
+                    igb::build_postings(cx, rows, n, k, L, j->P, true, true);
+                    for (DevBuf* b : {&j->P.dense, &j->P.df, &j->P.nz_off, &j->P.nz_idx, &j->P.perm, &j->P.group,
+                                      &j->P.rep})
+                        b->persist();  // read by evidence on other streams
+                    IGB_CUDA(cudaEventRecord(j->done, cx.stream));
+                } catch (...) {
+                    j->err = std::current_exception();
+                }
+                j->launches = cx.launches;
+            });
+        } else {
+            IGB_CUDA(cudaEventRecord(job->done, ctx->index));
+        }
+        e->job = std::move(job);
         *out = e.release();
     });
 }
+
+namespace {
+// rows of a background test encoding are usable once packed
+void rows_ready(ig_ctx* ctx, const ig_encoding* e) {
+    if (e && e->job) IGB_CUDA(cudaStreamWaitEvent(ctx->stream, e->job->rows_ready, 0));
+}
+}  // namespace
 
 uint32_t ig_encoding_logical_len(const ig_encoding* e) { return e ? e->L : 0; }
 static const DevRows* enc_rows(const ig_encoding* e, int which) {
@@ -773,10 +843,12 @@ static const DevRows* enc_rows(const ig_encoding* e, int which) {
 }
 size_t ig_encoding_rows(const ig_encoding* e, int which) { return e ? enc_rows(e, which)->n : 0; }
 const int64_t* ig_encoding_device_rows(const ig_encoding* e, int which) {
+    if (e && e->job) cudaEventSynchronize(e->job->rows_ready);  // raw pointer: the caller's stream is unknown
     return e ? enc_rows(e, which)->data() : nullptr;
 }
 int ig_encoding_copy_rows(ig_ctx* ctx, const ig_encoding* e, int which, int64_t* out) {
     return guard(ctx, [&] {
+        rows_ready(ctx, e);
         const DevRows* r = enc_rows(e, which);
         if (r->n * r->k)
             IGB_CUDA(cudaMemcpyAsync(out, r->data(), r->n * r->k * 8, cudaMemcpyDeviceToHost, ctx->stream));
@@ -804,15 +876,35 @@ int ig_fit_encoded(ig_ctx* ctx, const ig_encoding* train, const ig_kernel_config
     });
 }
 
+namespace {
+void evidence_of_encoding(ig_ctx* ctx, const ig_model* m, const ig_encoding* tests, int64_t* d_A, int64_t* d_N) {
+    const size_t nt = tests->all.n;
+    const igb::Postings* pre = nullptr;
+    if (tests->job) {
+        tests->job->wait(ctx);
+        IGB_CUDA(cudaStreamWaitEvent(ctx->stream, tests->job->done, 0));
+        if (tests->job->has_postings) pre = &tests->job->P;
+    }
+    evidence_impl(*ctx, *m, tests->all.data(), nt, tests->L, d_A, d_N, pre);
+}
+}  // namespace
+
 int ig_evidence_encoded(ig_ctx* ctx, const ig_model* m, const ig_encoding* tests, int64_t* A, int64_t* N) {
     return guard(ctx, [&] {
         const size_t nt = tests->all.n;
         if (nt == 0) return;
         DevBuf a(nt * 8, ctx->stream), b(nt * 8, ctx->stream);
-        evidence_impl(*ctx, *m, tests->all.data(), nt, tests->L, a.as<int64_t>(), b.as<int64_t>());
+        evidence_of_encoding(ctx, m, tests, a.as<int64_t>(), b.as<int64_t>());
         IGB_CUDA(cudaMemcpyAsync(A, a.p, nt * 8, cudaMemcpyDeviceToHost, ctx->stream));
         IGB_CUDA(cudaMemcpyAsync(N, b.p, nt * 8, cudaMemcpyDeviceToHost, ctx->stream));
         IGB_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int ig_evidence_encoded_device(ig_ctx* ctx, const ig_model* m, const ig_encoding* tests, int64_t* d_A, int64_t* d_N) {
+    return guard(ctx, [&] {
+        if (tests->all.n == 0) return;
+        evidence_of_encoding(ctx, m, tests, d_A, d_N);
     });
 }
 

@@ -211,8 +211,7 @@ size_t select_flagged(Ctx& ctx, const uint8_t* d_flags, size_t n, DevBuf& idx_ou
     IGB_CUDA(cub::DeviceSelect::Flagged(temp.p, tb, iota.as<uint32_t>(), d_flags, idx_out.as<uint32_t>(),
                                         nsel.as<int64_t>(), (int64_t)n, ctx.stream));
     int64_t m = 0;
-    IGB_CUDA(cudaMemcpyAsync(&m, nsel.p, 8, cudaMemcpyDeviceToHost, ctx.stream));
-    IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+    read_back(ctx, &m, nsel.p, 8);
     return (size_t)m;
 }
 
@@ -236,7 +235,8 @@ struct PrefetchCols {
 };
 }  // namespace
 
-void upload_and_code(Ctx& ctx, const ig_columns& c, DeviceCols& d) {
+// returns true when it queued copies that read the columns' host memory
+bool upload_and_code(Ctx& ctx, const ig_columns& c, DeviceCols& d) {
     d.n = c.n_rows;
     std::vector<ColDesc> desc;
     for (size_t j = 0; j < c.n_cols; ++j) {
@@ -255,6 +255,7 @@ void upload_and_code(Ctx& ctx, const ig_columns& c, DeviceCols& d) {
                                  ctx.stream));
     const double* vals;
     const int32_t* cats;
+    bool host_read = false;
     auto* pf = static_cast<PrefetchCols*>(c.prefetch.get());
     if (pf && pf->device == ctx.device) {
         // a prefetch is in flight: order after it, then own its buffers
@@ -274,6 +275,7 @@ void upload_and_code(Ctx& ctx, const ig_columns& c, DeviceCols& d) {
         cats = static_cast<const int32_t*>(c.d_cat.get());
         d.attack_ptr = static_cast<const uint8_t*>(c.d_attack.get());
     } else {
+        host_read = true;
         d.values.alloc(c.values.size() * 8, ctx.stream);
         d.cat.alloc(c.cat.size() * 4, ctx.stream);
         if (!c.values.empty())
@@ -294,6 +296,7 @@ void upload_and_code(Ctx& ctx, const ig_columns& c, DeviceCols& d) {
     if (cells)
         IGB_LAUNCH(ctx, cell_codes, grid_for(ctx, cells, 256), 256, 0, vals, cats, d.cols.as<ColDesc>(), d.n_feat,
                    d.n, c.scale, d.codes.as<int64_t>());
+    return host_read;
 }
 
 // Upload a vocabulary's lookup tables and pack `d`'s cells into rows.
@@ -385,14 +388,12 @@ void encode_training_dev(Ctx& ctx, const ig_columns& c, ig_encoding& e) {
         IGB_LAUNCH(ctx, distinct_codes, dim3((unsigned)chunks, (unsigned)d.n_feat), 256, 0, d.codes.as<int64_t>(), d.n,
                    lcode.as<int64_t>(), lcol.as<int32_t>(), lcnt.as<unsigned long long>());
     unsigned long long m = 0;
-    IGB_CUDA(cudaMemcpyAsync(&m, lcnt.p, 8, cudaMemcpyDeviceToHost, ctx.stream));
-    IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+    read_back(ctx, &m, lcnt.p, 8);
     std::vector<int64_t> hcode(m);
     std::vector<int32_t> hcol(m);
     if (m) {
-        IGB_CUDA(cudaMemcpyAsync(hcode.data(), lcode.p, m * 8, cudaMemcpyDeviceToHost, ctx.stream));
-        IGB_CUDA(cudaMemcpyAsync(hcol.data(), lcol.p, m * 4, cudaMemcpyDeviceToHost, ctx.stream));
-        IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+        read_back(ctx, hcode.data(), lcode.p, m * 8);
+        read_back(ctx, hcol.data(), lcol.p, m * 4);
     }
 
     // Host: token text for each distinct (column, code), byte-order sort → bits.
@@ -471,8 +472,7 @@ void encode_training_dev(Ctx& ctx, const ig_columns& c, ig_encoding& e) {
     if (na == 0 || nn == 0) fail(IG_E_DATA, "anti-contradiction filtering emptied a class; training impossible");
     if (nr) {
         std::vector<uint32_t> h(nr);
-        IGB_CUDA(cudaMemcpyAsync(h.data(), idx_r.p, nr * 4, cudaMemcpyDeviceToHost, ctx.stream));
-        IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+        read_back(ctx, h.data(), idx_r.p, nr * 4);
         e.removed.assign(h.begin(), h.end());
     }
     for (int cls = 0; cls < 2; ++cls) {
@@ -489,7 +489,7 @@ void encode_training_dev(Ctx& ctx, const ig_columns& c, ig_encoding& e) {
     IGB_CUDA(cudaStreamSynchronize(ctx.stream));
 }
 
-void encode_rows_dev(Ctx& ctx, const ig_columns& c, const ig_encoding& train, ig_encoding& e) {
+void encode_rows_dev(Ctx& ctx, const ig_columns& c, const ig_encoding& train, ig_encoding& e, bool queue_only) {
     if (c.n_cols != train.n_cols || c.label_index != train.label_index)
         fail(IG_E_DATA, "encode_rows: columns do not match the training schema");
     e = ig_encoding{};
@@ -498,7 +498,7 @@ void encode_rows_dev(Ctx& ctx, const ig_columns& c, const ig_encoding& train, ig
     e.label_index = train.label_index;
     e.decimals = train.decimals;
     DeviceCols d;
-    upload_and_code(ctx, c, d);
+    const bool host_read = upload_and_code(ctx, c, d);
     // Categorical ids of this table → training bits through the token text.
     std::vector<std::vector<int32_t>> cat_id_to_bit(c.n_cols);
     for (size_t j = 0; j < c.n_cols; ++j) {
@@ -510,7 +510,9 @@ void encode_rows_dev(Ctx& ctx, const ig_columns& c, const ig_encoding& train, ig
         }
     }
     pack_with(ctx, train, d, cat_id_to_bit, e.all);
-    IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+    // copies from the caller's host columns must finish before we return; with
+    // resident or prefetched columns the work stays queued on the stream
+    if (host_read || !queue_only) IGB_CUDA(cudaStreamSynchronize(ctx.stream));
 }
 
 void upload_columns(Ctx& ctx, ig_columns& c) {

@@ -1,5 +1,6 @@
 // encode.cuh — resident vocabulary + packed rows (kernel 1 outputs).
 #pragma once
+#include <memory>
 
 #include <string>
 #include <unordered_map>
@@ -21,6 +22,10 @@ struct ig_encoding {
     std::vector<int> empty_bit;                               // per column bit of "j:" or -1
     igb::DevRows attack, normal, all;
     std::vector<uint64_t> removed;                            // anti-contradiction source rows
+    // test encodings: the rows' postings, built in the background by the
+    // encode (capi.cu RowIndexJob) for the next evidence call; last member so
+    // it is joined before the rows it reads are released
+    std::shared_ptr<struct RowIndexJob> job;
 };
 
 namespace igb {
@@ -29,7 +34,10 @@ void upload_columns(Ctx& ctx, ig_columns& c);
 void prefetch_columns(Ctx& ctx, ig_columns& c);
 // wait for an unconsumed prefetch (its host source is about to go away) and drop it
 void drop_prefetch(ig_columns& c);
-void encode_rows_dev(Ctx& ctx, const ig_columns& c, const ig_encoding& train, ig_encoding& e);
+// queue_only: leave the device work queued on ctx.stream when the columns are
+// resident or prefetched (no host memory is read after return)
+void encode_rows_dev(Ctx& ctx, const ig_columns& c, const ig_encoding& train, ig_encoding& e,
+                     bool queue_only = false);
 // archive.cu
 std::string schema_to_text(const ig_schema& s);
 void schema_from_text(const std::string& text, ig_schema& s);

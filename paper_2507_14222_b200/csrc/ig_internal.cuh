@@ -3,6 +3,9 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstring>
+
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -90,6 +93,7 @@ struct Ctx {
     cudaStream_t stream = nullptr;
     cudaStream_t aux = nullptr;  // second class's stream (for_both_classes)
     cudaStream_t copy = nullptr; // host->device prefetches (ig_columns_prefetch)
+    cudaStream_t index = nullptr;  // background test-row encode + postings (ig_encode_rows)
     std::string err;
     uint64_t launches = 0;
     int sm_count = 148;
@@ -100,6 +104,32 @@ struct Ctx {
     uint64_t diag_match_words = 0; // posting word-ANDs of the matcher (Σ_p |b_p| * nnz(rarest token))
     uint64_t diag_match_launches = 0;
 };
+
+// Device->host readback of a small result (counts, flags, totals) and a wait
+// for it, through a per-thread page-locked bounce buffer: a pageable
+// destination is staged by the driver and can queue behind a large in-flight
+// host->device copy (e.g. a columns prefetch) on the copy engines.
+inline void read_back(const Ctx& ctx, void* host_dst, const void* d_src, size_t bytes) {
+    struct Pinned {
+        void* p = nullptr;
+        size_t cap = 0;
+        ~Pinned() {
+            if (p) cudaFreeHost(p);
+        }
+    };
+    thread_local Pinned buf;
+    if (bytes > buf.cap) {
+        if (buf.p) cudaFreeHost(buf.p);
+        buf.p = nullptr;
+        buf.cap = 0;
+        const size_t cap = std::max<size_t>(bytes, 64 << 10);
+        IGB_CUDA(cudaMallocHost(&buf.p, cap));
+        buf.cap = cap;
+    }
+    if (bytes) IGB_CUDA(cudaMemcpyAsync(buf.p, d_src, bytes, cudaMemcpyDeviceToHost, ctx.stream));
+    IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+    if (bytes) std::memcpy(host_dst, buf.p, bytes);
+}
 
 // IG_TRACE=1: per-operation wall times on stderr (synchronises the stream at
 // every mark; diagnostics only).

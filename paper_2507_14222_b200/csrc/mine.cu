@@ -506,8 +506,7 @@ uint64_t dedup_pairs(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, const 
                            pending.as<uint2>(), n_pending, T);
             }
             unsigned long long h[4];
-            IGB_CUDA(cudaMemcpyAsync(h, tm.ctr.p, sizeof(h), cudaMemcpyDeviceToHost, ctx.stream));
-            IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+            read_back(ctx, h, tm.ctr.p, sizeof(h));
             const int failbits = (int)(h[3] & 0xffffffffu);
             if (failbits) {
                 ok = false;
@@ -583,8 +582,7 @@ void bucket_by_owner(Ctx& ctx, const int64_t* d_rows, size_t k, const uint2* d_r
     IGB_LAUNCH(ctx, fp_keys, 1, 256, 0, kOwnerSeed, (int)k, keys.as<unsigned long long>());
     IGB_LAUNCH(ctx, owner_of, grid_for(ctx, count, 256), 256, 0, d_rows, (int)k, d_reps, count, world,
                keys.as<unsigned long long>(), owner.as<uint32_t>(), cnt.as<unsigned long long>());
-    IGB_CUDA(cudaMemcpyAsync(counts.data(), cnt.p, world * 8, cudaMemcpyDeviceToHost, ctx.stream));
-    IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+    read_back(ctx, counts.data(), cnt.p, world * 8);
     std::vector<uint64_t> start(world, 0);
     for (int r = 1; r < world; ++r) start[r] = start[r - 1] + counts[r - 1];
     IGB_CUDA(cudaMemcpyAsync(cur.p, start.data(), world * 8, cudaMemcpyHostToDevice, ctx.stream));
@@ -599,8 +597,7 @@ int score_dev(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const int64_t
     IGB_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), ctx.stream));
     IGB_LAUNCH(ctx, score_k, grid_for(ctx, np, 256), 256, 0, d_pat, np, (int)k, d_support, d_score, flag.as<int>());
     int h = 0;
-    IGB_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
-    IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+    read_back(ctx, &h, flag.p, sizeof(int));
     return h ? IG_E_OVERFLOW : IG_OK;
 }
 
@@ -612,9 +609,8 @@ int total_score_dev(Ctx& ctx, const int64_t* d_score, size_t np, int64_t* total)
     IGB_LAUNCH(ctx, sum128, g, 256, 0, d_score, np, lo.as<unsigned long long>(), hi.as<long long>());
     std::vector<unsigned long long> hl(g);
     std::vector<long long> hh(g);
-    IGB_CUDA(cudaMemcpyAsync(hl.data(), lo.p, g * 8, cudaMemcpyDeviceToHost, ctx.stream));
-    IGB_CUDA(cudaMemcpyAsync(hh.data(), hi.p, g * 8, cudaMemcpyDeviceToHost, ctx.stream));
-    IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+    read_back(ctx, hl.data(), lo.p, g * 8);
+    read_back(ctx, hh.data(), hi.p, g * 8);
     __int128 acc = 0;
     for (unsigned i = 0; i < g; ++i) acc += ((__int128)hh[i] << 32) + (__int128)hl[i];
     // Scores are non-negative (support >= 0), so the running-sum overflow of
@@ -650,8 +646,7 @@ size_t compact_unflagged(Ctx& ctx, const int64_t* d_words, const int64_t* d_sup,
     IGB_CUDA(cub::DeviceSelect::Flagged(temp.p, tb, iota.as<uint32_t>(), keep.as<uint8_t>(), idx.as<uint32_t>(),
                                         nsel.as<int64_t>(), (int64_t)n, ctx.stream));
     int64_t m = 0;
-    IGB_CUDA(cudaMemcpyAsync(&m, nsel.p, 8, cudaMemcpyDeviceToHost, ctx.stream));
-    IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+    read_back(ctx, &m, nsel.p, 8);
     if (m) {
         IGB_LAUNCH(ctx, compact_rows_k, grid_for(ctx, m * k, 256), 256, 0, d_words, idx.as<uint32_t>(), (size_t)m,
                    (int)k, o_words);

@@ -326,11 +326,6 @@ __global__ void gather_u64k(const unsigned long long* __restrict__ src, const ui
         dst[i] = src[idx[i]];
 }
 
-__global__ void gather_u32(const uint32_t* __restrict__ src, const uint32_t* __restrict__ idx, size_t n,
-                           uint32_t* __restrict__ dst) {
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
-        dst[i] = src[idx[i]];
-}
 
 
 // ------------------------------------------------------------------ grouped scan
@@ -686,8 +681,7 @@ void launch_scan(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Post
     IGB_CUDA(cub::DeviceScan::ExclusiveSum(temp4.p, tb4, ub.as<unsigned long long>(), poff.as<unsigned long long>(),
                                            (int64_t)G2 + 1, ctx.stream));
     unsigned long long E2 = 0;
-    IGB_CUDA(cudaMemcpyAsync(&E2, poff.as<unsigned long long>() + G2, 8, cudaMemcpyDeviceToHost, ctx.stream));
-    IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+    read_back(ctx, &E2, poff.as<unsigned long long>() + G2, 8);
     DevBuf pw(std::max<unsigned long long>(E2, 1) * 4, ctx.stream), pm(std::max<unsigned long long>(E2, 1) * 8, ctx.stream);
     if (G2)
         IGB_LAUNCH(ctx, group_lists, grid_for(ctx, G2 * 32, 256), 256, 0, I->pkey.as<uint32_t>(), G2,
@@ -701,8 +695,7 @@ void launch_scan(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Post
     IGB_CUDA(cub::DeviceScan::ExclusiveSum(temp4.p, tb4, ub3.as<unsigned long long>(), goff.as<unsigned long long>(),
                                            (int64_t)G + 1, ctx.stream));
     unsigned long long E = 0;
-    IGB_CUDA(cudaMemcpyAsync(&E, goff.as<unsigned long long>() + G, 8, cudaMemcpyDeviceToHost, ctx.stream));
-    IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+    read_back(ctx, &E, goff.as<unsigned long long>() + G, 8);
     DevBuf ew(std::max<unsigned long long>(E, 1) * 4, ctx.stream), em(std::max<unsigned long long>(E, 1) * 8, ctx.stream);
     if (G)
         IGB_LAUNCH(ctx, child_lists, grid_for(ctx, G * 32, 256), 256, 0, I->gkey.as<unsigned long long>(),
@@ -727,8 +720,7 @@ void launch_scan(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Post
             IGB_LAUNCH(ctx, group_work, grid_for(ctx, G2, 256), 256, 0, I->pkey.as<uint32_t>(),
                        ub.as<unsigned long long>(), G2, w.as<unsigned long long>());
         unsigned long long hw = 0;
-        IGB_CUDA(cudaMemcpyAsync(&hw, w.p, 8, cudaMemcpyDeviceToHost, ctx.stream));
-        IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+        read_back(ctx, &hw, w.p, 8);
         float ms = 0;
         IGB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
         ctx.diag_match_ms += ms;
@@ -793,8 +785,7 @@ void build_pattern_index(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, co
     IGB_CUDA(cub::DeviceScan::ExclusiveSum(temp.p, tb, I.len.as<uint32_t>(), I.beg.as<uint32_t>(), (int64_t)np + 1,
                                            ctx.stream));
     uint32_t total = 0;
-    IGB_CUDA(cudaMemcpyAsync(&total, I.beg.as<uint32_t>() + np, 4, cudaMemcpyDeviceToHost, ctx.stream));
-    IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+    read_back(ctx, &total, I.beg.as<uint32_t>() + np, 4);
     I.toks = std::make_shared<DevBuf>();
     I.toks->alloc(std::max<size_t>(total, 1) * 2, ctx.stream);
     if (np == 0) return;
@@ -861,8 +852,7 @@ void group_ids(Ctx& ctx, const unsigned long long* d_sorted_key, size_t np, Patt
                                         I.gkey.as<unsigned long long>(), nsel.as<int64_t>(), (int64_t)np, ctx.stream));
     IGB_LAUNCH(ctx, minus_one, grid_for(ctx, np, 256), 256, 0, I.gid.as<uint32_t>(), np);
     int64_t G = 0;
-    IGB_CUDA(cudaMemcpyAsync(&G, nsel.p, 8, cudaMemcpyDeviceToHost, ctx.stream));
-    IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+    read_back(ctx, &G, nsel.p, 8);
     I.G = (size_t)G;
     // parents: the groups are sorted by (t1, t2, t3), so equal (t1, t2) are adjacent
     const size_t Gs = std::max<size_t>(I.G, 1);
@@ -887,8 +877,7 @@ void group_ids(Ctx& ctx, const unsigned long long* d_sorted_key, size_t np, Patt
                                         nsel.as<int64_t>(), (int64_t)I.G, ctx.stream));
     IGB_LAUNCH(ctx, minus_one, grid_for(ctx, I.G, 256), 256, 0, I.pid.as<uint32_t>(), I.G);
     int64_t G2 = 0;
-    IGB_CUDA(cudaMemcpyAsync(&G2, nsel.p, 8, cudaMemcpyDeviceToHost, ctx.stream));
-    IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+    read_back(ctx, &G2, nsel.p, 8);
     I.G2 = (size_t)G2;
 }
 
@@ -1048,8 +1037,7 @@ void build_postings(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, uint32_
                                             P.rep.as<uint32_t>(), nsel.as<int64_t>(), (int64_t)n, ctx.stream));
         IGB_LAUNCH(ctx, fix_group, grid_for(ctx, n, 256), 256, 0, head.as<uint32_t>(), n, P.group.as<uint32_t>());
         int64_t m = 0;
-        IGB_CUDA(cudaMemcpyAsync(&m, nsel.p, 8, cudaMemcpyDeviceToHost, ctx.stream));
-        IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+        read_back(ctx, &m, nsel.p, 8);
         nd = (size_t)m;
         rows_of = P.rep.as<uint32_t>();
     }
@@ -1076,8 +1064,7 @@ void build_postings(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, uint32_
     IGB_CUDA(cub::DeviceScan::ExclusiveSum(temp.p, tb, nzc.as<uint32_t>(), P.nz_off.as<uint32_t>(), (int64_t)L + 1,
                                            ctx.stream));
     uint32_t total = 0;
-    IGB_CUDA(cudaMemcpyAsync(&total, P.nz_off.as<uint32_t>() + L, 4, cudaMemcpyDeviceToHost, ctx.stream));
-    IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+    read_back(ctx, &total, P.nz_off.as<uint32_t>() + L, 4);
     P.nz_total = total;
     P.nz_idx.alloc(std::max<size_t>(total, 1) * 4, ctx.stream);
     IGB_LAUNCH(ctx, fill_nonzero, grid_for(ctx, (size_t)L * 32, 256), 256, 0, P.dense.as<unsigned long long>(), L,

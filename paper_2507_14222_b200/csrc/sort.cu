@@ -322,9 +322,8 @@ void sort_rows_canonical(Ctx& ctx, const int64_t* d_words, size_t n, size_t k, u
         IGB_LAUNCH(ctx, column_insert, grid_for(ctx, n * k, 256), 256, 0, d_words, n, (int)k, tables.as<ulonglong2>(),
                    slots, counts.as<unsigned int>(), full.as<int>());
         int hfull = 0;
-        IGB_CUDA(cudaMemcpyAsync(hc.data(), counts.p, k * 4, cudaMemcpyDeviceToHost, ctx.stream));
-        IGB_CUDA(cudaMemcpyAsync(&hfull, full.p, 4, cudaMemcpyDeviceToHost, ctx.stream));
-        IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+        read_back(ctx, hc.data(), counts.p, k * 4);
+        read_back(ctx, &hfull, full.p, 4);
         if (!hfull) break;
         if (slots >= (1u << 20) || slots >= 2 * n + 16) {
             sort_rows_canonical_lsd(ctx, d_words, n, k, d_perm);
@@ -473,8 +472,7 @@ size_t distinct_rows(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, DevBuf
     IGB_CUDA(cub::DeviceSelect::Flagged(temp.p, tb, perm.as<uint32_t>(), head.as<uint8_t>(), rep.as<uint32_t>(),
                                         nsel.as<int64_t>(), (int64_t)n, ctx.stream));
     int64_t m = 0;
-    IGB_CUDA(cudaMemcpyAsync(&m, nsel.p, 8, cudaMemcpyDeviceToHost, ctx.stream));
-    IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+    read_back(ctx, &m, nsel.p, 8);
     out.alloc(std::max<size_t>((size_t)m * k, 1) * 8, ctx.stream);
     IGB_LAUNCH(ctx, gather_rows_u32, grid_for(ctx, (size_t)m * k, 256), 256, 0, d_rows, rep.as<uint32_t>(), (size_t)m,
                (int)k, out.as<int64_t>());

@@ -292,8 +292,7 @@ int fused_score_dev(Ctx& ctx, const int64_t* d_pat, size_t np, const int64_t* d_
     IGB_CUDA(cudaMemsetAsync(d_flags, 0, 2 * sizeof(int), ctx.stream));
     IGB_LAUNCH(ctx, any_negative, 256, 256, 0, d_scores, np, d_flags + 1);
     int h_flags[2];
-    IGB_CUDA(cudaMemcpyAsync(h_flags, d_flags, sizeof(h_flags), cudaMemcpyDeviceToHost, ctx.stream));
-    IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+    read_back(ctx, h_flags, d_flags, sizeof(h_flags));
     if (h_flags[1]) {
         // Mixed-sign scores: overflow depends on the order of partial sums, so
         // every test row walks the patterns in index order (kernels.cpp:70-75).
@@ -314,8 +313,7 @@ int fused_score_dev(Ctx& ctx, const int64_t* d_pat, size_t np, const int64_t* d_
         IGB_LAUNCH(ctx, reduce_partials, (unsigned)((nt + 255) / 256), 256, 0, partial.as<uint64_t>(), nt,
                    slices, d_out, d_flags);
     }
-    IGB_CUDA(cudaMemcpyAsync(h_flags, d_flags, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
-    IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+    read_back(ctx, h_flags, d_flags, sizeof(int));
     return h_flags[0] ? IG_E_OVERFLOW : IG_OK;
 }
 

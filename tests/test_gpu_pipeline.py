@@ -138,3 +138,29 @@ def test_prefetched_columns_encode_identically(api, golden_dir):
                                                           ratio_k=g["ratio_k"]).test.matrix(2))
     cte.prefetch(ctx)  # dropped unconsumed when the columns are freed
     del cte
+
+
+def test_background_test_index_overlapping_the_fit(api, golden_dir):
+    """encode_rows before the fit (resident columns: packed and indexed on the
+    index stream while the fit runs) gives the same A/N, host or device outputs."""
+    import torch
+    g = json.load(open(os.path.join(golden_dir, "nsl_c1.json")))
+    csv = synth.nsl_csv(g["rows"], seed=g["seed"])
+    table = api.read_csv(csv)
+    ntr = g["ratio_k"] * table.rows // 10
+    tr, te = table.slice(0, ntr), table.slice(ntr, table.rows)
+    schema = api.infer_schema(tr, "label", decimals=g["decimals"])
+    ctx = api.default_context()
+    dtr = api.Columns(tr, schema, True).upload(ctx)
+    dte = api.Columns(te, schema, False).upload(ctx)
+    enc = api.encode_training(dtr, ctx)
+    tenc = api.encode_rows(dte, enc, ctx)
+    model = api.fit_encoded(enc)
+    dA = torch.zeros(tenc.rows(2), dtype=torch.int64, device="cuda")
+    dN = torch.zeros_like(dA)
+    model.evidence_encoded_device(tenc, dA.data_ptr(), dN.data_ptr())
+    torch.cuda.synchronize()
+    A, N = model.evidence_encoded(tenc)
+    assert _digest(A) == g["A_digest"] and _digest(N) == g["N_digest"]
+    assert np.array_equal(dA.cpu().numpy(), A) and np.array_equal(dN.cpu().numpy(), N)
+    assert _digest(tenc.matrix(2)) == _digest(api.encode_rows(api.Columns(te, schema, False), enc, ctx).matrix(2))
