@@ -236,7 +236,8 @@ void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m, bool enumerate 
     igb::RankSpace R;
     igb::PatternIndex CI[2];
     if (vertical) igb::combined_rank_space(ctx, PX[0], PX[1], R);
-    // phase A2 (per class): candidate index, support, score, checked total
+    tm.mark();  // 1
+    // phase B (per class): candidate index, support, score, checked total, purify
     for_both_classes(ctx, [&](igb::Ctx& cx, int c) {
         igb::Trace tr(cx, "fitA", c);
         ig_candidates& C = m.cand[c];
@@ -258,15 +259,10 @@ void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m, bool enumerate 
         m.partial_total[c] = (uint64_t)total;
         C.has_support = C.has_score = true;
         tr.mark("score+total");
-    }, concurrent);
-    tm.mark();  // 1
-    // phase B (per class): reject_covered against the other class's postings,
-    // compaction, canonical order of the pure dictionary (the model output; the
-    // candidate sets B^c are ordered on first copy-out)
-    for_both_classes(ctx, [&](igb::Ctx& cx, int c) {
-        ig_candidates& C = m.cand[c];
-        const size_t np = C.rows.n;
-        igb::Trace tr(cx, "purify", c);
+        // then (same class, no wait for the other class's support): reject_covered
+        // against the other class's postings, compaction, canonical order of the
+        // pure dictionary (the model output; the candidate sets B^c are ordered
+        // on first copy-out)
         DevBuf mask(std::max<size_t>(np, 1), cx.stream);
         if (vertical && X[1 - c].n > 0)
             igb::posting_cover(cx, C.rows.data(), np, k, PX[1 - c], mask.as<uint8_t>(), &CI[c]);
@@ -307,9 +303,9 @@ void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m, bool enumerate 
     IGB_CUDA(cudaStreamSynchronize(ctx.stream));
     IGB_CUDA(cudaStreamSynchronize(ctx.aux));
     m.ms[0] = 0;
-    m.ms[1] = tm.ms(0, 1);  // enumerate + support + score (both classes, concurrent)
+    m.ms[1] = tm.ms(0, 1);  // canonical rows + enumerate + postings (both classes, concurrent)
     m.ms[2] = 0;
-    m.ms[3] = tm.ms(1, 2);  // purify + order
+    m.ms[3] = tm.ms(1, 2);  // index + support + score + purify + order
     m.ms[4] = 0;
     m.ms[5] = tm.ms(0, 2);
     for (int c = 0; c < 2; ++c) {
