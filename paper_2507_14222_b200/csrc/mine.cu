@@ -135,10 +135,15 @@ __device__ __forceinline__ void tile_of(uint64_t t, uint32_t& bi, uint32_t& bj) 
 constexpr int kLocalSlots = 4096;
 constexpr int kLocalProbes = 64;
 
-template <int TILE>
+// KC > 0: the row width K is a compile-time constant (the common NSL shapes),
+// so the word loops unroll; KC <= 16 also keeps the pair's AND in registers
+// for the duplicate check.
+template <int TILE, int KC>
 __global__ void __launch_bounds__(kPairThreads)
-pair_enum(const int64_t* __restrict__ X, uint32_t n, int k, int stride, uint64_t n_tiles, Table T,
+pair_enum(const int64_t* __restrict__ X, uint32_t n, int k_rt, int stride, uint64_t n_tiles, Table T,
           uint64_t tile_begin, uint64_t tile_step) {
+    const int k = KC > 0 ? KC : k_rt;
+    constexpr bool kRegs = KC > 0 && KC <= 16;
     extern __shared__ int64_t sm[];
     unsigned long long* local = reinterpret_cast<unsigned long long*>(sm);  // kLocalSlots
     int64_t* sI = sm + kLocalSlots;
@@ -172,8 +177,11 @@ pair_enum(const int64_t* __restrict__ X, uint32_t n, int k, int stride, uint64_t
             const int64_t* b = sJ + c * stride;
             Fp fp;
             uint64_t nz = 0;
+            uint64_t xr[kRegs ? KC : 1];
+#pragma unroll
             for (int w = 0; w < k; ++w) {
                 const uint64_t x = (uint64_t)(a[w] & b[w]);
+                if constexpr (kRegs) xr[w] = x;
                 nz |= x;
                 fp.add(x, sKey[w]);
             }
@@ -194,7 +202,12 @@ pair_enum(const int64_t* __restrict__ X, uint32_t n, int k, int stride, uint64_t
                 const int64_t* a2 = sI + (q2 / TILE) * stride;
                 const int64_t* b2 = sJ + (q2 % TILE) * stride;
                 bool same = true;
-                for (int w = 0; w < k && same; ++w) same = ((a2[w] & b2[w]) == (a[w] & b[w]));
+                if constexpr (kRegs) {
+#pragma unroll
+                    for (int w = 0; w < KC; ++w) same &= ((uint64_t)(a2[w] & b2[w]) == xr[w]);
+                } else {
+                    for (int w = 0; w < k && same; ++w) same = ((a2[w] & b2[w]) == (a[w] & b[w]));
+                }
                 if (same) {
                     dup = true;
                     break;
@@ -454,9 +467,11 @@ uint64_t dedup_pairs(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, const 
     const int tile = tile_rows;
     const size_t smem = (size_t)kLocalSlots * 8 + 2 * (size_t)tile * stride * 8 + k * 8;
     if (smem > 200 * 1024) fail(IG_E_INVALID_ARG, "enumerate: rows wider than the shared-memory tile (K > 700)");
-    IGB_CUDA(cudaFuncSetAttribute(pair_enum<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    IGB_CUDA(cudaFuncSetAttribute(pair_enum<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    IGB_CUDA(cudaFuncSetAttribute(pair_enum<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    IGB_CUDA(cudaFuncSetAttribute(pair_enum<64, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    IGB_CUDA(cudaFuncSetAttribute(pair_enum<64, 14>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    IGB_CUDA(cudaFuncSetAttribute(pair_enum<64, 17>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    IGB_CUDA(cudaFuncSetAttribute(pair_enum<32, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    IGB_CUDA(cudaFuncSetAttribute(pair_enum<16, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
 
     // Initial capacity from a sub-linear guess of the distinct count; doubled
     // (x4) and rerun if the table fills.  Results never depend on capacity.
@@ -491,15 +506,21 @@ uint64_t dedup_pairs(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, const 
             } else if (level == 0) {
                 const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(my_tiles, (uint64_t)ctx.sm_count * 16));
                 if (my_tiles) {
-                    if (tile == 64)
-                        IGB_LAUNCH(ctx, pair_enum<64>, grid, kPairThreads, smem, d_rows, (uint32_t)n, (int)k, stride,
-                                   n_tiles, T, src.tile_begin, src.tile_step);
+                    if (tile == 64 && k == 14)
+                        IGB_LAUNCH(ctx, (pair_enum<64, 14>), grid, kPairThreads, smem, d_rows, (uint32_t)n, (int)k,
+                                   stride, n_tiles, T, src.tile_begin, src.tile_step);
+                    else if (tile == 64 && k == 17)
+                        IGB_LAUNCH(ctx, (pair_enum<64, 17>), grid, kPairThreads, smem, d_rows, (uint32_t)n, (int)k,
+                                   stride, n_tiles, T, src.tile_begin, src.tile_step);
+                    else if (tile == 64)
+                        IGB_LAUNCH(ctx, (pair_enum<64, 0>), grid, kPairThreads, smem, d_rows, (uint32_t)n, (int)k,
+                                   stride, n_tiles, T, src.tile_begin, src.tile_step);
                     else if (tile == 32)
-                        IGB_LAUNCH(ctx, pair_enum<32>, grid, kPairThreads, smem, d_rows, (uint32_t)n, (int)k, stride,
-                                   n_tiles, T, src.tile_begin, src.tile_step);
+                        IGB_LAUNCH(ctx, (pair_enum<32, 0>), grid, kPairThreads, smem, d_rows, (uint32_t)n, (int)k,
+                                   stride, n_tiles, T, src.tile_begin, src.tile_step);
                     else
-                        IGB_LAUNCH(ctx, pair_enum<16>, grid, kPairThreads, smem, d_rows, (uint32_t)n, (int)k, stride,
-                                   n_tiles, T, src.tile_begin, src.tile_step);
+                        IGB_LAUNCH(ctx, (pair_enum<16, 0>), grid, kPairThreads, smem, d_rows, (uint32_t)n, (int)k,
+                                   stride, n_tiles, T, src.tile_begin, src.tile_step);
                 }
             } else {
                 IGB_LAUNCH(ctx, pair_insert_list, grid_for(ctx, n_pending, 256), 256, 0, d_rows, (int)k,
