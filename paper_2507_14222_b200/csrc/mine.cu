@@ -153,11 +153,15 @@ pair_enum(const int64_t* __restrict__ X, uint32_t n, int k_rt, int stride, uint6
     for (uint64_t it = blockIdx.x;; it += gridDim.x) {
         const uint64_t t = tile_begin + it * tile_step;  // this rank's tiles: begin, begin + step, ...
         if (t >= n_tiles) break;
-        if (*(volatile int*)T.fail) return;
+        // one reader for the failure flag, so the whole block leaves together
+        __shared__ int s_stop;
+        __syncthreads();
+        if (threadIdx.x == 0) s_stop = *(volatile int*)T.fail;
+        __syncthreads();
+        if (s_stop) return;
         uint32_t bi, bj;
         tile_of(t, bi, bj);
         const uint32_t i0 = bi * TILE, j0 = bj * TILE;
-        __syncthreads();
         for (int q = threadIdx.x; q < TILE * k; q += kPairThreads) {
             const int r = q / k, w = q % k;
             sI[r * stride + w] = (i0 + r < n) ? X[(size_t)(i0 + r) * k + w] : 0;
