@@ -171,6 +171,7 @@ int ig_infer_schema(const ig_table* t, const char* label_column, const char* att
                     const char* normal_values, int decimals, ig_schema** out);
 int ig_schema_column(const ig_schema* s, size_t j, int* kind, double* mean, double* stddev);
 size_t ig_schema_label_index(const ig_schema* s);
+size_t ig_schema_cols(const ig_schema* s);
 void ig_schema_free(ig_schema* s);
 
 /* Host parse of a table under a schema into typed arrays (the "parsed
@@ -185,6 +186,17 @@ int ig_columns_upload(ig_ctx* ctx, ig_columns* c);
  * return at once; the next encode of these columns waits for it (one-shot).
  * Lets a caller overlap the test columns' transfer with the fit. */
 int ig_columns_prefetch(ig_ctx* ctx, ig_columns* c);
+/* Device CSV ingest: CSV bytes -> schema + typed
+ * train/test columns resident on the context's device, identical to
+ * ig_read_csv -> slice (first train_rows records, or ratio_k tenths when
+ * train_rows < 0) -> ig_infer_schema (training rows) -> ig_columns_build +
+ * ig_columns_upload.  Records, numbers (from_chars-exact fast path, host for
+ * the rest), sequential-sum statistics and first-appearance categorical ids are
+ * computed on the device; quoted input takes the host reader.  *test is an
+ * empty table when every record trains. */
+int ig_ingest_csv(ig_ctx* ctx, const char* bytes, size_t len, const char* label_column, const char* attack_values,
+                  const char* normal_values, int decimals, long long train_rows, int ratio_k, ig_schema** schema,
+                  ig_columns** train, ig_columns** test);
 size_t ig_columns_rows(const ig_columns* c);
 size_t ig_columns_bytes(const ig_columns* c);
 void ig_columns_free(ig_columns* c);

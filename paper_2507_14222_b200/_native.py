@@ -80,10 +80,13 @@ SIGNATURES = [
     ("ig_infer_schema", C.c_int, [vp, C.c_char_p, C.c_char_p, C.c_char_p, C.c_int, C.POINTER(vp)]),
     ("ig_schema_column", C.c_int, [vp, sz, C.POINTER(C.c_int), C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     ("ig_schema_label_index", sz, [vp]),
+    ("ig_schema_cols", sz, [vp]),
     ("ig_schema_free", None, [vp]),
     ("ig_columns_build", C.c_int, [vp, vp, C.c_int, C.POINTER(vp)]),
     ("ig_columns_upload", C.c_int, [vp, vp]),
     ("ig_columns_prefetch", C.c_int, [vp, vp]),
+    ("ig_ingest_csv", C.c_int, [vp, C.c_char_p, sz, C.c_char_p, C.c_char_p, C.c_char_p, C.c_int, C.c_longlong,
+                                C.c_int, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]),
     ("ig_columns_rows", sz, [vp]),
     ("ig_columns_bytes", sz, [vp]),
     ("ig_columns_free", None, [vp]),

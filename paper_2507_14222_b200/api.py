@@ -451,6 +451,12 @@ def infer_schema(table: Table, label_column: str, attack_values=(), normal_value
 class Columns:
     """Parsed, typed columns of a table under a schema (host; the fit's input)."""
 
+    @classmethod
+    def _wrap(cls, handle) -> "Columns":
+        c = cls.__new__(cls)
+        c.handle = handle
+        return c
+
     def __init__(self, table: Table, schema: Schema, with_labels: bool = True):
         h = C.c_void_p()
         st = lib.ig_columns_build(table.handle, schema.handle, 1 if with_labels else 0, C.byref(h))
@@ -481,6 +487,21 @@ class Columns:
         if getattr(self, "handle", None):
             lib.ig_columns_free(self.handle)
             self.handle = None
+
+
+def ingest_csv(data: bytes, label_column: str = "label", attack_values=(), normal_values=(), decimals: int = 2,
+               train_rows: Optional[int] = None, ratio_k: int = 8,
+               ctx: Optional[Context] = None) -> tuple["Schema", "Columns", "Columns"]:
+    """Device CSV ingest: (schema, train columns, test columns), resident on the
+    device — the same as read_csv -> slice -> infer_schema -> Columns(...).upload."""
+    ctx = ctx or default_context()
+    hs, ht, he = C.c_void_p(), C.c_void_p(), C.c_void_p()
+    ctx.check(lib.ig_ingest_csv(ctx.handle, data, len(data), label_column.encode(), ",".join(attack_values).encode(),
+                                ",".join(normal_values).encode(), decimals,
+                                -1 if train_rows is None else int(train_rows), ratio_k,
+                                C.byref(hs), C.byref(ht), C.byref(he)))
+    schema = Schema(hs, int(lib.ig_schema_cols(hs)))
+    return schema, Columns._wrap(ht), Columns._wrap(he)
 
 
 class Encoding:

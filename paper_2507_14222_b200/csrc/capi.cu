@@ -731,6 +731,7 @@ int ig_schema_column(const ig_schema* s, size_t j, int* kind, double* mean, doub
     return IG_OK;
 }
 size_t ig_schema_label_index(const ig_schema* s) { return s ? s->label_index : 0; }
+size_t ig_schema_cols(const ig_schema* s) { return s ? s->names.size() : 0; }
 void ig_schema_free(ig_schema* s) { delete s; }
 
 int ig_columns_build(const ig_table* t, const ig_schema* s, int with_labels, ig_columns** out) {
@@ -752,6 +753,48 @@ int ig_columns_build(const ig_table* t, const ig_schema* s, int with_labels, ig_
         *out = c.release();
     });
 }
+int ig_ingest_csv(ig_ctx* ctx, const char* bytes, size_t len, const char* label_column, const char* attack_values,
+                  const char* normal_values, int decimals, long long train_rows, int ratio_k, ig_schema** schema,
+                  ig_columns** train, ig_columns** test) {
+    *schema = nullptr;
+    *train = *test = nullptr;
+    return guard(ctx, [&] {
+        auto S = std::make_unique<ig_schema>();
+        auto TR = std::make_unique<ig_columns>(), TE = std::make_unique<ig_columns>();
+        const auto attack = igb::split_csv_list(attack_values), normal = igb::split_csv_list(normal_values);
+        const std::string label = label_column ? label_column : "label";
+        if (!igb::ingest_csv(*ctx, bytes, len, label, attack, normal, decimals, train_rows, ratio_k, *S, *TR, *TE)) {
+            // the host reader (quoted fields, ...), then resident copies
+            ig_table t;
+            igb::read_csv(bytes, len, t);
+            const size_t n = t.n_rows;
+            const size_t ntr = train_rows >= 0 ? std::min<size_t>((size_t)train_rows, n) : (size_t)ratio_k * n / 10;
+            auto slice = [&](size_t lo, size_t hi) {
+                ig_table o;
+                o.header = t.header;
+                o.n_rows = hi - lo;
+                for (size_t r = lo; r < hi; ++r)
+                    for (size_t j = 0; j < t.header.size(); ++j) {
+                        auto c = t.cell(r, j);
+                        o.off.push_back(o.arena.size());
+                        o.len.push_back((uint32_t)c.size());
+                        o.arena.append(c);
+                    }
+                return o;
+            };
+            ig_table a = slice(0, ntr), b = slice(ntr, n);
+            igb::infer_schema(a, label, attack, normal, decimals, *S);
+            igb::build_columns(a, *S, true, *TR);
+            igb::build_columns(b, *S, false, *TE);
+            igb::upload_columns(*ctx, *TR);
+            igb::upload_columns(*ctx, *TE);
+        }
+        *schema = S.release();
+        *train = TR.release();
+        *test = TE.release();
+    });
+}
+
 int ig_columns_upload(ig_ctx* ctx, ig_columns* c) {
     return guard(ctx, [&] { igb::upload_columns(*ctx, *c); });
 }

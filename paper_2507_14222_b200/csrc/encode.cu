@@ -346,6 +346,7 @@ void pack_with(Ctx& ctx, const ig_encoding& e, const DeviceCols& d,
 }  // namespace
 
 void prefetch_columns(Ctx& ctx, ig_columns& c) {
+    if (c.d_values && c.device == ctx.device) return;  // already resident
     auto pf = std::make_shared<PrefetchCols>();
     pf->device = ctx.device;
     pf->values.alloc(std::max<size_t>(c.values.size(), 1) * 8, ctx.copy);

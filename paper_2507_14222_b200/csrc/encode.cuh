@@ -38,6 +38,10 @@ void drop_prefetch(ig_columns& c);
 // resident or prefetched (no host memory is read after return)
 void encode_rows_dev(Ctx& ctx, const ig_columns& c, const ig_encoding& train, ig_encoding& e,
                      bool queue_only = false);
+// ingest.cu: false -> the input needs the host reader (quoted fields, ...)
+bool ingest_csv(Ctx& ctx, const char* bytes, size_t len, const std::string& label,
+                const std::vector<std::string>& attack, const std::vector<std::string>& normal, int decimals,
+                long long train_rows, int ratio_k, ig_schema& S, ig_columns& TR, ig_columns& TE);
 // archive.cu
 std::string schema_to_text(const ig_schema& s);
 void schema_from_text(const std::string& text, ig_schema& s);
