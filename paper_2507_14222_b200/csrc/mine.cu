@@ -145,8 +145,8 @@ pair_enum(const int64_t* __restrict__ X, uint32_t n, int k_rt, int stride, uint6
     const int k = KC > 0 ? KC : k_rt;
     constexpr bool kRegs = KC > 0 && KC <= 16;
     extern __shared__ int64_t sm[];
-    unsigned long long* local = reinterpret_cast<unsigned long long*>(sm);  // kLocalSlots
-    int64_t* sI = sm + kLocalSlots;
+    unsigned int* local = reinterpret_cast<unsigned int*>(sm);  // kLocalSlots 32-bit entries
+    int64_t* sI = sm + kLocalSlots / 2;
     int64_t* sJ = sI + (size_t)TILE * stride;
     unsigned long long* sKey = reinterpret_cast<unsigned long long*>(sJ + (size_t)TILE * stride);  // k fingerprint keys
     for (int w = threadIdx.x; w < k; w += kPairThreads) sKey[w] = T.keys[w];
@@ -167,7 +167,7 @@ pair_enum(const int64_t* __restrict__ X, uint32_t n, int k_rt, int stride, uint6
             sI[r * stride + w] = (i0 + r < n) ? X[(size_t)(i0 + r) * k + w] : 0;
             sJ[r * stride + w] = (j0 + r < n) ? X[(size_t)(j0 + r) * k + w] : 0;
         }
-        for (int q = threadIdx.x; q < kLocalSlots; q += kPairThreads) local[q] = 0ull;
+        for (int q = threadIdx.x; q < kLocalSlots; q += kPairThreads) local[q] = 0u;
         __syncthreads();
         for (int q = threadIdx.x; q < TILE * TILE; q += kPairThreads) {
             // every lane runs the same trip count: re-converge the warp each
@@ -191,15 +191,17 @@ pair_enum(const int64_t* __restrict__ X, uint32_t n, int k_rt, int stride, uint6
             }
             if (!nz) continue;  // SPEC.md:338 empty intersections dropped at the source
             const uint64_t f = (fp.final(k) & T.fp_mask) | 1ull;
-            // local entry: 51-bit tag (never zero) | 12-bit pair index within the tile
-            const unsigned long long entry = ((((f >> 13) | (1ull << 50))) << 12) | (unsigned)q;
+            // local entry: 20-bit tag from the fingerprint's top bits (never zero;
+            // the slot comes from its low bits) | 12-bit pair index within the tile.
+            // A tag match is only a hint: the words decide.
+            const unsigned int entry = ((unsigned int)(f >> 44) | 1u) << 12 | (unsigned int)q;
             bool dup = false;
             uint32_t s = (uint32_t)(f & (kLocalSlots - 1));
             for (int probe = 0; probe < kLocalProbes; ++probe, s = (s + 1) & (kLocalSlots - 1)) {
-                unsigned long long cur = local[s];
-                if (cur == 0ull) {
-                    cur = atomicCAS(local + s, 0ull, entry);
-                    if (cur == 0ull) break;  // first of its content in this tile
+                unsigned int cur = local[s];
+                if (cur == 0u) {
+                    cur = atomicCAS(local + s, 0u, entry);
+                    if (cur == 0u) break;  // first of its content in this tile
                 }
                 if ((cur >> 12) != (entry >> 12)) continue;
                 const int q2 = (int)(cur & 0xfffu);
@@ -461,7 +463,7 @@ uint64_t dedup_pairs(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, const 
     if (n > 0xffffffffull) fail(IG_E_INVALID_ARG, "enumerate: more than 2^32 rows");
     const int stride = (int)(k | 1);
     int tile_rows = 64;
-    while (tile_rows > 16 && (size_t)kLocalSlots * 8 + 2 * (size_t)tile_rows * stride * 8 + k * 8 > 200 * 1024) tile_rows /= 2;
+    while (tile_rows > 16 && (size_t)kLocalSlots * 4 + 2 * (size_t)tile_rows * stride * 8 + k * 8 > 200 * 1024) tile_rows /= 2;
     const uint64_t blocks = (n + tile_rows - 1) / tile_rows;
     const uint64_t n_tiles = blocks * (blocks + 1) / 2;
     const uint64_t my_tiles = src.list ? 0 : (n_tiles > src.tile_begin ? (n_tiles - src.tile_begin + src.tile_step - 1) / src.tile_step : 0);
@@ -469,7 +471,7 @@ uint64_t dedup_pairs(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, const 
     // 64-row tiles; narrower tiles for wide rows (CICIDS shape, K up to ~750) so
     // both row blocks still fit in shared memory
     const int tile = tile_rows;
-    const size_t smem = (size_t)kLocalSlots * 8 + 2 * (size_t)tile * stride * 8 + k * 8;
+    const size_t smem = (size_t)kLocalSlots * 4 + 2 * (size_t)tile * stride * 8 + k * 8;
     if (smem > 200 * 1024) fail(IG_E_INVALID_ARG, "enumerate: rows wider than the shared-memory tile (K > 700)");
     IGB_CUDA(cudaFuncSetAttribute(pair_enum<64, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     IGB_CUDA(cudaFuncSetAttribute(pair_enum<64, 14>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
