@@ -139,7 +139,7 @@ constexpr int kLocalProbes = 64;
 // so the word loops unroll; KC <= 16 also keeps the pair's AND in registers
 // for the duplicate check.
 template <int TILE, int KC>
-__global__ void __launch_bounds__(kPairThreads)
+__global__ void __launch_bounds__(kPairThreads, KC > 0 && KC <= 16 ? 5 : 6)
 pair_enum(const int64_t* __restrict__ X, uint32_t n, int k_rt, int stride, uint64_t n_tiles, Table T,
           uint64_t tile_begin, uint64_t tile_step) {
     const int k = KC > 0 ? KC : k_rt;
