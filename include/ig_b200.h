@@ -186,7 +186,9 @@ int ig_columns_upload(ig_ctx* ctx, ig_columns* c);
  * return at once; the next encode of these columns waits for it (one-shot).
  * Lets a caller overlap the test columns' transfer with the fit. */
 int ig_columns_prefetch(ig_ctx* ctx, ig_columns* c);
-/* Device CSV ingest: CSV bytes -> schema + typed
+/* Device CSV ingest (replaces read_csv csv.cpp:14-89,
+ * split_by_ratio SPEC.md:508-516, infer_schema pipeline.cpp:107-169 and the
+ * cell parsing of tokenize_row pipeline.cpp:171-202): CSV bytes -> schema + typed
  * train/test columns resident on the context's device, identical to
  * ig_read_csv -> slice (first train_rows records, or ratio_k tenths when
  * train_rows < 0) -> ig_infer_schema (training rows) -> ig_columns_build +
@@ -222,7 +224,7 @@ void ig_encoding_free(ig_encoding* e);
 int ig_fit_encoded(ig_ctx* ctx, const ig_encoding* train, const ig_kernel_config* cfg, ig_model** out);
 int ig_evidence_encoded(ig_ctx* ctx, const ig_model* m, const ig_encoding* tests, int64_t* A,
                         int64_t* N);
-/* Same with device outputs d_A / d_N (int64[rows]), ordered on the context
+/* evidence_scores with device outputs d_A / d_N (int64[rows]), ordered on the context
  * stream.  A test encoding made by ig_encode_rows from resident or prefetched
  * columns is packed and indexed (row postings) in the background on the
  * context's index stream, overlapping a fit issued meanwhile; evidence and every
