@@ -110,3 +110,32 @@ def test_forced_fingerprint_collisions_stay_exact(api, monkeypatch, bits):
             assert which == 1 or len(want.words) > (8 << bits if bits == 10 else 4000)
             assert np.array_equal(d.words, want.words), (c, which)
             assert np.array_equal(d.supports, want.supports), (c, which)
+
+
+def test_fit_fuzz_small_shapes(api):
+    """Many small random fits (duplicate and empty rows, 1..3 token patterns,
+    single-row classes, widths around word boundaries) against the oracle."""
+    rng = np.random.default_rng(2024)
+    for case in range(30):
+        L = int(rng.choice([1, 3, 40, 63, 64, 65, 127, 200, 513]))
+        na, nn = (int(x) for x in rng.integers(1, 120, 2))
+        dens = float(rng.uniform(0.05, 0.95))
+        Xa = random_rows(rng, na, L, dens)
+        Xn = random_rows(rng, nn, L, dens)
+        if na > 3:
+            Xa[1] = Xa[0]                      # duplicate rows
+            Xa[2] = 0                          # an empty row
+        if nn > 2:
+            Xn[0] = Xa[0]                      # a row shared by both classes
+        ref = oracle.fit(Xa, Xn)
+        m = api.fit(Xa, Xn, L)
+        for c in range(2):
+            for which, want in ((0, ref.candidates[c]), (1, ref.pure[c])):
+                d = m.dictionary(c, which)
+                assert np.array_equal(d.words, want.words), (case, c, which)
+                assert np.array_equal(d.supports, want.supports), (case, c, which)
+                assert np.array_equal(d.scores, want.scores), (case, c, which)
+        T = random_rows(rng, int(rng.integers(1, 300)), L, dens)
+        A, N = m.evidence(T)
+        assert np.array_equal(A, oracle.fused_score(ref.pure[0].words, ref.pure[0].scores, T)), case
+        assert np.array_equal(N, oracle.fused_score(ref.pure[1].words, ref.pure[1].scores, T)), case
