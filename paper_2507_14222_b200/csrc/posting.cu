@@ -7,11 +7,15 @@
 // L2-resident at NSL shape).  Then
 //     {r ∈ R : b ⊆ r} = AND_{t ∈ b} post[t]
 // so a pattern costs |b| word-ANDs per 64 rows instead of K word tests per row
-// (|b| ≈ 17 tokens vs 64·K = 896 bits at NSL shape).  Rows are put in
-// canonical order first so rows sharing tokens share posting words.  Each
-// pattern's tokens are listed rarest first (document frequency over R);
-// patterns sharing their two rarest tokens share one word list (grouped_scan),
-// and a warp walks that list 32 words per step, ANDing the next tokens until
+// (|b| ≈ 17 tokens vs 64·K = 896 bits at NSL shape).  Rows are ordered first
+// so that rows sharing tokens share posting words: training rows canonically,
+// test rows in cluster order (reflected-Gray lexicographic over tokens ranked
+// most frequent first), which makes a pattern's matching rows long runs.  Each
+// pattern's tokens are listed rarest first in one rank space (a PatternIndex,
+// built once per pattern set and reused by every scan of it); patterns sharing
+// their three rarest tokens (t1, t2, t3) share one word list, filtered from
+// their (t1, t2) parent's list, and a warp walks that list 32 words per step,
+// ANDing the next tokens until
 // no lane has a surviving row.  Exact and independent of every order involved:
 //   support  = Σ popcount(...)
 //   covered  = any word non-zero                             (kernels.cpp:59-65)
