@@ -259,8 +259,8 @@ def run_b200(args):
         if sharded_mode:
             # pair tiles round-robin, candidates to fingerprint owners (NCCL all-to-all),
             # owner-local support/coverage, partial evidence all-reduced.
+            tenc = api.encode_rows(dev_te, enc, ctx)  # background pack + index during the fit
             res = sharded.fit_distributed(ctx, enc, rank, world, ex)
-            tenc = api.encode_rows(dev_te, enc, ctx)
             a, n = sharded.evidence_distributed(res, tenc, ex)
             dA.copy_(a)
             dN.copy_(n)
@@ -276,8 +276,8 @@ def run_b200(args):
         enc = api.encode_training(cols_tr, ctx)
         cols_te.prefetch(ctx)  # test columns' H2D (copy stream) overlaps the fit
         if sharded_mode:
-            res = sharded.fit_distributed(ctx, enc, rank, world, ex)
             tenc = api.encode_rows(cols_te, enc, ctx)
+            res = sharded.fit_distributed(ctx, enc, rank, world, ex)
             a, n = sharded.evidence_distributed(res, tenc, ex)
             return res.model, a.cpu().numpy(), n.cpu().numpy()
         tenc = api.encode_rows(cols_te, enc, ctx)  # from the prefetch: background pack + index

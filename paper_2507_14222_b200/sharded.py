@@ -85,7 +85,8 @@ class Shard:
         dA = torch.zeros(n, dtype=torch.int64, device="cuda")
         dN = torch.zeros(n, dtype=torch.int64, device="cuda")
         if n:
-            self.model.evidence_device(tenc.device_rows(2), n, dA.data_ptr(), dN.data_ptr())
+            # the encoding's background index of the test rows (ig_encode_rows) is reused
+            self.model.evidence_encoded_device(tenc, dA.data_ptr(), dN.data_ptr())
         return dA, dN
 
     def __del__(self):
