@@ -995,9 +995,12 @@ int ig_shard_enumerate(ig_ctx* ctx, ig_shard* s, int cls, uint64_t* counts, cons
         src.tile_begin = (uint64_t)s->rank;
         src.tile_step = (uint64_t)s->world;
         igb::DevBuf reps;
+        igb::Trace tr(*ctx, "shard_enumerate", cls);
         const uint64_t c = igb::dedup_pairs(*ctx, s->U[cls].as<int64_t>(), s->m[cls], s->k, src, reps, nullptr);
+        tr.mark("dedup");
         igb::bucket_by_owner(*ctx, s->U[cls].as<int64_t>(), s->k, reps.as<uint2>(), c, s->world, s->send[cls],
                              s->counts[cls]);
+        tr.mark("bucket");
         s->send[cls].persist();
         for (int r = 0; r < s->world; ++r) counts[r] = s->counts[cls][r];
         *d_send = s->send[cls].p;

@@ -579,6 +579,10 @@ namespace {
 __global__ void owner_of(const int64_t* __restrict__ X, int k, const uint2* __restrict__ reps, uint64_t n, int world,
                          const unsigned long long* __restrict__ keys, uint32_t* __restrict__ owner,
                          unsigned long long* __restrict__ counts) {
+    // per-block histogram in shared memory: one global atomic per block and owner
+    extern __shared__ unsigned int hist[];
+    for (int r = threadIdx.x; r < world; r += blockDim.x) hist[r] = 0;
+    __syncthreads();
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint2 p = reps[i];
         const int64_t* a = X + (size_t)p.x * k;
@@ -587,14 +591,11 @@ __global__ void owner_of(const int64_t* __restrict__ X, int k, const uint2* __re
         for (int w = 0; w < k; ++w) fp.add((uint64_t)(a[w] & b[w]), keys[w]);
         const uint32_t o = (uint32_t)((fp.final(k) >> 32) % (uint64_t)world);
         owner[i] = o;
-        atomicAdd(counts + o, 1ull);
+        atomicAdd(hist + o, 1u);
     }
-}
-
-__global__ void scatter_owner(const uint2* __restrict__ reps, const uint32_t* __restrict__ owner, uint64_t n,
-                              unsigned long long* __restrict__ cursor, uint2* __restrict__ send) {
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-        send[atomicAdd(cursor + owner[i], 1ull)] = reps[i];
+    __syncthreads();
+    for (int r = threadIdx.x; r < world; r += blockDim.x)
+        if (hist[r]) atomicAdd(counts + r, (unsigned long long)hist[r]);
 }
 }  // namespace
 
@@ -603,19 +604,26 @@ void bucket_by_owner(Ctx& ctx, const int64_t* d_rows, size_t k, const uint2* d_r
     counts.assign(world, 0);
     send.alloc(std::max<uint64_t>(count, 1) * sizeof(uint2), ctx.stream);
     if (count == 0) return;
-    DevBuf owner(count * 4, ctx.stream), cnt(world * 8, ctx.stream), cur(world * 8, ctx.stream);
+    DevBuf owner(count * 4, ctx.stream), cnt(world * 8, ctx.stream);
     IGB_CUDA(cudaMemsetAsync(cnt.p, 0, world * 8, ctx.stream));
     DevBuf keys(std::max<size_t>(k, 1) * 8, ctx.stream);
     IGB_LAUNCH(ctx, fp_keys, 1, 256, 0, kOwnerSeed, (int)k, keys.as<unsigned long long>());
-    IGB_LAUNCH(ctx, owner_of, grid_for(ctx, count, 256), 256, 0, d_rows, (int)k, d_reps, count, world,
+    IGB_LAUNCH(ctx, owner_of, grid_for(ctx, count, 256), 256, (size_t)world * 4, d_rows, (int)k, d_reps, count, world,
                keys.as<unsigned long long>(), owner.as<uint32_t>(), cnt.as<unsigned long long>());
+    // records grouped by owner: one stable radix sort on the owner id (a
+    // scatter through per-owner cursors would serialise on a few hot atomics)
+    int bits = 1;
+    while ((1 << bits) < world) ++bits;
+    DevBuf owner2(count * 4, ctx.stream);
+    size_t tb = 0;
+    IGB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, owner.as<uint32_t>(), owner2.as<uint32_t>(),
+                                             reinterpret_cast<const unsigned long long*>(d_reps),
+                                             send.as<unsigned long long>(), (int64_t)count, 0, bits, ctx.stream));
+    DevBuf temp(tb, ctx.stream);
+    IGB_CUDA(cub::DeviceRadixSort::SortPairs(temp.p, tb, owner.as<uint32_t>(), owner2.as<uint32_t>(),
+                                             reinterpret_cast<const unsigned long long*>(d_reps),
+                                             send.as<unsigned long long>(), (int64_t)count, 0, bits, ctx.stream));
     read_back(ctx, counts.data(), cnt.p, world * 8);
-    std::vector<uint64_t> start(world, 0);
-    for (int r = 1; r < world; ++r) start[r] = start[r - 1] + counts[r - 1];
-    IGB_CUDA(cudaMemcpyAsync(cur.p, start.data(), world * 8, cudaMemcpyHostToDevice, ctx.stream));
-    IGB_LAUNCH(ctx, scatter_owner, grid_for(ctx, count, 256), 256, 0, d_reps, owner.as<uint32_t>(), count,
-               cur.as<unsigned long long>(), send.as<uint2>());
-    IGB_CUDA(cudaStreamSynchronize(ctx.stream));
 }
 
 int score_dev(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const int64_t* d_support, int64_t* d_score) {
