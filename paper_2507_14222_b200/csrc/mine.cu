@@ -88,7 +88,13 @@ __device__ void table_insert(const Table& T, const int64_t* __restrict__ X, int 
         if (cur.x == 0) {
             const ulonglong2 old = cas128(slot, make_ulonglong2(0ull, 0ull), make_ulonglong2(fp, rep));
             if (old.x == 0) {
-                const unsigned long long idx = atomicAdd(T.count, 1ull);
+                // warp-aggregated slot in the reps list: the count is one hot address
+                const unsigned int mask = __activemask();
+                const int lane = threadIdx.x & 31, leader = __ffs(mask) - 1;
+                unsigned long long base = 0;
+                if (lane == leader) base = atomicAdd(T.count, (unsigned long long)__popc(mask));
+                base = __shfl_sync(mask, base, leader);
+                const unsigned long long idx = base + __popc(mask & ((1u << lane) - 1u));
                 if (idx < T.limit)
                     T.reps[idx] = make_uint2(u, v);
                 else
