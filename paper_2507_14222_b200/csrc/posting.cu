@@ -36,7 +36,6 @@ namespace igb {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kMaxSorted = 64;  // token lists longer than this keep bit order past the rarest
 
 unsigned grid_for(const Ctx& ctx, size_t work, int threads) {
     size_t g = (work + threads - 1) / threads;
@@ -126,54 +125,60 @@ __global__ void pattern_token_count(const int64_t* __restrict__ pat, size_t np, 
     }
 }
 
-// Token list of each pattern sorted by (df, token) when it has at most
-// kMaxSorted tokens; longer lists keep bit order after moving the rarest first.
-// df is staged in shared memory (L <= 64*K words of 4 bytes).
+// Token lists for rows wider than the rank-bitmap kernel takes (K > 64); df is
+// staged in shared memory (L <= 64*K words of 4 bytes).
 __global__ void pattern_token_fill(const int64_t* __restrict__ pat, size_t np, int k, const uint32_t* __restrict__ gdf,
                                    uint32_t L, const uint32_t* __restrict__ off, uint16_t* __restrict__ toks) {
+    // Wide rows (K > 64): the kTop rarest tokens first, in (df, token) order
+    // (they hold the group key), then the rest in bit order — O(|b| * kTop)
+    // instead of a per-pattern sort.  Any order is exact; rarest-first only
+    // makes the scans exit sooner.
+    constexpr int kTop = 8;
     extern __shared__ uint32_t df[];
     for (uint32_t i = threadIdx.x; i < L; i += blockDim.x) df[i] = gdf[i];
     __syncthreads();
     for (size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += (size_t)gridDim.x * blockDim.x) {
         const uint32_t o = off[p];
-        const uint32_t total = off[p + 1] - o;
-        if (total <= kMaxSorted) {
-            uint64_t key[kMaxSorted];  // (df << 16) | token: sorts by (df, token)
-            int m = 0;
+        uint64_t top[kTop];
+#pragma unroll
+        for (int i = 0; i < kTop; ++i) top[i] = ~0ull;
+        uint32_t m = 0;
+        for (int w = 0; w < k; ++w) {
+            uint64_t x = (uint64_t)pat[p * k + w];
+            while (x) {
+                const int b = __ffsll((long long)x) - 1;
+                x &= x - 1;
+                const uint32_t t = (uint32_t)w * 64 + b;
+                const uint64_t kt = ((uint64_t)df[t] << 16) | t;
+                ++m;
+                if (kt < top[kTop - 1]) {
+                    top[kTop - 1] = kt;
+#pragma unroll
+                    for (int i = kTop - 1; i > 0; --i)
+                        if (top[i] < top[i - 1]) {
+                            const uint64_t tmp = top[i];
+                            top[i] = top[i - 1];
+                            top[i - 1] = tmp;
+                        }
+                }
+            }
+        }
+        const uint32_t nt = m < (uint32_t)kTop ? m : (uint32_t)kTop;
+#pragma unroll
+        for (int i = 0; i < kTop; ++i)
+            if ((uint32_t)i < nt) toks[o + i] = (uint16_t)(top[i] & 0xffffu);
+        if (m > (uint32_t)kTop) {
+            const uint64_t thr = top[kTop - 1];
+            uint32_t idx = kTop;
             for (int w = 0; w < k; ++w) {
                 uint64_t x = (uint64_t)pat[p * k + w];
                 while (x) {
                     const int b = __ffsll((long long)x) - 1;
                     x &= x - 1;
                     const uint32_t t = (uint32_t)w * 64 + b;
-                    const uint64_t kt = ((uint64_t)df[t] << 16) | t;
-                    int i = m++;
-                    while (i > 0 && key[i - 1] > kt) {
-                        key[i] = key[i - 1];
-                        --i;
-                    }
-                    key[i] = kt;
+                    if ((((uint64_t)df[t] << 16) | t) > thr) toks[o + idx++] = (uint16_t)t;
                 }
             }
-            for (int i = 0; i < m; ++i) toks[o + i] = (uint16_t)(key[i] & 0xffffu);
-        } else {
-            uint32_t n = 0, best = 0, bestdf = 0xffffffffu;
-            for (int w = 0; w < k; ++w) {
-                uint64_t x = (uint64_t)pat[p * k + w];
-                while (x) {
-                    const int b = __ffsll((long long)x) - 1;
-                    x &= x - 1;
-                    const uint32_t t = (uint32_t)w * 64 + b;
-                    if (df[t] < bestdf) {
-                        bestdf = df[t];
-                        best = n;
-                    }
-                    toks[o + n++] = (uint16_t)t;
-                }
-            }
-            const uint16_t tmp = toks[o];
-            toks[o] = toks[o + best];
-            toks[o + best] = tmp;
         }
     }
 }

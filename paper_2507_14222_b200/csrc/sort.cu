@@ -166,9 +166,10 @@ struct FieldTable {
 __global__ void pack_keys(const int64_t* __restrict__ words, size_t n, int k, const ulonglong2* __restrict__ tables,
                           uint32_t slots, const Field* __restrict__ fields, FieldTable ft, int n_keys,
                           unsigned long long* __restrict__ keys) {
+    // fields are laid out in word order, so the key words fill one after another
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-        unsigned long long acc[8];
-        for (int j = 0; j < n_keys; ++j) acc[j] = 0;
+        unsigned long long cur = 0;
+        int ck = 0;
         for (int w = 0; w < k; ++w) {
             const unsigned long long v = (unsigned long long)words[i * k + w];
             const ulonglong2* T = tables + (size_t)w * slots;
@@ -176,11 +177,15 @@ __global__ void pack_keys(const int64_t* __restrict__ words, size_t n, int k, co
             while (T[s].x != v || T[s].y == 0) s = (s + 1) & (slots - 1);
             const unsigned long long r = T[s].y - 2;
             const Field f = fields ? fields[w] : ft.f[w];
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-                if (j == f.key) acc[j] |= r << f.shift;
+            if (f.key != ck) {
+                keys[(size_t)ck * n + i] = cur;
+                cur = 0;
+                ck = f.key;
+            }
+            cur |= r << f.shift;
         }
-        for (int j = 0; j < n_keys; ++j) keys[(size_t)j * n + i] = acc[j];
+        keys[(size_t)ck * n + i] = cur;
+        (void)n_keys;
     }
 }
 
@@ -348,7 +353,7 @@ void sort_rows_canonical(Ctx& ctx, const int64_t* d_words, size_t n, size_t k, u
         fields[w].shift = 64 - used;
     }
     used_bits.push_back(used);
-    if (n_keys > 8 || n_keys >= (int)k) {
+    if (n_keys > 48 || n_keys >= (int)k) {
         sort_rows_canonical_lsd(ctx, d_words, n, k, d_perm);
         return;
     }
@@ -413,7 +418,7 @@ void sort_rows_canonical(Ctx& ctx, const int64_t* d_words, size_t n, size_t k, u
     }
     IGB_LAUNCH(ctx, pack_keys, grid_for(ctx, n, 128), 128, 0, d_words, n, (int)k, tables.as<ulonglong2>(), slots,
                dfields.p ? dfields.as<Field>() : nullptr, ft, n_keys, keys.as<unsigned long long>());
-    if (n <= kSmallSort) {
+    if (n <= kSmallSort && n_keys <= 32) {
         // few rows: rank by counting on the packed keys (<= 8 words, most
         // comparisons end at the first) instead of ~B/8 launch-bound radix passes
         DevBuf krows(n * n_keys * 8, ctx.stream);
