@@ -268,8 +268,8 @@ def run_b200(args):
         # the test rows are packed and indexed in the background (index stream)
         # while the fit runs
         tenc = api.encode_rows(dev_te, enc, ctx)
-        model = api.fit_encoded(enc)
-        model.evidence_encoded_device(tenc, dA.data_ptr(), dN.data_ptr())
+        # fit + evidence: each class's matcher starts when its dictionary is ready
+        model = api.fit_evidence_encoded(enc, tenc, d_A_ptr=dA.data_ptr(), d_N_ptr=dN.data_ptr())
         return enc, model, tenc
 
     def step_e2e():
@@ -281,9 +281,7 @@ def run_b200(args):
             a, n = sharded.evidence_distributed(res, tenc, ex)
             return res.model, a.cpu().numpy(), n.cpu().numpy()
         tenc = api.encode_rows(cols_te, enc, ctx)  # from the prefetch: background pack + index
-        model = api.fit_encoded(enc)
-        A, N = model.evidence_encoded(tenc)
-        return model, A, N
+        return api.fit_evidence_encoded(enc, tenc)
 
     def barrier():
         torch.cuda.synchronize()
@@ -390,8 +388,7 @@ def run_b200(args):
             _, ctr_, cte_ = api.ingest_csv(csv, decimals=args.decimals, ratio_k=args.ratio, ctx=ctx)
             enc_ = api.encode_training(ctr_, ctx)
             tenc_ = api.encode_rows(cte_, enc_, ctx)
-            model_ = api.fit_encoded(enc_)
-            return model_.evidence_encoded(tenc_)
+            return api.fit_evidence_encoded(enc_, tenc_)
         for _ in range(max(1, args.warmup // 2)):
             step_csv()
         csv_ms = []

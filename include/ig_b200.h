@@ -231,6 +231,16 @@ int ig_evidence_encoded(ig_ctx* ctx, const ig_model* m, const ig_encoding* tests
  * accessor wait for it. */
 int ig_evidence_encoded_device(ig_ctx* ctx, const ig_model* m, const ig_encoding* tests, int64_t* d_A,
                                int64_t* d_N);
+/* fit (mine.hpp:38-51 + reject_covered) and evidence_scores
+ * of a test encoding in one call — the train-and-score of the reference's
+ * pipeline: each class's matcher starts as soon as that class's pure
+ * dictionary is ready, overlapping the other class's fit.  Results identical to
+ * ig_fit_encoded + ig_evidence_encoded(_device).  _host writes A / N to host
+ * memory. */
+int ig_fit_evidence_encoded(ig_ctx* ctx, const ig_encoding* train, const ig_encoding* tests,
+                            const ig_kernel_config* cfg, ig_model** out, int64_t* d_A, int64_t* d_N);
+int ig_fit_evidence_encoded_host(ig_ctx* ctx, const ig_encoding* train, const ig_encoding* tests,
+                                 const ig_kernel_config* cfg, ig_model** out, int64_t* A, int64_t* N);
 
 /* ---------------------------------------------------------------- archive / explain
  * SURVEY.md §8(f) ranks 1-2.  ModelArchive: schema

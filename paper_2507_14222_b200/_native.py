@@ -114,6 +114,8 @@ SIGNATURES = [
     ("ig_shard_free", None, [vp]),
     ("ig_evidence_encoded", C.c_int, [vp, vp, vp, p64, p64]),
     ("ig_evidence_encoded_device", C.c_int, [vp, vp, vp, vp, vp]),
+    ("ig_fit_evidence_encoded", C.c_int, [vp, vp, vp, vp, C.POINTER(vp), vp, vp]),
+    ("ig_fit_evidence_encoded_host", C.c_int, [vp, vp, vp, vp, C.POINTER(vp), p64, p64]),
 ]
 
 for _name, _res, _args in SIGNATURES:

@@ -566,6 +566,25 @@ def fit_encoded(train: Encoding, config: Optional[KernelConfig] = None) -> Model
     return Model(train.ctx, h)
 
 
+def fit_evidence_encoded(train: Encoding, tests: Encoding, config: Optional[KernelConfig] = None,
+                         d_A_ptr: Optional[int] = None, d_N_ptr: Optional[int] = None):
+    """fit + evidence of `tests` in one call (per-class overlap).  With device
+    pointers the evidence lands there and only the Model is returned; otherwise
+    (Model, A, N) with host arrays."""
+    cfg = (config or KernelConfig()).c()
+    h = C.c_void_p()
+    if d_A_ptr is not None:
+        train.ctx.check(lib.ig_fit_evidence_encoded(train.ctx.handle, train.handle, tests.handle, C.byref(cfg),
+                                                    C.byref(h), C.c_void_p(d_A_ptr), C.c_void_p(d_N_ptr)))
+        return Model(train.ctx, h)
+    n = tests.rows(2)
+    A = np.zeros(n, np.int64)
+    Nv = np.zeros(n, np.int64)
+    train.ctx.check(lib.ig_fit_evidence_encoded_host(train.ctx.handle, train.handle, tests.handle, C.byref(cfg),
+                                                     C.byref(h), _p64(A), _p64(Nv)))
+    return Model(train.ctx, h), A, Nv
+
+
 # ---------------------------------------------------------------- infer / eval (host arithmetic)
 def fit_normal_stats(nvals) -> tuple[float, float]:
     """mean / population std of strictly positive N; <2 positives -> (0, 0)."""

@@ -200,7 +200,16 @@ void for_both_classes(igb::Ctx& ctx, F&& fn, bool concurrent = true) {
 // class, canonical order.
 // enumerate = false: m.cand[c].rows already hold the candidates (multi-GPU
 // owner shard); only support -> score -> purify -> order run.
-void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m, bool enumerate = true) {
+// Optional evidence of a test encoding fused into the fit: each class's
+// matcher runs on its own stream right after that class's pure dictionary is
+// ready, overlapping the other class's fit.
+struct FusedEvidence {
+    RowIndexJob* job = nullptr;  // the test rows' background index
+    int64_t* out[2] = {nullptr, nullptr};
+    bool done = false;           // set when both classes' evidence ran here
+};
+
+void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m, bool enumerate = true, FusedEvidence* ev = nullptr) {
     m.L = L;
     const size_t k = igb::words_for(L);
     for (int c = 0; c < 2; ++c)
@@ -236,6 +245,9 @@ void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m, bool enumerate 
     igb::RankSpace R;
     igb::PatternIndex CI[2];
     if (vertical) igb::combined_rank_space(ctx, PX[0], PX[1], R);
+    const bool fuse = ev && ev->job && vertical;
+    if (fuse) ev->job->wait(&ctx);  // the test index was built during phase A
+    const bool fused = fuse && ev->job->has_postings && ev->job->P.L == (uint32_t)(64 * k);
     tm.mark();  // 1
     // phase B (per class): candidate index, support, score, checked total, purify
     for_both_classes(ctx, [&](igb::Ctx& cx, int c) {
@@ -295,10 +307,18 @@ void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m, bool enumerate 
                               &m.pidx[c].gkey, &m.pidx[c].pid, &m.pidx[c].pkey})
                 b->persist();
             tr.mark("pure_index");
+            if (fused) {
+                // Σ scores <= Σ candidate scores, checked <= INT64_MAX above: unchecked sums
+                IGB_CUDA(cudaStreamWaitEvent(cx.stream, ev->job->done, 0));
+                igb::posting_match(cx, P.rows.data(), P.rows.n, k, P.score.as<int64_t>(), ev->job->P, ev->out[c],
+                                   nullptr, true, &m.pidx[c]);
+                tr.mark("evidence");
+            }
         }
         IGB_CUDA(cudaStreamSynchronize(cx.stream));
     }, concurrent);
     m.has_pidx = vertical;
+    if (ev) ev->done = fused;
     tm.mark();  // 2
     IGB_CUDA(cudaStreamSynchronize(ctx.stream));
     IGB_CUDA(cudaStreamSynchronize(ctx.aux));
@@ -936,6 +956,47 @@ int ig_evidence_encoded(ig_ctx* ctx, const ig_model* m, const ig_encoding* tests
         evidence_of_encoding(ctx, m, tests, a.as<int64_t>(), b.as<int64_t>());
         IGB_CUDA(cudaMemcpyAsync(A, a.p, nt * 8, cudaMemcpyDeviceToHost, ctx->stream));
         IGB_CUDA(cudaMemcpyAsync(N, b.p, nt * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        IGB_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int ig_fit_evidence_encoded(ig_ctx* ctx, const ig_encoding* train, const ig_encoding* tests, const ig_kernel_config* cfg,
+                            ig_model** out, int64_t* d_A, int64_t* d_N) {
+    *out = nullptr;
+    return guard(ctx, [&] {
+        check_cfg(cfg);
+        if (tests->L != train->L) fail(IG_E_INVALID_ARG, "fused_score: logical length mismatch");
+        View X[2] = {{train->attack.data(), train->attack.n, train->attack.k},
+                     {train->normal.data(), train->normal.n, train->normal.k}};
+        auto m = std::make_unique<ig_model>();
+        FusedEvidence ev;
+        ev.job = tests->job.get();
+        ev.out[0] = d_A;
+        ev.out[1] = d_N;
+        if (tests->all.n == 0) ev.job = nullptr;
+        fit_impl(*ctx, X, train->L, *m, true, &ev);
+        if (!ev.done && tests->all.n) evidence_of_encoding(ctx, m.get(), tests, d_A, d_N);
+        *out = m.release();
+    });
+}
+
+int ig_fit_evidence_encoded_host(ig_ctx* ctx, const ig_encoding* train, const ig_encoding* tests,
+                                 const ig_kernel_config* cfg, ig_model** out, int64_t* A, int64_t* N) {
+    *out = nullptr;
+    const size_t nt = tests ? tests->all.n : 0;
+    igb::DevBuf a, b;
+    int st = guard(ctx, [&] {
+        a.alloc(std::max<size_t>(nt, 1) * 8, ctx->stream);
+        b.alloc(std::max<size_t>(nt, 1) * 8, ctx->stream);
+    });
+    if (st) return st;
+    st = ig_fit_evidence_encoded(ctx, train, tests, cfg, out, a.as<int64_t>(), b.as<int64_t>());
+    if (st) return st;
+    return guard(ctx, [&] {
+        if (nt) {
+            IGB_CUDA(cudaMemcpyAsync(A, a.p, nt * 8, cudaMemcpyDeviceToHost, ctx->stream));
+            IGB_CUDA(cudaMemcpyAsync(N, b.p, nt * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        }
         IGB_CUDA(cudaStreamSynchronize(ctx->stream));
     });
 }

@@ -164,3 +164,24 @@ def test_background_test_index_overlapping_the_fit(api, golden_dir):
     assert _digest(A) == g["A_digest"] and _digest(N) == g["N_digest"]
     assert np.array_equal(dA.cpu().numpy(), A) and np.array_equal(dN.cpu().numpy(), N)
     assert _digest(tenc.matrix(2)) == _digest(api.encode_rows(api.Columns(te, schema, False), enc, ctx).matrix(2))
+
+
+def test_fused_fit_evidence_matches_separate_calls(api, golden_dir):
+    import torch
+    g = json.load(open(os.path.join(golden_dir, "nsl_c1.json")))
+    csv = synth.nsl_csv(g["rows"], seed=g["seed"])
+    ctx = api.default_context()
+    _, tr, te = api.ingest_csv(csv, decimals=g["decimals"], ratio_k=g["ratio_k"], ctx=ctx)
+    enc = api.encode_training(tr, ctx)
+    tenc = api.encode_rows(te, enc, ctx)
+    model, A, N = api.fit_evidence_encoded(enc, tenc)
+    assert _digest(A) == g["A_digest"] and _digest(N) == g["N_digest"]
+    for c in range(2):
+        p = model.dictionary(c, 1)
+        assert _digest(p.words, p.supports, p.scores) == g["pure_digest"][c]
+    dA = torch.zeros(tenc.rows(2), dtype=torch.int64, device="cuda")
+    dN = torch.zeros_like(dA)
+    tenc2 = api.encode_rows(te, enc, ctx)
+    api.fit_evidence_encoded(enc, tenc2, d_A_ptr=dA.data_ptr(), d_N_ptr=dN.data_ptr())
+    torch.cuda.synchronize()
+    assert np.array_equal(dA.cpu().numpy(), A) and np.array_equal(dN.cpu().numpy(), N)
