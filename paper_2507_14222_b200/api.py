@@ -663,11 +663,10 @@ def train_and_score(csv: bytes, label_column: str = "label", decimals: int = 1, 
     te = table.slice(ntr, n)
     schema = infer_schema(tr, label_column, attack_values, normal_values, decimals)
     enc = encode_training(Columns(tr, schema, True), ctx)
-    model = fit_encoded(enc, config)
     if te.rows == 0:
-        return RunResult(model, enc, None, None, None)
+        return RunResult(fit_encoded(enc, config), enc, None, None, None)
     tenc = encode_rows(Columns(te, schema, False), enc, ctx)
-    A, Nv = model.evidence_encoded(tenc)
+    model, A, Nv = fit_evidence_encoded(enc, tenc, config)
     return RunResult(model, enc, tenc, A, Nv)
 
 
