@@ -662,10 +662,14 @@ def train_and_score(csv: bytes, label_column: str = "label", decimals: int = 1, 
     tr = table.slice(0, ntr)
     te = table.slice(ntr, n)
     schema = infer_schema(tr, label_column, attack_values, normal_values, decimals)
-    enc = encode_training(Columns(tr, schema, True), ctx)
+    ctr, cte = Columns(tr, schema, True), Columns(te, schema, False)
+    ctr.prefetch(ctx)  # H2D on the copy stream: training columns first, test columns behind them
+    if te.rows:
+        cte.prefetch(ctx)
+    enc = encode_training(ctr, ctx)
     if te.rows == 0:
         return RunResult(fit_encoded(enc, config), enc, None, None, None)
-    tenc = encode_rows(Columns(te, schema, False), enc, ctx)
+    tenc = encode_rows(cte, enc, ctx)
     model, A, Nv = fit_evidence_encoded(enc, tenc, config)
     return RunResult(model, enc, tenc, A, Nv)
 
