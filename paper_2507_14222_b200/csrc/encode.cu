@@ -517,6 +517,7 @@ void encode_rows_dev(Ctx& ctx, const ig_columns& c, const ig_encoding& train, ig
 }
 
 void upload_columns(Ctx& ctx, ig_columns& c) {
+    if (c.d_values && c.device == ctx.device) return;  // already resident (uploaded or device-ingested)
     auto up = [&](const void* src, size_t bytes) {
         void* p = nullptr;
         IGB_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 8)));

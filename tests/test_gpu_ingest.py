@@ -104,3 +104,18 @@ def test_ingested_columns_fit_like_host_columns(api):
     A1, N1 = m1.evidence_encoded(api.encode_rows(te1, api.encode_training(tr1, ctx), ctx))
     A2, N2 = m2.evidence_encoded(api.encode_rows(te2, e2, ctx))
     assert np.array_equal(A1, A2) and np.array_equal(N1, N2)
+
+
+def test_all_rows_train_and_explicit_counts(api):
+    csv = synth.nsl_csv(1500, seed=21)
+    ctx = api.default_context()
+    s, tr, te = api.ingest_csv(csv, decimals=1, ratio_k=10, ctx=ctx)
+    assert tr.rows == 1500 and te.rows == 0
+    s2, tr2, te2 = api.ingest_csv(csv, decimals=1, train_rows=999, ctx=ctx)
+    assert tr2.rows == 999 and te2.rows == 501
+    _same(api, csv, decimals=1, train_rows=999)
+    # the ingested training columns prefetch / upload as no-ops (already resident)
+    tr2.prefetch(ctx)
+    tr2.upload(ctx)
+    assert np.array_equal(api.encode_training(tr2, ctx).matrix(0),
+                          api.encode_training(_host(api, csv, "label", 1, train_rows=999)[1], ctx).matrix(0))
