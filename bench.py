@@ -408,6 +408,47 @@ def run_b200(args):
                    "note": "CSV bytes -> ig_ingest_csv (records, numbers, schema, columns on the GPU) -> encode -> "
                            "fit -> evidence -> A/N; the host parse this replaces is host_prep_s"}
 
+    # ---- SURVEY.md §8(d) "fit seconds": H2D of the parsed training columns ->
+    # tokenise -> enumerate / dedup / support / score / purify -> the pure
+    # dictionaries (patterns, supports, scores) on the host; and the matcher
+    # alone (resident test encoding -> A/N on the host), as separate numbers
+    fit_leg = None
+    if not sharded_mode:
+        dev_tenc = api.encode_rows(dev_te, api.encode_training(dev_tr, ctx), ctx)
+
+        def step_fit():
+            enc_ = api.encode_training(cols_tr, ctx)
+            model_ = api.fit_encoded(enc_)
+            return model_, [model_.dictionary(c, 1) for c in range(2)]
+
+        def step_match(model_):
+            return model_.evidence_encoded(dev_tenc)
+
+        for _ in range(max(1, args.warmup // 2)):
+            m_, _ = step_fit()
+            step_match(m_)
+        fit_ms, match_ms, dict_bytes = [], [], 0
+        gc.disable()
+        for _ in range(args.steps):
+            m_ = None
+            torch.cuda.synchronize()
+            w0 = time.perf_counter()
+            m_, dicts = step_fit()
+            torch.cuda.synchronize()
+            w1 = time.perf_counter()
+            step_match(m_)
+            torch.cuda.synchronize()
+            w2 = time.perf_counter()
+            fit_ms.append((w1 - w0) * 1e3)
+            match_ms.append((w2 - w1) * 1e3)
+            dict_bytes = sum(d.words.nbytes + d.supports.nbytes + d.scores.nbytes for d in dicts)
+        gc.enable()
+        m_ = dicts = None
+        fit_leg = {"fit_s": statistics.median(fit_ms) / 1e3, "matcher_s": statistics.median(match_ms) / 1e3,
+                   "unit": "s", "h2d_bytes_per_step": cols_tr.nbytes, "d2h_bytes_per_step": dict_bytes,
+                   "note": "fit: parsed training columns (host) -> encode -> fit -> both pure dictionaries copied "
+                           "to the host; matcher: resident test encoding -> A/N on the host"}
+
 
     line = {"metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
@@ -419,6 +460,7 @@ def run_b200(args):
             "host_prep_s": host_prep, "gen_s": t_gen,
             "e2e": {"value": e2e / 1e3, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "e2e_csv": csv_leg,
+            "fit_and_matcher": fit_leg,
             "gpu_launches": launches, "clocks": clk, "roofline": roofline}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_reference(csv, args, args.cpu_sample_tests)
