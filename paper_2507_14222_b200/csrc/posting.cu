@@ -186,38 +186,48 @@ __global__ void pattern_token_fill(const int64_t* __restrict__ pat, size_t np, i
 // Rank-space variant: with byrank[] = tokens sorted by (df, token) and rank[]
 // its inverse, re-indexing a pattern's bits by rank and reading them back in
 // bit order lists its tokens rarest first with no per-pattern sort: O(|b| + K).
+// The rank-space bitmap of each thread lives in shared memory (word-major,
+// thread-minor: conflict-free) and is set with shared atomics whose result is
+// unused, so consecutive bits do not wait on each other's read-modify-write
+// (a local-memory array made every bit one dependent L1 round trip: -22 %).
+// Staging the rows and the output through shared memory as well was slower
+// (occupancy).
 constexpr int kRankWords = 64;
+constexpr int kFillThreads = 128;
 template <int KW>
-__global__ void pattern_token_fill_rank(const int64_t* __restrict__ pat, size_t np, int k,
-                                        const uint16_t* __restrict__ grank, const uint16_t* __restrict__ gbyrank,
-                                        uint32_t L, const uint32_t* __restrict__ off, uint16_t* __restrict__ toks) {
-    extern __shared__ uint16_t rsm[];
-    uint16_t* rank = rsm;
-    uint16_t* byrank = rsm + L;
+__global__ void __launch_bounds__(kFillThreads)
+pattern_token_fill_rank(const int64_t* __restrict__ pat, size_t np, int k, const uint16_t* __restrict__ grank,
+                        const uint16_t* __restrict__ gbyrank, uint32_t L, const uint32_t* __restrict__ off,
+                        uint16_t* __restrict__ toks) {
+    extern __shared__ uint32_t fsm[];
+    uint32_t* rb = fsm;  // [2 * KW][kFillThreads]
+    uint16_t* rank = reinterpret_cast<uint16_t*>(fsm + 2 * KW * kFillThreads);
+    uint16_t* byrank = rank + L;
     for (uint32_t i = threadIdx.x; i < L; i += blockDim.x) {
         rank[i] = grank[i];
         byrank[i] = gbyrank[i];
     }
     __syncthreads();
+    uint32_t* my = rb + threadIdx.x;
+    const int nw = 2 * k;  // 32-bit rank words
     for (size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += (size_t)gridDim.x * blockDim.x) {
-        uint64_t rb[KW];  // rank-space bitmap (local memory: dynamic indices)
-        for (int q = 0; q < k; ++q) rb[q] = 0;
+        for (int q = 0; q < nw; ++q) my[q * kFillThreads] = 0u;
         for (int w = 0; w < k; ++w) {
             uint64_t x = (uint64_t)pat[p * k + w];
             while (x) {
                 const int b = __ffsll((long long)x) - 1;
                 x &= x - 1;
                 const uint32_t r = rank[w * 64 + b];
-                rb[r >> 6] |= 1ull << (r & 63);
+                atomicOr(my + (r >> 5) * kFillThreads, 1u << (r & 31));
             }
         }
         uint32_t o = off[p];
-        for (int q = 0; q < k; ++q) {
-            uint64_t y = rb[q];
+        for (int q = 0; q < nw; ++q) {
+            uint32_t y = atomicOr(my + q * kFillThreads, 0u);  // ordered after this thread's ORs
             while (y) {
-                const int b = __ffsll((long long)y) - 1;
+                const int b = __ffs((int)y) - 1;
                 y &= y - 1;
-                toks[o++] = byrank[q * 64 + b];
+                toks[o++] = byrank[q * 32 + b];
             }
         }
     }
@@ -800,13 +810,14 @@ void build_pattern_index(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, co
     if (np == 0) return;
     const uint32_t L = R.L;
     if (k <= kRankWords) {
-        const size_t smem = (size_t)L * 4;
 #define IGB_FILL_RANK(KW)                                                                                          \
     {                                                                                                              \
+        const size_t smem = (size_t)L * 4 + (size_t)2 * KW * kFillThreads * 4;                                    \
         if (smem > 48 * 1024)                                                                                      \
             IGB_CUDA(cudaFuncSetAttribute(pattern_token_fill_rank<KW>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                           (int)smem));                                                             \
-        IGB_LAUNCH(ctx, pattern_token_fill_rank<KW>, grid_for(ctx, np, 128), 128, smem, d_pat, np, (int)k,         \
+        IGB_LAUNCH(ctx, pattern_token_fill_rank<KW>, grid_for(ctx, np, kFillThreads), kFillThreads, smem, d_pat,   \
+                   np, (int)k,                                                                                     \
                    R.rank.as<uint16_t>(), R.byrank.as<uint16_t>(), L, I.beg.as<uint32_t>(), I.toks->as<uint16_t>()); \
     }
         if (k <= 16)
