@@ -233,7 +233,7 @@ class CandidateSet:
     _ctx: object = None
 
     def __del__(self):
-        if self._handle:
+        if self._handle and lib is not None:
             lib.ig_candidates_free(self._handle)
             self._handle = None
 
@@ -344,7 +344,7 @@ class Model:
         return A, Nn
 
     def __del__(self):
-        if getattr(self, "handle", None):
+        if getattr(self, "handle", None) and lib is not None:  # lib is None at interpreter teardown
             lib.ig_model_free(self.handle)
             self.handle = None
 
@@ -404,7 +404,7 @@ class Table:
         return Table(h)
 
     def __del__(self):
-        if getattr(self, "handle", None):
+        if getattr(self, "handle", None) and lib is not None:  # lib is None at interpreter teardown
             lib.ig_table_free(self.handle)
             self.handle = None
 
@@ -434,7 +434,7 @@ class Schema:
         return ("numeric" if kind.value == 0 else "categorical"), mean.value, sd.value
 
     def __del__(self):
-        if getattr(self, "handle", None):
+        if getattr(self, "handle", None) and lib is not None:  # lib is None at interpreter teardown
             lib.ig_schema_free(self.handle)
             self.handle = None
 
@@ -484,7 +484,7 @@ class Columns:
         return int(lib.ig_columns_bytes(self.handle))
 
     def __del__(self):
-        if getattr(self, "handle", None):
+        if getattr(self, "handle", None) and lib is not None:  # lib is None at interpreter teardown
             lib.ig_columns_free(self.handle)
             self.handle = None
 
@@ -540,7 +540,7 @@ class Encoding:
         return out
 
     def __del__(self):
-        if getattr(self, "handle", None):
+        if getattr(self, "handle", None) and lib is not None:  # lib is None at interpreter teardown
             lib.ig_encoding_free(self.handle)
             self.handle = None
 

@@ -90,7 +90,7 @@ class Shard:
         return dA, dN
 
     def __del__(self):
-        if getattr(self, "handle", None):
+        if getattr(self, "handle", None) and lib is not None:  # lib is None at interpreter teardown
             lib.ig_shard_free(self.handle)
             self.handle = None
 

@@ -89,7 +89,7 @@ def main():
     tr, te = table.slice(0, ntr), table.slice(ntr, table.rows)
     schema = api.infer_schema(tr, "label", decimals=1)
     ctr, cte = api.Columns(tr, schema, True).upload(ctx), api.Columns(te, schema, False).upload(ctx)
-    for _ in range(2):
+    for _ in range(4):  # the first encodes of a process grow the memory pool
         enc, t_enc = _t(lambda: api.encode_training(ctr, ctx))
         tenc, t_tenc = _t(lambda: api.encode_rows(cte, enc, ctx))
     # single-device reference step: the fused fit + evidence
