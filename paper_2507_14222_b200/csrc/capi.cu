@@ -686,9 +686,8 @@ int ig_evidence(ig_ctx* ctx, const ig_model* m, const int64_t* tests, size_t nt,
         upload_rows(*ctx, tests, nt, L, T);
         DevBuf a(nt * 8, ctx->stream), b(nt * 8, ctx->stream);
         evidence_impl(*ctx, *m, T.data(), nt, L, a.as<int64_t>(), b.as<int64_t>());
-        IGB_CUDA(cudaMemcpyAsync(A, a.p, nt * 8, cudaMemcpyDeviceToHost, ctx->stream));
-        IGB_CUDA(cudaMemcpyAsync(N, b.p, nt * 8, cudaMemcpyDeviceToHost, ctx->stream));
-        IGB_CUDA(cudaStreamSynchronize(ctx->stream));
+        igb::read_back(*ctx, A, a.p, nt * 8);  // page-locked bounce buffer
+        igb::read_back(*ctx, N, b.p, nt * 8);
     });
 }
 
@@ -954,9 +953,8 @@ int ig_evidence_encoded(ig_ctx* ctx, const ig_model* m, const ig_encoding* tests
         if (nt == 0) return;
         DevBuf a(nt * 8, ctx->stream), b(nt * 8, ctx->stream);
         evidence_of_encoding(ctx, m, tests, a.as<int64_t>(), b.as<int64_t>());
-        IGB_CUDA(cudaMemcpyAsync(A, a.p, nt * 8, cudaMemcpyDeviceToHost, ctx->stream));
-        IGB_CUDA(cudaMemcpyAsync(N, b.p, nt * 8, cudaMemcpyDeviceToHost, ctx->stream));
-        IGB_CUDA(cudaStreamSynchronize(ctx->stream));
+        igb::read_back(*ctx, A, a.p, nt * 8);  // page-locked bounce buffer
+        igb::read_back(*ctx, N, b.p, nt * 8);
     });
 }
 
@@ -993,11 +991,10 @@ int ig_fit_evidence_encoded_host(ig_ctx* ctx, const ig_encoding* train, const ig
     st = ig_fit_evidence_encoded(ctx, train, tests, cfg, out, a.as<int64_t>(), b.as<int64_t>());
     if (st) return st;
     return guard(ctx, [&] {
-        if (nt) {
-            IGB_CUDA(cudaMemcpyAsync(A, a.p, nt * 8, cudaMemcpyDeviceToHost, ctx->stream));
-            IGB_CUDA(cudaMemcpyAsync(N, b.p, nt * 8, cudaMemcpyDeviceToHost, ctx->stream));
-        }
-        IGB_CUDA(cudaStreamSynchronize(ctx->stream));
+        // through the page-locked bounce buffer: a pageable D2H is staged by
+        // the driver at a fraction of the link rate
+        igb::read_back(*ctx, A, a.p, nt * 8);
+        igb::read_back(*ctx, N, b.p, nt * 8);
     });
 }
 
