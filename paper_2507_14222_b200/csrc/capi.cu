@@ -209,7 +209,10 @@ struct FusedEvidence {
     bool done = false;           // set when both classes' evidence ran here
 };
 
-void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m, bool enumerate = true, FusedEvidence* ev = nullptr) {
+// row_perm (optional): each class's canonical row permutation, already known
+// (a shard computed it for its distinct rows).
+void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m, bool enumerate = true, FusedEvidence* ev = nullptr,
+              const uint32_t* const* row_perm = nullptr) {
     m.L = L;
     const size_t k = igb::words_for(L);
     for (int c = 0; c < 2; ++c)
@@ -227,16 +230,22 @@ void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m, bool enumerate 
     // postings), candidates, postings
     for_both_classes(ctx, [&](igb::Ctx& cx, int c) {
         igb::Trace tr(cx, "fitA", c);
-        perm[c].alloc(X[c].n * 4, cx.stream);
-        igb::sort_rows_canonical(cx, X[c].p, X[c].n, k, perm[c].as<uint32_t>());
+        const uint32_t* pc;
+        if (row_perm && row_perm[c]) {
+            pc = row_perm[c];
+        } else {
+            perm[c].alloc(X[c].n * 4, cx.stream);
+            igb::sort_rows_canonical(cx, X[c].p, X[c].n, k, perm[c].as<uint32_t>());
+            pc = perm[c].as<uint32_t>();
+        }
         tr.mark("sort_rows");
         if (enumerate) {
-            igb::enumerate_dev(cx, X[c].p, X[c].n, k, L, m.cand[c].rows, &m.stats[c], perm[c].as<uint32_t>());
+            igb::enumerate_dev(cx, X[c].p, X[c].n, k, L, m.cand[c].rows, &m.stats[c], pc);
             m.cand[c].pairs = m.stats[c].pairs;
             m.cand[c].ordered = false;
         }
         tr.mark("enumerate");
-        if (vertical) igb::build_postings(cx, X[c].p, X[c].n, k, L, PX[c], true, false, perm[c].as<uint32_t>());
+        if (vertical) igb::build_postings(cx, X[c].p, X[c].n, k, L, PX[c], true, false, pc);
         tr.mark("postings");
     }, concurrent);
     // one token rank space for every scan of this fit: frequencies over all
@@ -1016,6 +1025,7 @@ struct ig_shard {
     size_t k = 0;
     const ig_encoding* train = nullptr;
     igb::DevBuf U[2];
+    igb::DevBuf perm[2];  // canonical order of each class's rows (reused by the finish)
     size_t m[2] = {0, 0};
     igb::DevBuf send[2];
     std::vector<uint64_t> counts[2];
@@ -1038,8 +1048,9 @@ int ig_shard_create(ig_ctx* ctx, const ig_encoding* train, int rank, int world, 
         const igb::DevRows* X[2] = {&train->attack, &train->normal};
         for (int c = 0; c < 2; ++c) {
             if (X[c]->n == 0) fail(IG_E_DATA, "enumerate_candidates: empty class");
-            s->m[c] = igb::distinct_rows(*ctx, X[c]->data(), X[c]->n, s->k, s->U[c]);
+            s->m[c] = igb::distinct_rows(*ctx, X[c]->data(), X[c]->n, s->k, s->U[c], nullptr, &s->perm[c]);
             s->U[c].persist();
+            s->perm[c].persist();
         }
         IGB_CUDA(cudaStreamSynchronize(ctx->stream));
         *out = s.release();
@@ -1087,7 +1098,9 @@ int ig_shard_finish(ig_ctx* ctx, ig_shard* s, uint64_t* partial_totals) {
         if (!s->received[0] || !s->received[1]) fail(IG_E_INVALID_ARG, "shard: receive both classes first");
         View X[2] = {{s->train->attack.data(), s->train->attack.n, s->train->attack.k},
                      {s->train->normal.data(), s->train->normal.n, s->train->normal.k}};
-        fit_impl(*ctx, X, s->L, s->model, /*enumerate=*/false);
+        const uint32_t* rp[2] = {s->perm[0].p ? s->perm[0].as<uint32_t>() : nullptr,
+                                 s->perm[1].p ? s->perm[1].as<uint32_t>() : nullptr};
+        fit_impl(*ctx, X, s->L, s->model, /*enumerate=*/false, nullptr, rp);
         partial_totals[0] = s->model.partial_total[0];
         partial_totals[1] = s->model.partial_total[1];
     });

@@ -206,7 +206,9 @@ void sort_rows_canonical(Ctx& ctx, const int64_t* d_words, size_t n, size_t k, u
 void sort_rows_canonical_lsd(Ctx& ctx, const int64_t* d_words, size_t n, size_t k, uint32_t* d_perm);
 // Distinct rows of d_rows in canonical order -> out (m x k); returns m.
 // d_perm: the rows' canonical permutation when already known (else computed).
-size_t distinct_rows(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, DevBuf& out, const uint32_t* d_perm = nullptr);
+// o_perm (optional): receives that permutation.
+size_t distinct_rows(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, DevBuf& out, const uint32_t* d_perm = nullptr,
+                     DevBuf* o_perm = nullptr);
 void gather_rows(Ctx& ctx, const int64_t* d_src, const uint32_t* d_perm, size_t n, size_t k, int64_t* d_dst);
 
 }  // namespace igb

@@ -458,7 +458,8 @@ void sort_rows_canonical(Ctx& ctx, const int64_t* d_words, size_t n, size_t k, u
     tr.mark("lsd");
 }
 
-size_t distinct_rows(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, DevBuf& out, const uint32_t* d_perm) {
+size_t distinct_rows(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, DevBuf& out, const uint32_t* d_perm,
+                     DevBuf* o_perm) {
     if (n == 0) {
         out.alloc(8, ctx.stream);
         return 0;
@@ -481,6 +482,7 @@ size_t distinct_rows(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, DevBuf
     out.alloc(std::max<size_t>((size_t)m * k, 1) * 8, ctx.stream);
     IGB_LAUNCH(ctx, gather_rows_u32, grid_for(ctx, (size_t)m * k, 256), 256, 0, d_rows, rep.as<uint32_t>(), (size_t)m,
                (int)k, out.as<int64_t>());
+    if (o_perm) *o_perm = std::move(perm);
     return (size_t)m;
 }
 
