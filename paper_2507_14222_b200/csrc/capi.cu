@@ -147,6 +147,7 @@ struct Timer {
 // independent within each phase, so their host-side syncs overlap with the
 // other class's kernels.
 constexpr size_t kConcurrentRows = 40000;        // training rows (C3: 14,851; C4: 118,813)
+constexpr size_t kConcurrentCandidates = 12000000;  // shard finish (C4 per rank: ~8.4 M at world 4, ~4.2 M at 8)
 constexpr size_t kConcurrentPatterns = 8u << 20; // pure patterns (C3: 2.2 M; C4: 32 M)
 
 template <class F>
@@ -223,7 +224,9 @@ void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m, bool enumerate 
     // Small fits are launch/sync bound: overlap the classes.  Large ones fill the
     // GPU with each class alone, and concurrent multi-GB allocations on two
     // streams only fragment the memory pool, so they run one after the other.
-    const bool concurrent = X[0].n + X[1].n <= kConcurrentRows;
+    // (an owner shard's finish: decided by its candidate counts)
+    const bool concurrent = enumerate ? X[0].n + X[1].n <= kConcurrentRows
+                                      : m.cand[0].rows.n + m.cand[1].rows.n <= kConcurrentCandidates;
     DevBuf perm[2];
     igb::Postings PX[2];
     // phase A1 (per class): canonical row order (shared by enumeration and the
