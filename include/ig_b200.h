@@ -138,6 +138,13 @@ size_t ig_model_count(const ig_model* m, int cls, int which);
 uint32_t ig_model_logical_len(const ig_model* m);
 int ig_model_copy(ig_ctx* ctx, const ig_model* m, int cls, int which, int64_t* words,
                   int64_t* supports, int64_t* scores);
+/* Page-locked host storage for results (the reference returns its dictionaries
+ * as host std::vectors, mine.hpp:13-29).  Blocks are cached
+ * by size, so repeated fits reuse them: cudaHostAlloc costs ~0.1 ms/MB, and a
+ * pageable device-to-host copy into fresh pages runs at a few GB/s against
+ * ~55 GB/s into page-locked memory.  IG_E_OOM when the host cannot pin.     */
+int ig_host_alloc(size_t bytes, void** out);
+void ig_host_free(void* p);
 /* Phase timings of the last fit in ms: [rows, enumerate, support, purify, order, total]. */
 int ig_model_phase_ms(const ig_model* m, double* ms6);
 void ig_model_free(ig_model* m);

@@ -69,6 +69,8 @@ SIGNATURES = [
     ("ig_model_logical_len", u32, [vp]),
     ("ig_model_copy", C.c_int, [vp, vp, C.c_int, C.c_int, p64, p64, p64]),
     ("ig_model_phase_ms", C.c_int, [vp, C.POINTER(C.c_double)]),
+    ("ig_host_alloc", C.c_int, [sz, C.POINTER(vp)]),
+    ("ig_host_free", None, [vp]),
     ("ig_model_free", None, [vp]),
     ("ig_evidence", C.c_int, [vp, vp, p64, sz, u32, p64, p64]),
     ("ig_evidence_device", C.c_int, [vp, vp, vp, sz, u32, vp, vp]),

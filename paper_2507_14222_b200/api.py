@@ -292,6 +292,36 @@ class Dictionary:
     scores: np.ndarray
 
 
+class _PinnedBlock:
+    """One page-locked block of the library's host pool (ig_host_alloc)."""
+    __slots__ = ("ptr",)
+
+    def __init__(self, nbytes: int):
+        p = C.c_void_p()
+        st = lib.ig_host_alloc(nbytes, C.byref(p))
+        if st:
+            _raise(st, None)
+        self.ptr = p.value
+
+    def __del__(self):
+        if self.ptr and lib is not None:  # lib is None at interpreter teardown
+            lib.ig_host_free(C.c_void_p(self.ptr))
+            self.ptr = None
+
+
+def pinned_array(shape, dtype) -> np.ndarray:
+    """numpy array in page-locked host memory; the block returns to the pool
+    when the last view of it is gone."""
+    dtype = np.dtype(dtype)
+    nbytes = int(np.prod(shape)) * dtype.itemsize
+    if nbytes == 0:
+        return np.zeros(shape, dtype)
+    blk = _PinnedBlock(nbytes)
+    buf = (C.c_char * nbytes).from_address(blk.ptr)
+    buf._ig_block = blk  # the array's base keeps the block alive
+    return np.frombuffer(buf, dtype=dtype, count=int(np.prod(shape))).reshape(shape)
+
+
 class Model:
     """Pure dictionaries P+ / P- (and candidate sets B+ / B-) resident on the device."""
 
@@ -304,12 +334,13 @@ class Model:
         return int(lib.ig_model_count(self.handle, cls, which))
 
     def dictionary(self, cls: int, which: int = 1) -> Dictionary:
-        """cls 0 attack / 1 normal; which 0 candidates B^c / 1 pure P^c."""
+        """cls 0 attack / 1 normal; which 0 candidates B^c / 1 pure P^c.  The
+        arrays live in page-locked host memory (reused across calls once freed)."""
         n = self.count(cls, which)
         k = (self.logical_len + 63) // 64
-        w = np.zeros((n, k), np.int64)
-        s = np.zeros(n, np.int64)
-        sc = np.zeros(n, np.int64)
+        w = pinned_array((n, k), np.int64)
+        s = pinned_array((n,), np.int64)
+        sc = pinned_array((n,), np.int64)
         self.ctx.check(lib.ig_model_copy(self.ctx.handle, self.handle, cls, which, _p64(w), _p64(s), _p64(sc)))
         return Dictionary(w, s, sc)
 

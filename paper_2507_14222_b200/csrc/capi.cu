@@ -8,6 +8,9 @@
 #include <chrono>
 #include <cstring>
 #include <memory>
+#include <unordered_map>
+#include <map>
+#include <mutex>
 #include <exception>
 #include <string>
 #include <thread>
@@ -690,6 +693,75 @@ int ig_model_phase_ms(const ig_model* m, double* ms6) {
 }
 
 void ig_model_free(ig_model* m) { delete m; }
+
+// ------------------------------------------------------------------ page-locked result storage
+namespace {
+struct HostPool {
+    std::mutex mu;
+    std::multimap<size_t, void*> free_blocks;  // capacity -> block
+    std::unordered_map<void*, size_t> cap;     // every block this pool made
+    size_t cached = 0;
+    static constexpr size_t kKeep = size_t{16} << 30;  // cached bytes kept for reuse
+    ~HostPool() {
+        for (auto& kv : free_blocks) cudaFreeHost(kv.second);
+    }
+};
+HostPool& host_pool() {
+    static HostPool* p = new HostPool();  // never destroyed: frees may run at interpreter teardown
+    return *p;
+}
+size_t host_class(size_t bytes) {
+    if (bytes <= (size_t{1} << 20)) {
+        size_t c = 4096;
+        while (c < bytes) c <<= 1;
+        return c;
+    }
+    const size_t g = size_t{2} << 20;
+    return (bytes + g - 1) / g * g;
+}
+}  // namespace
+
+int ig_host_alloc(size_t bytes, void** out) {
+    *out = nullptr;
+    return guard(nullptr, [&] {
+        if (bytes == 0) fail(IG_E_INVALID_ARG, "ig_host_alloc: zero bytes");
+        const size_t want = host_class(bytes);
+        HostPool& P = host_pool();
+        {
+            std::lock_guard<std::mutex> lk(P.mu);
+            auto it = P.free_blocks.lower_bound(want);
+            if (it != P.free_blocks.end() && it->first <= 2 * want) {
+                *out = it->second;
+                P.cached -= it->first;
+                P.free_blocks.erase(it);
+                return;
+            }
+        }
+        void* p = nullptr;
+        if (cudaHostAlloc(&p, want, cudaHostAllocPortable) != cudaSuccess || !p) {
+            cudaGetLastError();
+            fail(IG_E_OOM, "ig_host_alloc: cannot page-lock " + std::to_string(want) + " bytes");
+        }
+        std::lock_guard<std::mutex> lk(P.mu);
+        P.cap[p] = want;
+        *out = p;
+    });
+}
+
+void ig_host_free(void* p) {
+    if (!p) return;
+    HostPool& P = host_pool();
+    std::lock_guard<std::mutex> lk(P.mu);
+    auto it = P.cap.find(p);
+    if (it == P.cap.end()) return;  // not ours
+    if (P.cached + it->second > HostPool::kKeep) {
+        cudaFreeHost(p);
+        P.cap.erase(it);
+        return;
+    }
+    P.cached += it->second;
+    P.free_blocks.emplace(it->second, p);
+}
 
 int ig_evidence(ig_ctx* ctx, const ig_model* m, const int64_t* tests, size_t nt, uint32_t L, int64_t* A, int64_t* N) {
     return guard(ctx, [&] {
