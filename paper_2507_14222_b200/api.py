@@ -369,8 +369,8 @@ class Model:
 
     def evidence_encoded(self, enc: "Encoding") -> tuple[np.ndarray, np.ndarray]:
         n = enc.rows(2)
-        A = np.empty(n, np.int64)
-        Nn = np.empty(n, np.int64)
+        A = pinned_array((n,), np.int64)
+        Nn = pinned_array((n,), np.int64)
         self.ctx.check(lib.ig_evidence_encoded(self.ctx.handle, self.handle, enc.handle, _p64(A), _p64(Nn)))
         return A, Nn
 
@@ -609,8 +609,8 @@ def fit_evidence_encoded(train: Encoding, tests: Encoding, config: Optional[Kern
                                                     C.byref(h), C.c_void_p(d_A_ptr), C.c_void_p(d_N_ptr)))
         return Model(train.ctx, h)
     n = tests.rows(2)
-    A = np.empty(n, np.int64)  # every element is written
-    Nv = np.empty(n, np.int64)
+    A = pinned_array((n,), np.int64)  # every element is written
+    Nv = pinned_array((n,), np.int64)
     train.ctx.check(lib.ig_fit_evidence_encoded_host(train.ctx.handle, train.handle, tests.handle, C.byref(cfg),
                                                      C.byref(h), _p64(A), _p64(Nv)))
     return Model(train.ctx, h), A, Nv

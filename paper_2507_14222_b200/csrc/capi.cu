@@ -770,8 +770,8 @@ int ig_evidence(ig_ctx* ctx, const ig_model* m, const int64_t* tests, size_t nt,
         upload_rows(*ctx, tests, nt, L, T);
         DevBuf a(nt * 8, ctx->stream), b(nt * 8, ctx->stream);
         evidence_impl(*ctx, *m, T.data(), nt, L, a.as<int64_t>(), b.as<int64_t>());
-        igb::read_back(*ctx, A, a.p, nt * 8);  // page-locked bounce buffer
-        igb::read_back(*ctx, N, b.p, nt * 8);
+        igb::copy_to_host(*ctx, A, a.p, nt * 8);
+        igb::copy_to_host(*ctx, N, b.p, nt * 8);
     });
 }
 
@@ -1037,8 +1037,8 @@ int ig_evidence_encoded(ig_ctx* ctx, const ig_model* m, const ig_encoding* tests
         if (nt == 0) return;
         DevBuf a(nt * 8, ctx->stream), b(nt * 8, ctx->stream);
         evidence_of_encoding(ctx, m, tests, a.as<int64_t>(), b.as<int64_t>());
-        igb::read_back(*ctx, A, a.p, nt * 8);  // page-locked bounce buffer
-        igb::read_back(*ctx, N, b.p, nt * 8);
+        igb::copy_to_host(*ctx, A, a.p, nt * 8);
+        igb::copy_to_host(*ctx, N, b.p, nt * 8);
     });
 }
 
@@ -1077,8 +1077,8 @@ int ig_fit_evidence_encoded_host(ig_ctx* ctx, const ig_encoding* train, const ig
     return guard(ctx, [&] {
         // through the page-locked bounce buffer: a pageable D2H is staged by
         // the driver at a fraction of the link rate
-        igb::read_back(*ctx, A, a.p, nt * 8);
-        igb::read_back(*ctx, N, b.p, nt * 8);
+        igb::copy_to_host(*ctx, A, a.p, nt * 8);
+        igb::copy_to_host(*ctx, N, b.p, nt * 8);
     });
 }
 

@@ -131,6 +131,19 @@ inline void read_back(const Ctx& ctx, void* host_dst, const void* d_src, size_t 
     if (bytes) std::memcpy(host_dst, buf.p, bytes);
 }
 
+// Device -> host result copy: straight into page-locked destinations (the
+// library's host pool), through the bounce buffer otherwise.
+inline void copy_to_host(const Ctx& ctx, void* host_dst, const void* d_src, size_t bytes) {
+    cudaPointerAttributes a{};
+    if (bytes && cudaPointerGetAttributes(&a, host_dst) == cudaSuccess && a.type == cudaMemoryTypeHost) {
+        IGB_CUDA(cudaMemcpyAsync(host_dst, d_src, bytes, cudaMemcpyDeviceToHost, ctx.stream));
+        IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+        return;
+    }
+    cudaGetLastError();  // older runtimes report (and record) an error for unregistered pointers
+    read_back(ctx, host_dst, d_src, bytes);
+}
+
 // IG_TRACE=1: per-operation wall times on stderr (synchronises the stream at
 // every mark; diagnostics only).
 struct Trace {
