@@ -110,8 +110,23 @@ __device__ void table_insert(const Table& T, const int64_t* __restrict__ X, int 
         const uint32_t ru = (uint32_t)(r >> 32), rv = (uint32_t)r;
         const int64_t* a = X + (size_t)ru * k;
         const int64_t* c = X + (size_t)rv * k;
+        // the representative's words in chunks of independent loads: one L2
+        // round trip per chunk instead of one per word (the word-at-a-time
+        // early-exit loop was the largest stall of pair_enum)
+        constexpr int kChunk = 7;
         bool same = true;
-        for (int w = 0; w < k && same; ++w) same = ((__ldg(a + w) & __ldg(c + w)) == b(w));
+        for (int w0 = 0; w0 < k && same; w0 += kChunk) {
+            uint64_t va[kChunk], vc[kChunk];
+#pragma unroll
+            for (int j = 0; j < kChunk; ++j)
+                if (w0 + j < k) {
+                    va[j] = (uint64_t)__ldg(a + w0 + j);
+                    vc[j] = (uint64_t)__ldg(c + w0 + j);
+                }
+#pragma unroll
+            for (int j = 0; j < kChunk; ++j)
+                if (w0 + j < k) same &= ((va[j] & vc[j]) == (uint64_t)b(w0 + j));
+        }
         if (same) return;
         // equal fingerprint, different content: defer to the next level
         atomicAdd(T.collisions, 1ull);
