@@ -74,9 +74,18 @@ __device__ __forceinline__ uint64_t ld_volatile(const unsigned long long* p) {
 
 // Insert candidate (u,v) with fingerprint fp.  `b(w)` yields word w of the
 // candidate; X is the class row matrix used to re-materialise representatives.
+// Per-CTA staging of new representatives (pair_enum): a claim takes a slot in
+// shared memory (a shared atomic, not an L2 round trip on the one hot counter);
+// the CTA reserves its range of the reps list once per tile.
+constexpr int kStageReps = 1024;
+struct RepStage {
+    uint2* reps;          // shared [kStageReps]
+    unsigned int* count;  // shared
+};
+
 template <class WordFn>
 __device__ void table_insert(const Table& T, const int64_t* __restrict__ X, int k, uint32_t u, uint32_t v,
-                             uint64_t fp, WordFn b) {
+                             uint64_t fp, WordFn b, const RepStage* stage = nullptr) {
     const uint64_t rep = (((uint64_t)u << 32) | v) + 1;
     uint64_t s = (fp ^ T.seed) & T.mask;
     for (uint64_t probes = 0; probes <= T.mask; ++probes, s = (s + 1) & T.mask) {
@@ -88,6 +97,20 @@ __device__ void table_insert(const Table& T, const int64_t* __restrict__ X, int 
         if (cur.x == 0) {
             const ulonglong2 old = cas128(slot, make_ulonglong2(0ull, 0ull), make_ulonglong2(fp, rep));
             if (old.x == 0) {
+                if (stage) {
+                    const unsigned int i = atomicAdd(stage->count, 1u);
+                    if (i < (unsigned int)kStageReps) {
+                        stage->reps[i] = make_uint2(u, v);
+                        return;
+                    }
+                    // staging full: straight to the reps list
+                    const unsigned long long idx = atomicAdd(T.count, 1ull);
+                    if (idx < T.limit)
+                        T.reps[idx] = make_uint2(u, v);
+                    else
+                        atomicOr(T.fail, 1);
+                    return;
+                }
                 // warp-aggregated slot in the reps list: the count is one hot address
                 const unsigned int mask = __activemask();
                 const int lane = threadIdx.x & 31, leader = __ffs(mask) - 1;
@@ -160,7 +183,7 @@ constexpr int kLocalProbes = 64;
 // so the word loops unroll; KC <= 16 also keeps the pair's AND in registers
 // for the duplicate check.
 template <int TILE, int KC>
-__global__ void __launch_bounds__(kPairThreads, KC > 0 && KC <= 16 ? 5 : 6)
+__global__ void __launch_bounds__(kPairThreads, KC > 0 && KC <= 17 ? 5 : 6)
 pair_enum(const int64_t* __restrict__ X, uint32_t n, int k_rt, int stride, uint64_t n_tiles, Table T,
           uint64_t tile_begin, uint64_t tile_step) {
     const int k = KC > 0 ? KC : k_rt;
@@ -170,16 +193,38 @@ pair_enum(const int64_t* __restrict__ X, uint32_t n, int k_rt, int stride, uint6
     int64_t* sI = sm + kLocalSlots / 2;
     int64_t* sJ = sI + (size_t)TILE * stride;
     unsigned long long* sKey = reinterpret_cast<unsigned long long*>(sJ + (size_t)TILE * stride);  // k fingerprint keys
+    __shared__ uint2 s_reps[kStageReps];
+    __shared__ unsigned int s_nrep;
+    __shared__ unsigned long long s_base;
+    __shared__ int s_stop;
+    const RepStage stage{s_reps, &s_nrep};
     for (int w = threadIdx.x; w < k; w += kPairThreads) sKey[w] = T.keys[w];
+    if (threadIdx.x == 0) s_nrep = 0;
     for (uint64_t it = blockIdx.x;; it += gridDim.x) {
         const uint64_t t = tile_begin + it * tile_step;  // this rank's tiles: begin, begin + step, ...
-        if (t >= n_tiles) break;
-        // one reader for the failure flag, so the whole block leaves together
-        __shared__ int s_stop;
+        // the previous tile's staged representatives -> one reserved range of
+        // the reps list; one reader for the failure flag, so the whole block
+        // leaves together
         __syncthreads();
-        if (threadIdx.x == 0) s_stop = *(volatile int*)T.fail;
+        if (threadIdx.x == 0) {
+            const unsigned int n = min(s_nrep, (unsigned int)kStageReps);
+            s_base = n ? atomicAdd(T.count, (unsigned long long)n) : 0ull;
+            s_stop = *(volatile int*)T.fail;
+        }
         __syncthreads();
-        if (s_stop) return;
+        {
+            const unsigned int n = min(s_nrep, (unsigned int)kStageReps);
+            for (unsigned int i = threadIdx.x; i < n; i += kPairThreads) {
+                const unsigned long long idx = s_base + i;
+                if (idx < T.limit)
+                    T.reps[idx] = s_reps[i];
+                else
+                    atomicOr(T.fail, 1);
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) s_nrep = 0;
+        if (t >= n_tiles || s_stop) return;
         uint32_t bi, bj;
         tile_of(t, bi, bj);
         const uint32_t i0 = bi * TILE, j0 = bj * TILE;
@@ -241,7 +286,7 @@ pair_enum(const int64_t* __restrict__ X, uint32_t n, int k_rt, int stride, uint6
                 }
             }
             if (dup) continue;
-            table_insert(T, X, k, u, v, f, [&](int w) { return a[w] & b[w]; });
+            table_insert(T, X, k, u, v, f, [&](int w) { return a[w] & b[w]; }, &stage);
         }
     }
 }
