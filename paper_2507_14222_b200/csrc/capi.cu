@@ -760,7 +760,10 @@ void ig_host_free(void* p) {
         return;
     }
     P.cached += it->second;
-    P.free_blocks.emplace(it->second, p);
+    // LIFO among equal capacities: the block just freed is the next one handed
+    // out (its pages are still mapped hot), instead of rotating through all
+    // cached blocks of that class
+    P.free_blocks.emplace_hint(P.free_blocks.lower_bound(it->second), it->second, p);
 }
 
 int ig_evidence(ig_ctx* ctx, const ig_model* m, const int64_t* tests, size_t nt, uint32_t L, int64_t* A, int64_t* N) {
