@@ -139,3 +139,34 @@ def test_fit_fuzz_small_shapes(api):
         A, N = m.evidence(T)
         assert np.array_equal(A, oracle.fused_score(ref.pure[0].words, ref.pure[0].scores, T)), case
         assert np.array_equal(N, oracle.fused_score(ref.pure[1].words, ref.pure[1].scores, T)), case
+
+
+def _canonical_pair_set(X):
+    """Distinct non-empty {X[i] & X[j] : i < j} ∪ {X[i]} in words::less order
+    (unsigned lexicographic over words 0..K-1, bitpack.hpp:61-68)."""
+    n, k = X.shape
+    iu, ju = np.triu_indices(n, 1)
+    c = np.concatenate([X & X, X[iu] & X[ju]]).view(np.uint64)
+    c = c[(c != 0).any(axis=1)]
+    c = np.unique(c, axis=0)  # lexicographic over unsigned columns
+    return c.view(np.int64)
+
+
+@pytest.mark.parametrize("word0_values,expect", [(64, "runs"), (1, "one run")])
+def test_canonical_order_long_and_short_key_runs(api, word0_values, expect):
+    """> 24,576 candidates, K = 66: the canonical sort (csrc/sort.cu) takes its
+    MSD branch (stable sort on the first packed rank key, then ranks by
+    counting inside runs of equal first key) when word 0 leaves short runs, and
+    its LSD fallback when the first 64 rank bits are constant (one run of every
+    candidate).  Both must return exactly the reference's order."""
+    rng = np.random.default_rng(7 + word0_values)
+    n, k = 250, 66
+    X = np.empty((n, k), np.uint64)
+    X[:, 1:64] = np.uint64(0x8000000000000001)
+    X[:, 0] = rng.integers(1, 2**63, size=word0_values, dtype=np.uint64)[rng.integers(0, word0_values, size=n)]
+    X[:, 64:] = rng.integers(0, 2**63, size=(n, 2), dtype=np.uint64) | rng.integers(0, 2**63, size=(n, 2), dtype=np.uint64) << np.uint64(1)
+    X = X.view(np.int64)
+    want = _canonical_pair_set(X)
+    assert want.shape[0] > 24576
+    cs = api.enumerate_candidates(api.PackedMatrix(X, 64 * k))
+    assert np.array_equal(cs.patterns.words, want)
