@@ -80,12 +80,14 @@ __global__ void cell_codes(const double* __restrict__ values, const int32_t* __r
 
 // Block-level distinct codes of one column chunk (shared-memory hash), appended
 // to a global (column, code) list.  grid = (chunks, n_feat).
-constexpr int kDistinctRows = 2048;
-constexpr int kDistinctSlots = 4096;
+// 8,192-row chunks (128 KB of slots, dynamic shared memory): fewer chunks,
+// fewer repeats of a column's codes across chunks for the host to merge.
+constexpr int kDistinctRows = 8192;
+constexpr int kDistinctSlots = 16384;
 __global__ void __launch_bounds__(256)
 distinct_codes(const int64_t* __restrict__ codes, size_t n, int64_t* __restrict__ out_code,
                int32_t* __restrict__ out_col, unsigned long long* __restrict__ out_count) {
-    __shared__ int64_t slots[kDistinctSlots];
+    extern __shared__ int64_t slots[];
     const int f = blockIdx.y;
     const size_t r0 = (size_t)blockIdx.x * kDistinctRows;
     for (int i = threadIdx.x; i < kDistinctSlots; i += blockDim.x) slots[i] = kFreeSlot;
@@ -386,7 +388,11 @@ void encode_training_dev(Ctx& ctx, const ig_columns& c, ig_encoding& e) {
     DevBuf lcode(cap * 8, ctx.stream), lcol(cap * 4, ctx.stream), lcnt(8, ctx.stream);
     IGB_CUDA(cudaMemsetAsync(lcnt.p, 0, 8, ctx.stream));
     if (d.n && d.n_feat)
-        IGB_LAUNCH(ctx, distinct_codes, dim3((unsigned)chunks, (unsigned)d.n_feat), 256, 0, d.codes.as<int64_t>(), d.n,
+        IGB_CUDA(cudaFuncSetAttribute(distinct_codes, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kDistinctSlots * (int)sizeof(int64_t)));
+    if (d.n && d.n_feat)
+        IGB_LAUNCH(ctx, distinct_codes, dim3((unsigned)chunks, (unsigned)d.n_feat), 256,
+                   kDistinctSlots * sizeof(int64_t), d.codes.as<int64_t>(), d.n,
                    lcode.as<int64_t>(), lcol.as<int32_t>(), lcnt.as<unsigned long long>());
     unsigned long long m = 0;
     read_back(ctx, &m, lcnt.p, 8);
