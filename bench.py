@@ -471,8 +471,21 @@ def run_b200(args):
         dist.destroy_process_group()
 
 
+def _all_host_threads():
+    """The CPU reference (oracle/_ref, OpenMP) runs with every host thread this
+    process may use.  torch.distributed.run exports OMP_NUM_THREADS=1 to each
+    rank, which would time the reference arm single-threaded under torchrun;
+    libgomp reads the variable when oracle/_ref is loaded, so set it first."""
+    try:
+        n = len(os.sched_getaffinity(0))
+    except AttributeError:
+        n = os.cpu_count() or 1
+    os.environ["OMP_NUM_THREADS"] = str(n)
+
+
 def main():
     args = parse_args()
+    _all_host_threads()
     if args.impl == "reference":
         run_reference(args)
     else:
