@@ -249,6 +249,18 @@ int ig_fit_evidence_encoded(ig_ctx* ctx, const ig_encoding* train, const ig_enco
 int ig_fit_evidence_encoded_host(ig_ctx* ctx, const ig_encoding* train, const ig_encoding* tests,
                                  const ig_kernel_config* cfg, ig_model** out, int64_t* A, int64_t* N);
 
+/* ---------------------------------------------------------------- infer (host arithmetic)
+ * SPEC.md:434-452 (spec-only in the reference).  fit_normal_stats: mean and
+ * population std of the strictly positive N (batch fit); fewer than
+ * two -> (0, 0).  classify: R2 A=N=0 -> attack (reg 3), R1 A>=N -> attack
+ * (reg 1), R3 N < mu - r*sigma -> attack (reg 4), else normal (reg 2).  The
+ * squared deviations and the R3 threshold round as single FMAs, as the
+ * reference's -march=native build (proj/CMakeLists.txt:10-18) contracts them.
+ * label / regulation may be NULL.                                          */
+int ig_fit_normal_stats(const int64_t* n_vals, size_t n, double* mu, double* sigma);
+int ig_classify(const int64_t* A, const int64_t* N, size_t n, double mu, double sigma, double r, uint8_t* label,
+                uint8_t* regulation);
+
 /* ---------------------------------------------------------------- archive / explain
  * SURVEY.md §8(f) ranks 1-2.  ModelArchive: schema
  * text with exact hex-float statistics + vocabulary in bit order + the pure

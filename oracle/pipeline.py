@@ -20,11 +20,22 @@ Plus the spec-only infer/eval arithmetic.
 """
 from __future__ import annotations
 
+import ctypes
+import ctypes.util
 import math
 import re
 from dataclasses import dataclass, field
 
 import numpy as np
+
+# Correctly rounded fused multiply-add (C99 fma from libm; Python 3.12 has no
+# math.fma).  The reference is compiled with -march=native
+# (proj/CMakeLists.txt:10-18): GCC contracts `ss += d * d` (pipeline.cpp:159)
+# into vfmadd231sd, so the standard deviation rounds once per term.
+_libm = ctypes.CDLL(ctypes.util.find_library("m") or "libm.so.6")
+_libm.fma.restype = ctypes.c_double
+_libm.fma.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.c_double]
+fma = _libm.fma
 
 
 class DataError(Exception):
@@ -198,7 +209,7 @@ def infer_schema(header, rows, label_column, attack_values=(), normal_values=(),
             if not cell:
                 continue
             d = parse_double_strict(cell) - m
-            ss += d * d
+            ss = fma(d, d, ss)  # the reference's -march=native build contracts pipeline.cpp:159
         kind.append("numeric"), mean.append(m), std.append(math.sqrt(ss / parsed))
     sch = Schema(list(header), kind, mean, std, li, list(attack_values), list(normal_values), decimals)
     for r in rows:
@@ -303,7 +314,7 @@ def fit_normal_stats(nvals) -> tuple[float, float]:
     mu = s / len(pos)
     ss = 0.0
     for v in pos:
-        ss += (v - mu) * (v - mu)
+        ss = fma(v - mu, v - mu, ss)  # as the FMA-contracted restatement in oracle/ref_shim.cpp
     return mu, math.sqrt(ss / len(pos))
 
 
@@ -313,7 +324,7 @@ def classify(a: int, n: int, mu: float, sigma: float, r: float) -> tuple[int, in
         return 1, 3
     if a >= n:
         return 1, 1
-    if float(n) < mu - r * sigma:
+    if float(n) < fma(-r, sigma, mu):  # mu - r*sigma, contracted like oracle/ref_shim.cpp's build
         return 1, 4
     return 0, 2
 

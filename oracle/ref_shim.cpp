@@ -236,7 +236,9 @@ NormalStats fit_normal_stats(const std::vector<std::int64_t>& nvals) {
     for (double v : pos) sum += v;
     st.mu = sum / static_cast<double>(pos.size());
     double ss = 0;
-    for (double v : pos) ss += (v - st.mu) * (v - st.mu);
+    // Written as the FMA the -march=native build (proj/CMakeLists.txt:10-18)
+    // contracts this loop to, so the rounding does not depend on compiler flags.
+    for (double v : pos) ss = std::fma(v - st.mu, v - st.mu, ss);
     st.sigma = std::sqrt(ss / static_cast<double>(pos.size()));
     return st;
 }
@@ -251,7 +253,7 @@ inline void classify(std::int64_t a, std::int64_t n, const NormalStats& st, doub
     } else if (a >= n) {
         *label = 1;
         *reg = 1;
-    } else if (static_cast<double>(n) < st.mu - r * st.sigma) {
+    } else if (static_cast<double>(n) < std::fma(-r, st.sigma, st.mu)) {  // mu - r*sigma, contracted
         *label = 1;
         *reg = 4;
     } else {

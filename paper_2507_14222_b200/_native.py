@@ -59,6 +59,8 @@ SIGNATURES = [
     ("ig_count_support_rows", C.c_int, [vp, p64, sz, u32, p64, sz, u32, p64]),
     ("ig_score_patterns", C.c_int, [vp, vp]),
     ("ig_total_score", C.c_int, [p64, sz, p64]),
+    ("ig_fit_normal_stats", C.c_int, [p64, sz, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    ("ig_classify", C.c_int, [p64, p64, sz, C.c_double, C.c_double, C.c_double, pu8, pu8]),
     ("ig_candidates_count", sz, [vp]),
     ("ig_candidates_logical_len", u32, [vp]),
     ("ig_candidates_copy", C.c_int, [vp, vp, p64, p64, p64]),

@@ -618,30 +618,29 @@ def fit_evidence_encoded(train: Encoding, tests: Encoding, config: Optional[Kern
 
 # ---------------------------------------------------------------- infer / eval (host arithmetic)
 def fit_normal_stats(nvals) -> tuple[float, float]:
-    """mean / population std of strictly positive N; <2 positives -> (0, 0)."""
-    pos = [float(v) for v in np.asarray(nvals).tolist() if v > 0]
-    if len(pos) < 2:
-        return 0.0, 0.0
-    s = 0.0
-    for v in pos:
-        s += v
-    mu = s / len(pos)
-    ss = 0.0
-    for v in pos:
-        ss += (v - mu) * (v - mu)
-    return mu, math.sqrt(ss / len(pos))
+    """mean / population std of strictly positive N; <2 positives -> (0, 0)
+    (ig_fit_normal_stats: host C++, FMA-rounded like the reference's native build)."""
+    nv = np.ascontiguousarray(nvals, np.int64)
+    mu, sg = C.c_double(), C.c_double()
+    st = lib.ig_fit_normal_stats(_p64(nv), nv.shape[0], C.byref(mu), C.byref(sg))
+    if st:
+        _raise(st)
+    return mu.value, sg.value
 
 
 def classify(A, Nv, mu: float, sigma: float, r: float = 0.568):
-    """SPEC.md:444-452 vectorised. Returns (label, regulation) with regulation
+    """SPEC.md:444-452 (ig_classify). Returns (label, regulation) with regulation
     1 = R1-attack, 2 = R1-normal, 3 = R2, 4 = R3."""
-    A = np.asarray(A, np.int64)
-    Nv = np.asarray(Nv, np.int64)
-    r2 = (A == 0) & (Nv == 0)
-    r1 = ~r2 & (A >= Nv)
-    r3 = ~r2 & ~r1 & (Nv.astype(np.float64) < mu - r * sigma)
-    label = (r1 | r2 | r3).astype(np.uint8)
-    reg = np.where(r2, 3, np.where(r1, 1, np.where(r3, 4, 2))).astype(np.uint8)
+    A = np.ascontiguousarray(A, np.int64)
+    Nv = np.ascontiguousarray(Nv, np.int64)
+    if A.shape != Nv.shape:
+        raise ValueError("classify: A and N lengths differ")
+    label = np.empty(A.shape[0], np.uint8)
+    reg = np.empty(A.shape[0], np.uint8)
+    st = lib.ig_classify(_p64(A), _p64(Nv), A.shape[0], float(mu), float(sigma), float(r),
+                         label.ctypes.data_as(N.pu8), reg.ctypes.data_as(N.pu8))
+    if st:
+        _raise(st)
     return label, reg
 
 

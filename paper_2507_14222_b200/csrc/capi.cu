@@ -633,6 +633,21 @@ int ig_total_score(const int64_t* s, size_t n, int64_t* out) {
     });
 }
 
+int ig_fit_normal_stats(const int64_t* n_vals, size_t n, double* mu, double* sigma) {
+    return guard(nullptr, [&] {
+        if ((!n_vals && n) || !mu || !sigma) fail(IG_E_INVALID_ARG, "fit_normal_stats: null pointer");
+        igb::fit_normal_stats(n_vals, n, mu, sigma);
+    });
+}
+
+int ig_classify(const int64_t* A, const int64_t* N, size_t n, double mu, double sigma, double r, uint8_t* label,
+                uint8_t* regulation) {
+    return guard(nullptr, [&] {
+        if (n && (!A || !N)) fail(IG_E_INVALID_ARG, "classify: null pointer");
+        igb::classify(A, N, n, mu, sigma, r, label, regulation);
+    });
+}
+
 size_t ig_candidates_count(const ig_candidates* c) { return c ? c->rows.n : 0; }
 uint32_t ig_candidates_logical_len(const ig_candidates* c) { return c ? c->rows.L : 0; }
 

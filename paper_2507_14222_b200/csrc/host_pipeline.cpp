@@ -177,7 +177,10 @@ void infer_schema(const ig_table& t, const std::string& label, const std::vector
             auto cell = t.cell(r, j);
             if (cell.empty()) continue;
             const double d = *parse_double_strict(cell) - s.mean[j];
-            ss += d * d;
+            // The reference is built with -march=native (proj/CMakeLists.txt:10-18), so
+            // GCC contracts `ss += d * d` (pipeline.cpp:159) into one FMA (vfmadd231sd,
+            // checked in oracle/_ref's infer_schema).  State that rounding explicitly.
+            ss = std::fma(d, d, ss);
         }
         s.sd[j] = std::sqrt(ss / static_cast<double>(parsed));
     }
@@ -263,6 +266,55 @@ std::string format_units(int64_t units, int decimals) {
         out += f;
     }
     return out;
+}
+
+// SPEC.md:434-442 (infer, spec-only): mean and population standard deviation
+// of the strictly positive N values in batch order; fewer than two -> (0, 0).
+// Sums are sequential IEEE doubles; the squared deviations accumulate as one
+// fma per term, the rounding the reference's -march=native build gives such a
+// loop (the same contraction as infer_schema's, pipeline.cpp:159).
+void fit_normal_stats(const int64_t* n_vals, size_t n, double* mu, double* sigma) {
+    size_t cnt = 0;
+    double sum = 0.0;
+    for (size_t i = 0; i < n; ++i)
+        if (n_vals[i] > 0) {
+            sum += static_cast<double>(n_vals[i]);
+            ++cnt;
+        }
+    *mu = 0.0;
+    *sigma = 0.0;
+    if (cnt < 2) return;
+    const double m = sum / static_cast<double>(cnt);
+    double ss = 0.0;
+    for (size_t i = 0; i < n; ++i)
+        if (n_vals[i] > 0) {
+            const double d = static_cast<double>(n_vals[i]) - m;
+            ss = std::fma(d, d, ss);
+        }
+    *mu = m;
+    *sigma = std::sqrt(ss / static_cast<double>(cnt));
+}
+
+// R2 (A = N = 0) -> attack; R1 (A >= N) -> attack; R3
+// (N < mu - r*sigma, the threshold rounded once as the contracted build does)
+// -> attack; else normal.  reg: 1 = R1-attack, 2 = normal, 3 = R2, 4 = R3.
+void classify(const int64_t* A, const int64_t* N, size_t n, double mu, double sigma, double r, uint8_t* label,
+              uint8_t* reg) {
+    const double thr = std::fma(-r, sigma, mu);
+    for (size_t i = 0; i < n; ++i) {
+        uint8_t l, g;
+        if (A[i] == 0 && N[i] == 0) {
+            l = 1, g = 3;
+        } else if (A[i] >= N[i]) {
+            l = 1, g = 1;
+        } else if (static_cast<double>(N[i]) < thr) {
+            l = 1, g = 4;
+        } else {
+            l = 0, g = 2;
+        }
+        if (label) label[i] = l;
+        if (reg) reg[i] = g;
+    }
 }
 
 }  // namespace igb

@@ -72,5 +72,8 @@ void infer_schema(const ig_table& t, const std::string& label, const std::vector
 void build_columns(const ig_table& t, const ig_schema& s, bool with_labels, ig_columns& out);
 std::string format_units(int64_t units, int decimals);
 std::vector<std::string> split_csv_list(const char* s);
+void fit_normal_stats(const int64_t* n_vals, size_t n, double* mu, double* sigma);
+void classify(const int64_t* A, const int64_t* N, size_t n, double mu, double sigma, double r, uint8_t* label,
+              uint8_t* reg);
 
 }  // namespace igb

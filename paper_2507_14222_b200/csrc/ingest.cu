@@ -17,7 +17,9 @@
 //   number goes back to the host's from_chars; everything else is text.
 // * statistics: one warp per numeric column streams the training rows and lane
 //   0 adds them in row order (sum, then sum of squared deviations) with _rn
-//   intrinsics, exactly the host's sequential double sums; sqrt is _rn.
+//   intrinsics, exactly the host's sequential double sums; the squared
+//   deviations accumulate as fma(d, d, ss), the rounding of the reference's
+//   -march=native build (GCC contracts pipeline.cpp:159); sqrt is _rn.
 // * categorical ids and the label mapping follow first appearance in row
 //   order (an exact-content hash table records each string's first row), as
 //   build_columns assigns them.
@@ -304,7 +306,7 @@ __global__ void column_stats(const double* __restrict__ val, const uint8_t* __re
             const double y = __shfl_sync(0xffffffffu, x, l);
             if (lane == 0 && ((m >> l) & 1u)) {
                 const double d = __dsub_rn(y, mu);
-                ss = __dadd_rn(ss, __dmul_rn(d, d));
+                ss = __fma_rn(d, d, ss);  // the reference's contracted ss += d * d (host_pipeline.cpp)
             }
         }
     }

@@ -106,7 +106,7 @@ def test_decision_table_property():
     sg = float(rng.uniform(0, 20))
     r = float(rng.uniform(0, 2))
     label, reg = api.classify(A, Nv, mu, sg, r)
-    closed = (A >= Nv) | (Nv.astype(float) < mu - r * sg)
+    closed = (A >= Nv) | (Nv.astype(float) < opipe.fma(-r, sg, mu))
     assert np.array_equal(label.astype(bool), closed)
     idx = rng.integers(0, n, 2000)
     for i in idx:
@@ -160,3 +160,51 @@ def test_schema_text_round_trip():
     for j in range(3):
         assert s.column(j) == s2.column(j)
     assert s2.label_index == 2
+
+
+def _fma_sensitive_csv(seed=159, rows=3000, cols=24):
+    """Numeric columns whose population std differs between `ss += d*d` rounded
+    twice and the reference's FMA-contracted loop (pipeline.cpp:159)."""
+    rng = np.random.default_rng(seed)
+    lines = [",".join(f"c{j}" for j in range(cols)) + ",label"]
+    scale = 10.0 ** rng.integers(-3, 7, cols)
+    for i in range(rows):
+        v = rng.normal(0, 1, cols) * scale + scale * 3.1
+        lines.append(",".join(repr(float(x)) for x in v) + ("," + ("normal" if i % 3 else "neptune")))
+    return ("\n".join(lines) + "\n").encode()
+
+
+def test_schema_std_rounds_like_the_reference():
+    """infer_schema's std: the product's host pipeline and the Python restatement
+    equal oracle/_ref (the reference's own pipeline.cpp, FMA-contracted like its
+    -march=native build) bit for bit, on columns where the unfused sum differs."""
+    from oracle import ref
+    from paper_2507_14222_b200 import api
+    if not ref.available():
+        pytest.skip("oracle/_ref not built (needs /root/reference)")
+    csv = _fma_sensitive_csv()
+    r = ref.run(csv, decimals=1, train_rows=3000, stages=0)
+    s = api.infer_schema(api.read_csv(csv), "label", decimals=1)
+    hdr, rows = opipe.read_csv(csv)
+    ps = opipe.infer_schema(hdr, rows, "label", decimals=1)
+    unfused_differs = 0
+    for j in range(len(hdr) - 1):
+        _, mean, sd = s.column(j)
+        assert mean == r.mean[j] and sd == r.std[j], j
+        assert ps.mean[j] == r.mean[j] and ps.std[j] == r.std[j], j
+        vals = [float(row[j]) for row in rows]
+        ss = 0.0
+        for v in vals:
+            ss += (v - mean) * (v - mean)
+        unfused_differs += math.sqrt(ss / len(vals)) != sd
+    assert unfused_differs > 0  # the fixture discriminates the two roundings
+
+
+def test_normal_stats_fma_rounding():
+    """fit_normal_stats: the product's C++ equals the Python
+    restatement bit for bit (both FMA-rounded as the reference's native build)."""
+    from paper_2507_14222_b200 import api
+    rng = np.random.default_rng(434)
+    for _ in range(50):
+        nv = rng.integers(-5, 1 << 40, int(rng.integers(0, 2000)))
+        assert api.fit_normal_stats(nv) == opipe.fit_normal_stats(nv.tolist())
