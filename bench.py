@@ -14,10 +14,15 @@ CSV parsing and schema statistics (host) are reported separately (`host_prep_s`)
 `value`  — seconds per step with the parsed columns already resident in HBM.
 `e2e`    — the same step through the public C-ABI with HOST columns: H2D of the
            parsed columns and D2H of A/N inside the timed region.
-`roofline` — the matcher (kernel 6, the dominant kernel), algorithmic
-           word-tests / its CUDA-event duration vs the measured LOP3 peak.
+`roofline` — per hot kernel (pair_enum, support, cover, matcher): exact useful
+           64-bit word-ANDs / CUDA-event kernel time vs the measured LOP3 peak,
+           from one extra step with the classes serialised; the top-level entry
+           is the kernel with the most time (the matcher).
+`scale_leg` — BASELINE.json configs[3] (the same records at 80/20), timed like
+           `value`: the strong-scaling number of the driver's N-GPU runs.
 `cpu_baseline` — the reference (oracle/_ref: the reference's own C++ +
-           restated mine/purify/infer) on this box's host cores, bounded sample.
+           restated mine/purify/infer) on this box's host cores: full fit, a
+           bounded slice of the matcher scaled to all test rows.
 
 `--impl reference` runs only the reference CPU path (rank 0) and prints its line.
 """
@@ -48,7 +53,8 @@ def parse_args():
     ap.add_argument("--ratio", type=int, default=1, help="train tenths (1 = 10/90)")
     ap.add_argument("--seed", type=int, default=2507)
     ap.add_argument("--decimals", type=int, default=1)
-    ap.add_argument("--cpu-sample-tests", type=int, default=400)
+    ap.add_argument("--scale-ratio", type=int, default=8, help="train tenths of the scale leg (0 = off)")
+    ap.add_argument("--cpu-sample-tests", type=int, default=2000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -96,9 +102,9 @@ class Clocks:
                 "reasons": reasons, "samples": len(samples)}
 
 
-def ncu_summary(path):
-    """`traffic` (dram read+write bytes per launch) and pipe utilisation of the
-    matcher from the committed `ncu --set full` capture of the same kernel."""
+def ncu_summary(path, launches=1):
+    """`traffic` (DRAM read + write bytes per launch) and pipe utilisation from
+    the committed `ncu --set full` capture of the same kernel (one launch)."""
     import csv
     if not os.path.exists(path):
         return {}
@@ -111,21 +117,69 @@ def ncu_summary(path):
                        "lts__throughput.avg.pct_of_peak_sustained_elapsed",
                        "l1tex__throughput.avg.pct_of_peak_sustained_active")}
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    tscale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}
     try:
         traffic = sum(get[k][0] * scale.get(get[k][1], 1) for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
         return {"traffic": traffic,
-                "int_pipe_frac": get["sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"][0] / 100,
                 "ncu": {"source": os.path.relpath(path, ROOT),
                         "alu_pipe_pct": get["sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"][0],
                         "issue_active_pct": get["smsp__issue_active.avg.pct_of_peak_sustained_active"][0],
                         "l2_throughput_pct": get["lts__throughput.avg.pct_of_peak_sustained_elapsed"][0],
-                        "duration_ms_cold": get["gpu__time_duration.sum"][0],
                         "l1tex_throughput_pct": get.get("l1tex__throughput.avg.pct_of_peak_sustained_active",
                                                         (None,))[0],
-                        "note": "L1 and issue bound: every lane loads a different posting word, and each AND "
-                                "costs a shuffle, an address, a load and a vote besides its LOP3"}}
+                        "duration_ms_cold": get["gpu__time_duration.sum"][0] *
+                        tscale.get(get["gpu__time_duration.sum"][1], 1.0)}}
     except KeyError:
         return {}
+
+
+KERNEL_INFO = {
+    "pair_enum": ("pair_enum (kernels 2+3: pair AND + fingerprint + tile/device dedup)",
+                  "SURVEY.md §8(d) (2): K word-ANDs per pair u <= v of the class's distinct canonical rows",
+                  "r02_ncu_raw_pair_enum.csv"),
+    "support": ("grouped_scan<kSupport> (kernel 5: f_c(b) by posting AND + POPC)",
+                "posting word-ANDs on live list words (counted exactly by a counting re-run)",
+                "r02_ncu_raw_grouped_scan_support.csv"),
+    "cover": ("grouped_scan<kCover> (kernel 4: opposite-class subset filter, warp-vote early exit)",
+              "posting word-ANDs on live list words up to the first covering word (counted exactly)",
+              "r02_ncu_raw_grouped_scan_cover.csv"),
+    "match": ("grouped_scan<kMatch> (kernel 6: matcher, difference-array runs)",
+              "posting word-ANDs on live list words (counted exactly)",
+              "r02_ncu_raw_grouped_scan_match.csv"),
+}
+
+
+def kernel_rooflines(diag, peak_words, lop3_s, step_ms, horiz):
+    """achieved = useful 64-bit word-ANDs / kernel time against
+    the measured LOP3 peak (2 LOP3.32 per word-AND).  The useful work is what
+    the kernel actually performs (the posting form skips the reference's dense
+    (b & x) == b tests; that dense W is kept only as `effective_rate`)."""
+    kernels = []
+    for name, (label, work_def, ncu_file) in KERNEL_INFO.items():
+        kms, work, nl = diag[name]
+        if nl == 0 or kms <= 0:
+            continue
+        achieved = work / (kms * 1e-3) / 1e9
+        e = {"kernel": label, "id": name, "launches_per_step": nl, "ms_per_step": kms,
+             "ms_per_launch": kms / nl, "useful_word_ands_per_step": work, "work_definition": work_def,
+             "achieved": achieved, "peak": peak_words, "unit": "Gword/s", "frac": achieved / peak_words,
+             "share_of_step": kms / step_ms}
+        e.update(ncu_summary(os.path.join(ROOT, "profiles", ncu_file), nl))
+        kernels.append(e)
+    top = max(kernels, key=lambda e: e["ms_per_step"])
+    out = {"bound": "int", "kernel": top["kernel"], "achieved": top["achieved"], "peak": peak_words,
+           "unit": "Gword/s", "frac": top["frac"], "traffic": top.get("traffic"),
+           "peak_source": f"measured LOP3 micro-kernel {lop3_s / 1e12:.2f} T LOP3.32/s (diag.cu) / 2 per 64-bit AND",
+           "timing": "one extra step with diagnostics on: classes serialised, CUDA events around each hot launch "
+                     "on its stream; work from a counting re-run of the same launch",
+           "kernels": kernels}
+    m = diag["match"]
+    if m[2]:
+        out["effective_rate"] = {
+            "kernel": "matcher", "dense_word_tests_per_step": horiz, "Gword_per_s": horiz / (m[0] * 1e-3) / 1e9,
+            "note": "SURVEY.md §8(d) (6) W = (|P+|+|P-|) * n_test * K, the reference's dense (b & x) == b word "
+                    "tests, over the matcher's time: an effective rate, not a hardware fraction"}
+    return out
 
 
 def workload_config(args, n_train, n_test, extra=None):
@@ -139,41 +193,45 @@ def workload_config(args, n_train, n_test, extra=None):
     return cfg
 
 
-def cpu_reference(csv: bytes, args, sample_tests: int):
-    """Time the reference CPU path on this host; matcher on `sample_tests` rows,
-    extrapolated linearly to all test rows (fused_score is linear in n_test)."""
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_reference(csv: bytes, args, sample_tests: int, step: int = 0):
+    """One step of the reference's own CPU path (oracle/_ref: proj/src/*.cpp
+    compiled by oracle/Makefile + the restated mine/purify/infer) on this host,
+    every host thread: encode + full fit of all training rows, then tokenise +
+    match a bounded slice of the test rows, [step * S, (step + 1) * S) mod
+    n_test, so successive steps measure different parts of the test set.  The
+    matcher is linear in the test rows (one independent fused_score per row,
+    kernels.cpp:156-178), so the full step is the fit plus the slice's matcher
+    time scaled to all test rows.  No fallback: the reference must be built."""
     from oracle import ref
-    if ref.available():
-        kind = "reference"
-        t0 = time.perf_counter()
-        r = ref.run(csv, decimals=args.decimals, ratio_k=args.ratio, backend="parallel-cpu",
-                    test_limit=sample_tests, stages=2)
-        wall = time.perf_counter() - t0
-        n_test_full = args.rows - args.ratio * args.rows // 10
-        t = r.times
-        scale = n_test_full / max(1, r.n_test)
-        step = t["encode"] + t["enumerate"] + t["support"] + t["purify"] + (t["test_encode"] + t["match"]) * scale
-        cores = ref.lib().igref_max_threads()
-        sample = (f"full encode+fit ({r.n_train} train rows) + tokenise/match {r.n_test} of {n_test_full} test rows, "
-                  f"matcher extrapolated x{scale:.1f}; wall {wall:.1f}s")
-        return {"value": step, "unit": "s", "cores": cores, "kind": kind, "sample": sample,
-                "phases_s": {k: round(v, 4) for k, v in t.items()}}
-    # plain-C oracle port (no reference build on this box)
-    import numpy as np
-    from oracle import oracle
-    from paper_2507_14222_b200 import api
-    r = api.train_and_score(csv, decimals=args.decimals, ratio_k=args.ratio)
-    Xa, Xn, T = r.train.matrix(0), r.train.matrix(1), r.test.matrix(2)
+    if not ref.available():
+        raise SystemExit("oracle/_ref/libigref.so missing: build it with `make -C oracle ref` where "
+                         "/root/reference exists (it ships to the GPU box in the snapshot)")
+    n_test_full = args.rows - args.ratio * args.rows // 10
+    S = max(1, min(sample_tests, n_test_full))
+    off = (step * S) % n_test_full
     t0 = time.perf_counter()
-    f = oracle.fit(Xa, Xn)
-    t1 = time.perf_counter()
-    idx = np.arange(min(sample_tests, T.shape[0]))
-    oracle.fused_score(f.pure[0].words, f.pure[0].scores, T[idx])
-    oracle.fused_score(f.pure[1].words, f.pure[1].scores, T[idx])
-    t2 = time.perf_counter()
-    scale = T.shape[0] / max(1, len(idx))
-    return {"value": (t1 - t0) + (t2 - t1) * scale, "unit": "s", "cores": os.cpu_count(), "kind": "port",
-            "sample": f"oracle fit + matcher on {len(idx)} test rows x{scale:.1f}"}
+    r = ref.run(csv, decimals=args.decimals, ratio_k=args.ratio, backend="parallel-cpu",
+                test_offset=off, test_limit=S, stages=2)
+    wall = time.perf_counter() - t0
+    t = r.times
+    scale = n_test_full / max(1, r.n_test)
+    full = t["encode"] + t["enumerate"] + t["support"] + t["purify"] + (t["test_encode"] + t["match"]) * scale
+    cores = ref.lib().igref_max_threads()
+    return {"value": full, "unit": "s", "cores": cores, "kind": "reference", "wall_s": wall,
+            "sample": (f"encode + full fit of all {r.n_train} training rows, then tokenise + match test rows "
+                       f"[{off}, {off + r.n_test}) of {n_test_full} (matcher scaled x{scale:.2f} to all test rows)"),
+            "cpu": cpu_model(), "isa": "oracle/_ref built -march=x86-64-v3 (AVX2, FMA, POPCNT)",
+            "phases_s": {k: round(v, 4) for k, v in t.items()}, "matched_rows": int(r.n_test)}
 
 
 def run_reference(args):
@@ -183,19 +241,30 @@ def run_reference(args):
     from paper_2507_14222_b200 import synth
     csv = synth.nsl_csv(args.rows, seed=args.seed)
     n_train = args.ratio * args.rows // 10
-    vals = []
-    for i in range(args.warmup + args.steps):
-        # warm-up steps use a smaller matcher sample; timed steps the full bounded sample
-        r = cpu_reference(csv, args, 8 if i < args.warmup else args.cpu_sample_tests)
-        if i >= args.warmup:
-            vals.append(r["value"])
+    n_test = args.rows - n_train
+    # warm-up: the reference on the first 2,000 records (thread pool, page cache, allocator)
+    small = b"\n".join(csv.split(b"\n")[:2001]) + b"\n"
+    for _ in range(args.warmup):
+        from oracle import ref
+        ref.run(small, decimals=args.decimals, ratio_k=8, backend="parallel-cpu")
+    vals, walls, matched = [], [], 0
+    for i in range(args.steps):
+        r = cpu_reference(csv, args, args.cpu_sample_tests, step=i)
+        vals.append(r["value"])
+        walls.append(r["wall_s"])
+        matched += r["matched_rows"]
     v = statistics.median(vals)
     line = {"metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "strong",
-            "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-            "config": workload_config(args, n_train, args.rows - n_train), "impl": "reference",
-            "cpu_baseline": {**{k: r[k] for k in ("unit", "cores", "kind", "sample")}, "value": v,
-                             "steps_s": vals},
+            "warmup": args.warmup, "ms_per_step": statistics.median(walls) * 1e3, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": workload_config(args, n_train, n_test), "impl": "reference",
+            "value_definition": ("full C3 step time: encode + fit measured in full every step, the matcher measured "
+                                 "on a rotating slice of the test rows and scaled linearly; ms_per_step is the "
+                                 "measured wall time of one such step"),
+            "cpu_baseline": {**{k: r[k] for k in ("unit", "cores", "kind", "cpu", "isa")}, "value": v,
+                             "sample": (f"{args.steps} steps, each encode + full fit + a {args.cpu_sample_tests}-row "
+                                        f"test slice (rotating; {matched} of {n_test} test rows matched over the run)"),
+                             "steps_s": vals, "steps_wall_s": walls},
             "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -320,37 +389,22 @@ def run_b200(args):
         ms = float(t.item())
     phases = model.phase_ms()
 
-    # ---- roofline of the dominant kernel: the matcher (kernel 6, grouped_scan<kMatch>)
+    # ---- roofline, per hot kernel: one more step with diagnostics on (classes
+    # one after the other, every hot launch timed with CUDA events on its own
+    # stream, then re-run in a counting variant for its exact useful work)
     P = [model.count(0, 1), model.count(1, 1)]
     K = (tenc.logical_len + 63) // 64
+    horiz = (P[0] + P[1]) * n_test * K  # dense word tests of the reference
+    enc = model = tenc = None
     ctx.set_diagnostics(True)
-    reps = 3
-    for _ in range(reps):
-        model.evidence_device(tenc.device_rows(2), n_test, dA.data_ptr(), dN.data_ptr())
-    kms, words, nl = ctx.diag_match()
+    torch.cuda.synchronize()
+    enc, model, tenc = step_resident()
+    torch.cuda.synchronize()
+    diag = {name: ctx.diag_kernel(name) for name in api.Context.DIAG_KERNELS}
     ctx.set_diagnostics(False)
     lop3_s, popc_s = ctx.int_peaks()
-    peak_words = lop3_s / 2 / 1e9   # a 64-bit word AND = 2 LOP3.32
-    # the matcher's algorithmic work is W = (|P+| + |P-|) * n_test * K
-    # word tests (the reference's dense (b & x) == b), per evidence call
-    horiz = (P[0] + P[1]) * n_test * K
-    launches_per_call = max(nl // reps, 1)
-    ms_per_call = kms / reps
-    achieved = horiz / (ms_per_call * 1e-3) / 1e9
-    roofline = {"bound": "int", "kernel": "grouped_scan<kMatch> (matcher, kernel 6)", "achieved": achieved,
-                "peak": peak_words, "unit": "Gword/s", "frac": achieved / peak_words, "traffic": None,
-                "frac_is_effective": True,
-                "algorithmic_work": (f"SURVEY.md §8(d) W = (|P+|+|P-|) * n_test * K = {horiz} 64-bit word tests per "
-                                     f"evidence call ({launches_per_call} launches, {ms_per_call:.3f} ms)"),
-                "note": ("W counts the dense (b & x) == b tests of the reference; the posting form skips almost all "
-                         "of them, so W/t exceeds the LOP3 peak (an effective rate, SURVEY.md §8(d)).  The "
-                         "hardware fraction is int_pipe_frac: the kernel's ALU-pipe utilisation measured by ncu."),
-                "posting_word_ands": words // reps,
-                "posting_word_and_rate_frac": (words / (kms * 1e-3) / 1e9) / peak_words,
-                "peak_source": f"measured lop3 micro-kernel {lop3_s / 1e12:.2f} T LOP3.32/s (diag.cu)",
-                "kernel_ms_per_launch": kms / max(nl, 1), "launches_per_step": launches_per_call,
-                "share_of_step": ms_per_call / ms}
-    roofline.update(ncu_summary(os.path.join(ROOT, "profiles", "r01_ncu_raw_grouped_scan_match.csv")))
+    peak_words = lop3_s / 2 / 1e9   # a 64-bit word AND = 2 LOP3.32 (measured micro-kernel, diag.cu)
+    roofline = kernel_rooflines(diag, peak_words, lop3_s, ms, horiz)
     cfg_extra = {"L": tenc.logical_len, "K": K, "candidates": [model.count(0, 0), model.count(1, 0)], "pure": P}
     # release the resident leg's model before the e2e leg: at C4 it holds ~12 GB
     # and would force the memory pool to grow inside the e2e timed region
@@ -450,6 +504,65 @@ def run_b200(args):
                            "to the host (into page-locked arrays from the library's host pool, reused across fits "
                            "once freed); matcher: resident test encoding -> A/N on the host"}
 
+    # ---- scale leg: BASELINE.json configs[3] (C4: the same 148,517 records at
+    # 80/20, 118,813 training rows), the strong-scaling configuration of the
+    # driver's N-GPU runs; resident columns, fit + evidence per step, timed like
+    # `value` (CUDA events, max over ranks).  At N > 1 the sharded path.
+    scale_leg = None
+    if args.scale_ratio and args.scale_ratio != args.ratio:
+        enc = model = tenc = None
+        gc.collect()
+        ntr4 = args.scale_ratio * n // 10
+        tr4, te4 = table.slice(0, ntr4), table.slice(ntr4, n)
+        schema4 = api.infer_schema(tr4, "label", decimals=args.decimals)
+        d_tr4 = api.Columns(tr4, schema4, True).upload(ctx)
+        d_te4 = api.Columns(te4, schema4, False).upload(ctx)
+        n_te4 = d_te4.rows
+        dA4 = torch.empty(n_te4, dtype=torch.int64, device="cuda")
+        dN4 = torch.empty(n_te4, dtype=torch.int64, device="cuda")
+
+        def step_scale():
+            enc_ = api.encode_training(d_tr4, ctx)
+            tenc_ = api.encode_rows(d_te4, enc_, ctx)
+            if sharded_mode:
+                res_ = sharded.fit_distributed(ctx, enc_, rank, world, ex)
+                a_, n_ = sharded.evidence_distributed(res_, tenc_, ex)
+                dA4.copy_(a_)
+                dN4.copy_(n_)
+                return res_.model
+            return api.fit_evidence_encoded(enc_, tenc_, d_A_ptr=dA4.data_ptr(), d_N_ptr=dN4.data_ptr())
+
+        m4 = step_scale()
+        m4 = None
+        barrier()
+        sc_steps = max(3, min(args.steps, 10))
+        ev4 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(sc_steps)]
+        gc.disable()
+        for i in range(sc_steps):
+            m4 = None
+            ev4[i][0].record(stream)
+            m4 = step_scale()
+            ev4[i][1].record(stream)
+        barrier()
+        gc.enable()
+        sc_ms_all = [a.elapsed_time(b) for a, b in ev4]
+        sc_ms = statistics.median(sc_ms_all)
+        if dist is not None:
+            t = torch.tensor([sc_ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            sc_ms = float(t.item())
+        scale_leg = {"config": {"workload": f"synthetic NSL-KDD-shape {n} records, {args.scale_ratio * 10}/"
+                                            f"{100 - args.scale_ratio * 10} train/test, p={args.decimals} "
+                                            "(BASELINE.json configs[3])",
+                                "train_rows": ntr4, "test_rows": n_te4,
+                                "candidates": [m4.count(0, 0), m4.count(1, 0)] if not sharded_mode else None,
+                                "pure": [m4.count(0, 1), m4.count(1, 1)] if not sharded_mode else None},
+                     "value": sc_ms / 1e3, "unit": "s", "ms_per_step": sc_ms, "steps": sc_steps, "steps_ms": sc_ms_all,
+                     "n_gpus": world, "scaling": "strong",
+                     "note": "resident columns; encode + fit + evidence of all test rows per step; the number the "
+                             "1/2/4/8-GPU strong-scaling efficiency of configs[3] is read from"}
+        m4 = d_tr4 = d_te4 = None
+        gc.collect()
 
     line = {"metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
@@ -462,9 +575,11 @@ def run_b200(args):
             "e2e": {"value": e2e / 1e3, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "e2e_csv": csv_leg,
             "fit_and_matcher": fit_leg,
+            "scale_leg": scale_leg,
             "gpu_launches": launches, "clocks": clk, "roofline": roofline}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_reference(csv, args, args.cpu_sample_tests)
+        line["cpu_baseline"]["sample"] += "; one step"
     if rank == 0:
         print(json.dumps(line), file=out, flush=True)
     if dist is not None:

@@ -54,11 +54,16 @@ int ig_ctx_set_stream(ig_ctx* ctx, void* stream);
 /* Number of kernels this context has launched so far (bench `gpu_launches`). */
 uint64_t ig_ctx_launch_count(const ig_ctx* ctx);
 const char* ig_version(void);
-/* Diagnostics for the bench roofline (off by default; adds syncs when on):
- * matcher kernel time (CUDA events) and its posting word-ANDs
- * Σ_p |b_p| * nnz_words(rarest token of p), accumulated since the last reset. */
+/* Diagnostics for the bench roofline (off by default; when on, the two
+ * classes run one after the other and every hot kernel launch is timed with
+ * CUDA events on its stream and followed by a counting re-run, so the timed
+ * path is untouched when off).  Per kernel since the last
+ * ig_ctx_set_diagnostics: event time, exact useful 64-bit word-ANDs, launches.
+ * kernel: 0 pair_enum (kernels 2+3: pairs x K), 1 support scan (kernel 5),
+ * 2 coverage scan (kernel 4), 3 matcher (kernel 6); posting word-ANDs of live
+ * list words, early exits honoured. */
 int ig_ctx_set_diagnostics(ig_ctx* ctx, int on);
-int ig_ctx_diag_match(ig_ctx* ctx, double* kernel_ms, uint64_t* word_ands, uint64_t* launches);
+int ig_ctx_diag_kernel(ig_ctx* ctx, int kernel, double* kernel_ms, uint64_t* word_ands, uint64_t* launches);
 /* Integer-pipe micro-benchmark: sustained LOP3.32/s and POPC.32/s of the whole
  * device (roofline denominator of the AND/POPC kernels). */
 int ig_measure_int_peaks(ig_ctx* ctx, double* lop3_per_s, double* popc_per_s);

@@ -63,7 +63,7 @@ def lib(b200: bool = False):
         L.igref_score_patterns.argtypes = [C.c_void_p]
         L.igref_total_score.argtypes = [p64, sz, p64]
         L.igref_run_create.argtypes = [C.c_char_p, sz, C.c_char_p, C.c_char_p, C.c_char_p, C.c_int, C.c_int,
-                                       sz, C.c_char_p, C.c_int, sz, sz, sz, C.c_int, C.c_double,
+                                       sz, C.c_char_p, C.c_int, sz, sz, sz, sz, C.c_int, C.c_double,
                                        C.POINTER(C.c_void_p)]
         L.igref_run_free.argtypes = [C.c_void_p]
         L.igref_run_L.argtypes = [C.c_void_p]
@@ -212,7 +212,7 @@ class RefRun:
 def run(csv: bytes, label_col: str = "label", attack_values: str = "", normal_values: str = "",
         decimals: int = 1, ratio_k: int = 8, train_rows: int = 0, backend: str = "parallel-cpu",
         threads: int = 0, pair_batch: int = 8192, coverage_block: int = 4096,
-        test_limit: int | None = None, stages: int = 2, r: float = 0.568) -> RefRun:
+        test_limit: int | None = None, stages: int = 2, r: float = 0.568, test_offset: int = 0) -> RefRun:
     """Full reference pipeline: parse → schema → encode → mine → purify → evidence."""
     b200 = backend == "b200"
     L_ = lib(b200)
@@ -220,7 +220,7 @@ def run(csv: bytes, label_col: str = "label", attack_values: str = "", normal_va
     tl = (1 << 63) if test_limit is None else test_limit
     _check(L_.igref_run_create(csv, len(csv), label_col.encode(), attack_values.encode(),
                                normal_values.encode(), decimals, ratio_k, train_rows, backend.encode(),
-                               threads, pair_batch, coverage_block, tl, stages, r, C.byref(h)), b200)
+                               threads, pair_batch, coverage_block, test_offset, tl, stages, r, C.byref(h)), b200)
     try:
         L = L_.igref_run_L(h)
         k = (L + 63) // 64

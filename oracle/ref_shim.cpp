@@ -457,7 +457,7 @@ int igref_run_create(const char* csv, std::size_t len, const char* label_col,
                      const char* attack_values, const char* normal_values, int decimals,
                      int ratio_k, std::size_t train_rows_override, const char* backend,
                      int threads, std::size_t pair_batch, std::size_t coverage_block,
-                     std::size_t test_limit, int stages, double r, void** out) {
+                     std::size_t test_offset, std::size_t test_limit, int stages, double r, void** out) {
     return guard([&] {
         auto run = std::make_unique<Run>();
         double t0 = now_s();
@@ -472,6 +472,12 @@ int igref_run_create(const char* csv, std::size_t len, const char* label_col,
         run->test.header = all.header;
         run->train.rows.assign(all.rows.begin(), all.rows.begin() + ntr);
         run->test.rows.assign(all.rows.begin() + ntr, all.rows.end());
+        // a bounded sample of the test rows: [test_offset, test_offset + test_limit)
+        // (bench.py's reference arm rotates the offset across steps)
+        if (test_offset) {
+            const std::size_t off = std::min(test_offset, run->test.rows.size());
+            run->test.rows.erase(run->test.rows.begin(), run->test.rows.begin() + off);
+        }
         if (test_limit < run->test.rows.size()) run->test.rows.resize(test_limit);
         double t1 = now_s();
         run->t[0] = t1 - t0;

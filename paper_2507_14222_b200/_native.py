@@ -48,7 +48,8 @@ SIGNATURES = [
     ("ig_ctx_launch_count", C.c_uint64, [vp]),
     ("ig_version", C.c_char_p, []),
     ("ig_ctx_set_diagnostics", C.c_int, [vp, C.c_int]),
-    ("ig_ctx_diag_match", C.c_int, [vp, C.POINTER(C.c_double), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    ("ig_ctx_diag_kernel", C.c_int, [vp, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_uint64),
+                               C.POINTER(C.c_uint64)]),
     ("ig_measure_int_peaks", C.c_int, [vp, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     ("ig_kernel_config_default", None, [C.POINTER(KernelConfigC)]),
     ("ig_pair_intersect_batch", C.c_int, [vp, p64, sz, u32, sz, sz, sz, p64]),

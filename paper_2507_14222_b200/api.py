@@ -114,10 +114,14 @@ class Context:
     def set_diagnostics(self, on: bool) -> None:
         self.check(lib.ig_ctx_set_diagnostics(self.handle, 1 if on else 0))
 
-    def diag_match(self) -> tuple[float, int, int]:
-        """(matcher kernel ms, posting word-ANDs, launches) since set_diagnostics(True)."""
+    DIAG_KERNELS = ("pair_enum", "support", "cover", "match")
+
+    def diag_kernel(self, kernel: str) -> tuple[float, int, int]:
+        """(kernel ms, exact useful 64-bit word-ANDs, launches) of one hot kernel
+        ("pair_enum", "support", "cover", "match") since set_diagnostics(True)."""
         ms, w, n = C.c_double(), C.c_uint64(), C.c_uint64()
-        self.check(lib.ig_ctx_diag_match(self.handle, C.byref(ms), C.byref(w), C.byref(n)))
+        self.check(lib.ig_ctx_diag_kernel(self.handle, self.DIAG_KERNELS.index(kernel), C.byref(ms), C.byref(w),
+                                          C.byref(n)))
         return ms.value, int(w.value), int(n.value)
 
     def int_peaks(self) -> tuple[float, float]:

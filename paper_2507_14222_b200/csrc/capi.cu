@@ -156,7 +156,8 @@ constexpr size_t kConcurrentPatterns = 8u << 20; // pure patterns (C3: 2.2 M; C4
 template <class F>
 void for_both_classes(igb::Ctx& ctx, F&& fn, bool concurrent = true) {
     static const bool serial = getenv("IG_SERIAL_CLASSES") != nullptr;  // profiling: one class at a time
-    if (!concurrent || serial) {
+    // diagnostics time each hot kernel alone: the classes run one after the other
+    if (!concurrent || serial || ctx.diag) {
         fn(ctx, 0);
         fn(ctx, 1);
         return;
@@ -169,9 +170,7 @@ void for_both_classes(igb::Ctx& ctx, F&& fn, bool concurrent = true) {
     igb::Ctx c1 = ctx;
     c1.stream = ctx.aux;
     c1.launches = 0;
-    c1.diag_match_ms = 0;
-    c1.diag_match_words = 0;
-    c1.diag_match_launches = 0;
+    for (auto& d : c1.diag_k) d = igb::DiagStat{};
     std::exception_ptr e0, e1;
     std::thread th([&] {
         try {
@@ -192,9 +191,7 @@ void for_both_classes(igb::Ctx& ctx, F&& fn, bool concurrent = true) {
     cudaEventDestroy(fork);
     cudaEventDestroy(join);
     ctx.launches += c1.launches;
-    ctx.diag_match_ms += c1.diag_match_ms;
-    ctx.diag_match_words += c1.diag_match_words;
-    ctx.diag_match_launches += c1.diag_match_launches;
+    ctx.diag_merge(c1);
     if (e0) std::rethrow_exception(e0);
     if (e1) std::rethrow_exception(e1);
 }
@@ -484,17 +481,17 @@ uint64_t ig_ctx_launch_count(const ig_ctx* ctx) { return ctx ? ctx->launches : 0
 int ig_ctx_set_diagnostics(ig_ctx* ctx, int on) {
     return guard(ctx, [&] {
         ctx->diag = on != 0;
-        ctx->diag_match_ms = 0;
-        ctx->diag_match_words = 0;
-        ctx->diag_match_launches = 0;
+        for (auto& d : ctx->diag_k) d = igb::DiagStat{};
     });
 }
 
-int ig_ctx_diag_match(ig_ctx* ctx, double* kernel_ms, uint64_t* word_ands, uint64_t* launches) {
+int ig_ctx_diag_kernel(ig_ctx* ctx, int kernel, double* kernel_ms, uint64_t* word_ands, uint64_t* launches) {
     return guard(ctx, [&] {
-        *kernel_ms = ctx->diag_match_ms;
-        *word_ands = ctx->diag_match_words;
-        *launches = ctx->diag_match_launches;
+        if (kernel < 0 || kernel >= igb::kDiagKinds) fail(IG_E_INVALID_ARG, "diag: unknown kernel id");
+        const igb::DiagStat& d = ctx->diag_k[kernel];
+        if (kernel_ms) *kernel_ms = d.ms;
+        if (word_ands) *word_ands = d.work;
+        if (launches) *launches = d.launches;
     });
 }
 

@@ -87,6 +87,14 @@ struct DevRows {
     int64_t* data() const { return buf.as<int64_t>(); }
 };
 
+// Hot kernels the bench reports a roofline for (ig_ctx_diag_kernel).
+enum DiagKind { kDiagEnum = 0, kDiagSupport = 1, kDiagCover = 2, kDiagMatch = 3, kDiagKinds = 4 };
+struct DiagStat {
+    double ms = 0;          // CUDA-event time of the launches
+    uint64_t work = 0;      // useful 64-bit word-ANDs they performed (counted exactly)
+    uint64_t launches = 0;
+};
+
 struct Ctx {
     int device = 0;
     cudaStream_t own = nullptr;
@@ -98,11 +106,52 @@ struct Ctx {
     uint64_t launches = 0;
     int sm_count = 148;
     size_t smem_optin = 0;
-    // diagnostics (bench roofline only; off on the timed path)
+    // diagnostics (bench roofline only; off on the timed path): per hot kernel,
+    // CUDA-event time of its launches and their exact useful work
     bool diag = false;
-    double diag_match_ms = 0;      // CUDA-event time of the matcher kernels
-    uint64_t diag_match_words = 0; // posting word-ANDs of the matcher (Σ_p |b_p| * nnz(rarest token))
-    uint64_t diag_match_launches = 0;
+    DiagStat diag_k[kDiagKinds];
+    void diag_merge(const Ctx& o) {
+        for (int i = 0; i < kDiagKinds; ++i) {
+            diag_k[i].ms += o.diag_k[i].ms;
+            diag_k[i].work += o.diag_k[i].work;
+            diag_k[i].launches += o.diag_k[i].launches;
+        }
+    }
+};
+
+// Times one hot-kernel launch on the context stream with CUDA events when
+// diagnostics are on (the stream is synchronised at end(): diagnostics only).
+struct DiagSpan {
+    Ctx& ctx;
+    int kind;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    DiagSpan(Ctx& c, int k) : ctx(c), kind(k) {
+        if (!ctx.diag) return;
+        IGB_CUDA(cudaEventCreate(&e0));
+        IGB_CUDA(cudaEventCreate(&e1));
+        IGB_CUDA(cudaEventRecord(e0, ctx.stream));
+    }
+    DiagSpan(const DiagSpan&) = delete;
+    // record the end of the timed launch (before any counting launch)
+    void stop() {
+        if (e1) IGB_CUDA(cudaEventRecord(e1, ctx.stream));
+    }
+    void end(uint64_t work) {
+        if (!e0) return;
+        IGB_CUDA(cudaEventSynchronize(e1));
+        float ms = 0;
+        IGB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        ctx.diag_k[kind].ms += ms;
+        ctx.diag_k[kind].work += work;
+        ctx.diag_k[kind].launches += 1;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        e0 = e1 = nullptr;
+    }
+    ~DiagSpan() {
+        if (e0) cudaEventDestroy(e0);
+        if (e1) cudaEventDestroy(e1);
+    }
 };
 
 // Device->host readback of a small result (counts, flags, totals) and a wait

@@ -577,6 +577,7 @@ uint64_t dedup_pairs(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, const 
                                src.n_list, T);
             } else if (level == 0) {
                 const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(my_tiles, (uint64_t)ctx.sm_count * 16));
+                DiagSpan dspan(ctx, kDiagEnum);
                 if (my_tiles) {
                     if (tile == 64 && k == 14)
                         IGB_LAUNCH(ctx, (pair_enum<64, 14>), grid, kPairThreads, smem, d_rows, (uint32_t)n, (int)k,
@@ -593,6 +594,20 @@ uint64_t dedup_pairs(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, const 
                     else
                         IGB_LAUNCH(ctx, (pair_enum<16, 0>), grid, kPairThreads, smem, d_rows, (uint32_t)n, (int)k,
                                    stride, n_tiles, T, src.tile_begin, src.tile_step);
+                }
+                if (ctx.diag) {
+                    // useful work: K word-ANDs per pair (u <= v) of this launch's tiles
+                    dspan.stop();
+                    uint64_t tile_pairs = 0;
+                    for (uint64_t t = src.tile_begin; t < n_tiles; t += src.tile_step) {
+                        uint64_t j = (uint64_t)((std::sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+                        while (j * (j + 1) / 2 > t) --j;
+                        while ((j + 1) * (j + 2) / 2 <= t) ++j;
+                        const uint64_t i = t - j * (j + 1) / 2;
+                        const uint64_t ri = std::min<uint64_t>(tile, n - i * tile), rj = std::min<uint64_t>(tile, n - j * tile);
+                        tile_pairs += i == j ? ri * (ri + 1) / 2 : ri * rj;
+                    }
+                    dspan.end(tile_pairs * k);
                 }
             } else {
                 IGB_LAUNCH(ctx, pair_insert_list, grid_for(ctx, n_pending, 256), 256, 0, d_rows, (int)k,

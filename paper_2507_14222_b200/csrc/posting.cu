@@ -548,7 +548,10 @@ __device__ __forceinline__ unsigned long long ld_tok(const unsigned long long* c
     return v;
 }
 
-template <int MODE>
+// COUNT (diagnostics): the same control flow with every output suppressed;
+// each lane counts the posting word-ANDs it performs on live list words (the
+// useful work of the roofline), summed into *work.
+template <int MODE, bool COUNT = false>
 __global__ void __launch_bounds__(256)
 grouped_scan(const unsigned long long* __restrict__ dense, size_t W, size_t n_rows,
              const uint32_t* __restrict__ tok_beg, const uint32_t* __restrict__ tok_len,
@@ -557,10 +560,12 @@ grouped_scan(const unsigned long long* __restrict__ dense, size_t W, size_t n_ro
              const unsigned long long* __restrict__ goff, const uint32_t* __restrict__ glen,
              const uint32_t* __restrict__ ew, const unsigned long long* __restrict__ em,
              const int64_t* __restrict__ scores, unsigned long long* __restrict__ acc,
-             int64_t* __restrict__ support_out, uint8_t* __restrict__ cover_out, int* __restrict__ flags) {
+             int64_t* __restrict__ support_out, uint8_t* __restrict__ cover_out, int* __restrict__ flags,
+             unsigned long long* __restrict__ work) {
     const int lane = threadIdx.x & 31;
     const size_t warps = ((size_t)gridDim.x * blockDim.x) >> 5;
     bool ovf = false;
+    unsigned long long nand = 0;  // COUNT only
     for (size_t i = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < np; i += warps) {
         const uint32_t p = order[i];
         const uint32_t g = gid[i];
@@ -594,11 +599,13 @@ grouped_scan(const unsigned long long* __restrict__ dense, size_t W, size_t n_ro
                 if (!__any_sync(kFull, live)) break;
                 const uint32_t o0 = __shfl_sync(kFull, toff, t), o1 = __shfl_sync(kFull, toff, (t + 1) & 31);
                 const uint32_t o2 = __shfl_sync(kFull, toff, (t + 2) & 31), o3 = __shfl_sync(kFull, toff, (t + 3) & 31);
+                if (COUNT && live) nand += min(4u, m - (uint32_t)t);
                 if (live) mw &= (ld_tok(col, o0, wb) & ld_tok(col, o1, wb)) & (ld_tok(col, o2, wb) & ld_tok(col, o3, wb));
             }
             for (uint32_t t = 32; t < m; ++t) {
                 if (!__any_sync(kFull, mw != 0ull)) break;
                 const uint32_t tt = toks[o + t];
+                if (COUNT && mw) ++nand;
                 if (mw) mw &= col[tt * Wu];
             }
             if (MODE == kSupport) {
@@ -608,7 +615,7 @@ grouped_scan(const unsigned long long* __restrict__ dense, size_t W, size_t n_ro
                     hit = true;
                     break;
                 }
-            } else {
+            } else if (!COUNT) {
                 if (__any_sync(kFull, mw != 0ull)) {
                     if (MODE == kMatch) {
                         // difference array: +s at each run start, -s after each run end
@@ -630,6 +637,7 @@ grouped_scan(const unsigned long long* __restrict__ dense, size_t W, size_t n_ro
                 }
             }
         }
+        if (COUNT) continue;
         if (MODE == kSupport) {
             for (int o2 = 16; o2; o2 >>= 1) cnt += __shfl_xor_sync(kFull, cnt, o2);
             if (lane == 0) support_out[p] = (int64_t)cnt;
@@ -637,31 +645,12 @@ grouped_scan(const unsigned long long* __restrict__ dense, size_t W, size_t n_ro
             if (lane == 0) cover_out[p] = hit ? 1 : 0;
         }
     }
-    if (MODE == kMatchChecked && ovf) atomicOr(flags, 1);
-}
-
-// diagnostics: word-ANDs of the grouped algorithm without early exit
-//   Σ_groups ub(g) * min(2, |t1,t2|) + Σ_patterns glen(g(p)) * max(0, m_p - 2)
-__global__ void grouped_work(const uint32_t* __restrict__ tok_len, size_t np, const uint32_t* __restrict__ order,
-                             const uint32_t* __restrict__ gid, const uint32_t* __restrict__ glen,
-                             unsigned long long* __restrict__ out) {
-    unsigned long long acc = 0;
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < np; i += (size_t)gridDim.x * blockDim.x) {
-        const uint32_t p = order[i];
-        const uint32_t m = tok_len[p];
-        if (m > 3) acc += (unsigned long long)glen[gid[i]] * (m - 3);
+    if (COUNT) {
+        for (int o2 = 16; o2; o2 >>= 1) nand += __shfl_xor_sync(kFull, nand, o2);
+        if (lane == 0 && nand) atomicAdd(work, nand);
+        return;
     }
-    for (int s = 16; s; s >>= 1) acc += __shfl_xor_sync(kFull, acc, s);
-    if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
-}
-
-__global__ void group_work(const uint32_t* __restrict__ pkey, const unsigned long long* __restrict__ ub, size_t G,
-                           unsigned long long* __restrict__ out) {
-    unsigned long long acc = 0;
-    for (size_t g = (size_t)blockIdx.x * blockDim.x + threadIdx.x; g < G; g += (size_t)gridDim.x * blockDim.x)
-        acc += ub[g] * (((pkey[g] & 0xffffu) != kNoTok) ? 2ull : 1ull);
-    for (int s = 16; s; s >>= 1) acc += __shfl_xor_sync(kFull, acc, s);
-    if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
+    if (MODE == kMatchChecked && ovf) atomicOr(flags, 1);
 }
 
 template <int MODE>
@@ -678,13 +667,6 @@ void launch_scan(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Post
         tr.mark("pattern_index");
     }
     if (I->np != np) fail(IG_E_CUDA, "pattern index does not match the pattern set");
-    const bool diag = ctx.diag && (MODE == kMatch || MODE == kMatchChecked);
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (diag) {
-        IGB_CUDA(cudaEventCreate(&e0));
-        IGB_CUDA(cudaEventCreate(&e1));
-        IGB_CUDA(cudaEventRecord(e0, ctx.stream));
-    }
     const size_t G = I->G, G2 = I->G2;
     // parent (t1, t2) lists S2 = non-zero (w, post[t1][w] & post[t2][w]) in P,
     // then each (t1, t2, t3) group's list S = S2 filtered by post[t3]
@@ -723,30 +705,25 @@ void launch_scan(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Post
                    glen.as<uint32_t>(), ew.as<uint32_t>(), em.as<unsigned long long>());
     tr.mark("group_lists");
     const size_t blocks = std::min<size_t>((np + 7) / 8, (size_t)ctx.sm_count * 64);
-    IGB_LAUNCH(ctx, grouped_scan<MODE>, (unsigned)blocks, 256, 0, P.dense.as<unsigned long long>(), P.W, P.n,
-               I->beg.as<uint32_t>(), I->len.as<uint32_t>(), I->toks->as<uint16_t>(), np, I->order.as<uint32_t>(),
-               I->gid.as<uint32_t>(),
-               goff.as<unsigned long long>(), glen.as<uint32_t>(), ew.as<uint32_t>(), em.as<unsigned long long>(),
-               scores, acc, support, cover, flags);
+    DiagSpan dspan(ctx, MODE == kSupport ? kDiagSupport : MODE == kCover ? kDiagCover : kDiagMatch);
+    IGB_LAUNCH(ctx, (grouped_scan<MODE, false>), (unsigned)blocks, 256, 0, P.dense.as<unsigned long long>(), P.W,
+               P.n, I->beg.as<uint32_t>(), I->len.as<uint32_t>(), I->toks->as<uint16_t>(), np, I->order.as<uint32_t>(),
+               I->gid.as<uint32_t>(), goff.as<unsigned long long>(), glen.as<uint32_t>(), ew.as<uint32_t>(),
+               em.as<unsigned long long>(), scores, acc, support, cover, flags, nullptr);
     tr.mark("grouped_scan");
-    if (diag) {
-        IGB_CUDA(cudaEventRecord(e1, ctx.stream));
+    if (ctx.diag) {
+        // the same launch again with outputs suppressed, counting its word-ANDs
+        dspan.stop();
         DevBuf w(8, ctx.stream);
         IGB_CUDA(cudaMemsetAsync(w.p, 0, 8, ctx.stream));
-        IGB_LAUNCH(ctx, grouped_work, grid_for(ctx, np, 256), 256, 0, I->len.as<uint32_t>(), np,
-                   I->order.as<uint32_t>(), I->gid.as<uint32_t>(), glen.as<uint32_t>(), w.as<unsigned long long>());
-        if (G2)
-            IGB_LAUNCH(ctx, group_work, grid_for(ctx, G2, 256), 256, 0, I->pkey.as<uint32_t>(),
-                       ub.as<unsigned long long>(), G2, w.as<unsigned long long>());
+        IGB_LAUNCH(ctx, (grouped_scan<MODE, true>), (unsigned)blocks, 256, 0, P.dense.as<unsigned long long>(), P.W,
+                   P.n, I->beg.as<uint32_t>(), I->len.as<uint32_t>(), I->toks->as<uint16_t>(), np,
+                   I->order.as<uint32_t>(), I->gid.as<uint32_t>(), goff.as<unsigned long long>(), glen.as<uint32_t>(),
+                   ew.as<uint32_t>(), em.as<unsigned long long>(), scores, acc, support, cover, flags,
+                   w.as<unsigned long long>());
         unsigned long long hw = 0;
         read_back(ctx, &hw, w.p, 8);
-        float ms = 0;
-        IGB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-        ctx.diag_match_ms += ms;
-        ctx.diag_match_words += hw;
-        ctx.diag_match_launches += 1;
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
+        dspan.end(hw);
     }
 }
 
