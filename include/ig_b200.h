@@ -42,12 +42,16 @@ enum ig_status {
 
 typedef struct ig_ctx ig_ctx;
 
-/* Context = one device + one stream + the resident buffers.  Not thread-safe:
- * concurrent callers use one context each (kernels.hpp:23-26 purity holds
- * because every call is a pure function of its inputs). */
+/* Context = one device + its streams + the resident buffers.  Calls on one
+ * context from several threads are safe and serialised (a per-context lock);
+ * callers that want them to run concurrently use one context per thread
+ * (kernels.hpp:23-26: backend methods are pure and may be called
+ * concurrently; every call is a pure function of its inputs).  Result objects
+ * (models, encodings, candidate sets) may be read from several threads. */
 int ig_ctx_create(int device, ig_ctx** out);
 void ig_ctx_destroy(ig_ctx* ctx);
-/* Message of the last failing call on this context (thread-local when ctx is NULL). */
+/* Message of the calling thread's last failing call (on any context; ctx is
+ * accepted for symmetry and ignored). */
 const char* ig_last_error(const ig_ctx* ctx);
 /* Run subsequent work on `stream` (a cudaStream_t); NULL restores the context's own. */
 int ig_ctx_set_stream(ig_ctx* ctx, void* stream);
@@ -107,7 +111,11 @@ typedef void (*ig_progress_fn)(uint64_t pairs_done, uint64_t pairs_total, uint64
 
 /* {rows[i] & rows[j] : i<j, non-empty} U {rows[i]} deduplicated by content, in
  * canonical words::less order (mine.hpp:35-40).
- * Progress is reported from the calling thread (mine.hpp:31-33). */
+ * Progress (mine.hpp:31-33) is reported from the calling thread while the
+ * kernel runs: pairs_done / pairs_total count the pairs (u <= v) of the
+ * distinct rows the device enumerates (identical rows collapse first),
+ * candidates_found the distinct candidates so far; the last call is
+ * (pairs_total, pairs_total, final count). */
 int ig_enumerate_candidates(ig_ctx* ctx, const int64_t* rows, size_t n_rows, uint32_t logical_len,
                             const ig_kernel_config* cfg, ig_progress_fn progress, void* user,
                             ig_candidates** out);

@@ -19,6 +19,9 @@
 // reference) load this library.
 
 #include <algorithm>
+#include <atomic>
+#include <mutex>
+#include <thread>
 #include <chrono>
 #include <cmath>
 #include <cstdint>
@@ -606,5 +609,89 @@ void igref_run_schema(void* r, std::uint8_t* kind, double* mean, double* sd, std
     *label_index = R->schema.label_index;
 }
 std::size_t igref_run_cols(void* r) { return static_cast<Run*>(r)->schema.columns.size(); }
+
+
+#ifdef IG_WITH_B200
+// kernels.hpp:23-26 under concurrency: `threads` host threads share ONE "b200"
+// backend object and call pair_intersect_batch / coverage_any / fused_score on
+// shared read-only inputs, `iters` times each, with thread-dependent windows;
+// every result is compared with ParallelCpuBackend's.  Returns the number of
+// mismatching results in *mismatches.
+int igref_b200_concurrency(const std::int64_t* rows, std::size_t n, std::uint32_t L, const std::int64_t* pats,
+                           std::size_t np, const std::int64_t* scores, int threads, int iters,
+                           std::uint64_t* mismatches, std::uint64_t* calls) {
+    return guard([&] {
+        ig::PackedMatrix X(L, ig::ClassTag::attack), P(L, ig::ClassTag::attack);
+        const std::size_t k = X.word_count();
+        for (std::size_t i = 0; i < n; ++i) X.append_words(rows + i * k);
+        for (std::size_t i = 0; i < np; ++i) P.append_words(pats + i * k);
+        std::vector<std::int64_t> sc(scores, scores + np);
+        auto b200 = backend_for("b200", 0);
+        auto cpu = ig::make_backend("parallel-cpu", 1);
+        const auto cov_want = cpu->coverage_any(P, X, 4096);
+        const auto fs_want = cpu->fused_score(P, sc, X);
+        std::atomic<std::uint64_t> bad{0}, ncalls{0};
+        std::atomic<bool> failed{false};
+        std::string first_err;
+        std::mutex err_mu;
+        std::vector<std::thread> pool;
+        for (int t = 0; t < threads; ++t) {
+            pool.emplace_back([&, t] {
+                try {
+                    for (int it = 0; it < iters; ++it) {
+                        const std::size_t left = (std::size_t)(t * 7 + it * 3) % (n - 1);
+                        const std::size_t jb = left + 1, je = std::min(n, jb + 1 + (std::size_t)(t * 13 + it) % 97);
+                        std::vector<std::int64_t> got((je - jb) * k), want((je - jb) * k);
+                        b200->pair_intersect_batch(X, left, jb, je, got.data());
+                        cpu->pair_intersect_batch(X, left, jb, je, want.data());
+                        bad += got != want;
+                        const std::size_t block = 1 + (std::size_t)(t * 31 + it) % 5000;  // never changes results
+                        bad += b200->coverage_any(P, X, block) != cov_want;
+                        bad += b200->fused_score(P, sc, X) != fs_want;
+                        ncalls += 3;
+                    }
+                } catch (const std::exception& e) {
+                    std::lock_guard<std::mutex> lk(err_mu);
+                    if (!failed.exchange(true)) first_err = e.what();
+                }
+            });
+        }
+        for (auto& th : pool) th.join();
+        if (failed) throw std::runtime_error("b200 backend call failed under concurrency: " + first_err);
+        *mismatches = bad;
+        *calls = ncalls;
+    });
+}
+
+// enumerate_candidates on the device with a ProgressFn (mine.hpp:31-40):
+// records how often it was called, whether pairs_done and candidates_found
+// never decreased, and the last triple; returns the candidates' words.
+int igref_b200_enumerate_progress(const std::int64_t* rows, std::size_t n, std::uint32_t L, std::uint64_t* ncalls,
+                                  int* monotone, std::uint64_t* last3, void** out) {
+    return guard([&] {
+        ig::PackedMatrix X(L, ig::ClassTag::attack);
+        for (std::size_t i = 0; i < n; ++i) X.append_words(rows + i * X.word_count());
+        std::uint64_t calls = 0, pd = 0, cf = 0;
+        bool mono = true;
+        std::uint64_t last[3] = {0, 0, 0};
+        ig::ProgressFn fn = [&](std::uint64_t done, std::uint64_t total, std::uint64_t found) {
+            ++calls;
+            mono = mono && done >= pd && found >= cf && done <= total;
+            pd = done;
+            cf = found;
+            last[0] = done;
+            last[1] = total;
+            last[2] = found;
+        };
+        ig::KernelConfig cfg;
+        auto c = std::make_unique<Cand>();
+        c->c = ig::b200_enumerate_candidates(X, cfg, fn);
+        *ncalls = calls;
+        *monotone = mono ? 1 : 0;
+        std::copy(last, last + 3, last3);
+        *out = c.release();
+    });
+}
+#endif
 
 }  // extern "C"

@@ -23,7 +23,13 @@
 #include "posting.cuh"
 #include "subset.cuh"
 
-struct ig_ctx : igb::Ctx {};
+// A context serialises the ABI calls made on it (kernels.hpp:23-26: backend
+// methods may be called concurrently; callers wanting parallelism use one
+// context per thread, as integration/ig_b200_backend.cpp does).  Recursive:
+// an entry point may call another.
+struct ig_ctx : igb::Ctx {
+    std::recursive_mutex mu;
+};
 
 struct ig_candidates {
     igb::DevRows rows;
@@ -59,8 +65,10 @@ struct RowIndexJob {
     std::exception_ptr err;
     uint64_t launches = 0;
     bool joined = false;
+    std::mutex mu;  // an encoding may be used by several contexts / threads
     // join the builder (rethrows its error); launches are added to `ctx` once
     void wait(igb::Ctx* ctx) {
+        std::lock_guard<std::mutex> lock(mu);
         if (!joined) {
             if (th.joinable()) th.join();
             joined = true;
@@ -84,20 +92,24 @@ using igb::DevRows;
 using igb::Error;
 using igb::fail;
 
+// Every entry point: the context's call lock, its device, and status codes
+// instead of exceptions.  Error text is per calling thread (ig_last_error).
 template <class F>
 int guard(ig_ctx* ctx, F&& f) {
+    std::unique_lock<std::recursive_mutex> lock;
+    if (ctx) lock = std::unique_lock<std::recursive_mutex>(ctx->mu);
     try {
         if (ctx) IGB_CUDA(cudaSetDevice(ctx->device));
         f();
         return IG_OK;
     } catch (const Error& e) {
-        (ctx ? ctx->err : g_err) = e.msg;
+        g_err = e.msg;
         return e.status;
     } catch (const std::bad_alloc&) {
-        (ctx ? ctx->err : g_err) = "host allocation failed";
+        g_err = "host allocation failed";
         return IG_E_OOM;
     } catch (const std::exception& e) {
-        (ctx ? ctx->err : g_err) = e.what();
+        g_err = e.what();
         return IG_E_CUDA;
     }
 }
@@ -350,6 +362,10 @@ void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m, bool enumerate 
 }
 
 void copy_out(igb::Ctx& ctx, ig_candidates& c, int64_t* words, int64_t* sup, int64_t* sc) {
+    // the first copy-out orders the set in place; concurrent readers of one set
+    // (from different contexts) wait for that
+    static std::mutex order_mu;
+    std::lock_guard<std::mutex> lock(order_mu);
     if (!c.ordered) {
         igb::canonical_order(ctx, c.rows, c.has_support ? &c.support : nullptr, c.has_score ? &c.score : nullptr);
         c.rows.buf.persist();
@@ -412,7 +428,7 @@ extern "C" {
 
 const char* ig_version(void) { return "ig_b200 0.1.0 (sm_100a)"; }
 
-const char* ig_last_error(const ig_ctx* ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
+const char* ig_last_error(const ig_ctx* /*ctx*/) { return g_err.c_str(); }
 
 void ig_kernel_config_default(ig_kernel_config* cfg) {
     cfg->pair_batch = 8192;  // kernels.hpp:15-18 defaults
@@ -453,10 +469,7 @@ int ig_ctx_create(int device, ig_ctx** out) {
             IGB_CUDA(cudaStreamSynchronize(c->own));
         }
     });
-    if (st != IG_OK) {
-        g_err = c->err;
-        return st;
-    }
+    if (st != IG_OK) return st;
     *out = c.release();
     return IG_OK;
 }
@@ -476,7 +489,11 @@ int ig_ctx_set_stream(ig_ctx* ctx, void* stream) {
     return guard(ctx, [&] { ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own; });
 }
 
-uint64_t ig_ctx_launch_count(const ig_ctx* ctx) { return ctx ? ctx->launches : 0; }
+uint64_t ig_ctx_launch_count(const ig_ctx* ctx) {
+    if (!ctx) return 0;
+    std::lock_guard<std::recursive_mutex> lock(const_cast<ig_ctx*>(ctx)->mu);
+    return ctx->launches;
+}
 
 int ig_ctx_set_diagnostics(ig_ctx* ctx, int on) {
     return guard(ctx, [&] {
@@ -568,12 +585,43 @@ int ig_enumerate_candidates(ig_ctx* ctx, const int64_t* rows, size_t n, uint32_t
         upload_rows(*ctx, rows, n, L, X);
         auto c = std::make_unique<ig_candidates>();
         igb::EnumStats st;
+        // progress (mine.hpp:31-33): pairs done over the pairs (u <= v) of the
+        // distinct rows the device enumerates, candidates found so far
+        igb::ProgressHook hook;
+        struct Mapped {
+            unsigned long long* h = nullptr;
+            ~Mapped() {
+                if (h) cudaFreeHost(h);
+            }
+        } mapped;
+        igb::DevBuf pctr;
+        if (progress) {
+            IGB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&mapped.h), 2 * sizeof(unsigned long long),
+                                   cudaHostAllocMapped));
+            mapped.h[0] = mapped.h[1] = 0;
+            IGB_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&hook.dev), mapped.h, 0));
+            pctr.alloc(8, ctx->stream);
+            IGB_CUDA(cudaMemsetAsync(pctr.p, 0, 8, ctx->stream));
+            hook.fn = progress;
+            hook.user = user;
+            hook.host = mapped.h;
+            hook.ctr = pctr.as<unsigned long long>();
+            ctx->progress = &hook;
+        }
+        struct Unhook {
+            igb::Ctx& c;
+            ~Unhook() { c.progress = nullptr; }
+        } unhook{*ctx};
         igb::enumerate_dev(*ctx, X.data(), n, X.k, L, c->rows, &st);
+        ctx->progress = nullptr;
         igb::canonical_order(*ctx, c->rows, nullptr, nullptr);
         IGB_CUDA(cudaStreamSynchronize(ctx->stream));
         c->rows.buf.persist();
         c->pairs = st.pairs;
-        if (progress) progress(st.pairs, st.pairs, c->rows.n, user);
+        if (progress) {
+            const uint64_t m = st.distinct_rows, total = m * (m + 1) / 2;
+            progress(total, total, c->rows.n, user);
+        }
         *out = c.release();
     });
 }

@@ -95,6 +95,20 @@ struct DiagStat {
     uint64_t launches = 0;
 };
 
+// Progress of a long enumeration (ig_enumerate_candidates' ig_progress_fn,
+// mine.hpp:31-33): the kernel publishes pairs done / candidates found into
+// page-locked mapped memory after each tile; the calling thread polls it while
+// the stream runs and calls fn.
+struct ProgressHook {
+    void (*fn)(uint64_t, uint64_t, uint64_t, void*) = nullptr;
+    void* user = nullptr;
+    unsigned long long* host = nullptr;  // [0] pairs done, [1] candidates found (mapped)
+    unsigned long long* dev = nullptr;   // device alias of host
+    unsigned long long* ctr = nullptr;   // device counters the kernel adds to
+    uint64_t pairs_total = 0;
+    uint64_t seen[2] = {0, 0};
+};
+
 struct Ctx {
     int device = 0;
     cudaStream_t own = nullptr;
@@ -102,7 +116,6 @@ struct Ctx {
     cudaStream_t aux = nullptr;  // second class's stream (for_both_classes)
     cudaStream_t copy = nullptr; // host->device prefetches (ig_columns_prefetch)
     cudaStream_t index = nullptr;  // background test-row encode + postings (ig_encode_rows)
-    std::string err;
     uint64_t launches = 0;
     int sm_count = 148;
     size_t smem_optin = 0;
@@ -110,6 +123,7 @@ struct Ctx {
     // CUDA-event time of its launches and their exact useful work
     bool diag = false;
     DiagStat diag_k[kDiagKinds];
+    ProgressHook* progress = nullptr;  // set by ig_enumerate_candidates for one call
     void diag_merge(const Ctx& o) {
         for (int i = 0; i < kDiagKinds; ++i) {
             diag_k[i].ms += o.diag_k[i].ms;

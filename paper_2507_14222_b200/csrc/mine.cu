@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <ctime>
 
 #include "ig_internal.cuh"
 #include "subset.cuh"
@@ -185,7 +186,8 @@ constexpr int kLocalProbes = 64;
 template <int TILE, int KC>
 __global__ void __launch_bounds__(kPairThreads, KC > 0 && KC <= 17 ? 5 : 6)
 pair_enum(const int64_t* __restrict__ X, uint32_t n, int k_rt, int stride, uint64_t n_tiles, Table T,
-          uint64_t tile_begin, uint64_t tile_step) {
+          uint64_t tile_begin, uint64_t tile_step, unsigned long long* __restrict__ prog_ctr,
+          unsigned long long* __restrict__ prog_host) {
     const int k = KC > 0 ? KC : k_rt;
     constexpr bool kRegs = KC > 0 && KC <= 16;
     extern __shared__ int64_t sm[];
@@ -197,9 +199,13 @@ pair_enum(const int64_t* __restrict__ X, uint32_t n, int k_rt, int stride, uint6
     __shared__ unsigned int s_nrep;
     __shared__ unsigned long long s_base;
     __shared__ int s_stop;
+    __shared__ unsigned long long s_pairs;  // pairs of the tile just finished (progress)
     const RepStage stage{s_reps, &s_nrep};
     for (int w = threadIdx.x; w < k; w += kPairThreads) sKey[w] = T.keys[w];
-    if (threadIdx.x == 0) s_nrep = 0;
+    if (threadIdx.x == 0) {
+        s_nrep = 0;
+        s_pairs = 0;
+    }
     for (uint64_t it = blockIdx.x;; it += gridDim.x) {
         const uint64_t t = tile_begin + it * tile_step;  // this rank's tiles: begin, begin + step, ...
         // the previous tile's staged representatives -> one reserved range of
@@ -210,6 +216,14 @@ pair_enum(const int64_t* __restrict__ X, uint32_t n, int k_rt, int stride, uint6
             const unsigned int n = min(s_nrep, (unsigned int)kStageReps);
             s_base = n ? atomicAdd(T.count, (unsigned long long)n) : 0ull;
             s_stop = *(volatile int*)T.fail;
+            if (prog_ctr && s_pairs) {
+                // publish progress to the polling host thread (values only grow;
+                // the host keeps the largest it has seen)
+                const unsigned long long d = atomicAdd(prog_ctr, s_pairs) + s_pairs;
+                *(volatile unsigned long long*)prog_host = d;
+                *(volatile unsigned long long*)(prog_host + 1) = s_base + n;
+                s_pairs = 0;
+            }
         }
         __syncthreads();
         {
@@ -228,6 +242,10 @@ pair_enum(const int64_t* __restrict__ X, uint32_t n, int k_rt, int stride, uint6
         uint32_t bi, bj;
         tile_of(t, bi, bj);
         const uint32_t i0 = bi * TILE, j0 = bj * TILE;
+        if (threadIdx.x == 0 && prog_ctr) {
+            const unsigned long long ri = min((uint32_t)TILE, n - i0), rj = min((uint32_t)TILE, n - j0);
+            s_pairs = bi == bj ? ri * (ri + 1) / 2 : ri * rj;
+        }
         for (int q = threadIdx.x; q < TILE * k; q += kPairThreads) {
             const int r = q / k, w = q % k;
             sI[r * stride + w] = (i0 + r < n) ? X[(size_t)(i0 + r) * k + w] : 0;
@@ -423,6 +441,24 @@ struct TableMem {
     }
 };
 
+// Calling thread: report progress while the enumeration runs on the stream.
+void poll_progress(Ctx& ctx) {
+    ProgressHook& p = *ctx.progress;
+    for (;;) {
+        const cudaError_t q = cudaStreamQuery(ctx.stream);
+        const unsigned long long d = *(volatile unsigned long long*)p.host;
+        const unsigned long long f = *(volatile unsigned long long*)(p.host + 1);
+        if (d > p.seen[0] || f > p.seen[1]) {
+            p.seen[0] = std::max<uint64_t>(p.seen[0], d);
+            p.seen[1] = std::max<uint64_t>(p.seen[1], f);
+            if (p.seen[0] < p.pairs_total) p.fn(p.seen[0], p.pairs_total, p.seen[1], p.user);
+        }
+        if (q != cudaErrorNotReady) break;
+        struct timespec ts = {0, 2000000};  // 2 ms
+        nanosleep(&ts, nullptr);
+    }
+}
+
 uint64_t next_pow2(uint64_t x) {
     uint64_t p = 1;
     while (p < x) p <<= 1;
@@ -502,6 +538,7 @@ void enumerate_dev(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, uint32_t
                    EnumStats* stats, const uint32_t* d_perm) {
     DevBuf U;
     const size_t m = distinct_rows(ctx, d_rows, n, k, U, d_perm);
+    if (ctx.progress) ctx.progress->pairs_total = (uint64_t)m * (m + 1) / 2;
     PairSource src;  // every tile of the triangle
     DevBuf reps;
     const uint64_t c = dedup_pairs(ctx, U.as<int64_t>(), m, k, src, reps, stats);
@@ -578,22 +615,24 @@ uint64_t dedup_pairs(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, const 
             } else if (level == 0) {
                 const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(my_tiles, (uint64_t)ctx.sm_count * 16));
                 DiagSpan dspan(ctx, kDiagEnum);
+                unsigned long long* pc = ctx.progress ? ctx.progress->ctr : nullptr;
+                unsigned long long* ph = ctx.progress ? ctx.progress->dev : nullptr;
                 if (my_tiles) {
                     if (tile == 64 && k == 14)
                         IGB_LAUNCH(ctx, (pair_enum<64, 14>), grid, kPairThreads, smem, d_rows, (uint32_t)n, (int)k,
-                                   stride, n_tiles, T, src.tile_begin, src.tile_step);
+                                   stride, n_tiles, T, src.tile_begin, src.tile_step, pc, ph);
                     else if (tile == 64 && k == 17)
                         IGB_LAUNCH(ctx, (pair_enum<64, 17>), grid, kPairThreads, smem, d_rows, (uint32_t)n, (int)k,
-                                   stride, n_tiles, T, src.tile_begin, src.tile_step);
+                                   stride, n_tiles, T, src.tile_begin, src.tile_step, pc, ph);
                     else if (tile == 64)
                         IGB_LAUNCH(ctx, (pair_enum<64, 0>), grid, kPairThreads, smem, d_rows, (uint32_t)n, (int)k,
-                                   stride, n_tiles, T, src.tile_begin, src.tile_step);
+                                   stride, n_tiles, T, src.tile_begin, src.tile_step, pc, ph);
                     else if (tile == 32)
                         IGB_LAUNCH(ctx, (pair_enum<32, 0>), grid, kPairThreads, smem, d_rows, (uint32_t)n, (int)k,
-                                   stride, n_tiles, T, src.tile_begin, src.tile_step);
+                                   stride, n_tiles, T, src.tile_begin, src.tile_step, pc, ph);
                     else
                         IGB_LAUNCH(ctx, (pair_enum<16, 0>), grid, kPairThreads, smem, d_rows, (uint32_t)n, (int)k,
-                                   stride, n_tiles, T, src.tile_begin, src.tile_step);
+                                   stride, n_tiles, T, src.tile_begin, src.tile_step, pc, ph);
                 }
                 if (ctx.diag) {
                     // useful work: K word-ANDs per pair (u <= v) of this launch's tiles
@@ -613,6 +652,7 @@ uint64_t dedup_pairs(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, const 
                 IGB_LAUNCH(ctx, pair_insert_list, grid_for(ctx, n_pending, 256), 256, 0, d_rows, (int)k,
                            pending.as<uint2>(), n_pending, T);
             }
+            if (ctx.progress) poll_progress(ctx);
             unsigned long long h[4];
             read_back(ctx, h, tm.ctr.p, sizeof(h));
             const int failbits = (int)(h[3] & 0xffffffffu);

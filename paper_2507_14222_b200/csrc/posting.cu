@@ -27,6 +27,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
+#include <vector>
 
 #include "ig_internal.cuh"
 #include "posting.cuh"
@@ -653,6 +655,44 @@ grouped_scan(const unsigned long long* __restrict__ dense, size_t W, size_t n_ro
     if (MODE == kMatchChecked && ovf) atomicOr(flags, 1);
 }
 
+// IG_SCAN_STATS=1 (development): shape of one scan on stderr — patterns per
+// group, list words per pattern (lane occupancy of a warp per pattern), tokens
+// per pattern.
+void scan_stats(Ctx& ctx, int mode, const PatternIndex& I, const DevBuf& glen, size_t G, size_t np) {
+    std::vector<uint32_t> gl(G), gid(np), len(np), order(np);
+    read_back(ctx, gl.data(), glen.p, G * 4);
+    read_back(ctx, gid.data(), I.gid.p, np * 4);
+    read_back(ctx, len.data(), I.len.p, np * 4);
+    read_back(ctx, order.data(), I.order.p, np * 4);
+    std::vector<uint64_t> pg(G, 0);
+    uint64_t words = 0, rounds = 0, hist[8] = {0, 0, 0, 0, 0, 0, 0, 0}, toks = 0;
+    for (size_t i = 0; i < np; ++i) {
+        const uint32_t l = gl[gid[i]];
+        ++pg[gid[i]];
+        words += l;
+        rounds += (l + 31) / 32;
+        int b = 0;
+        while (b < 7 && (1u << (b + 1)) <= l) ++b;  // bucket: [2^b, 2^(b+1)), last = >= 128
+        ++hist[l == 0 ? 0 : std::min(b + 1, 7)];
+        toks += len[order[i]];
+    }
+    uint64_t pgh[6] = {0, 0, 0, 0, 0, 0};
+    for (size_t g = 0; g < G; ++g) {
+        const uint64_t c = pg[g];
+        pgh[c <= 1 ? 0 : c <= 4 ? 1 : c <= 16 ? 2 : c <= 64 ? 3 : c <= 256 ? 4 : 5] += c;
+    }
+    fprintf(stderr,
+            "[ig scan] mode %d np %zu G %zu G2 %zu W %s | list words/pattern %.2f, lane occupancy %.3f | patterns "
+            "with list len 0:%llu 1:%llu 2-3:%llu 4-7:%llu 8-15:%llu 16-31:%llu 32-63:%llu >=64:%llu | patterns in "
+            "groups of <=1:%llu <=4:%llu <=16:%llu <=64:%llu <=256:%llu >256:%llu | tokens/pattern %.2f\n",
+            mode, np, G, I.G2, "-", (double)words / np, rounds ? (double)words / (32.0 * rounds) : 0.0,
+            (unsigned long long)hist[0], (unsigned long long)hist[1], (unsigned long long)hist[2],
+            (unsigned long long)hist[3], (unsigned long long)hist[4], (unsigned long long)hist[5],
+            (unsigned long long)hist[6], (unsigned long long)hist[7], (unsigned long long)pgh[0],
+            (unsigned long long)pgh[1], (unsigned long long)pgh[2], (unsigned long long)pgh[3],
+            (unsigned long long)pgh[4], (unsigned long long)pgh[5], (double)toks / np);
+}
+
 template <int MODE>
 void launch_scan(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Postings& P, const PatternIndex* I,
                  const int64_t* scores, unsigned long long* acc, int64_t* support, uint8_t* cover, int* flags) {
@@ -704,6 +744,7 @@ void launch_scan(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Post
                    plen.as<uint32_t>(), pw.as<uint32_t>(), pm.as<unsigned long long>(), goff.as<unsigned long long>(),
                    glen.as<uint32_t>(), ew.as<uint32_t>(), em.as<unsigned long long>());
     tr.mark("group_lists");
+    if (getenv("IG_SCAN_STATS")) scan_stats(ctx, MODE, *I, glen, G, np);
     const size_t blocks = std::min<size_t>((np + 7) / 8, (size_t)ctx.sm_count * 64);
     DiagSpan dspan(ctx, MODE == kSupport ? kDiagSupport : MODE == kCover ? kDiagCover : kDiagMatch);
     IGB_LAUNCH(ctx, (grouped_scan<MODE, false>), (unsigned)blocks, 256, 0, P.dense.as<unsigned long long>(), P.W,

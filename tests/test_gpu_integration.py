@@ -44,3 +44,63 @@ def test_backend_primitives_through_reference_types():
     with pytest.raises(ref.RefError) as e:
         ref.pair_intersect_batch(rows, L, 5, 5, 300, backend="b200")
     assert e.value.status == 1  # std::invalid_argument, as the reference
+
+
+def _b200_lib():
+    import ctypes as C
+    L = ref.lib(b200=True)
+    p64 = C.POINTER(C.c_int64)
+    L.igref_b200_concurrency.argtypes = [p64, C.c_size_t, C.c_uint32, p64, C.c_size_t, p64, C.c_int, C.c_int,
+                                         C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+    L.igref_b200_enumerate_progress.argtypes = [p64, C.c_size_t, C.c_uint32, C.POINTER(C.c_uint64),
+                                                C.POINTER(C.c_int), C.POINTER(C.c_uint64), C.POINTER(C.c_void_p)]
+    return L
+
+
+def test_backend_concurrent_calls_match_parallel_cpu():
+    """kernels.hpp:23-26: eight host threads share ONE "b200" backend and call
+    pair_intersect_batch / coverage_any / fused_score concurrently on shared
+    inputs (as the OpenMP enumerate of the reference does); every result equals
+    ParallelCpuBackend's."""
+    import ctypes as C
+    rng = np.random.default_rng(23)
+    L = 150
+    k = (L + 63) // 64
+    rows = (rng.random((400, L)) < 0.7)
+    X = np.zeros((400, k), np.uint64)
+    for j in range(L):
+        X[:, j // 64] |= rows[:, j].astype(np.uint64) << np.uint64(j % 64)
+    X = X.view(np.int64)
+    pats = X[rng.integers(0, 400, 300)] & X[rng.integers(0, 400, 300)]
+    scores = rng.integers(0, 1 << 20, 300).astype(np.int64)
+    bad, calls = C.c_uint64(), C.c_uint64()
+    p64 = C.POINTER(C.c_int64)
+    lib = _b200_lib()
+    st = lib.igref_b200_concurrency(X.ctypes.data_as(p64), 400, L, pats.ctypes.data_as(p64), 300,
+                                    scores.ctypes.data_as(p64), 8, 12, C.byref(bad), C.byref(calls))
+    assert st == 0, lib.igref_last_error().decode()
+    assert calls.value == 8 * 12 * 3 and bad.value == 0
+
+
+def test_enumerate_progress_reported_while_running():
+    """mine.hpp:31-33: ProgressFn is called from the calling thread while the
+    device enumerates (pairs done and candidates found never decrease), and the
+    last call reports the total and the final candidate count."""
+    import ctypes as C
+    csv = synth.nsl_csv(15000, seed=2507)
+    r = ref.run(csv, decimals=1, ratio_k=8, stages=0)
+    X = np.ascontiguousarray(r.normal)
+    n_calls, mono, last, h = C.c_uint64(), C.c_int(), (C.c_uint64 * 3)(), C.c_void_p()
+    lib = _b200_lib()
+    p64 = C.POINTER(C.c_int64)
+    st = lib.igref_b200_enumerate_progress(X.ctypes.data_as(p64), X.shape[0], r.L, C.byref(n_calls), C.byref(mono),
+                                           last, C.byref(h))
+    assert st == 0, lib.igref_last_error().decode()
+    try:
+        n = lib.igref_cand_count(h)
+        assert mono.value == 1 and n_calls.value >= 2
+        assert last[0] == last[1] and last[2] == n
+        want = ref.mine(X, r.L, backend="parallel-cpu", support=False)
+        assert n == want.words.shape[0]
+    finally:
+        lib.igref_cand_free(h)
