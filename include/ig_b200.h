@@ -289,6 +289,32 @@ int ig_model_from_dictionaries(ig_ctx* ctx, uint32_t logical_len, const int64_t*
                                const int64_t* supports_attack, const int64_t* scores_attack, size_t n_attack,
                                const int64_t* words_normal, const int64_t* supports_normal,
                                const int64_t* scores_normal, size_t n_normal, ig_model** out);
+/* ModelArchive writer / reader (SPEC.md:568-573 fields, :607 round trip,
+ * :611 format): format_version, tool version, provenance (free text the caller
+ * supplies: input digest, timestamps, ...), classifier parameters (r, stats mode
+ * "batch" = mu_N / sigma_N fitted per predict batch, or "frozen" with the
+ * values), the schema (exact hex-float statistics), the vocabulary in bit
+ * order and both pure dictionaries (canonical order, packed words + supports +
+ * scores as base-64 sections).  save -> load -> save is byte-identical.
+ * ig_model_save: *len = archive size; copies min(cap-1, len) bytes + NUL when
+ * buf is given (call with buf = NULL first to size it).  vocabulary: the
+ * '\n'-terminated tokens in bit order (ig_encoding_vocabulary).
+ * ig_model_load: a model usable by ig_evidence* / ig_explain, its schema and
+ * an encoding that tokenises test rows exactly like the training encoding
+ * (ig_encode_rows); params->provenance is set to NULL, the text is copied to
+ * `provenance` (prov_len = its length). */
+typedef struct {
+    double r;              /* R3 parameter (default 0.568) */
+    int stats_frozen;      /* 0: batch statistics; 1: mu / sigma below */
+    double mu, sigma;
+    const char* provenance; /* NUL-terminated; NULL = empty */
+} ig_archive_params;
+int ig_model_save(ig_ctx* ctx, const ig_model* m, const ig_schema* schema, const char* vocabulary,
+                  const ig_archive_params* params, char* buf, size_t cap, size_t* len);
+int ig_model_load(ig_ctx* ctx, const char* data, size_t n_bytes, ig_model** model, ig_schema** schema,
+                  ig_encoding** encoding, ig_archive_params* params, char* provenance, size_t prov_cap,
+                  size_t* prov_len);
+
 /* explain: indices into P^cls (ascending) of the patterns
  * contained in one test row; *n_found may exceed cap (call again larger). */
 int ig_explain(ig_ctx* ctx, const ig_model* m, int cls, const int64_t* row, uint32_t logical_len, uint32_t* idx,

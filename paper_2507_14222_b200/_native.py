@@ -33,6 +33,11 @@ vp = C.c_void_p
 u32 = C.c_uint32
 
 
+class ArchiveParamsC(C.Structure):
+    _fields_ = [("r", C.c_double), ("stats_frozen", C.c_int), ("mu", C.c_double), ("sigma", C.c_double),
+                ("provenance", C.c_char_p)]
+
+
 class KernelConfigC(C.Structure):
     _fields_ = [("pair_batch", sz), ("coverage_block", sz), ("memory_budget_bytes", sz), ("threads", C.c_int)]
 
@@ -110,6 +115,9 @@ SIGNATURES = [
     ("ig_schema_from_text", C.c_int, [C.c_char_p, C.POINTER(vp)]),
     ("ig_encoding_from_vocabulary", C.c_int, [vp, C.c_char_p, C.POINTER(vp)]),
     ("ig_model_from_dictionaries", C.c_int, [vp, u32, p64, p64, p64, sz, p64, p64, p64, sz, C.POINTER(vp)]),
+    ("ig_model_save", C.c_int, [vp, vp, vp, C.c_char_p, C.POINTER(ArchiveParamsC), C.c_char_p, sz, C.POINTER(sz)]),
+    ("ig_model_load", C.c_int, [vp, C.c_char_p, sz, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp),
+                                C.POINTER(ArchiveParamsC), C.c_char_p, sz, C.POINTER(sz)]),
     ("ig_explain", C.c_int, [vp, vp, C.c_int, p64, u32, C.POINTER(C.c_uint32), sz, C.POINTER(sz)]),
     ("ig_shard_create", C.c_int, [vp, vp, C.c_int, C.c_int, C.POINTER(KernelConfigC), C.POINTER(vp)]),
     ("ig_shard_enumerate", C.c_int, [vp, vp, C.c_int, pu64, C.POINTER(vp)]),

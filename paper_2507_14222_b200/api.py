@@ -709,7 +709,6 @@ def train_and_score(csv: bytes, label_column: str = "label", decimals: int = 1, 
 
 
 # ---------------------------------------------------------------- archive / explain
-ARCHIVE_MAGIC = "ig-b200-archive 1"
 
 
 def _esc(s: str) -> str:
@@ -812,22 +811,26 @@ def explain_row(model: Model, row, vocabulary: list[str], dictionaries=None) -> 
     return out
 
 
-def save_model(model: Model, schema: Schema, vocabulary: list[str], r: float = 0.568) -> bytes:
-    """ModelArchive: stable-ordered text, canonical pattern
-    order, packed words base-64; save -> load -> save is byte-identical."""
-    import base64
-    lines = [ARCHIVE_MAGIC, f"r {float(r).hex()}", "stats_mode batch", "[schema]"]
-    lines += schema_to_text(schema).rstrip("\n").split("\n")
-    lines.append(f"[vocabulary] {len(vocabulary)}")
-    lines += [_esc(t) for t in vocabulary]
-    k = (model.logical_len + 63) // 64
-    for cls, name in ((0, "attack"), (1, "normal")):
-        d = model.dictionary(cls, 1)
-        lines.append(f"[dictionary {name}] {d.words.shape[0]} {k}")
-        for tag, a in (("words", d.words), ("supports", d.supports), ("scores", d.scores)):
-            lines.append(tag + " " + base64.b64encode(np.ascontiguousarray(a, "<i8").tobytes()).decode())
-    lines.append("[end]")
-    return ("\n".join(lines) + "\n").encode("utf-8", errors="surrogateescape")
+def save_model(model: Model, schema: Schema, vocabulary: list[str], r: float = 0.568,
+               stats: Optional[tuple[float, float]] = None, provenance: str = "") -> bytes:
+    """ModelArchive through ig_model_save: format_version,
+    tool version, provenance, r, stats mode ("batch", or "frozen" with
+    stats = (mu_N, sigma_N)), schema, vocabulary, both pure dictionaries;
+    save -> load -> save is byte-identical (S:607)."""
+    blob = "".join(t + "\n" for t in vocabulary).encode("utf-8", errors="surrogateescape")
+    prm = N.ArchiveParamsC(float(r), 1 if stats is not None else 0, float(stats[0]) if stats else 0.0,
+                           float(stats[1]) if stats else 0.0,
+                           provenance.encode("utf-8", errors="surrogateescape"))
+    n = C.c_size_t()
+    st = lib.ig_model_save(model.ctx.handle, model.handle, schema.handle, blob, C.byref(prm), None, 0, C.byref(n))
+    if st:
+        _raise(st)
+    buf = C.create_string_buffer(n.value + 1)
+    st = lib.ig_model_save(model.ctx.handle, model.handle, schema.handle, blob, C.byref(prm), buf, n.value + 1,
+                           C.byref(n))
+    if st:
+        _raise(st)
+    return buf.raw[:n.value]
 
 
 @dataclass
@@ -837,33 +840,30 @@ class LoadedModel:
     vocabulary: list
     encoding: Encoding
     r: float
+    stats: Optional[tuple[float, float]] = None  # frozen (mu_N, sigma_N), None = batch
+    provenance: str = ""
 
 
 def load_model(data: bytes, ctx: Optional[Context] = None) -> LoadedModel:
-    import base64
+    """ig_model_load: the archive's model (evidence / explain ready), schema and
+    the encoding that tokenises test rows like the training encoding."""
     ctx = ctx or default_context()
-    lines = data.decode("utf-8", errors="surrogateescape").split("\n")
-    if lines[0] != ARCHIVE_MAGIC:
-        raise DataError("not an ig-b200 archive")
-    r = float.fromhex(lines[1].split(" ", 1)[1])
-    i = lines.index("[schema]") + 1
-    j = next(t for t in range(i, len(lines)) if lines[t].startswith("[vocabulary]"))
-    schema = schema_from_text("\n".join(lines[i:j]) + "\n")
-    nv = int(lines[j].split(" ")[1])
-    vocab = [_unesc(t) for t in lines[j + 1:j + 1 + nv]]
-    L = len(vocab)
-    pos = j + 1 + nv
-    dicts = []
-    for _ in range(2):
-        _, rest = lines[pos].split("] ", 1)
-        n, k = (int(x) for x in rest.split())
-        vals = {}
-        for t in range(3):
-            tag, b64 = lines[pos + 1 + t].split(" ", 1)
-            vals[tag] = np.frombuffer(base64.b64decode(b64), "<i8").astype(np.int64)
-        dicts.append(Dictionary(vals["words"].reshape(n, k) if n else np.zeros((0, k), np.int64),
-                                vals["supports"], vals["scores"]))
-        pos += 4
-    model = model_from_dictionaries(L, dicts[0], dicts[1], ctx)
-    enc = encoding_from_vocabulary(schema, vocab, ctx)
-    return LoadedModel(model, schema, vocab, enc, r)
+    cap = 1 << 16
+    while True:
+        hm, hs, he = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        prm = N.ArchiveParamsC()
+        plen = C.c_size_t()
+        pbuf = C.create_string_buffer(cap)
+        st = lib.ig_model_load(ctx.handle, data, len(data), C.byref(hm), C.byref(hs), C.byref(he), C.byref(prm),
+                               pbuf, cap, C.byref(plen))
+        if st:
+            _raise(st)
+        model = Model(ctx, hm)
+        schema = Schema(hs, int(lib.ig_schema_cols(hs)))
+        enc = Encoding(ctx, he)
+        if plen.value < cap:
+            break
+        cap = plen.value + 1  # provenance longer than the buffer: load again with room for it
+    prov = pbuf.raw[:plen.value].decode("utf-8", errors="surrogateescape")
+    return LoadedModel(model, schema, enc.vocabulary, enc, prm.r,
+                       (prm.mu, prm.sigma) if prm.stats_frozen else None, prov)

@@ -328,7 +328,8 @@ void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m, bool enumerate 
                              src.as<uint32_t>());
             igb::subset_pattern_index(cx, CI[c], src.as<uint32_t>(), n, m.pidx[c]);
             for (DevBuf* b : {&m.pidx[c].beg, &m.pidx[c].len, m.pidx[c].toks.get(), &m.pidx[c].order, &m.pidx[c].gid,
-                              &m.pidx[c].gkey, &m.pidx[c].pid, &m.pidx[c].pkey})
+                              &m.pidx[c].gkey, &m.pidx[c].pid, &m.pidx[c].pkey, &m.pidx[c].lcp, &m.pidx[c].push,
+                              &m.pidx[c].seg, &m.pidx[c].nseg})
                 b->persist();
             tr.mark("pure_index");
             if (fused) {
@@ -424,9 +425,13 @@ void evidence_impl(igb::Ctx& ctx, const ig_model& m, const int64_t* d_tests, siz
 
 }  // namespace
 
+namespace igb {
+void set_last_error(const std::string& msg) { g_err = msg; }
+}  // namespace igb
+
 extern "C" {
 
-const char* ig_version(void) { return "ig_b200 0.1.0 (sm_100a)"; }
+const char* ig_version(void) { return "ig_b200 0.2.0 (sm_100a)"; }
 
 const char* ig_last_error(const ig_ctx* /*ctx*/) { return g_err.c_str(); }
 

@@ -454,7 +454,7 @@ void poll_progress(Ctx& ctx) {
             if (p.seen[0] < p.pairs_total) p.fn(p.seen[0], p.pairs_total, p.seen[1], p.user);
         }
         if (q != cudaErrorNotReady) break;
-        struct timespec ts = {0, 2000000};  // 2 ms
+        struct timespec ts = {0, 500000};  // 0.5 ms
         nanosleep(&ts, nullptr);
     }
 }

@@ -27,6 +27,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <string>
+#include <type_traits>
 #include <cstdlib>
 #include <vector>
 
@@ -319,6 +321,11 @@ __global__ void sub_lists(const uint32_t* __restrict__ src_beg, const uint32_t* 
     }
 }
 
+__global__ void iota_u32_k(uint32_t* __restrict__ p, size_t n) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        p[i] = (uint32_t)i;
+}
+
 __global__ void fill_u32(uint32_t* __restrict__ p, size_t n, uint32_t v) {
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] = v;
 }
@@ -357,30 +364,82 @@ __global__ void gather_u64k(const unsigned long long* __restrict__ src, const ui
 // C3 ~1M patterns fall into ~35k groups, so most of the (t1, t2) work is shared.
 constexpr uint32_t kNoTok = 0xffffu;
 
-// group key of a pattern: its three rarest tokens (t1, t2, t3), absent = all
-// ones, packed in b bits each (3b-bit radix sort); expand_keys restores the
-// (t1 << 32) | (t2 << 16) | t3 form with kNoTok, which sorts identically
+// sort key of a pattern: its q rarest tokens (t1, t2, t3, t4, ...; absent = all
+// ones), b bits each, t1 most significant (q*b <= 64 bits, one radix sort).
+// The group is (t1, t2, t3); the further tokens order the patterns inside a
+// group so that neighbours share prefixes (the trie scan).  expand_keys
+// restores the group part as (t1 << 32) | (t2 << 16) | t3 with kNoTok, which
+// sorts identically.
 __global__ void group_keys(const uint32_t* __restrict__ tok_beg, const uint32_t* __restrict__ tok_len,
-                           const uint16_t* __restrict__ toks, size_t np, int b,
+                           const uint16_t* __restrict__ toks, size_t np, int b, int q,
                            unsigned long long* __restrict__ key, uint32_t* __restrict__ idx) {
     const unsigned long long none = (1ull << b) - 1ull;
     for (size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += (size_t)gridDim.x * blockDim.x) {
         const uint32_t o = tok_beg[p], m = tok_len[p];
-        const unsigned long long t1 = m >= 1 ? toks[o] : none, t2 = m >= 2 ? toks[o + 1] : none,
-                                 t3 = m >= 3 ? toks[o + 2] : none;
-        key[p] = (t1 << (2 * b)) | (t2 << b) | t3;
+        unsigned long long k = 0;
+        for (int i = 0; i < q; ++i) k = (k << b) | ((uint32_t)i < m ? (unsigned long long)toks[o + i] : none);
+        key[p] = k;
         idx[p] = (uint32_t)p;
     }
 }
 
-__global__ void expand_keys(unsigned long long* __restrict__ key, size_t n, int b) {
+__global__ void expand_keys(unsigned long long* __restrict__ key, size_t n, int b, int q) {
     const unsigned long long none = (1ull << b) - 1ull;
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
         const unsigned long long x = key[i];
-        unsigned long long t[3] = {(x >> (2 * b)) & none, (x >> b) & none, x & none};
+        unsigned long long t[3] = {(x >> ((q - 1) * b)) & none, (x >> ((q - 2) * b)) & none, (x >> ((q - 3) * b)) & none};
         for (auto& v : t)
             if (v == none) v = kNoTok;
         key[i] = (t[0] << 32) | (t[1] << 16) | t[2];
+    }
+}
+
+// ---- prefix-trie links (PatternIndex::lcp / push / seg)
+// group start position of every group
+__global__ void group_starts(const uint32_t* __restrict__ gid, size_t np, uint32_t* __restrict__ gstart) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < np; i += (size_t)gridDim.x * blockDim.x)
+        if (i == 0 || gid[i] != gid[i - 1]) gstart[gid[i]] = (uint32_t)i;
+}
+
+// lcp of every position with its predecessor in the segment; segment heads
+__global__ void trie_lcp(const uint32_t* __restrict__ order, const uint32_t* __restrict__ gid,
+                         const uint32_t* __restrict__ gstart, const uint32_t* __restrict__ tok_beg,
+                         const uint32_t* __restrict__ tok_len, const uint16_t* __restrict__ toks, size_t np,
+                         uint8_t* __restrict__ lcp, uint8_t* __restrict__ head) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < np; i += (size_t)gridDim.x * blockDim.x) {
+        const uint32_t p = order[i], m = tok_len[p];
+        const bool h = ((i - gstart[gid[i]]) % kTrieSeg) == 0;
+        uint32_t l = m < 3 ? m : 3;
+        if (!h) {
+            const uint32_t q = order[i - 1], mq = tok_len[q];
+            const uint16_t* a = toks + tok_beg[p];
+            const uint16_t* c = toks + tok_beg[q];
+            const uint32_t lim = min(min(m, mq), 31u);
+            l = 0;
+            while (l < lim && a[l] == c[l]) ++l;
+            // same group: the first three tokens agree (or the shorter list ended)
+        }
+        lcp[i] = (uint8_t)l;
+        head[i] = h ? 1 : 0;
+    }
+}
+
+// push[i]: depths d (lcp[i] < d <= min(|b_i|, 31)) of position i's scan that a
+// later position j of the segment restarts from: lcp[j] == d with every
+// position strictly between them sharing at least d tokens (so the depth-d
+// prefix is the same) — the first position to compute a prefix keeps it.
+__global__ void trie_push(const uint32_t* __restrict__ order, const uint32_t* __restrict__ tok_len,
+                          const uint8_t* __restrict__ lcp, const uint8_t* __restrict__ head, size_t np,
+                          uint32_t* __restrict__ push) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < np; i += (size_t)gridDim.x * blockDim.x) {
+        const uint32_t li = lcp[i], mi = min(tok_len[order[i]], 31u);
+        uint32_t bits = 0, rm = 0xffu;
+        for (size_t j = i + 1; j < np && !head[j] && rm > li; ++j) {
+            const uint32_t lj = lcp[j];
+            if (lj > li && lj <= rm && lj <= mi) bits |= 1u << lj;
+            rm = min(rm, lj);
+        }
+        push[i] = bits;
     }
 }
 
@@ -655,6 +714,146 @@ grouped_scan(const unsigned long long* __restrict__ dense, size_t W, size_t n_ro
     if (MODE == kMatchChecked && ovf) atomicOr(flags, 1);
 }
 
+// Prefix-trie scan (the default for support, coverage and the matcher): one
+// warp per segment (<= kTrieSeg consecutive positions of one (t1, t2, t3)
+// group, sorted by their further rarest tokens, PatternIndex::lcp / push).
+// The warp walks the group's list 32 words at a time; for each chunk it runs
+// the segment's patterns in order, each starting from the deepest prefix mask
+// it shares with an earlier pattern of the segment — kept on a small per-warp
+// stack in shared memory — instead of from the list mask, so a token that
+// neighbouring patterns share is loaded and ANDed once per chunk, and the
+// list words are loaded once per segment instead of once per pattern.  A
+// prefix that is empty on every lane empties every pattern extending it, which
+// are then skipped.  Exact: each pattern's mask is the AND of the list mask and
+// all of its tokens, however it was reached.
+constexpr int kTrieStack = 12;
+constexpr int kTrieWarps = 8;
+
+__device__ __forceinline__ unsigned long long ld_at(const unsigned long long* col, uint32_t byte_off) {
+    return __ldg(reinterpret_cast<const unsigned long long*>(reinterpret_cast<const char*>(col) + byte_off));
+}
+
+template <int MODE, bool COUNT>
+__global__ void __launch_bounds__(kTrieWarps * 32)
+trie_scan(const unsigned long long* __restrict__ dense, size_t W, size_t np,
+          const uint32_t* __restrict__ tok_beg, const uint32_t* __restrict__ tok_len,
+          const uint16_t* __restrict__ toks, const uint32_t* __restrict__ order, const uint32_t* __restrict__ gid,
+          const uint8_t* __restrict__ lcp, const uint32_t* __restrict__ push, const uint32_t* __restrict__ seg,
+          const unsigned long long* __restrict__ nseg_p, const unsigned long long* __restrict__ goff,
+          const uint32_t* __restrict__ glen, const uint32_t* __restrict__ ew, const unsigned long long* __restrict__ em,
+          const int64_t* __restrict__ scores, unsigned long long* __restrict__ acc, int64_t* __restrict__ support_out,
+          uint8_t* __restrict__ cover_out, int* __restrict__ flags, unsigned long long* __restrict__ work) {
+    __shared__ unsigned long long stk[kTrieWarps][kTrieStack][32];
+    __shared__ uint32_t cnt[kTrieWarps][kTrieSeg];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const size_t warps = ((size_t)gridDim.x * blockDim.x) >> 5;
+    const size_t nseg = (size_t)*nseg_p;
+    const uint32_t Wu = (uint32_t)W, wb = Wu * 8u;
+    bool ovf = false;
+    unsigned long long nand = 0;  // COUNT only
+    for (size_t sgi = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; sgi < nseg; sgi += warps) {
+        const uint32_t b = seg[sgi];
+        const uint32_t e = sgi + 1 < nseg ? seg[sgi + 1] : (uint32_t)np;
+        const uint32_t g = gid[b];
+        const unsigned long long base = goff[g];
+        const uint32_t len = glen[g];
+        if (MODE == kSupport && !COUNT)
+            for (uint32_t i = lane; i < e - b; i += 32) cnt[wib][i] = 0u;
+        unsigned long long hit = 0;  // cover: positions of the segment with a covering row
+        __syncwarp();
+        for (uint32_t j0 = 0; j0 < len; j0 += 32) {
+            const uint32_t j = j0 + lane;
+            const uint32_t w = j < len ? ew[base + j] : 0u;
+            const unsigned long long m0 = j < len ? em[base + j] : 0ull;
+            const unsigned long long* col = dense + w;
+            int sp = 0;
+            unsigned long long sd = 0;  // depth of stack entry q in bits [5q, 5q + 5)
+            uint32_t dead = 0xffu;      // a prefix length known empty on every lane
+            for (uint32_t i = b; i < e; ++i) {
+                const uint32_t p = order[i];
+                const uint32_t m = tok_len[p];
+                const uint32_t l = lcp[i];
+                unsigned long long mk = 0ull;
+                if (l < dead) {
+                    dead = 0xffu;
+                    const uint32_t o = tok_beg[p];
+                    while (sp > 0 && (uint32_t)((sd >> (5 * (sp - 1))) & 31u) > l) --sp;
+                    uint32_t d = m < 3 ? m : 3;
+                    mk = m0;
+                    if (l > d && sp > 0 && (uint32_t)((sd >> (5 * (sp - 1))) & 31u) == l) {
+                        mk = stk[wib][sp - 1][lane];
+                        d = l;
+                    }
+                    const uint32_t pm = push[i];
+                    const uint32_t toff = (uint32_t)lane < m ? (uint32_t)toks[o + lane] * wb : 0u;
+                    const uint32_t mlim = m < 32u ? m : 32u;
+                    bool alive = true;
+                    for (; d < mlim; ++d) {
+                        if (!__any_sync(kFull, mk != 0ull)) {
+                            alive = false;
+                            break;
+                        }
+                        const uint32_t tb = __shfl_sync(kFull, toff, d);
+                        if (COUNT && mk) ++nand;
+                        if (mk) mk &= ld_at(col, tb);
+                        if (((pm >> (d + 1)) & 1u) && sp < kTrieStack) {
+                            stk[wib][sp][lane] = mk;
+                            sd = (sd & ~(31ull << (5 * sp))) | ((unsigned long long)(d + 1) << (5 * sp));
+                            ++sp;
+                        }
+                    }
+                    if (alive) {
+                        for (; d < m; ++d) {  // tokens past 32, from memory (rare)
+                            if (!__any_sync(kFull, mk != 0ull)) break;
+                            const uint32_t tt = toks[o + d];
+                            if (COUNT && mk) ++nand;
+                            if (mk) mk &= col[(size_t)tt * Wu];
+                        }
+                    }
+                    if (!__any_sync(kFull, mk != 0ull)) dead = d;  // the prefix of length d is empty
+                }
+                if (COUNT) continue;
+                if (MODE == kSupport) {
+                    const uint32_t c = __reduce_add_sync(kFull, (uint32_t)__popcll(mk));
+                    if (lane == 0 && c) cnt[wib][i - b] += c;
+                } else if (MODE == kCover) {
+                    if (__any_sync(kFull, mk != 0ull)) hit |= 1ull << (i - b);
+                } else if (__any_sync(kFull, mk != 0ull)) {
+                    const unsigned long long sc = (unsigned long long)scores[p];
+                    if (MODE == kMatch) {
+                        unsigned long long st = mk & ~(mk << 1), en = mk & ~(mk >> 1);
+                        unsigned long long* row = acc + (size_t)w * 64;
+                        while (st) {
+                            __builtin_assume(en != 0ull);
+                            const unsigned long long st1 = st - 1, en1 = en - 1;
+                            atomicAdd(row + __popcll(~st & st1), sc);
+                            atomicAdd(row + 1 + __popcll(~en & en1), 0ull - sc);
+                            st &= st1;
+                            en &= en1;
+                        }
+                    } else {
+                        warp_scatter_hits<true>(w, mk, sc, acc, ovf);
+                    }
+                }
+            }
+        }
+        if (COUNT) continue;
+        __syncwarp();
+        if (MODE == kSupport) {
+            for (uint32_t i = lane; i < e - b; i += 32) support_out[order[b + i]] = (int64_t)cnt[wib][i];
+            __syncwarp();
+        } else if (MODE == kCover) {
+            for (uint32_t i = lane; i < e - b; i += 32) cover_out[order[b + i]] = (uint8_t)((hit >> i) & 1ull);
+        }
+    }
+    if (COUNT) {
+        for (int o2 = 16; o2; o2 >>= 1) nand += __shfl_xor_sync(kFull, nand, o2);
+        if (lane == 0 && nand) atomicAdd(work, nand);
+        return;
+    }
+    if (MODE == kMatchChecked && ovf) atomicOr(flags, 1);
+}
+
 // IG_SCAN_STATS=1 (development): shape of one scan on stderr — patterns per
 // group, list words per pattern (lane occupancy of a warp per pattern), tokens
 // per pattern.
@@ -745,23 +944,35 @@ void launch_scan(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Post
                    glen.as<uint32_t>(), ew.as<uint32_t>(), em.as<unsigned long long>());
     tr.mark("group_lists");
     if (getenv("IG_SCAN_STATS")) scan_stats(ctx, MODE, *I, glen, G, np);
+    static const bool grouped = getenv("IG_SCAN") && std::string(getenv("IG_SCAN")) == "grouped";  // A/B only
+    const bool use_trie = !grouped && I->lcp.p != nullptr;
     const size_t blocks = std::min<size_t>((np + 7) / 8, (size_t)ctx.sm_count * 64);
+    const size_t tblocks = std::min<size_t>((np + 7) / 8 / 4 + 1, (size_t)ctx.sm_count * 64);
     DiagSpan dspan(ctx, MODE == kSupport ? kDiagSupport : MODE == kCover ? kDiagCover : kDiagMatch);
-    IGB_LAUNCH(ctx, (grouped_scan<MODE, false>), (unsigned)blocks, 256, 0, P.dense.as<unsigned long long>(), P.W,
-               P.n, I->beg.as<uint32_t>(), I->len.as<uint32_t>(), I->toks->as<uint16_t>(), np, I->order.as<uint32_t>(),
-               I->gid.as<uint32_t>(), goff.as<unsigned long long>(), glen.as<uint32_t>(), ew.as<uint32_t>(),
-               em.as<unsigned long long>(), scores, acc, support, cover, flags, nullptr);
-    tr.mark("grouped_scan");
+    auto launch = [&](auto count_tag, unsigned long long* work) {
+        constexpr bool C = decltype(count_tag)::value;
+        if (use_trie)
+            IGB_LAUNCH(ctx, (trie_scan<MODE, C>), (unsigned)tblocks, kTrieWarps * 32, 0,
+                       P.dense.as<unsigned long long>(), P.W, np, I->beg.as<uint32_t>(), I->len.as<uint32_t>(),
+                       I->toks->as<uint16_t>(), I->order.as<uint32_t>(), I->gid.as<uint32_t>(), I->lcp.as<uint8_t>(),
+                       I->push.as<uint32_t>(), I->seg.as<uint32_t>(), I->nseg.as<unsigned long long>(),
+                       goff.as<unsigned long long>(), glen.as<uint32_t>(), ew.as<uint32_t>(),
+                       em.as<unsigned long long>(), scores, acc, support, cover, flags, work);
+        else
+            IGB_LAUNCH(ctx, (grouped_scan<MODE, C>), (unsigned)blocks, 256, 0, P.dense.as<unsigned long long>(), P.W,
+                       P.n, I->beg.as<uint32_t>(), I->len.as<uint32_t>(), I->toks->as<uint16_t>(), np,
+                       I->order.as<uint32_t>(), I->gid.as<uint32_t>(), goff.as<unsigned long long>(),
+                       glen.as<uint32_t>(), ew.as<uint32_t>(), em.as<unsigned long long>(), scores, acc, support,
+                       cover, flags, work);
+    };
+    launch(std::false_type{}, nullptr);
+    tr.mark(use_trie ? "trie_scan" : "grouped_scan");
     if (ctx.diag) {
         // the same launch again with outputs suppressed, counting its word-ANDs
         dspan.stop();
         DevBuf w(8, ctx.stream);
         IGB_CUDA(cudaMemsetAsync(w.p, 0, 8, ctx.stream));
-        IGB_LAUNCH(ctx, (grouped_scan<MODE, true>), (unsigned)blocks, 256, 0, P.dense.as<unsigned long long>(), P.W,
-                   P.n, I->beg.as<uint32_t>(), I->len.as<uint32_t>(), I->toks->as<uint16_t>(), np,
-                   I->order.as<uint32_t>(), I->gid.as<uint32_t>(), goff.as<unsigned long long>(), glen.as<uint32_t>(),
-                   ew.as<uint32_t>(), em.as<unsigned long long>(), scores, acc, support, cover, flags,
-                   w.as<unsigned long long>());
+        launch(std::true_type{}, w.as<unsigned long long>());
         unsigned long long hw = 0;
         read_back(ctx, &hw, w.p, 8);
         dspan.end(hw);
@@ -856,25 +1067,58 @@ void build_pattern_index(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, co
     // group patterns by their three rarest tokens
     int b = 1;
     while ((1u << b) <= L) ++b;  // token ids < L < 2^b - 1 stays free for "absent"
+    const int q = std::max(3, 64 / b);  // tokens in the sort key: the group (3) + as many as fit
     DevBuf key(np * 8, ctx.stream), key2(np * 8, ctx.stream), idx(np * 4, ctx.stream);
     IGB_LAUNCH(ctx, group_keys, grid_for(ctx, np, 256), 256, 0, I.beg.as<uint32_t>(), I.len.as<uint32_t>(),
-               I.toks->as<uint16_t>(), np, b, key.as<unsigned long long>(), idx.as<uint32_t>());
+               I.toks->as<uint16_t>(), np, b, q, key.as<unsigned long long>(), idx.as<uint32_t>());
     size_t tb1 = 0;
     IGB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb1, key.as<unsigned long long>(), key2.as<unsigned long long>(),
-                                             idx.as<uint32_t>(), I.order.as<uint32_t>(), (int64_t)np, 0, 3 * b,
+                                             idx.as<uint32_t>(), I.order.as<uint32_t>(), (int64_t)np, 0, q * b,
                                              ctx.stream));
     DevBuf temp1(tb1, ctx.stream);
     IGB_CUDA(cub::DeviceRadixSort::SortPairs(temp1.p, tb1, key.as<unsigned long long>(), key2.as<unsigned long long>(),
-                                             idx.as<uint32_t>(), I.order.as<uint32_t>(), (int64_t)np, 0, 3 * b,
+                                             idx.as<uint32_t>(), I.order.as<uint32_t>(), (int64_t)np, 0, q * b,
                                              ctx.stream));
-    IGB_LAUNCH(ctx, expand_keys, grid_for(ctx, np, 256), 256, 0, key2.as<unsigned long long>(), np, b);
+    IGB_LAUNCH(ctx, expand_keys, grid_for(ctx, np, 256), 256, 0, key2.as<unsigned long long>(), np, b, q);
     group_ids(ctx, key2.as<unsigned long long>(), np, I);
     tr.mark("group_sort");
 }
 
 // gid (0-based, per sorted position) and gkey (per group) from the sorted keys,
 // then the (t1, t2) parent of every group (pid, pkey)
+void group_ids_only(Ctx& ctx, const unsigned long long* d_sorted_key, size_t np, PatternIndex& I);
+
+void trie_links(Ctx& ctx, PatternIndex& I) {
+    const size_t np = I.np;
+    I.lcp.alloc(std::max<size_t>(np, 1), ctx.stream);
+    I.push.alloc(std::max<size_t>(np, 1) * 4, ctx.stream);
+    I.seg.alloc(std::max<size_t>(np, 1) * 4, ctx.stream);
+    I.nseg.alloc(8, ctx.stream);
+    IGB_CUDA(cudaMemsetAsync(I.nseg.p, 0, 8, ctx.stream));
+    if (np == 0 || I.G == 0) return;
+    DevBuf gstart(I.G * 4, ctx.stream), head(np, ctx.stream), iota(np * 4, ctx.stream), nsel(8, ctx.stream);
+    IGB_LAUNCH(ctx, group_starts, grid_for(ctx, np, 256), 256, 0, I.gid.as<uint32_t>(), np, gstart.as<uint32_t>());
+    IGB_LAUNCH(ctx, trie_lcp, grid_for(ctx, np, 256), 256, 0, I.order.as<uint32_t>(), I.gid.as<uint32_t>(),
+               gstart.as<uint32_t>(), I.beg.as<uint32_t>(), I.len.as<uint32_t>(), I.toks->as<uint16_t>(), np,
+               I.lcp.as<uint8_t>(), head.as<uint8_t>());
+    IGB_LAUNCH(ctx, trie_push, grid_for(ctx, np, 256), 256, 0, I.order.as<uint32_t>(), I.len.as<uint32_t>(),
+               I.lcp.as<uint8_t>(), head.as<uint8_t>(), np, I.push.as<uint32_t>());
+    IGB_LAUNCH(ctx, iota_u32_k, grid_for(ctx, np, 256), 256, 0, iota.as<uint32_t>(), np);
+    size_t tb = 0;
+    IGB_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, iota.as<uint32_t>(), head.as<uint8_t>(), I.seg.as<uint32_t>(),
+                                        nsel.as<int64_t>(), (int64_t)np, ctx.stream));
+    DevBuf temp(tb, ctx.stream);
+    IGB_CUDA(cub::DeviceSelect::Flagged(temp.p, tb, iota.as<uint32_t>(), head.as<uint8_t>(), I.seg.as<uint32_t>(),
+                                        nsel.as<int64_t>(), (int64_t)np, ctx.stream));
+    IGB_CUDA(cudaMemcpyAsync(I.nseg.p, nsel.p, 8, cudaMemcpyDeviceToDevice, ctx.stream));  // int64 count, < 2^32
+}
+
 void group_ids(Ctx& ctx, const unsigned long long* d_sorted_key, size_t np, PatternIndex& I) {
+    group_ids_only(ctx, d_sorted_key, np, I);
+    trie_links(ctx, I);
+}
+
+void group_ids_only(Ctx& ctx, const unsigned long long* d_sorted_key, size_t np, PatternIndex& I) {
     DevBuf head(np, ctx.stream), head32(np * 4, ctx.stream), nsel(8, ctx.stream);
     IGB_LAUNCH(ctx, group_heads<unsigned long long>, grid_for(ctx, np, 256), 256, 0, d_sorted_key, np,
                head.as<uint8_t>(), head32.as<uint32_t>());
