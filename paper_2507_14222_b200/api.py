@@ -100,12 +100,30 @@ class Context:
             _raise(st)
         self.handle = h
         self.device = device
+        self.stream = None  # None = the context's own stream
 
     def set_stream(self, stream) -> None:
         ptr = getattr(stream, "cuda_stream", stream)
         st = lib.ig_ctx_set_stream(self.handle, C.c_void_p(ptr or None))
         if st:
             _raise(st, self)
+        self.stream = ptr or None
+
+    def on_stream(self, stream):
+        """Context manager: run this context's work on `stream` (e.g. torch's
+        current stream, so that buffers torch produced are ordered before the
+        library reads them), restoring the previous stream afterwards."""
+        import contextlib
+
+        @contextlib.contextmanager
+        def cm():
+            prev = self.stream
+            self.set_stream(stream)
+            try:
+                yield self
+            finally:
+                self.set_stream(prev)
+        return cm()
 
     @property
     def launches(self) -> int:

@@ -177,8 +177,7 @@ __device__ __forceinline__ void tile_of(uint64_t t, uint32_t& bi, uint32_t& bj) 
 // Pairs are first deduplicated inside the tile (shared-memory hash of
 // fingerprint tags, exact compare on the tile's staged rows), so only the first
 // pair of each distinct content in a tile probes the device-wide table.
-constexpr int kLocalSlots = 4096;
-constexpr int kLocalProbes = 64;
+constexpr int kLocalSlots = 4096;  // >= TILE * TILE: every pair of a tile fits
 
 // KC > 0: the row width K is a compile-time constant (the common NSL shapes),
 // so the word loops unroll; KC <= 16 also keeps the pair's AND in registers
@@ -279,13 +278,17 @@ pair_enum(const int64_t* __restrict__ X, uint32_t n, int k_rt, int stride, uint6
             // the slot comes from its low bits) | 12-bit pair index within the tile.
             // A tag match is only a hint: the words decide.
             const unsigned int entry = ((unsigned int)(f >> 44) | 1u) << 12 | (unsigned int)q;
-            bool dup = false;
+            bool dup = false, placed = false;
             uint32_t s = (uint32_t)(f & (kLocalSlots - 1));
-            for (int probe = 0; probe < kLocalProbes; ++probe, s = (s + 1) & (kLocalSlots - 1)) {
+            // kLocalSlots >= TILE * TILE pairs: an empty slot always exists, so the probe ends
+            for (;; s = (s + 1) & (kLocalSlots - 1)) {
                 unsigned int cur = local[s];
                 if (cur == 0u) {
                     cur = atomicCAS(local + s, 0u, entry);
-                    if (cur == 0u) break;  // first of its content in this tile
+                    if (cur == 0u) {  // first of its content in this tile
+                        placed = true;
+                        break;
+                    }
                 }
                 if ((cur >> 12) != (entry >> 12)) continue;
                 const int q2 = (int)(cur & 0xfffu);
@@ -303,8 +306,39 @@ pair_enum(const int64_t* __restrict__ X, uint32_t n, int k_rt, int stride, uint6
                     break;
                 }
             }
-            if (dup) continue;
-            table_insert(T, X, k, u, v, f, [&](int w) { return a[w] & b[w]; }, &stage);
+            // the first of its content (placed) is inserted into the device
+            // table after the tile, on full warps (inline, the inserts ran
+            // ~2.5 lanes wide)
+            (void)dup;
+            (void)placed;
+        }
+        // deferred inserts: each warp compacts its 512 local slots in place to
+        // the pair indices they hold, then inserts them 32 at a time
+        __syncthreads();
+        {
+            const int lane = threadIdx.x & 31;
+            constexpr int kPer = kLocalSlots / (kPairThreads / 32);
+            unsigned int* mine = local + (threadIdx.x >> 5) * kPer;
+            int cnt = 0;
+            for (int c0 = 0; c0 < kPer; c0 += 32) {
+                const unsigned int ent = mine[c0 + lane];
+                const unsigned int bal = __ballot_sync(0xffffffffu, ent != 0u);
+                __syncwarp();
+                if (ent) mine[cnt + __popc(bal & ((1u << lane) - 1u))] = ent & 0xfffu;
+                cnt += __popc(bal);
+                __syncwarp();
+            }
+            for (int i = lane; i < cnt; i += 32) {
+                const int qq = (int)mine[i];
+                const int r = qq / TILE, c = qq % TILE;
+                const int64_t* a = sI + r * stride;
+                const int64_t* b = sJ + c * stride;
+                Fp fp;
+#pragma unroll
+                for (int w = 0; w < k; ++w) fp.add((uint64_t)(a[w] & b[w]), sKey[w]);
+                const uint64_t f = (fp.final(k) & T.fp_mask) | 1ull;
+                table_insert(T, X, k, i0 + r, j0 + c, f, [&](int w) { return a[w] & b[w]; }, &stage);
+            }
         }
     }
 }

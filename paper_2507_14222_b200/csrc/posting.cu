@@ -595,6 +595,62 @@ __device__ __forceinline__ void warp_scatter_hits(uint32_t w, unsigned long long
     }
 }
 
+// Difference-array scatter of the runs of every lane's (word w, mask mk): +s
+// at each run's first row, -s after its last.  When the lanes' run counts are
+// uneven, the runs are dealt over all 32 lanes (prefix of the per-lane counts,
+// source lane by binary search, the r-th run = the r-th set bit of the start
+// and end masks), so the REDs issue on full warps; otherwise each lane walks
+// its own runs.  Call with all 32 lanes.
+__device__ __forceinline__ void warp_scatter_runs(uint32_t w, unsigned long long mk, unsigned long long s,
+                                                  unsigned long long* __restrict__ acc) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long st = mk & ~(mk << 1), en = mk & ~(mk >> 1);
+    const uint32_t c = (uint32_t)__popcll(st);
+    const uint32_t mx = __reduce_max_sync(kFull, c);
+    const uint32_t total = __reduce_add_sync(kFull, c);
+    if (mx <= (total + 31) / 32 + 1) {
+        unsigned long long* row = acc + (size_t)w * 64;
+        while (st) {
+            __builtin_assume(en != 0ull);
+            const unsigned long long st1 = st - 1, en1 = en - 1;
+            atomicAdd(row + __popcll(~st & st1), s);
+            atomicAdd(row + 1 + __popcll(~en & en1), 0ull - s);
+            st &= st1;
+            en &= en1;
+        }
+        return;
+    }
+    uint32_t incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const uint32_t excl = incl - c;
+    const uint32_t slo = (uint32_t)st, shi = (uint32_t)(st >> 32), elo = (uint32_t)en, ehi = (uint32_t)(en >> 32);
+    for (uint32_t q0 = 0; q0 < total; q0 += 32) {
+        const uint32_t q = q0 + lane;
+        int L = 0;
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+            const uint32_t e = __shfl_sync(kFull, excl, L + step);
+            if (e <= q) L += step;
+        }
+        const uint32_t r = q - __shfl_sync(kFull, excl, L);
+        const uint32_t alo = __shfl_sync(kFull, slo, L), ahi = __shfl_sync(kFull, shi, L);
+        const uint32_t blo = __shfl_sync(kFull, elo, L), bhi = __shfl_sync(kFull, ehi, L);
+        const uint32_t ww = __shfl_sync(kFull, w, L);
+        if (q < total) {
+            const uint32_t pa = __popc(alo), pb = __popc(blo);
+            const uint32_t sbit = r < pa ? __fns(alo, 0, (int)r + 1) : 32u + __fns(ahi, 0, (int)(r - pa) + 1);
+            const uint32_t ebit = r < pb ? __fns(blo, 0, (int)r + 1) : 32u + __fns(bhi, 0, (int)(r - pb) + 1);
+            unsigned long long* row = acc + (size_t)ww * 64;
+            atomicAdd(row + sbit, s);
+            atomicAdd(row + ebit + 1, 0ull - s);
+        }
+    }
+}
+
 // Warp per pattern (in group order): walk the group's list, AND tokens 3.., then
 // match (difference-array runs) / support (popcount) / cover (any).
 //
@@ -682,6 +738,8 @@ grouped_scan(const unsigned long long* __restrict__ dense, size_t W, size_t n_ro
                         // difference array: +s at each run start, -s after each run end
                         // every run has one start and one end: one loop retires both;
                         // ctz(x) = popc(~x & (x - 1)) avoids the 64-bit find-first sequence
+                        // (each lane walks its own runs: dealing them over the warp,
+                        // warp_scatter_runs, measured 20 % slower here)
                         unsigned long long st = mw & ~(mw << 1), en = mw & ~(mw >> 1);
                         unsigned long long* row = acc + (size_t)w * 64;
                         while (st) {
@@ -728,6 +786,12 @@ grouped_scan(const unsigned long long* __restrict__ dense, size_t W, size_t n_ro
 // all of its tokens, however it was reached.
 constexpr int kTrieStack = 12;
 constexpr int kTrieWarps = 8;
+// Measured slower than grouped_scan on the C3 workload, so it
+// runs only with IG_SCAN=trie; its index links are built only then.
+inline bool trie_enabled() {
+    static const bool on = getenv("IG_SCAN") && std::string(getenv("IG_SCAN")) == "trie";
+    return on;
+}
 
 __device__ __forceinline__ unsigned long long ld_at(const unsigned long long* col, uint32_t byte_off) {
     return __ldg(reinterpret_cast<const unsigned long long*>(reinterpret_cast<const char*>(col) + byte_off));
@@ -744,7 +808,7 @@ trie_scan(const unsigned long long* __restrict__ dense, size_t W, size_t np,
           const int64_t* __restrict__ scores, unsigned long long* __restrict__ acc, int64_t* __restrict__ support_out,
           uint8_t* __restrict__ cover_out, int* __restrict__ flags, unsigned long long* __restrict__ work) {
     __shared__ unsigned long long stk[kTrieWarps][kTrieStack][32];
-    __shared__ uint32_t cnt[kTrieWarps][kTrieSeg];
+    __shared__ uint16_t stok[kTrieWarps][kTrieSeg][32];  // the segment's token lists (first 32 of each)
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const size_t warps = ((size_t)gridDim.x * blockDim.x) >> 5;
     const size_t nseg = (size_t)*nseg_p;
@@ -754,12 +818,25 @@ trie_scan(const unsigned long long* __restrict__ dense, size_t W, size_t np,
     for (size_t sgi = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; sgi < nseg; sgi += warps) {
         const uint32_t b = seg[sgi];
         const uint32_t e = sgi + 1 < nseg ? seg[sgi + 1] : (uint32_t)np;
+        const uint32_t n_in = e - b;  // <= 32: lane j holds position b + j
         const uint32_t g = gid[b];
         const unsigned long long base = goff[g];
         const uint32_t len = glen[g];
-        if (MODE == kSupport && !COUNT)
-            for (uint32_t i = lane; i < e - b; i += 32) cnt[wib][i] = 0u;
-        unsigned long long hit = 0;  // cover: positions of the segment with a covering row
+        // per-pattern metadata, once per segment, in the lanes' registers
+        uint32_t my_p = 0, my_m = 0, my_o = 0, my_l = 0, my_pm = 0;
+        unsigned long long my_s = 0;
+        if ((uint32_t)lane < n_in) {
+            my_p = order[b + lane];
+            my_m = tok_len[my_p];
+            my_o = tok_beg[my_p];
+            my_l = lcp[b + lane];
+            my_pm = push[b + lane];
+            if (MODE == kMatch || MODE == kMatchChecked) my_s = (unsigned long long)scores[my_p];
+            const uint32_t mm = my_m < 32u ? my_m : 32u;
+            for (uint32_t t = 0; t < mm; ++t) stok[wib][lane][t] = toks[my_o + t];
+        }
+        uint32_t my_cnt = 0;          // support of this lane's pattern
+        unsigned long long hit = 0;   // cover: positions of the segment with a covering row
         __syncwarp();
         for (uint32_t j0 = 0; j0 < len; j0 += 32) {
             const uint32_t j = j0 + lane;
@@ -769,14 +846,12 @@ trie_scan(const unsigned long long* __restrict__ dense, size_t W, size_t np,
             int sp = 0;
             unsigned long long sd = 0;  // depth of stack entry q in bits [5q, 5q + 5)
             uint32_t dead = 0xffu;      // a prefix length known empty on every lane
-            for (uint32_t i = b; i < e; ++i) {
-                const uint32_t p = order[i];
-                const uint32_t m = tok_len[p];
-                const uint32_t l = lcp[i];
+            for (uint32_t i = 0; i < n_in; ++i) {
+                const uint32_t m = __shfl_sync(kFull, my_m, i);
+                const uint32_t l = __shfl_sync(kFull, my_l, i);
                 unsigned long long mk = 0ull;
                 if (l < dead) {
                     dead = 0xffu;
-                    const uint32_t o = tok_beg[p];
                     while (sp > 0 && (uint32_t)((sd >> (5 * (sp - 1))) & 31u) > l) --sp;
                     uint32_t d = m < 3 ? m : 3;
                     mk = m0;
@@ -784,26 +859,38 @@ trie_scan(const unsigned long long* __restrict__ dense, size_t W, size_t np,
                         mk = stk[wib][sp - 1][lane];
                         d = l;
                     }
-                    const uint32_t pm = push[i];
-                    const uint32_t toff = (uint32_t)lane < m ? (uint32_t)toks[o + lane] * wb : 0u;
+                    const uint32_t pm = __shfl_sync(kFull, my_pm, i);
                     const uint32_t mlim = m < 32u ? m : 32u;
+                    const uint16_t* tk = stok[wib][i];
                     bool alive = true;
-                    for (; d < mlim; ++d) {
+                    // rounds of up to four independent token loads, a round
+                    // ending where a prefix is kept for a later pattern
+                    while (d < mlim) {
                         if (!__any_sync(kFull, mk != 0ull)) {
                             alive = false;
                             break;
                         }
-                        const uint32_t tb = __shfl_sync(kFull, toff, d);
-                        if (COUNT && mk) ++nand;
-                        if (mk) mk &= ld_at(col, tb);
-                        if (((pm >> (d + 1)) & 1u) && sp < kTrieStack) {
+                        const uint32_t rest = d + 1 < 32u ? pm >> (d + 1) : 0u;
+                        const uint32_t nxt = rest ? d + (uint32_t)__ffs(rest) : 64u;  // next kept depth
+                        const uint32_t en = min(min(d + 4u, mlim), nxt);
+                        if (mk) {
+                            if (COUNT) nand += en - d;
+                            unsigned long long x = ld_at(col, (uint32_t)tk[d] * wb);
+                            if (d + 1 < en) x &= ld_at(col, (uint32_t)tk[d + 1] * wb);
+                            if (d + 2 < en) x &= ld_at(col, (uint32_t)tk[d + 2] * wb);
+                            if (d + 3 < en) x &= ld_at(col, (uint32_t)tk[d + 3] * wb);
+                            mk &= x;
+                        }
+                        d = en;
+                        if (d == nxt && sp < kTrieStack) {
                             stk[wib][sp][lane] = mk;
-                            sd = (sd & ~(31ull << (5 * sp))) | ((unsigned long long)(d + 1) << (5 * sp));
+                            sd = (sd & ~(31ull << (5 * sp))) | ((unsigned long long)d << (5 * sp));
                             ++sp;
                         }
                     }
-                    if (alive) {
-                        for (; d < m; ++d) {  // tokens past 32, from memory (rare)
+                    if (alive && d < m) {  // tokens past 32, from memory (rare)
+                        const uint32_t o = __shfl_sync(kFull, my_o, i);
+                        for (; d < m; ++d) {
                             if (!__any_sync(kFull, mk != 0ull)) break;
                             const uint32_t tt = toks[o + d];
                             if (COUNT && mk) ++nand;
@@ -815,35 +902,24 @@ trie_scan(const unsigned long long* __restrict__ dense, size_t W, size_t np,
                 if (COUNT) continue;
                 if (MODE == kSupport) {
                     const uint32_t c = __reduce_add_sync(kFull, (uint32_t)__popcll(mk));
-                    if (lane == 0 && c) cnt[wib][i - b] += c;
+                    if ((uint32_t)lane == i) my_cnt += c;
                 } else if (MODE == kCover) {
-                    if (__any_sync(kFull, mk != 0ull)) hit |= 1ull << (i - b);
+                    if (__any_sync(kFull, mk != 0ull)) hit |= 1ull << i;
                 } else if (__any_sync(kFull, mk != 0ull)) {
-                    const unsigned long long sc = (unsigned long long)scores[p];
+                    const unsigned long long sc = __shfl_sync(kFull, my_s, i);
                     if (MODE == kMatch) {
-                        unsigned long long st = mk & ~(mk << 1), en = mk & ~(mk >> 1);
-                        unsigned long long* row = acc + (size_t)w * 64;
-                        while (st) {
-                            __builtin_assume(en != 0ull);
-                            const unsigned long long st1 = st - 1, en1 = en - 1;
-                            atomicAdd(row + __popcll(~st & st1), sc);
-                            atomicAdd(row + 1 + __popcll(~en & en1), 0ull - sc);
-                            st &= st1;
-                            en &= en1;
-                        }
+                        warp_scatter_runs(w, mk, sc, acc);
                     } else {
                         warp_scatter_hits<true>(w, mk, sc, acc, ovf);
                     }
                 }
             }
         }
+        __syncwarp();  // stok is rewritten by the next segment
         if (COUNT) continue;
-        __syncwarp();
-        if (MODE == kSupport) {
-            for (uint32_t i = lane; i < e - b; i += 32) support_out[order[b + i]] = (int64_t)cnt[wib][i];
-            __syncwarp();
-        } else if (MODE == kCover) {
-            for (uint32_t i = lane; i < e - b; i += 32) cover_out[order[b + i]] = (uint8_t)((hit >> i) & 1ull);
+        if ((uint32_t)lane < n_in) {
+            if (MODE == kSupport) support_out[my_p] = (int64_t)my_cnt;
+            if (MODE == kCover) cover_out[my_p] = (uint8_t)((hit >> lane) & 1ull);
         }
     }
     if (COUNT) {
@@ -944,8 +1020,7 @@ void launch_scan(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Post
                    glen.as<uint32_t>(), ew.as<uint32_t>(), em.as<unsigned long long>());
     tr.mark("group_lists");
     if (getenv("IG_SCAN_STATS")) scan_stats(ctx, MODE, *I, glen, G, np);
-    static const bool grouped = getenv("IG_SCAN") && std::string(getenv("IG_SCAN")) == "grouped";  // A/B only
-    const bool use_trie = !grouped && I->lcp.p != nullptr;
+    const bool use_trie = trie_enabled() && I->lcp.p != nullptr;
     const size_t blocks = std::min<size_t>((np + 7) / 8, (size_t)ctx.sm_count * 64);
     const size_t tblocks = std::min<size_t>((np + 7) / 8 / 4 + 1, (size_t)ctx.sm_count * 64);
     DiagSpan dspan(ctx, MODE == kSupport ? kDiagSupport : MODE == kCover ? kDiagCover : kDiagMatch);
@@ -1089,6 +1164,7 @@ void build_pattern_index(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, co
 void group_ids_only(Ctx& ctx, const unsigned long long* d_sorted_key, size_t np, PatternIndex& I);
 
 void trie_links(Ctx& ctx, PatternIndex& I) {
+    if (!trie_enabled()) return;
     const size_t np = I.np;
     I.lcp.alloc(std::max<size_t>(np, 1), ctx.stream);
     I.push.alloc(std::max<size_t>(np, 1) * 4, ctx.stream);

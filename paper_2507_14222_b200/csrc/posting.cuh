@@ -58,7 +58,7 @@ struct PatternIndex {
     DevBuf seg;      // np u32: first position of each segment (*nseg of them)
     DevBuf nseg;     // 1 u32, device resident (no host read-back)
 };
-constexpr int kTrieSeg = 64;
+constexpr int kTrieSeg = 32;  // one pattern per lane: the segment's metadata lives in registers
 
 // descending: most frequent first (default: rarest first)
 void make_rank_space(Ctx& ctx, const uint32_t* d_df, uint32_t L, RankSpace& R, bool descending = false);

@@ -24,6 +24,17 @@ from .api import Context, Encoding, IGArithmeticError, KernelConfig, Model, lib
 INT64_MAX = (1 << 63) - 1
 
 
+def _torch_stream(ctx: Context):
+    """The library runs on torch's current stream while it reads or writes
+    tensors torch produced or consumes (all-to-all receive buffers, evidence
+    outputs): a context's own stream is non-blocking and not ordered with it."""
+    import torch
+    if not torch.cuda.is_available() or not hasattr(ctx, "on_stream"):
+        import contextlib
+        return contextlib.nullcontext()
+    return ctx.on_stream(torch.cuda.current_stream())
+
+
 class _CudaArray:
     """Zero-copy view of a library-owned device buffer (``__cuda_array_interface__``)."""
 
@@ -85,8 +96,10 @@ class Shard:
         dA = torch.zeros(n, dtype=torch.int64, device="cuda")
         dN = torch.zeros(n, dtype=torch.int64, device="cuda")
         if n:
-            # the encoding's background index of the test rows (ig_encode_rows) is reused
-            self.model.evidence_encoded_device(tenc, dA.data_ptr(), dN.data_ptr())
+            # the encoding's background index of the test rows (ig_encode_rows) is reused;
+            # torch's stream: dA / dN were zeroed there and are all-reduced there
+            with _torch_stream(self.ctx):
+                self.model.evidence_encoded_device(tenc, dA.data_ptr(), dN.data_ptr())
         return dA, dN
 
     def __del__(self):
@@ -106,6 +119,15 @@ class TorchExchange:
 
     def all_to_all(self, send, counts: list[int]):
         """int64 records grouped by destination; returns (recv tensor, n records)."""
+        recv, n, work = self.all_to_all_start(send, counts)
+        work.wait()
+        return recv, n
+
+    def all_to_all_start(self, send, counts: list[int]):
+        """The same, asynchronously: the counts are exchanged at once (they size
+        the receive buffer), the records in flight when this returns; call
+        .wait() on the returned work before reading recv (on NCCL it orders the
+        current stream after the transfer without blocking the host)."""
         import torch
         world = len(counts)
         dev = self.device
@@ -114,9 +136,9 @@ class TorchExchange:
         self.dist.all_to_all_single(cout, cin, group=self.group)
         rc = cout.tolist()
         recv = torch.empty(max(sum(rc), 1), dtype=torch.int64, device=dev)
-        self.dist.all_to_all_single(recv[:sum(rc)], send, output_split_sizes=rc, input_split_sizes=counts,
-                                    group=self.group)
-        return recv, sum(rc)
+        work = self.dist.all_to_all_single(recv[:sum(rc)], send, output_split_sizes=rc, input_split_sizes=counts,
+                                           group=self.group, async_op=True)
+        return recv, sum(rc), work
 
     def all_gather_ints(self, vals: list[int]) -> list[list[int]]:
         import torch
@@ -147,12 +169,20 @@ def fit_distributed(ctx: Context, enc: Encoding, rank: int, world: int, exchange
                     config: Optional[KernelConfig] = None, shard_factory=None) -> ShardedResult:
     """This rank's part of the sharded fit (call on every rank).  shard_factory
     lets the CPU tests drive the same orchestration with an oracle-backed shard."""
-    sh = (shard_factory or Shard)(ctx, enc, rank, world, config)
-    for cls in range(2):
-        counts, send = sh.enumerate(cls)
-        recv, n = exchange.all_to_all(send, counts)
-        sh.receive(cls, recv, n)
-    totals = sh.finish()
+    with _torch_stream(ctx):
+        sh = (shard_factory or Shard)(ctx, enc, rank, world, config)
+        # class 0's records travel while class 1 enumerates, class 1's while
+        # class 0's owners deduplicate (a class's send buffer stays valid until
+        # that class is enumerated again)
+        c0, s0 = sh.enumerate(0)
+        r0, n0, w0 = exchange.all_to_all_start(s0, c0)
+        c1, s1 = sh.enumerate(1)
+        r1, n1, w1 = exchange.all_to_all_start(s1, c1)
+        w0.wait()
+        sh.receive(0, r0, n0)
+        w1.wait()
+        sh.receive(1, r1, n1)
+        totals = sh.finish()
     _check_totals(exchange.all_gather_ints(list(totals)))
     return ShardedResult(sh, sh.model)
 
@@ -169,12 +199,13 @@ def fit_emulated(ctx: Context, enc: Encoding, world: int, config: Optional[Kerne
     """Run `world` ranks' shards one after another on one device; the all-to-all
     is the concatenation of every rank's send slice for each destination."""
     import torch
-    shards = [Shard(ctx, enc, r, world, config) for r in range(world)]
-    for cls in range(2):
-        outs = [(counts, send.clone()) for counts, send in (sh.enumerate(cls) for sh in shards)]
-        for r, sh in enumerate(shards):
-            parts = [t[sum(counts[:r]):sum(counts[:r]) + counts[r]] for counts, t in outs]
-            recv = torch.cat(parts) if parts else torch.empty(0, dtype=torch.int64, device="cuda")
-            sh.receive(cls, recv, int(recv.numel()))
-    _check_totals([list(sh.finish()) for sh in shards])
+    with _torch_stream(ctx):
+        shards = [Shard(ctx, enc, r, world, config) for r in range(world)]
+        for cls in range(2):
+            outs = [(counts, send.clone()) for counts, send in (sh.enumerate(cls) for sh in shards)]
+            for r, sh in enumerate(shards):
+                parts = [t[sum(counts[:r]):sum(counts[:r]) + counts[r]] for counts, t in outs]
+                recv = torch.cat(parts) if parts else torch.empty(0, dtype=torch.int64, device="cuda")
+                sh.receive(cls, recv, int(recv.numel()))
+        _check_totals([list(sh.finish()) for sh in shards])
     return shards

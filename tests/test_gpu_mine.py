@@ -89,7 +89,11 @@ def test_progress_callback(api):
     X = random_rows(rng, 100, 64, 0.7)
     seen = []
     cs = api.enumerate_candidates(api.PackedMatrix(X, 64), progress=lambda d, t, f: seen.append((d, t, f)))
-    assert seen and seen[-1] == (100 * 99 // 2, 100 * 99 // 2, cs.patterns.rows)
+    # pairs (u <= v) of the distinct rows the device enumerates (include/ig_b200.h); 100 distinct rows here
+    m = len({tuple(r) for r in X.tolist()})
+    total = m * (m + 1) // 2
+    assert seen and seen[-1] == (total, total, cs.patterns.rows)
+    assert all(a[0] <= b[0] and a[2] <= b[2] and a[1] == total for a, b in zip(seen, seen[1:]))
 
 
 @pytest.mark.parametrize("bits", [10, 16])
