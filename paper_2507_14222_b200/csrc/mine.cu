@@ -183,12 +183,12 @@ constexpr int kLocalSlots = 4096;  // >= TILE * TILE: every pair of a tile fits
 // so the word loops unroll; KC <= 16 also keeps the pair's AND in registers
 // for the duplicate check.
 template <int TILE, int KC>
-__global__ void __launch_bounds__(kPairThreads, KC > 0 && KC <= 17 ? 5 : 6)
+__global__ void __launch_bounds__(kPairThreads, KC == 17 ? 4 : KC > 0 && KC <= 16 ? 5 : 6)
 pair_enum(const int64_t* __restrict__ X, uint32_t n, int k_rt, int stride, uint64_t n_tiles, Table T,
           uint64_t tile_begin, uint64_t tile_step, unsigned long long* __restrict__ prog_ctr,
           unsigned long long* __restrict__ prog_host) {
     const int k = KC > 0 ? KC : k_rt;
-    constexpr bool kRegs = KC > 0 && KC <= 16;
+    constexpr bool kRegs = KC > 0 && KC <= 17;
     extern __shared__ int64_t sm[];
     unsigned int* local = reinterpret_cast<unsigned int*>(sm);  // kLocalSlots 32-bit entries
     int64_t* sI = sm + kLocalSlots / 2;

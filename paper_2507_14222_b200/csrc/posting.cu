@@ -651,6 +651,180 @@ __device__ __forceinline__ void warp_scatter_runs(uint32_t w, unsigned long long
     }
 }
 
+// posting word at byte offset byte_off (token * W * 8, precomputed per lane) past col
+__device__ __forceinline__ unsigned long long ld_at(const unsigned long long* col, uint32_t byte_off) {
+    return __ldg(reinterpret_cast<const unsigned long long*>(reinterpret_cast<const char*>(col) + byte_off));
+}
+
+// Warp per PAIR of neighbouring patterns of one (t1, t2, t3) group (the index
+// orders a group's patterns by their further rarest tokens, so neighbours
+// share prefixes): the pair walks the group's list once; per 32-word chunk the
+// tokens both patterns share (3 .. lcp-1) are ANDed once, then the two tails
+// in rounds of two tokens each.  Up to half the list loads and the shared
+// tokens' loads are saved against grouped_scan, with the same four
+// independent loads per round.  A position whose neighbour is in another group
+// runs alone.  Exact: each mask is the list mask ANDed with all its tokens.
+template <int MODE, bool COUNT = false>
+__global__ void __launch_bounds__(256)
+paired_scan(const unsigned long long* __restrict__ dense, size_t W, const uint32_t* __restrict__ tok_beg,
+            const uint32_t* __restrict__ tok_len, const uint16_t* __restrict__ toks, size_t np,
+            const uint32_t* __restrict__ order, const uint32_t* __restrict__ gid,
+            const unsigned long long* __restrict__ goff, const uint32_t* __restrict__ glen,
+            const uint32_t* __restrict__ ew, const unsigned long long* __restrict__ em,
+            const int64_t* __restrict__ scores, unsigned long long* __restrict__ acc,
+            int64_t* __restrict__ support_out, uint8_t* __restrict__ cover_out, int* __restrict__ flags,
+            unsigned long long* __restrict__ work) {
+    const int lane = threadIdx.x & 31;
+    const size_t warps = ((size_t)gridDim.x * blockDim.x) >> 5;
+    const uint32_t Wu = (uint32_t)W, wb = Wu * 8u;
+    bool ovf = false;
+    unsigned long long nand = 0;  // COUNT only
+    const size_t npairs = (np + 1) / 2;
+    for (size_t pi = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; pi < npairs; pi += warps) {
+        const size_t i0 = 2 * pi, i1 = i0 + 1;
+        const uint32_t g0 = gid[i0];
+        const bool same = i1 < np && gid[i1] == g0;
+        // a position whose neighbour is in another group: each runs alone (two passes)
+        for (int pass = 0; pass < (i1 < np && !same ? 2 : 1); ++pass) {
+            const size_t ia = pass ? i1 : i0;
+            const uint32_t g = pass ? gid[i1] : g0;
+            const uint32_t pa = order[ia];
+            const uint32_t pb = same ? order[i1] : 0u;
+            const uint32_t ma = tok_len[pa], mb = same ? tok_len[pb] : 0u;
+            const uint32_t oa = tok_beg[pa], ob = same ? tok_beg[pb] : 0u;
+            const uint32_t ta0 = ma ? (uint32_t)toks[oa] : 0u;
+            const uint32_t tla = (uint32_t)lane < ma ? (uint32_t)toks[oa + lane] : ta0;
+            const uint32_t tlb = (uint32_t)lane < mb ? (uint32_t)toks[ob + lane] : 0u;
+            const uint32_t offa = tla * wb, offb = tlb * wb;
+            // shared prefix: tokens 0 .. lcp-1 equal (>= 3 within a group)
+            const uint32_t mab = min(min(ma, mb), 32u);
+            const uint32_t dif = __ballot_sync(kFull, (uint32_t)lane < mab && tla != tlb);
+            const uint32_t lcp = same ? (dif ? (uint32_t)__ffs(dif) - 1u : mab) : min(ma, 32u);
+            const unsigned long long base = goff[g];
+            const uint32_t len = glen[g];
+            unsigned long long sa = 0, sb = 0;
+            if (MODE == kMatch || MODE == kMatchChecked) {
+                sa = (unsigned long long)scores[pa];
+                if (same) sb = (unsigned long long)scores[pb];
+            }
+            uint32_t cnta = 0, cntb = 0;
+            bool hita = false, hitb = !same;  // cover: a pattern with a covering row is done
+            for (uint32_t j0 = 0; j0 < len; j0 += 32) {
+                const uint32_t j = j0 + lane;
+                const uint32_t w = j < len ? ew[base + j] : 0u;
+                unsigned long long mk = j < len ? em[base + j] : 0ull;
+                const unsigned long long* col = dense + w;
+                // shared tokens 3 .. lcp-1, four per round
+                uint32_t t = 3;
+                for (; t < lcp; t += 4) {
+                    const bool live = mk != 0ull;
+                    if (!__any_sync(kFull, live)) break;
+                    const uint32_t e = min(t + 4u, lcp);
+                    const uint32_t b0 = __shfl_sync(kFull, offa, t & 31u), b1 = __shfl_sync(kFull, offa, (t + 1) & 31u);
+                    const uint32_t b2 = __shfl_sync(kFull, offa, (t + 2) & 31u), b3 = __shfl_sync(kFull, offa, (t + 3) & 31u);
+                    if (live) {
+                        if (COUNT) nand += e - t;
+                        unsigned long long x = ld_at(col, b0);
+                        if (t + 1 < e) x &= ld_at(col, b1);
+                        if (t + 2 < e) x &= ld_at(col, b2);
+                        if (t + 3 < e) x &= ld_at(col, b3);
+                        mk &= x;
+                    }
+                }
+                const bool pre_dead = t < lcp;  // the shared prefix is empty on every lane
+                unsigned long long ka = (hita || pre_dead) ? 0ull : mk;
+                unsigned long long kb = (hitb || pre_dead) ? 0ull : mk;
+                // the two tails, two tokens of each per round
+                uint32_t ua = lcp, ub = lcp;
+                const uint32_t ea = min(ma, 32u), eb = min(mb, 32u);
+                for (;;) {
+                    const bool la = ka != 0ull && ua < ea, lb = kb != 0ull && ub < eb;
+                    const unsigned int bal = __ballot_sync(kFull, la) | (__ballot_sync(kFull, lb) ? 2u : 0u);
+                    if (!bal) break;
+                    const unsigned int ba = __ballot_sync(kFull, la);
+                    const uint32_t a0 = __shfl_sync(kFull, offa, ua & 31u), a1 = __shfl_sync(kFull, offa, (ua + 1) & 31u);
+                    const uint32_t c0 = __shfl_sync(kFull, offb, ub & 31u), c1 = __shfl_sync(kFull, offb, (ub + 1) & 31u);
+                    if (la) {
+                        if (COUNT) nand += min(2u, ea - ua);
+                        unsigned long long x = ld_at(col, a0);
+                        if (ua + 1 < ea) x &= ld_at(col, a1);
+                        ka &= x;
+                    }
+                    if (lb) {
+                        if (COUNT) nand += min(2u, eb - ub);
+                        unsigned long long x = ld_at(col, c0);
+                        if (ub + 1 < eb) x &= ld_at(col, c1);
+                        kb &= x;
+                    }
+                    if (ba) ua += 2;
+                    if (bal & 2u) ub += 2;
+                }
+                // tokens past 32 (rare), from memory
+                if (ma > 32u && __any_sync(kFull, ka != 0ull))
+                    for (uint32_t q = 32; q < ma; ++q) {
+                        if (!__any_sync(kFull, ka != 0ull)) break;
+                        if (COUNT && ka) ++nand;
+                        if (ka) ka &= col[(size_t)toks[oa + q] * Wu];
+                    }
+                if (mb > 32u && __any_sync(kFull, kb != 0ull))
+                    for (uint32_t q = 32; q < mb; ++q) {
+                        if (!__any_sync(kFull, kb != 0ull)) break;
+                        if (COUNT && kb) ++nand;
+                        if (kb) kb &= col[(size_t)toks[ob + q] * Wu];
+                    }
+                if (COUNT) continue;
+                if (MODE == kSupport) {
+                    cnta += __popcll(ka);
+                    cntb += __popcll(kb);
+                } else if (MODE == kCover) {
+                    if (__any_sync(kFull, ka != 0ull)) hita = true;
+                    if (__any_sync(kFull, kb != 0ull)) hitb = true;
+                    if (hita && hitb) break;
+                } else {
+                    for (int side = 0; side < 2; ++side) {
+                        const unsigned long long kk = side ? kb : ka;
+                        if (!__any_sync(kFull, kk != 0ull)) continue;
+                        const unsigned long long sc = side ? sb : sa;
+                        if (MODE == kMatch) {
+                            unsigned long long st = kk & ~(kk << 1), en = kk & ~(kk >> 1);
+                            unsigned long long* row = acc + (size_t)w * 64;
+                            while (st) {
+                                __builtin_assume(en != 0ull);
+                                const unsigned long long st1 = st - 1, en1 = en - 1;
+                                atomicAdd(row + __popcll(~st & st1), sc);
+                                atomicAdd(row + 1 + __popcll(~en & en1), 0ull - sc);
+                                st &= st1;
+                                en &= en1;
+                            }
+                        } else {
+                            warp_scatter_hits<true>(w, kk, sc, acc, ovf);
+                        }
+                    }
+                }
+            }
+            if (COUNT) continue;
+            if (MODE == kSupport) {
+                const uint32_t ca = __reduce_add_sync(kFull, cnta), cb = __reduce_add_sync(kFull, cntb);
+                if (lane == 0) {
+                    support_out[pa] = (int64_t)ca;
+                    if (same) support_out[pb] = (int64_t)cb;
+                }
+            } else if (MODE == kCover) {
+                if (lane == 0) {
+                    cover_out[pa] = hita ? 1 : 0;
+                    if (same) cover_out[pb] = hitb ? 1 : 0;
+                }
+            }
+        }
+    }
+    if (COUNT) {
+        for (int o2 = 16; o2; o2 >>= 1) nand += __shfl_xor_sync(kFull, nand, o2);
+        if (lane == 0 && nand) atomicAdd(work, nand);
+        return;
+    }
+    if (MODE == kMatchChecked && ovf) atomicOr(flags, 1);
+}
+
 // Warp per pattern (in group order): walk the group's list, AND tokens 3.., then
 // match (difference-array runs) / support (popcount) / cover (any).
 //
@@ -793,9 +967,6 @@ inline bool trie_enabled() {
     return on;
 }
 
-__device__ __forceinline__ unsigned long long ld_at(const unsigned long long* col, uint32_t byte_off) {
-    return __ldg(reinterpret_cast<const unsigned long long*>(reinterpret_cast<const char*>(col) + byte_off));
-}
 
 template <int MODE, bool COUNT>
 __global__ void __launch_bounds__(kTrieWarps * 32)
@@ -1021,12 +1192,20 @@ void launch_scan(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Post
     tr.mark("group_lists");
     if (getenv("IG_SCAN_STATS")) scan_stats(ctx, MODE, *I, glen, G, np);
     const bool use_trie = trie_enabled() && I->lcp.p != nullptr;
+    static const bool single = getenv("IG_SCAN") && std::string(getenv("IG_SCAN")) == "grouped";  // A/B only
+    const bool use_pair = !use_trie && !single;
     const size_t blocks = std::min<size_t>((np + 7) / 8, (size_t)ctx.sm_count * 64);
     const size_t tblocks = std::min<size_t>((np + 7) / 8 / 4 + 1, (size_t)ctx.sm_count * 64);
     DiagSpan dspan(ctx, MODE == kSupport ? kDiagSupport : MODE == kCover ? kDiagCover : kDiagMatch);
     auto launch = [&](auto count_tag, unsigned long long* work) {
         constexpr bool C = decltype(count_tag)::value;
-        if (use_trie)
+        if (use_pair)
+            IGB_LAUNCH(ctx, (paired_scan<MODE, C>), (unsigned)std::min<size_t>((np + 15) / 16, (size_t)ctx.sm_count * 64),
+                       256, 0, P.dense.as<unsigned long long>(), P.W, I->beg.as<uint32_t>(), I->len.as<uint32_t>(),
+                       I->toks->as<uint16_t>(), np, I->order.as<uint32_t>(), I->gid.as<uint32_t>(),
+                       goff.as<unsigned long long>(), glen.as<uint32_t>(), ew.as<uint32_t>(),
+                       em.as<unsigned long long>(), scores, acc, support, cover, flags, work);
+        else if (use_trie)
             IGB_LAUNCH(ctx, (trie_scan<MODE, C>), (unsigned)tblocks, kTrieWarps * 32, 0,
                        P.dense.as<unsigned long long>(), P.W, np, I->beg.as<uint32_t>(), I->len.as<uint32_t>(),
                        I->toks->as<uint16_t>(), I->order.as<uint32_t>(), I->gid.as<uint32_t>(), I->lcp.as<uint8_t>(),
@@ -1041,7 +1220,7 @@ void launch_scan(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Post
                        cover, flags, work);
     };
     launch(std::false_type{}, nullptr);
-    tr.mark(use_trie ? "trie_scan" : "grouped_scan");
+    tr.mark(use_pair ? "paired_scan" : use_trie ? "trie_scan" : "grouped_scan");
     if (ctx.diag) {
         // the same launch again with outputs suppressed, counting its word-ANDs
         dspan.stop();

@@ -11,7 +11,7 @@ from paper_2507_14222_b200 import api, synth
 csv = synth.nsl_csv(148517, seed=2507)
 ctx = api.Context(0)
 ctx.set_stream(torch.cuda.current_stream().cuda_stream)
-table = api.read_csv(csv); n = table.rows; ntr = n // 10
+table = api.read_csv(csv); n = table.rows; ntr = int(os.environ.get("RATIO", "1")) * n // 10
 tr, te = table.slice(0, ntr), table.slice(ntr, n)
 schema = api.infer_schema(tr, "label", decimals=1)
 dtr = api.Columns(tr, schema, True).upload(ctx); dte = api.Columns(te, schema, False).upload(ctx)
@@ -46,6 +46,12 @@ for s, e, name in iv:
         cur_e = max(cur_e, e)
 busy += cur_e - cur_s
 gaps.sort(reverse=True)
-print(json.dumps({"kernels": len(iv), "span_us": round(span, 1), "busy_us": round(busy, 1),
+per = {}
+for s, e, name in iv:
+    k = name.split("(")[0][-60:]
+    per[k] = per.get(k, 0.0) + (e - s)
+top = sorted(per.items(), key=lambda x: -x[1])[:15]
+print(json.dumps({"ratio": os.environ.get("RATIO", "1"), "kernels": len(iv), "span_us": round(span, 1), "busy_us": round(busy, 1),
+                  "kernel_us_top": [(k, round(v, 1)) for k, v in top],
                   "busy_frac": round(busy / span, 3), "idle_us": round(span - busy, 1),
                   "largest_gaps_us_before": [(round(g, 1), nm[:60]) for g, nm in gaps[:12]]}))
