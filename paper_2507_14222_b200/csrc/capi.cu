@@ -328,8 +328,7 @@ void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m, bool enumerate 
                              src.as<uint32_t>());
             igb::subset_pattern_index(cx, CI[c], src.as<uint32_t>(), n, m.pidx[c]);
             for (DevBuf* b : {&m.pidx[c].beg, &m.pidx[c].len, m.pidx[c].toks.get(), &m.pidx[c].order, &m.pidx[c].gid,
-                              &m.pidx[c].gkey, &m.pidx[c].pid, &m.pidx[c].pkey, &m.pidx[c].lcp, &m.pidx[c].push,
-                              &m.pidx[c].seg, &m.pidx[c].nseg})
+                              &m.pidx[c].gkey, &m.pidx[c].pid, &m.pidx[c].pkey})
                 b->persist();
             tr.mark("pure_index");
             if (fused) {

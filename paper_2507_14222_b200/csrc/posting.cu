@@ -321,11 +321,6 @@ __global__ void sub_lists(const uint32_t* __restrict__ src_beg, const uint32_t* 
     }
 }
 
-__global__ void iota_u32_k(uint32_t* __restrict__ p, size_t n) {
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
-        p[i] = (uint32_t)i;
-}
-
 __global__ void fill_u32(uint32_t* __restrict__ p, size_t n, uint32_t v) {
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] = v;
 }
@@ -367,7 +362,8 @@ constexpr uint32_t kNoTok = 0xffffu;
 // sort key of a pattern: its q rarest tokens (t1, t2, t3, t4, ...; absent = all
 // ones), b bits each, t1 most significant (q*b <= 64 bits, one radix sort).
 // The group is (t1, t2, t3); the further tokens order the patterns inside a
-// group so that neighbours share prefixes (the trie scan).  expand_keys
+// group so that neighbours share prefixes (consecutive warps then read the
+// same posting words).  expand_keys
 // restores the group part as (t1 << 32) | (t2 << 16) | t3 with kNoTok, which
 // sorts identically.
 __global__ void group_keys(const uint32_t* __restrict__ tok_beg, const uint32_t* __restrict__ tok_len,
@@ -391,55 +387,6 @@ __global__ void expand_keys(unsigned long long* __restrict__ key, size_t n, int 
         for (auto& v : t)
             if (v == none) v = kNoTok;
         key[i] = (t[0] << 32) | (t[1] << 16) | t[2];
-    }
-}
-
-// ---- prefix-trie links (PatternIndex::lcp / push / seg)
-// group start position of every group
-__global__ void group_starts(const uint32_t* __restrict__ gid, size_t np, uint32_t* __restrict__ gstart) {
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < np; i += (size_t)gridDim.x * blockDim.x)
-        if (i == 0 || gid[i] != gid[i - 1]) gstart[gid[i]] = (uint32_t)i;
-}
-
-// lcp of every position with its predecessor in the segment; segment heads
-__global__ void trie_lcp(const uint32_t* __restrict__ order, const uint32_t* __restrict__ gid,
-                         const uint32_t* __restrict__ gstart, const uint32_t* __restrict__ tok_beg,
-                         const uint32_t* __restrict__ tok_len, const uint16_t* __restrict__ toks, size_t np,
-                         uint8_t* __restrict__ lcp, uint8_t* __restrict__ head) {
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < np; i += (size_t)gridDim.x * blockDim.x) {
-        const uint32_t p = order[i], m = tok_len[p];
-        const bool h = ((i - gstart[gid[i]]) % kTrieSeg) == 0;
-        uint32_t l = m < 3 ? m : 3;
-        if (!h) {
-            const uint32_t q = order[i - 1], mq = tok_len[q];
-            const uint16_t* a = toks + tok_beg[p];
-            const uint16_t* c = toks + tok_beg[q];
-            const uint32_t lim = min(min(m, mq), 31u);
-            l = 0;
-            while (l < lim && a[l] == c[l]) ++l;
-            // same group: the first three tokens agree (or the shorter list ended)
-        }
-        lcp[i] = (uint8_t)l;
-        head[i] = h ? 1 : 0;
-    }
-}
-
-// push[i]: depths d (lcp[i] < d <= min(|b_i|, 31)) of position i's scan that a
-// later position j of the segment restarts from: lcp[j] == d with every
-// position strictly between them sharing at least d tokens (so the depth-d
-// prefix is the same) — the first position to compute a prefix keeps it.
-__global__ void trie_push(const uint32_t* __restrict__ order, const uint32_t* __restrict__ tok_len,
-                          const uint8_t* __restrict__ lcp, const uint8_t* __restrict__ head, size_t np,
-                          uint32_t* __restrict__ push) {
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < np; i += (size_t)gridDim.x * blockDim.x) {
-        const uint32_t li = lcp[i], mi = min(tok_len[order[i]], 31u);
-        uint32_t bits = 0, rm = 0xffu;
-        for (size_t j = i + 1; j < np && !head[j] && rm > li; ++j) {
-            const uint32_t lj = lcp[j];
-            if (lj > li && lj <= rm && lj <= mi) bits |= 1u << lj;
-            rm = min(rm, lj);
-        }
-        push[i] = bits;
     }
 }
 
@@ -595,236 +542,6 @@ __device__ __forceinline__ void warp_scatter_hits(uint32_t w, unsigned long long
     }
 }
 
-// Difference-array scatter of the runs of every lane's (word w, mask mk): +s
-// at each run's first row, -s after its last.  When the lanes' run counts are
-// uneven, the runs are dealt over all 32 lanes (prefix of the per-lane counts,
-// source lane by binary search, the r-th run = the r-th set bit of the start
-// and end masks), so the REDs issue on full warps; otherwise each lane walks
-// its own runs.  Call with all 32 lanes.
-__device__ __forceinline__ void warp_scatter_runs(uint32_t w, unsigned long long mk, unsigned long long s,
-                                                  unsigned long long* __restrict__ acc) {
-    const int lane = threadIdx.x & 31;
-    unsigned long long st = mk & ~(mk << 1), en = mk & ~(mk >> 1);
-    const uint32_t c = (uint32_t)__popcll(st);
-    const uint32_t mx = __reduce_max_sync(kFull, c);
-    const uint32_t total = __reduce_add_sync(kFull, c);
-    if (mx <= (total + 31) / 32 + 1) {
-        unsigned long long* row = acc + (size_t)w * 64;
-        while (st) {
-            __builtin_assume(en != 0ull);
-            const unsigned long long st1 = st - 1, en1 = en - 1;
-            atomicAdd(row + __popcll(~st & st1), s);
-            atomicAdd(row + 1 + __popcll(~en & en1), 0ull - s);
-            st &= st1;
-            en &= en1;
-        }
-        return;
-    }
-    uint32_t incl = c;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(kFull, incl, o);
-        if (lane >= o) incl += y;
-    }
-    const uint32_t excl = incl - c;
-    const uint32_t slo = (uint32_t)st, shi = (uint32_t)(st >> 32), elo = (uint32_t)en, ehi = (uint32_t)(en >> 32);
-    for (uint32_t q0 = 0; q0 < total; q0 += 32) {
-        const uint32_t q = q0 + lane;
-        int L = 0;
-#pragma unroll
-        for (int step = 16; step >= 1; step >>= 1) {
-            const uint32_t e = __shfl_sync(kFull, excl, L + step);
-            if (e <= q) L += step;
-        }
-        const uint32_t r = q - __shfl_sync(kFull, excl, L);
-        const uint32_t alo = __shfl_sync(kFull, slo, L), ahi = __shfl_sync(kFull, shi, L);
-        const uint32_t blo = __shfl_sync(kFull, elo, L), bhi = __shfl_sync(kFull, ehi, L);
-        const uint32_t ww = __shfl_sync(kFull, w, L);
-        if (q < total) {
-            const uint32_t pa = __popc(alo), pb = __popc(blo);
-            const uint32_t sbit = r < pa ? __fns(alo, 0, (int)r + 1) : 32u + __fns(ahi, 0, (int)(r - pa) + 1);
-            const uint32_t ebit = r < pb ? __fns(blo, 0, (int)r + 1) : 32u + __fns(bhi, 0, (int)(r - pb) + 1);
-            unsigned long long* row = acc + (size_t)ww * 64;
-            atomicAdd(row + sbit, s);
-            atomicAdd(row + ebit + 1, 0ull - s);
-        }
-    }
-}
-
-// posting word at byte offset byte_off (token * W * 8, precomputed per lane) past col
-__device__ __forceinline__ unsigned long long ld_at(const unsigned long long* col, uint32_t byte_off) {
-    return __ldg(reinterpret_cast<const unsigned long long*>(reinterpret_cast<const char*>(col) + byte_off));
-}
-
-// Warp per PAIR of neighbouring patterns of one (t1, t2, t3) group (the index
-// orders a group's patterns by their further rarest tokens, so neighbours
-// share prefixes): the pair walks the group's list once; per 32-word chunk the
-// tokens both patterns share (3 .. lcp-1) are ANDed once, then the two tails
-// in rounds of two tokens each.  Up to half the list loads and the shared
-// tokens' loads are saved against grouped_scan, with the same four
-// independent loads per round.  A position whose neighbour is in another group
-// runs alone.  Exact: each mask is the list mask ANDed with all its tokens.
-template <int MODE, bool COUNT = false>
-__global__ void __launch_bounds__(256)
-paired_scan(const unsigned long long* __restrict__ dense, size_t W, const uint32_t* __restrict__ tok_beg,
-            const uint32_t* __restrict__ tok_len, const uint16_t* __restrict__ toks, size_t np,
-            const uint32_t* __restrict__ order, const uint32_t* __restrict__ gid,
-            const unsigned long long* __restrict__ goff, const uint32_t* __restrict__ glen,
-            const uint32_t* __restrict__ ew, const unsigned long long* __restrict__ em,
-            const int64_t* __restrict__ scores, unsigned long long* __restrict__ acc,
-            int64_t* __restrict__ support_out, uint8_t* __restrict__ cover_out, int* __restrict__ flags,
-            unsigned long long* __restrict__ work) {
-    const int lane = threadIdx.x & 31;
-    const size_t warps = ((size_t)gridDim.x * blockDim.x) >> 5;
-    const uint32_t Wu = (uint32_t)W, wb = Wu * 8u;
-    bool ovf = false;
-    unsigned long long nand = 0;  // COUNT only
-    const size_t npairs = (np + 1) / 2;
-    for (size_t pi = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; pi < npairs; pi += warps) {
-        const size_t i0 = 2 * pi, i1 = i0 + 1;
-        const uint32_t g0 = gid[i0];
-        const bool same = i1 < np && gid[i1] == g0;
-        // a position whose neighbour is in another group: each runs alone (two passes)
-        for (int pass = 0; pass < (i1 < np && !same ? 2 : 1); ++pass) {
-            const size_t ia = pass ? i1 : i0;
-            const uint32_t g = pass ? gid[i1] : g0;
-            const uint32_t pa = order[ia];
-            const uint32_t pb = same ? order[i1] : 0u;
-            const uint32_t ma = tok_len[pa], mb = same ? tok_len[pb] : 0u;
-            const uint32_t oa = tok_beg[pa], ob = same ? tok_beg[pb] : 0u;
-            const uint32_t ta0 = ma ? (uint32_t)toks[oa] : 0u;
-            const uint32_t tla = (uint32_t)lane < ma ? (uint32_t)toks[oa + lane] : ta0;
-            const uint32_t tlb = (uint32_t)lane < mb ? (uint32_t)toks[ob + lane] : 0u;
-            const uint32_t offa = tla * wb, offb = tlb * wb;
-            // shared prefix: tokens 0 .. lcp-1 equal (>= 3 within a group)
-            const uint32_t mab = min(min(ma, mb), 32u);
-            const uint32_t dif = __ballot_sync(kFull, (uint32_t)lane < mab && tla != tlb);
-            const uint32_t lcp = same ? (dif ? (uint32_t)__ffs(dif) - 1u : mab) : min(ma, 32u);
-            const unsigned long long base = goff[g];
-            const uint32_t len = glen[g];
-            unsigned long long sa = 0, sb = 0;
-            if (MODE == kMatch || MODE == kMatchChecked) {
-                sa = (unsigned long long)scores[pa];
-                if (same) sb = (unsigned long long)scores[pb];
-            }
-            uint32_t cnta = 0, cntb = 0;
-            bool hita = false, hitb = !same;  // cover: a pattern with a covering row is done
-            for (uint32_t j0 = 0; j0 < len; j0 += 32) {
-                const uint32_t j = j0 + lane;
-                const uint32_t w = j < len ? ew[base + j] : 0u;
-                unsigned long long mk = j < len ? em[base + j] : 0ull;
-                const unsigned long long* col = dense + w;
-                // shared tokens 3 .. lcp-1, four per round
-                uint32_t t = 3;
-                for (; t < lcp; t += 4) {
-                    const bool live = mk != 0ull;
-                    if (!__any_sync(kFull, live)) break;
-                    const uint32_t e = min(t + 4u, lcp);
-                    const uint32_t b0 = __shfl_sync(kFull, offa, t & 31u), b1 = __shfl_sync(kFull, offa, (t + 1) & 31u);
-                    const uint32_t b2 = __shfl_sync(kFull, offa, (t + 2) & 31u), b3 = __shfl_sync(kFull, offa, (t + 3) & 31u);
-                    if (live) {
-                        if (COUNT) nand += e - t;
-                        unsigned long long x = ld_at(col, b0);
-                        if (t + 1 < e) x &= ld_at(col, b1);
-                        if (t + 2 < e) x &= ld_at(col, b2);
-                        if (t + 3 < e) x &= ld_at(col, b3);
-                        mk &= x;
-                    }
-                }
-                const bool pre_dead = t < lcp;  // the shared prefix is empty on every lane
-                unsigned long long ka = (hita || pre_dead) ? 0ull : mk;
-                unsigned long long kb = (hitb || pre_dead) ? 0ull : mk;
-                // the two tails, two tokens of each per round
-                uint32_t ua = lcp, ub = lcp;
-                const uint32_t ea = min(ma, 32u), eb = min(mb, 32u);
-                for (;;) {
-                    const bool la = ka != 0ull && ua < ea, lb = kb != 0ull && ub < eb;
-                    const unsigned int bal = __ballot_sync(kFull, la) | (__ballot_sync(kFull, lb) ? 2u : 0u);
-                    if (!bal) break;
-                    const unsigned int ba = __ballot_sync(kFull, la);
-                    const uint32_t a0 = __shfl_sync(kFull, offa, ua & 31u), a1 = __shfl_sync(kFull, offa, (ua + 1) & 31u);
-                    const uint32_t c0 = __shfl_sync(kFull, offb, ub & 31u), c1 = __shfl_sync(kFull, offb, (ub + 1) & 31u);
-                    if (la) {
-                        if (COUNT) nand += min(2u, ea - ua);
-                        unsigned long long x = ld_at(col, a0);
-                        if (ua + 1 < ea) x &= ld_at(col, a1);
-                        ka &= x;
-                    }
-                    if (lb) {
-                        if (COUNT) nand += min(2u, eb - ub);
-                        unsigned long long x = ld_at(col, c0);
-                        if (ub + 1 < eb) x &= ld_at(col, c1);
-                        kb &= x;
-                    }
-                    if (ba) ua += 2;
-                    if (bal & 2u) ub += 2;
-                }
-                // tokens past 32 (rare), from memory
-                if (ma > 32u && __any_sync(kFull, ka != 0ull))
-                    for (uint32_t q = 32; q < ma; ++q) {
-                        if (!__any_sync(kFull, ka != 0ull)) break;
-                        if (COUNT && ka) ++nand;
-                        if (ka) ka &= col[(size_t)toks[oa + q] * Wu];
-                    }
-                if (mb > 32u && __any_sync(kFull, kb != 0ull))
-                    for (uint32_t q = 32; q < mb; ++q) {
-                        if (!__any_sync(kFull, kb != 0ull)) break;
-                        if (COUNT && kb) ++nand;
-                        if (kb) kb &= col[(size_t)toks[ob + q] * Wu];
-                    }
-                if (COUNT) continue;
-                if (MODE == kSupport) {
-                    cnta += __popcll(ka);
-                    cntb += __popcll(kb);
-                } else if (MODE == kCover) {
-                    if (__any_sync(kFull, ka != 0ull)) hita = true;
-                    if (__any_sync(kFull, kb != 0ull)) hitb = true;
-                    if (hita && hitb) break;
-                } else {
-                    for (int side = 0; side < 2; ++side) {
-                        const unsigned long long kk = side ? kb : ka;
-                        if (!__any_sync(kFull, kk != 0ull)) continue;
-                        const unsigned long long sc = side ? sb : sa;
-                        if (MODE == kMatch) {
-                            unsigned long long st = kk & ~(kk << 1), en = kk & ~(kk >> 1);
-                            unsigned long long* row = acc + (size_t)w * 64;
-                            while (st) {
-                                __builtin_assume(en != 0ull);
-                                const unsigned long long st1 = st - 1, en1 = en - 1;
-                                atomicAdd(row + __popcll(~st & st1), sc);
-                                atomicAdd(row + 1 + __popcll(~en & en1), 0ull - sc);
-                                st &= st1;
-                                en &= en1;
-                            }
-                        } else {
-                            warp_scatter_hits<true>(w, kk, sc, acc, ovf);
-                        }
-                    }
-                }
-            }
-            if (COUNT) continue;
-            if (MODE == kSupport) {
-                const uint32_t ca = __reduce_add_sync(kFull, cnta), cb = __reduce_add_sync(kFull, cntb);
-                if (lane == 0) {
-                    support_out[pa] = (int64_t)ca;
-                    if (same) support_out[pb] = (int64_t)cb;
-                }
-            } else if (MODE == kCover) {
-                if (lane == 0) {
-                    cover_out[pa] = hita ? 1 : 0;
-                    if (same) cover_out[pb] = hitb ? 1 : 0;
-                }
-            }
-        }
-    }
-    if (COUNT) {
-        for (int o2 = 16; o2; o2 >>= 1) nand += __shfl_xor_sync(kFull, nand, o2);
-        if (lane == 0 && nand) atomicAdd(work, nand);
-        return;
-    }
-    if (MODE == kMatchChecked && ovf) atomicOr(flags, 1);
-}
-
 // Warp per pattern (in group order): walk the group's list, AND tokens 3.., then
 // match (difference-array runs) / support (popcount) / cover (any).
 //
@@ -832,6 +549,9 @@ paired_scan(const unsigned long long* __restrict__ dense, size_t W, const uint32
 // bytes, the address formed by one IMAD.WIDE.U32 on the FMA pipe (the
 // multiplier is a runtime value, so it is not strength-reduced into the
 // 64-bit add + LEA pair that would land on the ALU pipe this kernel saturates).
+// Through L1 (ld.global.nc): 64 % of the sectors hit there (neighbouring
+// patterns share tokens); L2-only loads (.cg, .L1::no_allocate) measured
+// 40-80 % slower.
 __device__ __forceinline__ unsigned long long ld_tok(const unsigned long long* col, uint32_t t, uint32_t wbytes) {
     unsigned long long v;
     asm("{\n\t.reg .u64 a;\n\tmad.wide.u32 a, %1, %2, %3;\n\tld.global.nc.u64 %0, [a];\n\t}"
@@ -912,8 +632,8 @@ grouped_scan(const unsigned long long* __restrict__ dense, size_t W, size_t n_ro
                         // difference array: +s at each run start, -s after each run end
                         // every run has one start and one end: one loop retires both;
                         // ctz(x) = popc(~x & (x - 1)) avoids the 64-bit find-first sequence
-                        // (each lane walks its own runs: dealing them over the warp,
-                        // warp_scatter_runs, measured 20 % slower here)
+                        // (each lane walks its own runs: dealing the runs over the
+                        // whole warp measured 20 % slower)
                         unsigned long long st = mw & ~(mw << 1), en = mw & ~(mw >> 1);
                         unsigned long long* row = acc + (size_t)w * 64;
                         while (st) {
@@ -936,161 +656,6 @@ grouped_scan(const unsigned long long* __restrict__ dense, size_t W, size_t n_ro
             if (lane == 0) support_out[p] = (int64_t)cnt;
         } else if (MODE == kCover) {
             if (lane == 0) cover_out[p] = hit ? 1 : 0;
-        }
-    }
-    if (COUNT) {
-        for (int o2 = 16; o2; o2 >>= 1) nand += __shfl_xor_sync(kFull, nand, o2);
-        if (lane == 0 && nand) atomicAdd(work, nand);
-        return;
-    }
-    if (MODE == kMatchChecked && ovf) atomicOr(flags, 1);
-}
-
-// Prefix-trie scan (the default for support, coverage and the matcher): one
-// warp per segment (<= kTrieSeg consecutive positions of one (t1, t2, t3)
-// group, sorted by their further rarest tokens, PatternIndex::lcp / push).
-// The warp walks the group's list 32 words at a time; for each chunk it runs
-// the segment's patterns in order, each starting from the deepest prefix mask
-// it shares with an earlier pattern of the segment — kept on a small per-warp
-// stack in shared memory — instead of from the list mask, so a token that
-// neighbouring patterns share is loaded and ANDed once per chunk, and the
-// list words are loaded once per segment instead of once per pattern.  A
-// prefix that is empty on every lane empties every pattern extending it, which
-// are then skipped.  Exact: each pattern's mask is the AND of the list mask and
-// all of its tokens, however it was reached.
-constexpr int kTrieStack = 12;
-constexpr int kTrieWarps = 8;
-// Measured slower than grouped_scan on the C3 workload, so it
-// runs only with IG_SCAN=trie; its index links are built only then.
-inline bool trie_enabled() {
-    static const bool on = getenv("IG_SCAN") && std::string(getenv("IG_SCAN")) == "trie";
-    return on;
-}
-
-
-template <int MODE, bool COUNT>
-__global__ void __launch_bounds__(kTrieWarps * 32)
-trie_scan(const unsigned long long* __restrict__ dense, size_t W, size_t np,
-          const uint32_t* __restrict__ tok_beg, const uint32_t* __restrict__ tok_len,
-          const uint16_t* __restrict__ toks, const uint32_t* __restrict__ order, const uint32_t* __restrict__ gid,
-          const uint8_t* __restrict__ lcp, const uint32_t* __restrict__ push, const uint32_t* __restrict__ seg,
-          const unsigned long long* __restrict__ nseg_p, const unsigned long long* __restrict__ goff,
-          const uint32_t* __restrict__ glen, const uint32_t* __restrict__ ew, const unsigned long long* __restrict__ em,
-          const int64_t* __restrict__ scores, unsigned long long* __restrict__ acc, int64_t* __restrict__ support_out,
-          uint8_t* __restrict__ cover_out, int* __restrict__ flags, unsigned long long* __restrict__ work) {
-    __shared__ unsigned long long stk[kTrieWarps][kTrieStack][32];
-    __shared__ uint16_t stok[kTrieWarps][kTrieSeg][32];  // the segment's token lists (first 32 of each)
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const size_t warps = ((size_t)gridDim.x * blockDim.x) >> 5;
-    const size_t nseg = (size_t)*nseg_p;
-    const uint32_t Wu = (uint32_t)W, wb = Wu * 8u;
-    bool ovf = false;
-    unsigned long long nand = 0;  // COUNT only
-    for (size_t sgi = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; sgi < nseg; sgi += warps) {
-        const uint32_t b = seg[sgi];
-        const uint32_t e = sgi + 1 < nseg ? seg[sgi + 1] : (uint32_t)np;
-        const uint32_t n_in = e - b;  // <= 32: lane j holds position b + j
-        const uint32_t g = gid[b];
-        const unsigned long long base = goff[g];
-        const uint32_t len = glen[g];
-        // per-pattern metadata, once per segment, in the lanes' registers
-        uint32_t my_p = 0, my_m = 0, my_o = 0, my_l = 0, my_pm = 0;
-        unsigned long long my_s = 0;
-        if ((uint32_t)lane < n_in) {
-            my_p = order[b + lane];
-            my_m = tok_len[my_p];
-            my_o = tok_beg[my_p];
-            my_l = lcp[b + lane];
-            my_pm = push[b + lane];
-            if (MODE == kMatch || MODE == kMatchChecked) my_s = (unsigned long long)scores[my_p];
-            const uint32_t mm = my_m < 32u ? my_m : 32u;
-            for (uint32_t t = 0; t < mm; ++t) stok[wib][lane][t] = toks[my_o + t];
-        }
-        uint32_t my_cnt = 0;          // support of this lane's pattern
-        unsigned long long hit = 0;   // cover: positions of the segment with a covering row
-        __syncwarp();
-        for (uint32_t j0 = 0; j0 < len; j0 += 32) {
-            const uint32_t j = j0 + lane;
-            const uint32_t w = j < len ? ew[base + j] : 0u;
-            const unsigned long long m0 = j < len ? em[base + j] : 0ull;
-            const unsigned long long* col = dense + w;
-            int sp = 0;
-            unsigned long long sd = 0;  // depth of stack entry q in bits [5q, 5q + 5)
-            uint32_t dead = 0xffu;      // a prefix length known empty on every lane
-            for (uint32_t i = 0; i < n_in; ++i) {
-                const uint32_t m = __shfl_sync(kFull, my_m, i);
-                const uint32_t l = __shfl_sync(kFull, my_l, i);
-                unsigned long long mk = 0ull;
-                if (l < dead) {
-                    dead = 0xffu;
-                    while (sp > 0 && (uint32_t)((sd >> (5 * (sp - 1))) & 31u) > l) --sp;
-                    uint32_t d = m < 3 ? m : 3;
-                    mk = m0;
-                    if (l > d && sp > 0 && (uint32_t)((sd >> (5 * (sp - 1))) & 31u) == l) {
-                        mk = stk[wib][sp - 1][lane];
-                        d = l;
-                    }
-                    const uint32_t pm = __shfl_sync(kFull, my_pm, i);
-                    const uint32_t mlim = m < 32u ? m : 32u;
-                    const uint16_t* tk = stok[wib][i];
-                    bool alive = true;
-                    // rounds of up to four independent token loads, a round
-                    // ending where a prefix is kept for a later pattern
-                    while (d < mlim) {
-                        if (!__any_sync(kFull, mk != 0ull)) {
-                            alive = false;
-                            break;
-                        }
-                        const uint32_t rest = d + 1 < 32u ? pm >> (d + 1) : 0u;
-                        const uint32_t nxt = rest ? d + (uint32_t)__ffs(rest) : 64u;  // next kept depth
-                        const uint32_t en = min(min(d + 4u, mlim), nxt);
-                        if (mk) {
-                            if (COUNT) nand += en - d;
-                            unsigned long long x = ld_at(col, (uint32_t)tk[d] * wb);
-                            if (d + 1 < en) x &= ld_at(col, (uint32_t)tk[d + 1] * wb);
-                            if (d + 2 < en) x &= ld_at(col, (uint32_t)tk[d + 2] * wb);
-                            if (d + 3 < en) x &= ld_at(col, (uint32_t)tk[d + 3] * wb);
-                            mk &= x;
-                        }
-                        d = en;
-                        if (d == nxt && sp < kTrieStack) {
-                            stk[wib][sp][lane] = mk;
-                            sd = (sd & ~(31ull << (5 * sp))) | ((unsigned long long)d << (5 * sp));
-                            ++sp;
-                        }
-                    }
-                    if (alive && d < m) {  // tokens past 32, from memory (rare)
-                        const uint32_t o = __shfl_sync(kFull, my_o, i);
-                        for (; d < m; ++d) {
-                            if (!__any_sync(kFull, mk != 0ull)) break;
-                            const uint32_t tt = toks[o + d];
-                            if (COUNT && mk) ++nand;
-                            if (mk) mk &= col[(size_t)tt * Wu];
-                        }
-                    }
-                    if (!__any_sync(kFull, mk != 0ull)) dead = d;  // the prefix of length d is empty
-                }
-                if (COUNT) continue;
-                if (MODE == kSupport) {
-                    const uint32_t c = __reduce_add_sync(kFull, (uint32_t)__popcll(mk));
-                    if ((uint32_t)lane == i) my_cnt += c;
-                } else if (MODE == kCover) {
-                    if (__any_sync(kFull, mk != 0ull)) hit |= 1ull << i;
-                } else if (__any_sync(kFull, mk != 0ull)) {
-                    const unsigned long long sc = __shfl_sync(kFull, my_s, i);
-                    if (MODE == kMatch) {
-                        warp_scatter_runs(w, mk, sc, acc);
-                    } else {
-                        warp_scatter_hits<true>(w, mk, sc, acc, ovf);
-                    }
-                }
-            }
-        }
-        __syncwarp();  // stok is rewritten by the next segment
-        if (COUNT) continue;
-        if ((uint32_t)lane < n_in) {
-            if (MODE == kSupport) support_out[my_p] = (int64_t)my_cnt;
-            if (MODE == kCover) cover_out[my_p] = (uint8_t)((hit >> lane) & 1ull);
         }
     }
     if (COUNT) {
@@ -1191,36 +756,18 @@ void launch_scan(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Post
                    glen.as<uint32_t>(), ew.as<uint32_t>(), em.as<unsigned long long>());
     tr.mark("group_lists");
     if (getenv("IG_SCAN_STATS")) scan_stats(ctx, MODE, *I, glen, G, np);
-    const bool use_trie = trie_enabled() && I->lcp.p != nullptr;
-    static const bool single = getenv("IG_SCAN") && std::string(getenv("IG_SCAN")) == "grouped";  // A/B only
-    const bool use_pair = !use_trie && !single;
     const size_t blocks = std::min<size_t>((np + 7) / 8, (size_t)ctx.sm_count * 64);
-    const size_t tblocks = std::min<size_t>((np + 7) / 8 / 4 + 1, (size_t)ctx.sm_count * 64);
     DiagSpan dspan(ctx, MODE == kSupport ? kDiagSupport : MODE == kCover ? kDiagCover : kDiagMatch);
     auto launch = [&](auto count_tag, unsigned long long* work) {
         constexpr bool C = decltype(count_tag)::value;
-        if (use_pair)
-            IGB_LAUNCH(ctx, (paired_scan<MODE, C>), (unsigned)std::min<size_t>((np + 15) / 16, (size_t)ctx.sm_count * 64),
-                       256, 0, P.dense.as<unsigned long long>(), P.W, I->beg.as<uint32_t>(), I->len.as<uint32_t>(),
-                       I->toks->as<uint16_t>(), np, I->order.as<uint32_t>(), I->gid.as<uint32_t>(),
-                       goff.as<unsigned long long>(), glen.as<uint32_t>(), ew.as<uint32_t>(),
-                       em.as<unsigned long long>(), scores, acc, support, cover, flags, work);
-        else if (use_trie)
-            IGB_LAUNCH(ctx, (trie_scan<MODE, C>), (unsigned)tblocks, kTrieWarps * 32, 0,
-                       P.dense.as<unsigned long long>(), P.W, np, I->beg.as<uint32_t>(), I->len.as<uint32_t>(),
-                       I->toks->as<uint16_t>(), I->order.as<uint32_t>(), I->gid.as<uint32_t>(), I->lcp.as<uint8_t>(),
-                       I->push.as<uint32_t>(), I->seg.as<uint32_t>(), I->nseg.as<unsigned long long>(),
-                       goff.as<unsigned long long>(), glen.as<uint32_t>(), ew.as<uint32_t>(),
-                       em.as<unsigned long long>(), scores, acc, support, cover, flags, work);
-        else
-            IGB_LAUNCH(ctx, (grouped_scan<MODE, C>), (unsigned)blocks, 256, 0, P.dense.as<unsigned long long>(), P.W,
-                       P.n, I->beg.as<uint32_t>(), I->len.as<uint32_t>(), I->toks->as<uint16_t>(), np,
-                       I->order.as<uint32_t>(), I->gid.as<uint32_t>(), goff.as<unsigned long long>(),
-                       glen.as<uint32_t>(), ew.as<uint32_t>(), em.as<unsigned long long>(), scores, acc, support,
-                       cover, flags, work);
+        IGB_LAUNCH(ctx, (grouped_scan<MODE, C>), (unsigned)blocks, 256, 0, P.dense.as<unsigned long long>(), P.W,
+                   P.n, I->beg.as<uint32_t>(), I->len.as<uint32_t>(), I->toks->as<uint16_t>(), np,
+                   I->order.as<uint32_t>(), I->gid.as<uint32_t>(), goff.as<unsigned long long>(),
+                   glen.as<uint32_t>(), ew.as<uint32_t>(), em.as<unsigned long long>(), scores, acc, support,
+                   cover, flags, work);
     };
     launch(std::false_type{}, nullptr);
-    tr.mark(use_pair ? "paired_scan" : use_trie ? "trie_scan" : "grouped_scan");
+    tr.mark("grouped_scan");
     if (ctx.diag) {
         // the same launch again with outputs suppressed, counting its word-ANDs
         dspan.stop();
@@ -1340,40 +887,7 @@ void build_pattern_index(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, co
 
 // gid (0-based, per sorted position) and gkey (per group) from the sorted keys,
 // then the (t1, t2) parent of every group (pid, pkey)
-void group_ids_only(Ctx& ctx, const unsigned long long* d_sorted_key, size_t np, PatternIndex& I);
-
-void trie_links(Ctx& ctx, PatternIndex& I) {
-    if (!trie_enabled()) return;
-    const size_t np = I.np;
-    I.lcp.alloc(std::max<size_t>(np, 1), ctx.stream);
-    I.push.alloc(std::max<size_t>(np, 1) * 4, ctx.stream);
-    I.seg.alloc(std::max<size_t>(np, 1) * 4, ctx.stream);
-    I.nseg.alloc(8, ctx.stream);
-    IGB_CUDA(cudaMemsetAsync(I.nseg.p, 0, 8, ctx.stream));
-    if (np == 0 || I.G == 0) return;
-    DevBuf gstart(I.G * 4, ctx.stream), head(np, ctx.stream), iota(np * 4, ctx.stream), nsel(8, ctx.stream);
-    IGB_LAUNCH(ctx, group_starts, grid_for(ctx, np, 256), 256, 0, I.gid.as<uint32_t>(), np, gstart.as<uint32_t>());
-    IGB_LAUNCH(ctx, trie_lcp, grid_for(ctx, np, 256), 256, 0, I.order.as<uint32_t>(), I.gid.as<uint32_t>(),
-               gstart.as<uint32_t>(), I.beg.as<uint32_t>(), I.len.as<uint32_t>(), I.toks->as<uint16_t>(), np,
-               I.lcp.as<uint8_t>(), head.as<uint8_t>());
-    IGB_LAUNCH(ctx, trie_push, grid_for(ctx, np, 256), 256, 0, I.order.as<uint32_t>(), I.len.as<uint32_t>(),
-               I.lcp.as<uint8_t>(), head.as<uint8_t>(), np, I.push.as<uint32_t>());
-    IGB_LAUNCH(ctx, iota_u32_k, grid_for(ctx, np, 256), 256, 0, iota.as<uint32_t>(), np);
-    size_t tb = 0;
-    IGB_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, iota.as<uint32_t>(), head.as<uint8_t>(), I.seg.as<uint32_t>(),
-                                        nsel.as<int64_t>(), (int64_t)np, ctx.stream));
-    DevBuf temp(tb, ctx.stream);
-    IGB_CUDA(cub::DeviceSelect::Flagged(temp.p, tb, iota.as<uint32_t>(), head.as<uint8_t>(), I.seg.as<uint32_t>(),
-                                        nsel.as<int64_t>(), (int64_t)np, ctx.stream));
-    IGB_CUDA(cudaMemcpyAsync(I.nseg.p, nsel.p, 8, cudaMemcpyDeviceToDevice, ctx.stream));  // int64 count, < 2^32
-}
-
 void group_ids(Ctx& ctx, const unsigned long long* d_sorted_key, size_t np, PatternIndex& I) {
-    group_ids_only(ctx, d_sorted_key, np, I);
-    trie_links(ctx, I);
-}
-
-void group_ids_only(Ctx& ctx, const unsigned long long* d_sorted_key, size_t np, PatternIndex& I) {
     DevBuf head(np, ctx.stream), head32(np * 4, ctx.stream), nsel(8, ctx.stream);
     IGB_LAUNCH(ctx, group_heads<unsigned long long>, grid_for(ctx, np, 256), 256, 0, d_sorted_key, np,
                head.as<uint8_t>(), head32.as<uint32_t>());

@@ -47,18 +47,7 @@ struct PatternIndex {
     size_t G2 = 0;   // parent groups (t1, t2)
     DevBuf pid;      // G u32: parent of each group
     DevBuf pkey;     // G2 u32: (t1 << 16) | t2
-    // Prefix-trie links of the ordered positions (within a group the patterns
-    // are sorted by their next rarest tokens, so neighbours share prefixes):
-    // segments of <= kTrieSeg consecutive positions of one group; lcp = tokens
-    // position i shares with position i-1 of its segment (segment start:
-    // min(3, |b|), the group key); push = bit d set when the scan of position i
-    // keeps its prefix mask of depth d for a later position of the segment.
-    DevBuf lcp;      // np u8
-    DevBuf push;     // np u32
-    DevBuf seg;      // np u32: first position of each segment (*nseg of them)
-    DevBuf nseg;     // 1 u32, device resident (no host read-back)
 };
-constexpr int kTrieSeg = 32;  // one pattern per lane: the segment's metadata lives in registers
 
 // descending: most frequent first (default: rarest first)
 void make_rank_space(Ctx& ctx, const uint32_t* d_df, uint32_t L, RankSpace& R, bool descending = false);

@@ -43,7 +43,7 @@ def _first_bad(want, got):
 
 
 def _golden(golden_dir, name):
-    path = os.path.join(golden_dir, f"nsl_{name}.json")
+    path = os.path.join(golden_dir, f"{'cicids' if name == 'c5s' else 'nsl'}_{name}.json")
     if not os.path.exists(path):
         pytest.skip(f"{path} not generated (tests/golden/make_fullsize.py {name})")
     return json.load(open(path))
@@ -100,19 +100,22 @@ def api():
     return a
 
 
-@pytest.mark.parametrize("name", ["c3", "c4"])
+@pytest.mark.parametrize("name", ["c3", "c4", "c5s"])
 def test_fullsize_host_pipeline_vs_reference(api, golden_dir, name):
     """Host CSV reader + schema -> device encode -> fused fit + evidence (the
-    bench's e2e path), every output against the reference's digests."""
+    bench's e2e path), every output against the reference's digests.  c5s:
+    configs[4]'s CICIDS shape (p = 2, wide rows) on a 25,000-record sample."""
     g = _golden(golden_dir, name)
-    csv = synth.nsl_csv(g["rows"], seed=g["seed"])
+    gen = synth.cicids_csv if g.get("shape") == "cicids" else synth.nsl_csv
+    csv = gen(g["rows"], seed=g["seed"])
     assert hashlib.sha256(csv).hexdigest() == g["csv_sha256"]
     ctx = api.default_context()
     table = api.read_csv(csv)
     ntr = g["ratio_k"] * table.rows // 10
     assert ntr == g["n_train"]
     tr, te = table.slice(0, ntr), table.slice(ntr, table.rows)
-    schema = api.infer_schema(tr, "label", decimals=g["decimals"])
+    normal = [g["normal_values"]] if g.get("normal_values") else []
+    schema = api.infer_schema(tr, g.get("label", "label"), normal_values=normal, decimals=g["decimals"])
     assert _schema_digest(schema, table.columns) == g["schema_digest"]
     enc = api.encode_training(api.Columns(tr, schema, True), ctx)
     tenc = api.encode_rows(api.Columns(te, schema, False), enc, ctx)
