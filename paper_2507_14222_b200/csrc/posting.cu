@@ -225,15 +225,31 @@ pattern_token_fill_rank(const int64_t* __restrict__ pat, size_t np, int k, const
                 atomicOr(my + (r >> 5) * kFillThreads, 1u << (r & 31));
             }
         }
+        // tokens out four at a time (one 8-byte store instead of four 2-byte
+        // ones: the scattered 2-byte stores were one L2 write each)
         uint32_t o = off[p];
+        unsigned long long buf = 0;
+        uint32_t nb = 0;
         for (int q = 0; q < nw; ++q) {
             uint32_t y = atomicOr(my + q * kFillThreads, 0u);  // ordered after this thread's ORs
             while (y) {
                 const int b = __ffs((int)y) - 1;
                 y &= y - 1;
-                toks[o++] = byrank[q * 32 + b];
+                const uint16_t t = byrank[q * 32 + b];
+                if (nb == 0 && (o & 3u)) {
+                    toks[o++] = t;  // up to the next 8-byte boundary
+                    continue;
+                }
+                buf |= (unsigned long long)t << (16 * nb);
+                if (++nb == 4) {
+                    *reinterpret_cast<unsigned long long*>(toks + o) = buf;
+                    o += 4;
+                    buf = 0;
+                    nb = 0;
+                }
             }
         }
+        for (uint32_t i = 0; i < nb; ++i) toks[o + i] = (uint16_t)(buf >> (16 * i));
     }
 }
 
