@@ -1064,7 +1064,15 @@ int ig_encoding_copy_rows(ig_ctx* ctx, const ig_encoding* e, int which, int64_t*
         IGB_CUDA(cudaStreamSynchronize(ctx->stream));
     });
 }
-const char* ig_encoding_vocabulary(const ig_encoding* e) { return e ? e->vocab_blob.c_str() : ""; }
+const char* ig_encoding_vocabulary(const ig_encoding* e) {
+    if (!e) return "";
+    try {
+        return e->host_vocab().vocab_blob.c_str();
+    } catch (const igb::Error& err) {
+        igb::set_last_error(err.msg);
+        return "";
+    }
+}
 size_t ig_encoding_removed_count(const ig_encoding* e) { return e ? e->removed.size() : 0; }
 int ig_encoding_removed_rows(const ig_encoding* e, uint64_t* rows) {
     if (!e) return IG_E_INVALID_ARG;

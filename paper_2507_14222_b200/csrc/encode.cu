@@ -21,6 +21,9 @@
 #include <string>
 #include <unordered_map>
 #include <unordered_set>
+#include <mutex>
+#include <thread>
+#include <exception>
 
 #include "encode.cuh"
 #include "host_pipeline.hpp"
@@ -113,15 +116,15 @@ distinct_codes(const int64_t* __restrict__ codes, size_t n, int64_t* __restrict_
 }
 
 struct Lut {
-    int kind;      // 0 numeric (sorted codes + bits), 1 categorical (id → bit)
-    int off, len;  // into codes/bits arrays
+    int kind;      // 0 numeric (sorted codes + bits), 1 categorical (id -> bit)
+    int off, len;  // numeric: into lcodes/lbits; categorical: into cbits
     int empty_bit; // bit of the "j:" token or -1
 };
 
 __device__ __forceinline__ int lookup(const Lut& L, int64_t code, const int64_t* __restrict__ lcodes,
-                                      const int32_t* __restrict__ lbits) {
+                                      const int32_t* __restrict__ lbits, const int32_t* __restrict__ cbits) {
     if (code == kEmptyCode) return L.empty_bit;
-    if (L.kind == 1) return (code >= 0 && code < L.len) ? lbits[L.off + code] : -1;
+    if (L.kind == 1) return (code >= 0 && code < L.len) ? cbits[L.off + code] : -1;
     int lo = 0, hi = L.len;
     while (lo < hi) {
         const int mid = (lo + hi) >> 1;
@@ -136,14 +139,239 @@ __device__ __forceinline__ int lookup(const Lut& L, int64_t code, const int64_t*
 // Set each cell's token bit in its packed row (bitpack.cpp:25-26); tokens not
 // in the vocabulary are dropped (pipeline.cpp:254).
 __global__ void pack_cells(const int64_t* __restrict__ codes, size_t n, int n_feat, const Lut* __restrict__ luts,
-                           const int64_t* __restrict__ lcodes, const int32_t* __restrict__ lbits, int k,
-                           unsigned long long* __restrict__ rows) {
+                           const int64_t* __restrict__ lcodes, const int32_t* __restrict__ lbits,
+                           const int32_t* __restrict__ cbits, int k, unsigned long long* __restrict__ rows) {
     const size_t total = (size_t)n_feat * n;
     for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += (size_t)gridDim.x * blockDim.x) {
         const int f = (int)(q / n);
         const size_t r = q % n;
-        const int bit = lookup(luts[f], codes[q], lcodes, lbits);
+        const int bit = lookup(luts[f], codes[q], lcodes, lbits, cbits);
         if (bit >= 0) atomicOr(rows + r * k + (bit >> 6), 1ull << (bit & 63));
+    }
+}
+
+// ------------------------------------------------------------------ device vocabulary
+// TokenVocabulary::build (pipeline.cpp:62-69: std::set<std::string>, byte order)
+// and the bit assignment of encode_training (:294-304) on the device, for up
+// to kVocabMax tokens (else the host builds it, as before).  A token is
+// "<j>:<value>"; its byte order is reproduced by a 128-bit key:
+//   [127:120] rank of the "<j>:" prefix among the feature columns (host, byte
+//             order: no prefix is a prefix of another, they all end in ':')
+//   [119:118] group: 0 the empty value, 1 a '-' value, 2 any other
+//   numeric:  19 nibbles, the integer part's decimal digits + 1, left aligned,
+//             0 after the last one ('.' and the end of the string sort below
+//             every digit), then the p fractional digits as an integer (they
+//             have a fixed width, so numeric order is byte order)
+//   categorical: the value's byte-order rank within its column's dictionary
+//             (host, computed with the columns)
+// The value text is format_zscore's (pipeline.cpp:77-105): sign only for
+// non-zero negatives, whole = |units| / 10^p, frac = |units| % 10^p.
+constexpr int kVocabMax = 8192;
+constexpr int kVocabSlots = 1 << 15;
+
+struct FeatDesc {
+    int kind;      // 0 numeric, 1 categorical
+    int col_rank;  // byte-order rank of "<j>:" among the features
+    int cat_off;   // categorical: offset into cbits / crank
+    int cat_len;   // categorical: dictionary size
+};
+
+__device__ __forceinline__ ulonglong2 cas128_enc(ulonglong2* addr, ulonglong2 cmp, ulonglong2 val) {
+    ulonglong2 old;
+    asm volatile(
+        "{\n\t.reg .b128 c, n, o;\n\t"
+        "mov.b128 c, {%2, %3};\n\t"
+        "mov.b128 n, {%4, %5};\n\t"
+        "atom.global.cas.b128 o, [%6], c, n;\n\t"
+        "mov.b128 {%0, %1}, o;\n\t}"
+        : "=l"(old.x), "=l"(old.y)
+        : "l"(cmp.x), "l"(cmp.y), "l"(val.x), "l"(val.y), "l"(addr)
+        : "memory");
+    return old;
+}
+
+// exact distinct (feature, code) of the per-chunk lists (distinct_codes repeats
+// a value once per 8,192-row chunk); slot = {code, feature + 1}, {0, 0} empty
+__global__ void vocab_unique(const int64_t* __restrict__ raw_code, const int32_t* __restrict__ raw_col,
+                             const unsigned long long* __restrict__ raw_count, ulonglong2* __restrict__ slots,
+                             int64_t* __restrict__ u_code, int32_t* __restrict__ u_feat,
+                             unsigned int* __restrict__ u_count) {
+    const unsigned long long m = *raw_count;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        const int64_t c = raw_code[i];
+        const int f = raw_col[i];
+        const ulonglong2 me = make_ulonglong2((unsigned long long)c, (unsigned long long)f + 1ull);
+        unsigned s = (unsigned)(mix64((uint64_t)c ^ (0x9e3779b97f4a7c15ull * (uint64_t)(f + 1))) & (kVocabSlots - 1));
+        for (unsigned probe = 0; probe < (unsigned)kVocabSlots; ++probe, s = (s + 1) & (kVocabSlots - 1)) {
+            const ulonglong2 old = cas128_enc(slots + s, make_ulonglong2(0ull, 0ull), me);
+            if (old.x == 0ull && old.y == 0ull) {
+                const unsigned idx = atomicAdd(u_count, 1u);
+                if (idx < (unsigned)kVocabMax) {
+                    u_code[idx] = c;
+                    u_feat[idx] = f;
+                }
+                break;
+            }
+            if (old.x == me.x && old.y == me.y) break;
+        }
+    }
+}
+
+__device__ __forceinline__ void token_key(const FeatDesc& d, int64_t code, const int32_t* __restrict__ crank,
+                                          uint64_t pow10p, unsigned long long& hi, unsigned long long& lo) {
+    hi = (unsigned long long)d.col_rank << 56;
+    lo = 0;
+    if (code == kEmptyCode) return;  // group 0
+    if (d.kind == 1) {
+        hi |= (1ull << 54) | (unsigned long long)(uint32_t)crank[d.cat_off + code];
+        return;
+    }
+    const bool neg = code < 0;
+    const uint64_t mag = neg ? (uint64_t)0 - (uint64_t)code : (uint64_t)code;
+    const uint64_t whole = mag / pow10p, frac = mag % pow10p;
+    hi |= (unsigned long long)((neg && mag != 0) ? 1 : 2) << 54;
+    // decimal digits of whole, most significant first (at least one digit)
+    int nd = 0;
+    uint8_t dig[20];
+    uint64_t w = whole;
+    do {
+        dig[nd++] = (uint8_t)(w % 10);
+        w /= 10;
+    } while (w);
+    // nibble i (0-based, left aligned) = digit i + 1; 13 nibbles in hi[53:2], 6 in lo[63:40]
+    for (int i = 0; i < nd; ++i) {
+        const unsigned long long nib = (unsigned long long)dig[nd - 1 - i] + 1ull;
+        if (i < 13)
+            hi |= nib << (50 - 4 * i);
+        else
+            lo |= nib << (60 - 4 * (i - 13));
+    }
+    lo |= (unsigned long long)frac;  // < 10^12 < 2^40
+}
+
+__device__ __forceinline__ bool key_gt(unsigned long long ah, unsigned long long al, unsigned long long bh,
+                                       unsigned long long bl) {
+    return ah > bh || (ah == bh && al > bl);
+}
+
+// ascending bitonic sort of (hi, lo, idx) in shared memory; n2 a power of two
+__device__ void block_bitonic(unsigned long long* hi, unsigned long long* lo, uint16_t* idx, int n2) {
+    for (int k = 2; k <= n2; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const bool up = (i & k) == 0;
+                    if (key_gt(hi[i], lo[i], hi[ixj], lo[ixj]) == up) {
+                        unsigned long long t = hi[i];
+                        hi[i] = hi[ixj];
+                        hi[ixj] = t;
+                        t = lo[i];
+                        lo[i] = lo[ixj];
+                        lo[ixj] = t;
+                        const uint16_t u = idx[i];
+                        idx[i] = idx[ixj];
+                        idx[ixj] = u;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+}
+
+// One block: rank the distinct tokens in byte order (bit = rank), then the pack
+// tables — numeric (feature, code) sorted with their bits, categorical id ->
+// bit, the empty token's bit per feature — and the token list in bit order for
+// the host text.  out_L = number of tokens (> kVocabMax: the host builds it).
+__global__ void __launch_bounds__(1024)
+vocab_build(const int64_t* __restrict__ u_code, const int32_t* __restrict__ u_feat,
+            const unsigned int* __restrict__ u_count, const FeatDesc* __restrict__ desc, int n_feat,
+            const int32_t* __restrict__ crank, int cat_total, uint64_t pow10p, Lut* __restrict__ lut,
+            int64_t* __restrict__ lcodes, int32_t* __restrict__ lbits, int32_t* __restrict__ cbits,
+            int32_t* __restrict__ ubits, int64_t* __restrict__ list_code, int32_t* __restrict__ list_feat,
+            unsigned int* __restrict__ out_L) {
+    extern __shared__ unsigned long long vsm[];
+    const unsigned U = *u_count;
+    if (threadIdx.x == 0) *out_L = U;
+    if (U > (unsigned)kVocabMax) return;
+    int n2 = 1;
+    while (n2 < (int)U) n2 <<= 1;
+    unsigned long long* hi = vsm;
+    unsigned long long* lo = vsm + kVocabMax;
+    uint16_t* idx = reinterpret_cast<uint16_t*>(vsm + 2 * kVocabMax);
+    for (int f = threadIdx.x; f < n_feat; f += blockDim.x) {
+        const FeatDesc d = desc[f];
+        lut[f] = Lut{d.kind, d.kind == 1 ? d.cat_off : 0, d.kind == 1 ? d.cat_len : 0, -1};
+    }
+    for (int i = threadIdx.x; i < cat_total; i += blockDim.x) cbits[i] = -1;
+    for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+        if (i < (int)U) {
+            token_key(desc[u_feat[i]], u_code[i], crank, pow10p, hi[i], lo[i]);
+        } else {
+            hi[i] = ~0ull;
+            lo[i] = ~0ull;
+        }
+        idx[i] = (uint16_t)i;
+    }
+    __syncthreads();
+    block_bitonic(hi, lo, idx, n2);
+    for (int pos = threadIdx.x; pos < (int)U; pos += blockDim.x) {
+        const int i = idx[pos];
+        const int f = u_feat[i];
+        const int64_t c = u_code[i];
+        ubits[i] = pos;
+        list_code[pos] = c;
+        list_feat[pos] = f;
+        if (c == kEmptyCode)
+            lut[f].empty_bit = pos;
+        else if (desc[f].kind == 1)
+            cbits[desc[f].cat_off + c] = pos;
+    }
+    __syncthreads();
+    // numeric tables: (feature, code) order
+    for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+        if (i < (int)U) {
+            hi[i] = (unsigned long long)u_feat[i];
+            lo[i] = (unsigned long long)u_code[i] ^ (1ull << 63);
+        } else {
+            hi[i] = ~0ull;
+            lo[i] = ~0ull;
+        }
+        idx[i] = (uint16_t)i;
+    }
+    __syncthreads();
+    block_bitonic(hi, lo, idx, n2);
+    for (int pos = threadIdx.x; pos < (int)U; pos += blockDim.x) {
+        const int i = idx[pos];
+        lcodes[pos] = u_code[i];
+        lbits[pos] = ubits[i];
+        const int f = (int)hi[pos];
+        if (desc[f].kind == 0 && (pos == 0 || (int)hi[pos - 1] != f)) lut[f].off = pos;
+    }
+    __syncthreads();
+    for (int pos = threadIdx.x; pos < (int)U; pos += blockDim.x) {
+        const int f = (int)hi[pos];
+        if (desc[f].kind == 0 && (pos + 1 == (int)U || (int)hi[pos + 1] != f)) lut[f].len = pos + 1 - lut[f].off;
+    }
+}
+
+// categorical features of a test table: their Lut points at its remapped table
+// (triples feature, offset, length)
+__global__ void patch_cat_lut(const int32_t* __restrict__ fol, int n, Lut* __restrict__ lut) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        lut[fol[3 * i]].off = fol[3 * i + 1];
+        lut[fol[3 * i]].len = fol[3 * i + 2];
+    }
+}
+
+// categorical test ids -> the training dictionary's bits (remap: test id ->
+// training id or -1, built on the host from the two dictionaries' strings)
+__global__ void remap_cat(const int32_t* __restrict__ remap, int n, const int32_t* __restrict__ train_cbits,
+                          const int32_t* __restrict__ train_off_of, int32_t* __restrict__ out) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int r = remap[i];
+        out[i] = r >= 0 ? train_cbits[train_off_of[i] + r] : -1;
     }
 }
 
@@ -301,99 +529,62 @@ bool upload_and_code(Ctx& ctx, const ig_columns& c, DeviceCols& d) {
     return host_read;
 }
 
-// Upload a vocabulary's lookup tables and pack `d`'s cells into rows.
+// Pack `d`'s cells into rows with lookup tables already on the device.
+void pack_tables(Ctx& ctx, uint32_t L, const DeviceCols& d, const Lut* luts, const int64_t* lcodes,
+                 const int32_t* lbits, const int32_t* cbits, DevRows& out) {
+    out.L = L;
+    out.k = words_for(L);
+    out.n = d.n;
+    out.buf.alloc(std::max<size_t>(out.n * out.k, 1) * 8, ctx.stream);
+    IGB_CUDA(cudaMemsetAsync(out.buf.p, 0, std::max<size_t>(out.n * out.k, 1) * 8, ctx.stream));
+    const size_t cells = (size_t)d.n_feat * d.n;
+    if (cells && out.k)
+        IGB_LAUNCH(ctx, pack_cells, grid_for(ctx, cells, 256), 256, 0, d.codes.as<int64_t>(), d.n, d.n_feat, luts,
+                   lcodes, lbits, cbits, (int)out.k, reinterpret_cast<unsigned long long*>(out.data()));
+}
+
+// Upload a host vocabulary's lookup tables and pack `d`'s cells into rows.
 void pack_with(Ctx& ctx, const ig_encoding& e, const DeviceCols& d,
                const std::vector<std::vector<int32_t>>& cat_id_to_bit, DevRows& out) {
     std::vector<Lut> luts(d.n_feat);
     std::vector<int64_t> lcodes;
-    std::vector<int32_t> lbits;
+    std::vector<int32_t> lbits, cbits;
     for (int f = 0; f < d.n_feat; ++f) {
         const int j = d.feat_col[f];
         Lut& L = luts[f];
         L.empty_bit = e.empty_bit[j];
-        L.off = (int)lbits.size();
         if (e.kind[j] == 0) {
             L.kind = 0;
+            L.off = (int)lbits.size();
             L.len = (int)e.num_codes[j].size();
             lcodes.insert(lcodes.end(), e.num_codes[j].begin(), e.num_codes[j].end());
             lbits.insert(lbits.end(), e.num_bits[j].begin(), e.num_bits[j].end());
         } else {
             L.kind = 1;
+            L.off = (int)cbits.size();
             L.len = (int)cat_id_to_bit[j].size();
-            lcodes.resize(lcodes.size() + cat_id_to_bit[j].size(), 0);
-            lbits.insert(lbits.end(), cat_id_to_bit[j].begin(), cat_id_to_bit[j].end());
+            cbits.insert(cbits.end(), cat_id_to_bit[j].begin(), cat_id_to_bit[j].end());
         }
     }
     DevBuf dl(std::max<size_t>(luts.size(), 1) * sizeof(Lut), ctx.stream);
-    DevBuf dc(std::max<size_t>(lcodes.size(), 1) * 8, ctx.stream), db(std::max<size_t>(lbits.size(), 1) * 4, ctx.stream);
+    DevBuf dc(std::max<size_t>(lcodes.size(), 1) * 8, ctx.stream), db(std::max<size_t>(lbits.size(), 1) * 4, ctx.stream),
+        dcb(std::max<size_t>(cbits.size(), 1) * 4, ctx.stream);
     if (!luts.empty())
         IGB_CUDA(cudaMemcpyAsync(dl.p, luts.data(), luts.size() * sizeof(Lut), cudaMemcpyHostToDevice, ctx.stream));
     if (!lcodes.empty())
         IGB_CUDA(cudaMemcpyAsync(dc.p, lcodes.data(), lcodes.size() * 8, cudaMemcpyHostToDevice, ctx.stream));
     if (!lbits.empty())
         IGB_CUDA(cudaMemcpyAsync(db.p, lbits.data(), lbits.size() * 4, cudaMemcpyHostToDevice, ctx.stream));
-    out.L = e.L;
-    out.k = words_for(e.L);
-    out.n = d.n;
-    out.buf.alloc(std::max<size_t>(out.n * out.k, 1) * 8, ctx.stream);
-    IGB_CUDA(cudaMemsetAsync(out.buf.p, 0, std::max<size_t>(out.n * out.k, 1) * 8, ctx.stream));
-    const size_t cells = (size_t)d.n_feat * d.n;
-    if (cells && out.k)
-        IGB_LAUNCH(ctx, pack_cells, grid_for(ctx, cells, 256), 256, 0, d.codes.as<int64_t>(), d.n, d.n_feat,
-                   dl.as<Lut>(), dc.as<int64_t>(), db.as<int32_t>(), (int)out.k,
-                   reinterpret_cast<unsigned long long*>(out.data()));
+    if (!cbits.empty())
+        IGB_CUDA(cudaMemcpyAsync(dcb.p, cbits.data(), cbits.size() * 4, cudaMemcpyHostToDevice, ctx.stream));
+    pack_tables(ctx, e.L, d, dl.as<Lut>(), dc.as<int64_t>(), db.as<int32_t>(), dcb.as<int32_t>(), out);
     // Lookup tables are freed stream-ordered after the kernel.
 }
 
-}  // namespace
-
-void prefetch_columns(Ctx& ctx, ig_columns& c) {
-    if (c.d_values && c.device == ctx.device) return;  // already resident
-    auto pf = std::make_shared<PrefetchCols>();
-    pf->device = ctx.device;
-    pf->values.alloc(std::max<size_t>(c.values.size(), 1) * 8, ctx.copy);
-    pf->cat.alloc(std::max<size_t>(c.cat.size(), 1) * 4, ctx.copy);
-    pf->attack.alloc(std::max<size_t>(c.is_attack.size(), 1), ctx.copy);
-    if (!c.values.empty())
-        IGB_CUDA(cudaMemcpyAsync(pf->values.p, c.values.data(), c.values.size() * 8, cudaMemcpyHostToDevice, ctx.copy));
-    if (!c.cat.empty())
-        IGB_CUDA(cudaMemcpyAsync(pf->cat.p, c.cat.data(), c.cat.size() * 4, cudaMemcpyHostToDevice, ctx.copy));
-    if (!c.is_attack.empty())
-        IGB_CUDA(cudaMemcpyAsync(pf->attack.p, c.is_attack.data(), c.is_attack.size(), cudaMemcpyHostToDevice,
-                                 ctx.copy));
-    IGB_CUDA(cudaEventCreateWithFlags(&pf->ready, cudaEventDisableTiming));
-    IGB_CUDA(cudaEventRecord(pf->ready, ctx.copy));
-    c.prefetch = pf;
-}
-
-void drop_prefetch(ig_columns& c) {
-    if (auto* pf = static_cast<PrefetchCols*>(c.prefetch.get())) cudaEventSynchronize(pf->ready);
-    c.prefetch.reset();
-}
-
-void encode_training_dev(Ctx& ctx, const ig_columns& c, ig_encoding& e) {
-    if (c.is_attack.size() != c.n_rows) fail(IG_E_INVALID_ARG, "encode_training: columns built without labels");
-    e = ig_encoding{};
-    e.n_cols = c.n_cols;
-    e.label_index = c.label_index;
-    e.decimals = c.decimals;
-    e.kind = c.kind;
-    e.dict = c.dict;
-    DeviceCols d;
-    upload_and_code(ctx, c, d);
-
-    // (1b) distinct (column, code) over ALL training rows (vocabulary precedes the filter).
-    const size_t chunks = (d.n + kDistinctRows - 1) / kDistinctRows;
-    const size_t cap = std::max<size_t>((size_t)d.n_feat * d.n, 1);
-    DevBuf lcode(cap * 8, ctx.stream), lcol(cap * 4, ctx.stream), lcnt(8, ctx.stream);
-    IGB_CUDA(cudaMemsetAsync(lcnt.p, 0, 8, ctx.stream));
-    if (d.n && d.n_feat)
-        IGB_CUDA(cudaFuncSetAttribute(distinct_codes, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      kDistinctSlots * (int)sizeof(int64_t)));
-    if (d.n && d.n_feat)
-        IGB_LAUNCH(ctx, distinct_codes, dim3((unsigned)chunks, (unsigned)d.n_feat), 256,
-                   kDistinctSlots * sizeof(int64_t), d.codes.as<int64_t>(), d.n,
-                   lcode.as<int64_t>(), lcol.as<int32_t>(), lcnt.as<unsigned long long>());
+// The vocabulary on the host (more than kVocabMax tokens, or IG_HOST_VOCAB=1):
+// read the distinct (column, code) list back, token text, byte-order sort.
+void host_vocab_build(Ctx& ctx, const ig_columns& c, const DeviceCols& d, const DevBuf& lcode, const DevBuf& lcol,
+                      const DevBuf& lcnt, ig_encoding& e, DevRows& all) {
     unsigned long long m = 0;
     read_back(ctx, &m, lcnt.p, 8);
     std::vector<int64_t> hcode(m);
@@ -454,8 +645,241 @@ void encode_training_dev(Ctx& ctx, const ig_columns& c, ig_encoding& e) {
     }
 
     // (1c) pack every training row.
-    DevRows all;
     pack_with(ctx, e, d, cat_id_to_bit, all);
+}
+
+}  // namespace
+}  // namespace igb
+
+// Host text of a device-built vocabulary (ig_encoding::hv): the tokens in bit
+// order are copied to page-locked memory on the encode stream; a host thread
+// waits for them and fills the host fields.  It also checks that the tokens'
+// text is strictly increasing in byte order — the device keys' contract.
+struct HostVocabJob {
+    std::thread th;
+    std::mutex mu;
+    bool joined = false;
+    std::exception_ptr err;
+    void* pinned = nullptr;
+    cudaEvent_t ready = nullptr;
+    ~HostVocabJob() {
+        if (th.joinable()) th.join();
+        if (ready) cudaEventDestroy(ready);
+        if (pinned) cudaFreeHost(pinned);
+    }
+};
+
+const ig_encoding& ig_encoding::host_vocab() const {
+    if (hv) {
+        std::lock_guard<std::mutex> lock(hv->mu);
+        if (!hv->joined) {
+            if (hv->th.joinable()) hv->th.join();
+            hv->joined = true;
+        }
+        if (hv->err) std::rethrow_exception(hv->err);
+    }
+    return *this;
+}
+
+namespace igb {
+namespace {
+
+bool device_vocab(Ctx& ctx, const ig_columns& c, const DeviceCols& d, const DevBuf& lcode, const DevBuf& lcol,
+                  const DevBuf& lcnt, ig_encoding& e) {
+    static const bool host_only = getenv("IG_HOST_VOCAB") != nullptr;  // A/B and fallback tests
+    const int nf = d.n_feat;
+    if (host_only || nf == 0 || nf > 255 || c.decimals > 12) return false;
+    // host descriptors: byte-order rank of each "<j>:" prefix, categorical
+    // dictionary offsets and each value's byte-order rank in its dictionary
+    std::vector<int> order(nf);
+    for (int f = 0; f < nf; ++f) order[f] = f;
+    std::sort(order.begin(), order.end(), [&](int a, int b) {
+        return std::to_string(d.feat_col[a]) + ":" < std::to_string(d.feat_col[b]) + ":";
+    });
+    std::vector<FeatDesc> desc(nf);
+    for (int r = 0; r < nf; ++r) desc[order[r]].col_rank = r;
+    std::vector<int32_t> crank;
+    e.dv.cat_off.assign(nf, 0);
+    for (int f = 0; f < nf; ++f) {
+        const int j = d.feat_col[f];
+        desc[f].kind = c.kind[j];
+        desc[f].cat_off = 0;
+        desc[f].cat_len = 0;
+        if (c.kind[j] != 1) continue;
+        const auto& dict = c.dict[j];
+        desc[f].cat_off = (int)crank.size();
+        desc[f].cat_len = (int)dict.size();
+        e.dv.cat_off[f] = desc[f].cat_off;
+        std::vector<int> ids(dict.size());
+        for (size_t i = 0; i < ids.size(); ++i) ids[i] = (int)i;
+        std::sort(ids.begin(), ids.end(), [&](int a, int b) { return dict[a] < dict[b]; });
+        crank.resize(crank.size() + dict.size());
+        for (size_t r = 0; r < ids.size(); ++r) crank[desc[f].cat_off + ids[r]] = (int32_t)r;
+    }
+    const int cat_total = (int)crank.size();
+    DevBuf ddesc(nf * sizeof(FeatDesc), ctx.stream), dcrank(std::max(cat_total, 1) * 4, ctx.stream);
+    IGB_CUDA(cudaMemcpyAsync(ddesc.p, desc.data(), nf * sizeof(FeatDesc), cudaMemcpyHostToDevice, ctx.stream));
+    if (cat_total)
+        IGB_CUDA(cudaMemcpyAsync(dcrank.p, crank.data(), cat_total * 4, cudaMemcpyHostToDevice, ctx.stream));
+    // exact distinct (feature, code), then the ranking and the pack tables
+    DevBuf slots((size_t)kVocabSlots * sizeof(ulonglong2), ctx.stream), u_code(kVocabMax * 8, ctx.stream),
+        u_feat(kVocabMax * 4, ctx.stream), u_count(8, ctx.stream);
+    IGB_CUDA(cudaMemsetAsync(slots.p, 0, (size_t)kVocabSlots * sizeof(ulonglong2), ctx.stream));
+    IGB_CUDA(cudaMemsetAsync(u_count.p, 0, 8, ctx.stream));
+    IGB_LAUNCH(ctx, vocab_unique, (unsigned)ctx.sm_count, 256, 0, lcode.as<int64_t>(), lcol.as<int32_t>(),
+               lcnt.as<unsigned long long>(), slots.as<ulonglong2>(), u_code.as<int64_t>(), u_feat.as<int32_t>(),
+               u_count.as<unsigned int>());
+    DeviceVocab& dv = e.dv;
+    dv.n_feat = nf;
+    dv.feat_col = d.feat_col;
+    dv.lut.alloc(nf * sizeof(Lut), ctx.stream);
+    dv.lcodes.alloc(kVocabMax * 8, ctx.stream);
+    dv.lbits.alloc(kVocabMax * 4, ctx.stream);
+    dv.cbits.alloc(std::max(cat_total, 1) * 4, ctx.stream);
+    DevBuf ubits(kVocabMax * 4, ctx.stream), list(kVocabMax * 12 + 8, ctx.stream);
+    int64_t* list_code = list.as<int64_t>();
+    int32_t* list_feat = reinterpret_cast<int32_t*>(list.as<char>() + kVocabMax * 8);
+    unsigned int* out_L = reinterpret_cast<unsigned int*>(list.as<char>() + kVocabMax * 12);
+    uint64_t pow10p = 1;
+    for (int i = 0; i < c.decimals; ++i) pow10p *= 10;
+    const int smem = kVocabMax * 18;
+    IGB_CUDA(cudaFuncSetAttribute(vocab_build, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    IGB_LAUNCH(ctx, vocab_build, 1, 1024, smem, u_code.as<int64_t>(), u_feat.as<int32_t>(),
+               u_count.as<unsigned int>(), ddesc.as<FeatDesc>(), nf, dcrank.as<int32_t>(), cat_total, pow10p,
+               dv.lut.as<Lut>(), dv.lcodes.as<int64_t>(), dv.lbits.as<int32_t>(), dv.cbits.as<int32_t>(),
+               ubits.as<int32_t>(), list_code, list_feat, out_L);
+    unsigned int L = 0;
+    read_back(ctx, &L, out_L, 4);
+    if (L > (unsigned)kVocabMax) {
+        dv = DeviceVocab{};
+        return false;
+    }
+    e.L = L;
+    dv.valid = true;
+    for (DevBuf* b : {&dv.lut, &dv.lcodes, &dv.lbits, &dv.cbits}) b->persist();
+    // the host text: tokens in bit order, copied back behind the tables
+    auto job = std::make_shared<HostVocabJob>();
+    const size_t bytes = (size_t)L * 12;
+    IGB_CUDA(cudaMallocHost(&job->pinned, std::max<size_t>(bytes, 16)));
+    if (L) {
+        IGB_CUDA(cudaMemcpyAsync(job->pinned, list_code, (size_t)L * 8, cudaMemcpyDeviceToHost, ctx.stream));
+        IGB_CUDA(cudaMemcpyAsync(static_cast<char*>(job->pinned) + (size_t)L * 8, list_feat, (size_t)L * 4,
+                                 cudaMemcpyDeviceToHost, ctx.stream));
+    }
+    IGB_CUDA(cudaEventCreateWithFlags(&job->ready, cudaEventDisableTiming));
+    IGB_CUDA(cudaEventRecord(job->ready, ctx.stream));
+    const int ncols = (int)c.n_cols, decimals = c.decimals;
+    std::vector<int> kind = c.kind, fcol = d.feat_col;
+    HostVocabJob* jp = job.get();
+    ig_encoding* ep = &e;
+    const auto* dict = &e.dict;  // e.dict = c.dict (copied before this call)
+    job->th = std::thread([jp, ep, dict, ncols, decimals, kind, fcol, L] {
+        try {
+            IGB_CUDA(cudaEventSynchronize(jp->ready));
+            const int64_t* code = static_cast<const int64_t*>(jp->pinned);
+            const int32_t* feat = reinterpret_cast<const int32_t*>(static_cast<const char*>(jp->pinned) + (size_t)L * 8);
+            ig_encoding& E = *ep;
+            E.num_codes.assign(ncols, {});
+            E.num_bits.assign(ncols, {});
+            E.cat_bits.assign(ncols, {});
+            E.empty_bit.assign(ncols, -1);
+            std::vector<std::vector<std::pair<int64_t, int32_t>>> num(ncols);
+            std::string prev, blob;
+            for (uint32_t b = 0; b < L; ++b) {
+                const int j = fcol[feat[b]];
+                std::string value;
+                if (code[b] == kEmptyCode)
+                    value.clear();
+                else if (kind[j] == 0)
+                    value = format_units(code[b], decimals);
+                else
+                    value = (*dict)[j][(size_t)code[b]];
+                std::string text = std::to_string(j) + ":" + value;
+                if (b && !(prev < text)) fail(IG_E_CUDA, "device vocabulary order differs from byte order at bit " +
+                                                             std::to_string(b) + " ('" + prev + "', '" + text + "')");
+                blob += text;
+                blob += '\n';
+                if (code[b] == kEmptyCode)
+                    E.empty_bit[j] = (int)b;
+                else if (kind[j] == 0)
+                    num[j].push_back({code[b], (int32_t)b});
+                else
+                    E.cat_bits[j].emplace(value, (int32_t)b);
+                prev = std::move(text);
+            }
+            for (int j = 0; j < ncols; ++j) {
+                std::sort(num[j].begin(), num[j].end());
+                for (auto& [cd, bit] : num[j]) {
+                    E.num_codes[j].push_back(cd);
+                    E.num_bits[j].push_back(bit);
+                }
+            }
+            E.vocab_blob = std::move(blob);
+        } catch (...) {
+            jp->err = std::current_exception();
+        }
+    });
+    e.hv = std::move(job);
+    return true;
+}
+
+}  // namespace
+
+void prefetch_columns(Ctx& ctx, ig_columns& c) {
+    if (c.d_values && c.device == ctx.device) return;  // already resident
+    auto pf = std::make_shared<PrefetchCols>();
+    pf->device = ctx.device;
+    pf->values.alloc(std::max<size_t>(c.values.size(), 1) * 8, ctx.copy);
+    pf->cat.alloc(std::max<size_t>(c.cat.size(), 1) * 4, ctx.copy);
+    pf->attack.alloc(std::max<size_t>(c.is_attack.size(), 1), ctx.copy);
+    if (!c.values.empty())
+        IGB_CUDA(cudaMemcpyAsync(pf->values.p, c.values.data(), c.values.size() * 8, cudaMemcpyHostToDevice, ctx.copy));
+    if (!c.cat.empty())
+        IGB_CUDA(cudaMemcpyAsync(pf->cat.p, c.cat.data(), c.cat.size() * 4, cudaMemcpyHostToDevice, ctx.copy));
+    if (!c.is_attack.empty())
+        IGB_CUDA(cudaMemcpyAsync(pf->attack.p, c.is_attack.data(), c.is_attack.size(), cudaMemcpyHostToDevice,
+                                 ctx.copy));
+    IGB_CUDA(cudaEventCreateWithFlags(&pf->ready, cudaEventDisableTiming));
+    IGB_CUDA(cudaEventRecord(pf->ready, ctx.copy));
+    c.prefetch = pf;
+}
+
+void drop_prefetch(ig_columns& c) {
+    if (auto* pf = static_cast<PrefetchCols*>(c.prefetch.get())) cudaEventSynchronize(pf->ready);
+    c.prefetch.reset();
+}
+
+void encode_training_dev(Ctx& ctx, const ig_columns& c, ig_encoding& e) {
+    if (c.is_attack.size() != c.n_rows) fail(IG_E_INVALID_ARG, "encode_training: columns built without labels");
+    e = ig_encoding{};
+    e.n_cols = c.n_cols;
+    e.label_index = c.label_index;
+    e.decimals = c.decimals;
+    e.kind = c.kind;
+    e.dict = c.dict;
+    DeviceCols d;
+    upload_and_code(ctx, c, d);
+
+    // (1b) distinct (column, code) over ALL training rows (vocabulary precedes the filter).
+    const size_t chunks = (d.n + kDistinctRows - 1) / kDistinctRows;
+    const size_t cap = std::max<size_t>((size_t)d.n_feat * d.n, 1);
+    DevBuf lcode(cap * 8, ctx.stream), lcol(cap * 4, ctx.stream), lcnt(8, ctx.stream);
+    IGB_CUDA(cudaMemsetAsync(lcnt.p, 0, 8, ctx.stream));
+    if (d.n && d.n_feat)
+        IGB_CUDA(cudaFuncSetAttribute(distinct_codes, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kDistinctSlots * (int)sizeof(int64_t)));
+    if (d.n && d.n_feat)
+        IGB_LAUNCH(ctx, distinct_codes, dim3((unsigned)chunks, (unsigned)d.n_feat), 256,
+                   kDistinctSlots * sizeof(int64_t), d.codes.as<int64_t>(), d.n,
+                   lcode.as<int64_t>(), lcol.as<int32_t>(), lcnt.as<unsigned long long>());
+    DevRows all;
+    if (device_vocab(ctx, c, d, lcode, lcol, lcnt, e)) {
+        // (1c) pack every training row with the device tables
+        pack_tables(ctx, e.L, d, e.dv.lut.as<Lut>(), e.dv.lcodes.as<int64_t>(), e.dv.lbits.as<int32_t>(),
+                    e.dv.cbits.as<int32_t>(), all);
+    } else {
+        host_vocab_build(ctx, c, d, lcode, lcol, lcnt, e, all);
+    }
     const size_t n = all.n, k = all.k;
 
     // Class checks + anti-contradiction filter (pipeline.cpp:306-318) on the device.
@@ -506,6 +930,51 @@ void encode_rows_dev(Ctx& ctx, const ig_columns& c, const ig_encoding& train, ig
     e.decimals = train.decimals;
     DeviceCols d;
     const bool host_read = upload_and_code(ctx, c, d);
+    if (train.dv.valid && train.dv.n_feat == d.n_feat && train.dv.feat_col == d.feat_col) {
+        // the training vocabulary's device tables: numeric codes and empty
+        // tokens as they are; categorical ids of this table -> training ids
+        // through the value text (host, from the two dictionaries) -> bits
+        const DeviceVocab& dv = train.dv;
+        std::vector<int32_t> remap, train_off;
+        std::vector<int> cfeat, coff, clen;
+        for (int f = 0; f < d.n_feat; ++f) {
+            const int j = d.feat_col[f];
+            if (c.kind[j] != 1) continue;
+            std::unordered_map<std::string, int32_t> tid;
+            for (size_t i = 0; i < train.dict[j].size(); ++i) tid.emplace(train.dict[j][i], (int32_t)i);
+            cfeat.push_back(f);
+            coff.push_back((int)remap.size());
+            clen.push_back((int)c.dict[j].size());
+            for (const auto& v : c.dict[j]) {
+                auto it = tid.find(v);
+                remap.push_back(it == tid.end() ? -1 : it->second);
+                train_off.push_back(dv.cat_off[f]);
+            }
+        }
+        DevBuf lut(d.n_feat * sizeof(Lut), ctx.stream), cb(std::max<size_t>(remap.size(), 1) * 4, ctx.stream);
+        IGB_CUDA(cudaMemcpyAsync(lut.p, dv.lut.p, d.n_feat * sizeof(Lut), cudaMemcpyDeviceToDevice, ctx.stream));
+        if (!cfeat.empty()) {
+            DevBuf rm(remap.size() * 4 + train_off.size() * 4 + cfeat.size() * 12, ctx.stream);
+            std::vector<int32_t> host(remap);
+            host.insert(host.end(), train_off.begin(), train_off.end());
+            for (size_t i = 0; i < cfeat.size(); ++i) {
+                host.push_back(cfeat[i]);
+                host.push_back(coff[i]);
+                host.push_back(clen[i]);
+            }
+            IGB_CUDA(cudaMemcpyAsync(rm.p, host.data(), host.size() * 4, cudaMemcpyHostToDevice, ctx.stream));
+            const int32_t* rmp = rm.as<int32_t>();
+            if (!remap.empty())
+                IGB_LAUNCH(ctx, remap_cat, grid_for(ctx, remap.size(), 256), 256, 0, rmp, (int)remap.size(),
+                           dv.cbits.as<int32_t>(), rmp + remap.size(), cb.as<int32_t>());
+            IGB_LAUNCH(ctx, patch_cat_lut, 1, 256, 0, rmp + 2 * remap.size(), (int)cfeat.size(), lut.as<Lut>());
+        }
+        pack_tables(ctx, train.L, d, lut.as<Lut>(), dv.lcodes.as<int64_t>(), dv.lbits.as<int32_t>(), cb.as<int32_t>(),
+                    e.all);
+        if (host_read || !queue_only) IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+        return;
+    }
+    train.host_vocab();
     // Categorical ids of this table → training bits through the token text.
     std::vector<std::vector<int32_t>> cat_id_to_bit(c.n_cols);
     for (size_t j = 0; j < c.n_cols; ++j) {

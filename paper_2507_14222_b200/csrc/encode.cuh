@@ -9,17 +9,38 @@
 #include "host_pipeline.hpp"
 #include "ig_internal.cuh"
 
+// Host text of a vocabulary built on the device (encode.cu): the tokens in bit
+// order are copied back and turned into text on a host thread while the fit
+// runs; readers of the host fields call ig_encoding::host_vocab() first.
+struct HostVocabJob;
+
+// A training vocabulary's pack lookup tables, resident on the device.
+struct DeviceVocab {
+    bool valid = false;
+    int n_feat = 0;
+    std::vector<int> feat_col;      // feature -> table column
+    std::vector<int> cat_off;       // per feature: offset of its dictionary in cbits (categorical)
+    igb::DevBuf lut;                // n_feat Lut (encode.cu)
+    igb::DevBuf lcodes, lbits;      // numeric (feature, code) sorted -> bit
+    igb::DevBuf cbits;              // categorical (feature, training id) -> bit
+};
+
 struct ig_encoding {
     uint32_t L = 0;
     size_t n_cols = 0, label_index = 0;
     int decimals = 2;
     std::vector<int> kind;
     std::vector<std::vector<std::string>> dict;
+    // host vocabulary fields (complete after host_vocab())
     std::string vocab_blob;                                   // tokens in bit order, '\n'-terminated
     std::vector<std::vector<int64_t>> num_codes;              // per column, sorted units
     std::vector<std::vector<int32_t>> num_bits;               // per column, matching bits
     std::vector<std::unordered_map<std::string, int32_t>> cat_bits;  // per column text -> bit
     std::vector<int> empty_bit;                               // per column bit of "j:" or -1
+    DeviceVocab dv;                                           // training encodings: device tables
+    std::shared_ptr<HostVocabJob> hv;                         // pending host text (device-built vocabulary)
+    // wait for the host vocabulary fields (rethrows the builder's error)
+    const ig_encoding& host_vocab() const;
     igb::DevRows attack, normal, all;
     std::vector<uint64_t> removed;                            // anti-contradiction source rows
     // test encodings: the rows' postings, built in the background by the
