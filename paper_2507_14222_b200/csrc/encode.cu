@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <limits>
 #include <string>
 #include <unordered_map>
@@ -430,19 +431,23 @@ __global__ void gather_rows_idx(const int64_t* __restrict__ src, const uint32_t*
 }
 
 // Stable selection of row indices whose flag is set.
-size_t select_flagged(Ctx& ctx, const uint8_t* d_flags, size_t n, DevBuf& idx_out) {
-    DevBuf iota(n * 4, ctx.stream), nsel(8, ctx.stream);
-    idx_out.alloc(std::max<size_t>(n, 1) * 4, ctx.stream);
+// Stable selection of row indices whose flag is set, for several flag arrays
+// at once: the counts come back in one read-back.
+void select_flagged_n(Ctx& ctx, const uint8_t* const* d_flags, int nsets, size_t n, DevBuf* idx_out, size_t* counts) {
+    DevBuf iota(std::max<size_t>(n, 1) * 4, ctx.stream), nsel(8 * nsets, ctx.stream);
     IGB_LAUNCH(ctx, iota32, grid_for(ctx, n, 256), 256, 0, iota.as<uint32_t>(), n);
     size_t tb = 0;
-    IGB_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, iota.as<uint32_t>(), d_flags, idx_out.as<uint32_t>(),
+    IGB_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, iota.as<uint32_t>(), d_flags[0], iota.as<uint32_t>(),
                                         nsel.as<int64_t>(), (int64_t)n, ctx.stream));
     DevBuf temp(tb, ctx.stream);
-    IGB_CUDA(cub::DeviceSelect::Flagged(temp.p, tb, iota.as<uint32_t>(), d_flags, idx_out.as<uint32_t>(),
-                                        nsel.as<int64_t>(), (int64_t)n, ctx.stream));
-    int64_t m = 0;
-    read_back(ctx, &m, nsel.p, 8);
-    return (size_t)m;
+    for (int s = 0; s < nsets; ++s) {
+        idx_out[s].alloc(std::max<size_t>(n, 1) * 4, ctx.stream);
+        IGB_CUDA(cub::DeviceSelect::Flagged(temp.p, tb, iota.as<uint32_t>(), d_flags[s], idx_out[s].as<uint32_t>(),
+                                            nsel.as<int64_t>() + s, (int64_t)n, ctx.stream));
+    }
+    std::vector<int64_t> h(nsets);
+    read_back(ctx, h.data(), nsel.p, 8 * nsets);
+    for (int s = 0; s < nsets; ++s) counts[s] = (size_t)h[s];
 }
 
 struct DeviceCols {
@@ -665,7 +670,7 @@ struct HostVocabJob {
     ~HostVocabJob() {
         if (th.joinable()) th.join();
         if (ready) cudaEventDestroy(ready);
-        if (pinned) cudaFreeHost(pinned);
+        if (pinned) ig_host_free(pinned);
     }
 };
 
@@ -684,24 +689,38 @@ const ig_encoding& ig_encoding::host_vocab() const {
 namespace igb {
 namespace {
 
-bool device_vocab(Ctx& ctx, const ig_columns& c, const DeviceCols& d, const DevBuf& lcode, const DevBuf& lcol,
-                  const DevBuf& lcnt, ig_encoding& e) {
+// Host descriptors of the device vocabulary, prepared before the encode
+// kernels are queued so that the host work overlaps them: byte-order rank of
+// each "<j>:" prefix, categorical dictionary offsets and each value's
+// byte-order rank in its dictionary; staged in page-locked memory.
+struct VocabPrep {
+    bool ok = false;
+    int nf = 0, cat_total = 0;
+    std::vector<int> cat_off;
+    void* pinned = nullptr;  // FeatDesc[nf] then int32 crank[cat_total] (the library's page-locked pool)
+    ~VocabPrep() {
+        if (pinned) ig_host_free(pinned);
+    }
+};
+
+void vocab_prepare(const ig_columns& c, VocabPrep& vp) {
     static const bool host_only = getenv("IG_HOST_VOCAB") != nullptr;  // A/B and fallback tests
-    const int nf = d.n_feat;
-    if (host_only || nf == 0 || nf > 255 || c.decimals > 12) return false;
-    // host descriptors: byte-order rank of each "<j>:" prefix, categorical
-    // dictionary offsets and each value's byte-order rank in its dictionary
+    std::vector<int> feat_col;
+    for (size_t j = 0; j < c.n_cols; ++j)
+        if (j != c.label_index) feat_col.push_back((int)j);
+    const int nf = (int)feat_col.size();
+    if (host_only || nf == 0 || nf > 255 || c.decimals > 12) return;
     std::vector<int> order(nf);
     for (int f = 0; f < nf; ++f) order[f] = f;
     std::sort(order.begin(), order.end(), [&](int a, int b) {
-        return std::to_string(d.feat_col[a]) + ":" < std::to_string(d.feat_col[b]) + ":";
+        return std::to_string(feat_col[a]) + ":" < std::to_string(feat_col[b]) + ":";
     });
     std::vector<FeatDesc> desc(nf);
     for (int r = 0; r < nf; ++r) desc[order[r]].col_rank = r;
     std::vector<int32_t> crank;
-    e.dv.cat_off.assign(nf, 0);
+    vp.cat_off.assign(nf, 0);
     for (int f = 0; f < nf; ++f) {
-        const int j = d.feat_col[f];
+        const int j = feat_col[f];
         desc[f].kind = c.kind[j];
         desc[f].cat_off = 0;
         desc[f].cat_len = 0;
@@ -709,18 +728,33 @@ bool device_vocab(Ctx& ctx, const ig_columns& c, const DeviceCols& d, const DevB
         const auto& dict = c.dict[j];
         desc[f].cat_off = (int)crank.size();
         desc[f].cat_len = (int)dict.size();
-        e.dv.cat_off[f] = desc[f].cat_off;
+        vp.cat_off[f] = desc[f].cat_off;
         std::vector<int> ids(dict.size());
         for (size_t i = 0; i < ids.size(); ++i) ids[i] = (int)i;
         std::sort(ids.begin(), ids.end(), [&](int a, int b) { return dict[a] < dict[b]; });
         crank.resize(crank.size() + dict.size());
         for (size_t r = 0; r < ids.size(); ++r) crank[desc[f].cat_off + ids[r]] = (int32_t)r;
     }
-    const int cat_total = (int)crank.size();
+    vp.nf = nf;
+    vp.cat_total = (int)crank.size();
+    const size_t bytes = nf * sizeof(FeatDesc) + crank.size() * 4;
+    if (ig_host_alloc(bytes, &vp.pinned) != IG_OK) return;
+    std::memcpy(vp.pinned, desc.data(), nf * sizeof(FeatDesc));
+    if (!crank.empty()) std::memcpy(static_cast<char*>(vp.pinned) + nf * sizeof(FeatDesc), crank.data(), crank.size() * 4);
+    vp.ok = true;
+}
+
+bool device_vocab(Ctx& ctx, const ig_columns& c, const DeviceCols& d, const VocabPrep& vp, const DevBuf& lcode,
+                  const DevBuf& lcol, const DevBuf& lcnt, ig_encoding& e) {
+    const int nf = d.n_feat;
+    if (!vp.ok || vp.nf != nf) return false;
+    const int cat_total = vp.cat_total;
+    e.dv.cat_off = vp.cat_off;
     DevBuf ddesc(nf * sizeof(FeatDesc), ctx.stream), dcrank(std::max(cat_total, 1) * 4, ctx.stream);
-    IGB_CUDA(cudaMemcpyAsync(ddesc.p, desc.data(), nf * sizeof(FeatDesc), cudaMemcpyHostToDevice, ctx.stream));
+    IGB_CUDA(cudaMemcpyAsync(ddesc.p, vp.pinned, nf * sizeof(FeatDesc), cudaMemcpyHostToDevice, ctx.stream));
     if (cat_total)
-        IGB_CUDA(cudaMemcpyAsync(dcrank.p, crank.data(), cat_total * 4, cudaMemcpyHostToDevice, ctx.stream));
+        IGB_CUDA(cudaMemcpyAsync(dcrank.p, static_cast<const char*>(vp.pinned) + nf * sizeof(FeatDesc),
+                                 (size_t)cat_total * 4, cudaMemcpyHostToDevice, ctx.stream));
     // exact distinct (feature, code), then the ranking and the pack tables
     DevBuf slots((size_t)kVocabSlots * sizeof(ulonglong2), ctx.stream), u_code(kVocabMax * 8, ctx.stream),
         u_feat(kVocabMax * 4, ctx.stream), u_count(8, ctx.stream);
@@ -760,7 +794,7 @@ bool device_vocab(Ctx& ctx, const ig_columns& c, const DeviceCols& d, const DevB
     // the host text: tokens in bit order, copied back behind the tables
     auto job = std::make_shared<HostVocabJob>();
     const size_t bytes = (size_t)L * 12;
-    IGB_CUDA(cudaMallocHost(&job->pinned, std::max<size_t>(bytes, 16)));
+    if (ig_host_alloc(std::max<size_t>(bytes, 16), &job->pinned) != IG_OK) fail(IG_E_OOM, "page-locked host memory");
     if (L) {
         IGB_CUDA(cudaMemcpyAsync(job->pinned, list_code, (size_t)L * 8, cudaMemcpyDeviceToHost, ctx.stream));
         IGB_CUDA(cudaMemcpyAsync(static_cast<char*>(job->pinned) + (size_t)L * 8, list_feat, (size_t)L * 4,
@@ -857,6 +891,8 @@ void encode_training_dev(Ctx& ctx, const ig_columns& c, ig_encoding& e) {
     e.decimals = c.decimals;
     e.kind = c.kind;
     e.dict = c.dict;
+    VocabPrep vp;
+    vocab_prepare(c, vp);
     DeviceCols d;
     upload_and_code(ctx, c, d);
 
@@ -873,7 +909,7 @@ void encode_training_dev(Ctx& ctx, const ig_columns& c, ig_encoding& e) {
                    kDistinctSlots * sizeof(int64_t), d.codes.as<int64_t>(), d.n,
                    lcode.as<int64_t>(), lcol.as<int32_t>(), lcnt.as<unsigned long long>());
     DevRows all;
-    if (device_vocab(ctx, c, d, lcode, lcol, lcnt, e)) {
+    if (device_vocab(ctx, c, d, vp, lcode, lcol, lcnt, e)) {
         // (1c) pack every training row with the device tables
         pack_tables(ctx, e.L, d, e.dv.lut.as<Lut>(), e.dv.lcodes.as<int64_t>(), e.dv.lbits.as<int32_t>(),
                     e.dv.cbits.as<int32_t>(), all);
@@ -896,10 +932,12 @@ void encode_training_dev(Ctx& ctx, const ig_columns& c, ig_encoding& e) {
     DevBuf keep_a(n, ctx.stream), keep_n(n, ctx.stream), removed(n, ctx.stream);
     IGB_LAUNCH(ctx, group_flags, grid_for(ctx, n, 256), 256, 0, grp.as<uint32_t>(), slot_cls.as<unsigned int>(),
                d.attack_ptr, n, keep_a.as<uint8_t>(), keep_n.as<uint8_t>(), removed.as<uint8_t>());
-    DevBuf idx_a, idx_n, idx_r;
-    const size_t na = select_flagged(ctx, keep_a.as<uint8_t>(), n, idx_a);
-    const size_t nn = select_flagged(ctx, keep_n.as<uint8_t>(), n, idx_n);
-    const size_t nr = select_flagged(ctx, removed.as<uint8_t>(), n, idx_r);
+    DevBuf idx[3];
+    size_t cnt[3];
+    const uint8_t* flags[3] = {keep_a.as<uint8_t>(), keep_n.as<uint8_t>(), removed.as<uint8_t>()};
+    select_flagged_n(ctx, flags, 3, n, idx, cnt);
+    DevBuf &idx_a = idx[0], &idx_n = idx[1], &idx_r = idx[2];
+    const size_t na = cnt[0], nn = cnt[1], nr = cnt[2];
     if (na == 0 || nn == 0) fail(IG_E_DATA, "anti-contradiction filtering emptied a class; training impossible");
     if (nr) {
         std::vector<uint32_t> h(nr);
