@@ -194,6 +194,10 @@ pair_enum(const int64_t* __restrict__ X, uint32_t n, int k_rt, int stride, uint6
     int64_t* sI = sm + kLocalSlots / 2;
     int64_t* sJ = sI + (size_t)TILE * stride;
     unsigned long long* sKey = reinterpret_cast<unsigned long long*>(sJ + (size_t)TILE * stride);  // k fingerprint keys
+    unsigned long long* sOr = sKey + k;  // 2k: OR of block I's rows, then of block J's
+    __shared__ unsigned long long s_h[2][TILE];     // hash of each projected row
+    __shared__ uint8_t s_list[2][TILE];             // distinct projected rows of I and J
+    __shared__ int s_cnt[2];
     __shared__ uint2 s_reps[kStageReps];
     __shared__ unsigned int s_nrep;
     __shared__ unsigned long long s_base;
@@ -251,13 +255,72 @@ pair_enum(const int64_t* __restrict__ X, uint32_t n, int k_rt, int stride, uint6
             sJ[r * stride + w] = (j0 + r < n) ? X[(size_t)(j0 + r) * k + w] : 0;
         }
         for (int q = threadIdx.x; q < kLocalSlots; q += kPairThreads) local[q] = 0u;
+        const bool diag = bi == bj;
+        const int nrI = (int)min((uint32_t)TILE, n - i0), nrJ = diag ? 0 : (int)min((uint32_t)TILE, n - j0);
+        if (!diag) {
+            // Row equivalence within an off-diagonal tile: with OR_J the OR of
+            // block J's rows, x_u & x_v = (x_u & OR_J) & (x_v & OR_I) for every
+            // u in I, v in J.  So each block is projected onto the other's OR
+            // and only its distinct projections are paired — the tile's set of
+            // intersections is unchanged (exact), and rows that differ only in
+            // tokens the other block never holds (prototype mutations) collapse.
+            __syncthreads();
+            for (int q = threadIdx.x; q < 2 * k; q += kPairThreads) {
+                const int side = q >= k, w = side ? q - k : q;
+                const int64_t* src = side ? sJ : sI;
+                const int nr = side ? nrJ : nrI;
+                unsigned long long acc = 0;
+                for (int r = 0; r < nr; ++r) acc |= (unsigned long long)src[r * stride + w];
+                sOr[q] = acc;
+            }
+            __syncthreads();
+            for (int q = threadIdx.x; q < TILE * k; q += kPairThreads) {
+                const int r = q / k, w = q % k;
+                sI[r * stride + w] &= (int64_t)sOr[k + w];
+                sJ[r * stride + w] &= (int64_t)sOr[w];
+            }
+            __syncthreads();
+            for (int q = threadIdx.x; q < 2 * TILE; q += kPairThreads) {
+                const int side = q >= TILE, r = side ? q - TILE : q;
+                const int64_t* row = (side ? sJ : sI) + r * stride;
+                unsigned long long h = 0x9e3779b97f4a7c15ull;
+                for (int w = 0; w < k; ++w) h = mix64(h ^ (unsigned long long)row[w]);
+                s_h[side][r] = h;
+            }
+            __syncthreads();
+            // a row is listed iff no earlier row of its block has the same projection
+            if (threadIdx.x < 64) {
+                const int side = threadIdx.x >> 5, lane = threadIdx.x & 31;
+                const int nr = side ? nrJ : nrI;
+                const int64_t* blk = side ? sJ : sI;
+                int cnt = 0;
+                for (int r0 = 0; r0 < TILE; r0 += 32) {
+                    const int r = r0 + lane;
+                    bool first = r < nr;
+                    if (first) {
+                        const unsigned long long h = s_h[side][r];
+                        for (int r2 = 0; r2 < r && first; ++r2) {
+                            if (s_h[side][r2] != h) continue;
+                            bool same = true;
+                            for (int w = 0; w < k && same; ++w) same = blk[r * stride + w] == blk[r2 * stride + w];
+                            first = !same;
+                        }
+                    }
+                    const unsigned int bal = __ballot_sync(0xffffffffu, first);
+                    if (first) s_list[side][cnt + __popc(bal & ((1u << lane) - 1u))] = (uint8_t)r;
+                    cnt += __popc(bal);
+                }
+                if (lane == 0) s_cnt[side] = cnt;
+            }
+        }
         __syncthreads();
-        for (int q = threadIdx.x; q < TILE * TILE; q += kPairThreads) {
+        const int nI = diag ? TILE : s_cnt[0], nJ = diag ? TILE : s_cnt[1];
+        for (int q = threadIdx.x; q < nI * nJ; q += kPairThreads) {
             // every lane runs the same trip count: re-converge the warp each
             // pair so the AND + fingerprint work runs on full warps (lanes
             // otherwise drift apart after the data-dependent probe paths)
             __syncwarp();
-            const int r = q / TILE, c = q % TILE;
+            const int r = diag ? q / TILE : s_list[0][q / nJ], c = diag ? q % TILE : s_list[1][q % nJ];
             const uint32_t u = i0 + r, v = j0 + c;
             if (u >= n || v >= n || u > v) continue;
             const int64_t* a = sI + r * stride;
@@ -330,7 +393,7 @@ pair_enum(const int64_t* __restrict__ X, uint32_t n, int k_rt, int stride, uint6
             }
             for (int i = lane; i < cnt; i += 32) {
                 const int qq = (int)mine[i];
-                const int r = qq / TILE, c = qq % TILE;
+                const int r = diag ? qq / TILE : s_list[0][qq / nJ], c = diag ? qq % TILE : s_list[1][qq % nJ];
                 const int64_t* a = sI + r * stride;
                 const int64_t* b = sJ + c * stride;
                 Fp fp;
@@ -600,7 +663,8 @@ uint64_t dedup_pairs(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, const 
     if (n > 0xffffffffull) fail(IG_E_INVALID_ARG, "enumerate: more than 2^32 rows");
     const int stride = (int)(k | 1);
     int tile_rows = 64;
-    while (tile_rows > 16 && (size_t)kLocalSlots * 4 + 2 * (size_t)tile_rows * stride * 8 + k * 8 > 200 * 1024) tile_rows /= 2;
+    while (tile_rows > 16 && (size_t)kLocalSlots * 4 + 2 * (size_t)tile_rows * stride * 8 + 3 * k * 8 > 190 * 1024)
+        tile_rows /= 2;
     const uint64_t blocks = (n + tile_rows - 1) / tile_rows;
     const uint64_t n_tiles = blocks * (blocks + 1) / 2;
     const uint64_t my_tiles = src.list ? 0 : (n_tiles > src.tile_begin ? (n_tiles - src.tile_begin + src.tile_step - 1) / src.tile_step : 0);
@@ -608,8 +672,8 @@ uint64_t dedup_pairs(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, const 
     // 64-row tiles; narrower tiles for wide rows (CICIDS shape, K up to ~750) so
     // both row blocks still fit in shared memory
     const int tile = tile_rows;
-    const size_t smem = (size_t)kLocalSlots * 4 + 2 * (size_t)tile * stride * 8 + k * 8;
-    if (smem > 200 * 1024) fail(IG_E_INVALID_ARG, "enumerate: rows wider than the shared-memory tile (K > 700)");
+    const size_t smem = (size_t)kLocalSlots * 4 + 2 * (size_t)tile * stride * 8 + 3 * k * 8;  // + keys, ORs
+    if (smem > 190 * 1024) fail(IG_E_INVALID_ARG, "enumerate: rows wider than the shared-memory tile (K > 700)");
     IGB_CUDA(cudaFuncSetAttribute(pair_enum<64, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     IGB_CUDA(cudaFuncSetAttribute(pair_enum<64, 14>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     IGB_CUDA(cudaFuncSetAttribute(pair_enum<64, 17>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -375,11 +375,9 @@ __global__ void gather_u64k(const unsigned long long* __restrict__ src, const ui
 // C3 ~1M patterns fall into ~35k groups, so most of the (t1, t2) work is shared.
 constexpr uint32_t kNoTok = 0xffffu;
 
-// sort key of a pattern: its q rarest tokens (t1, t2, t3, t4, ...; absent = all
+// sort key of a pattern: its q rarest tokens (t1, t2, t3, ...; absent = all
 // ones), b bits each, t1 most significant (q*b <= 64 bits, one radix sort).
-// The group is (t1, t2, t3); the further tokens order the patterns inside a
-// group so that neighbours share prefixes (consecutive warps then read the
-// same posting words).  expand_keys
+// The group is (t1, t2, t3).  expand_keys
 // restores the group part as (t1 << 32) | (t2 << 16) | t3 with kNoTok, which
 // sorts identically.
 __global__ void group_keys(const uint32_t* __restrict__ tok_beg, const uint32_t* __restrict__ tok_len,
@@ -884,7 +882,10 @@ void build_pattern_index(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, co
     // group patterns by their three rarest tokens
     int b = 1;
     while ((1u << b) <= L) ++b;  // token ids < L < 2^b - 1 stays free for "absent"
-    const int q = std::max(3, 64 / b);  // tokens in the sort key: the group (3) + as many as fit
+    // tokens in the sort key: the group (t1, t2, t3).  Sorting further tokens
+    // (neighbours sharing prefixes) only served the prefix-sharing scans that
+    // were measured slower and costs radix passes.
+    const int q = 3;
     DevBuf key(np * 8, ctx.stream), key2(np * 8, ctx.stream), idx(np * 4, ctx.stream);
     IGB_LAUNCH(ctx, group_keys, grid_for(ctx, np, 256), 256, 0, I.beg.as<uint32_t>(), I.len.as<uint32_t>(),
                I.toks->as<uint16_t>(), np, b, q, key.as<unsigned long long>(), idx.as<uint32_t>());
