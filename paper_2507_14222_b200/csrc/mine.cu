@@ -43,7 +43,10 @@ struct Table {
     unsigned long long* ovf_count;
     unsigned long long ovf_cap;
     unsigned long long* collisions;
-    int* fail;  // bit0 table full, bit1 overflow list full
+    int* fail;  // bit0 table full, bit1 overflow list full, bit2 retry list full
+    uint2* retry;                     // pairs the tile-local table could not place (inserted after the kernel)
+    unsigned long long* retry_count;
+    unsigned long long retry_cap;
     uint64_t seed;
     const unsigned long long* keys;  // K fingerprint keys of this level (derived from seed)
     uint64_t fp_mask;                // ~0; narrowed only by the IG_TEST_FP_BITS collision test knob
@@ -177,7 +180,8 @@ __device__ __forceinline__ void tile_of(uint64_t t, uint32_t& bi, uint32_t& bj) 
 // Pairs are first deduplicated inside the tile (shared-memory hash of
 // fingerprint tags, exact compare on the tile's staged rows), so only the first
 // pair of each distinct content in a tile probes the device-wide table.
-constexpr int kLocalSlots = 4096;  // >= TILE * TILE: every pair of a tile fits
+constexpr int kLocalSlots = 4096;
+constexpr int kLocalProbes = 64;  // then the pair goes to the retry list (adversarial fingerprints only)
 
 // KC > 0: the row width K is a compile-time constant (the common NSL shapes),
 // so the word loops unroll; KC <= 16 also keeps the pair's AND in registers
@@ -343,8 +347,7 @@ pair_enum(const int64_t* __restrict__ X, uint32_t n, int k_rt, int stride, uint6
             const unsigned int entry = ((unsigned int)(f >> 44) | 1u) << 12 | (unsigned int)q;
             bool dup = false, placed = false;
             uint32_t s = (uint32_t)(f & (kLocalSlots - 1));
-            // kLocalSlots >= TILE * TILE pairs: an empty slot always exists, so the probe ends
-            for (;; s = (s + 1) & (kLocalSlots - 1)) {
+            for (int probe = 0; probe < kLocalProbes; ++probe, s = (s + 1) & (kLocalSlots - 1)) {
                 unsigned int cur = local[s];
                 if (cur == 0u) {
                     cur = atomicCAS(local + s, 0u, entry);
@@ -371,9 +374,16 @@ pair_enum(const int64_t* __restrict__ X, uint32_t n, int k_rt, int stride, uint6
             }
             // the first of its content (placed) is inserted into the device
             // table after the tile, on full warps (inline, the inserts ran
-            // ~2.5 lanes wide)
-            (void)dup;
-            (void)placed;
+            // ~2.5 lanes wide); a pair the local table could not place within
+            // kLocalProbes probes (only with adversarial fingerprints) is
+            // inserted into the same table by a follow-up launch
+            if (!dup && !placed) {
+                const unsigned long long o = atomicAdd(T.retry_count, 1ull);
+                if (o < T.retry_cap)
+                    T.retry[o] = make_uint2(u, v);
+                else
+                    atomicOr(T.fail, 4);
+            }
         }
         // deferred inserts: each warp compacts its 512 local slots in place to
         // the pair indices they hold, then inserts them 32 at a time
@@ -505,8 +515,8 @@ unsigned grid_for(const Ctx& ctx, size_t work, int threads) {
 }
 
 struct TableMem {
-    DevBuf slots, reps, ovf, ctr, keys;  // ctr: count, ovf_count, collisions, fail
-    Table make(Ctx& ctx, uint64_t cap, uint64_t ovf_cap, uint64_t seed, size_t k) {
+    DevBuf slots, reps, ovf, ctr, keys, retry;  // ctr: count, ovf_count, collisions, fail, retry_count
+    Table make(Ctx& ctx, uint64_t cap, uint64_t ovf_cap, uint64_t seed, size_t k, uint64_t retry_cap = 1) {
         keys.alloc(std::max<size_t>(k, 1) * 8, ctx.stream);
         IGB_LAUNCH(ctx, fp_keys, 1, 256, 0, seed, (int)k, keys.as<unsigned long long>());
         slots.alloc(cap * sizeof(ulonglong2), ctx.stream);
@@ -514,8 +524,9 @@ struct TableMem {
         const uint64_t limit = cap / 4 * 3;
         reps.alloc(limit * sizeof(uint2), ctx.stream);
         ovf.alloc(ovf_cap * sizeof(uint2), ctx.stream);
-        ctr.alloc(4 * sizeof(unsigned long long), ctx.stream);
-        IGB_CUDA(cudaMemsetAsync(ctr.p, 0, 4 * sizeof(unsigned long long), ctx.stream));
+        ctr.alloc(5 * sizeof(unsigned long long), ctx.stream);
+        IGB_CUDA(cudaMemsetAsync(ctr.p, 0, 5 * sizeof(unsigned long long), ctx.stream));
+        retry.alloc(std::max<uint64_t>(retry_cap, 1) * sizeof(uint2), ctx.stream);
         Table T;
         T.slots = slots.as<ulonglong2>();
         T.mask = cap - 1;
@@ -527,6 +538,9 @@ struct TableMem {
         T.ovf_cap = ovf_cap;
         T.collisions = ctr.as<unsigned long long>() + 2;
         T.fail = reinterpret_cast<int*>(ctr.as<unsigned long long>() + 3);
+        T.retry = retry.as<uint2>();
+        T.retry_count = ctr.as<unsigned long long>() + 4;
+        T.retry_cap = std::max<uint64_t>(retry_cap, 1);
         T.seed = seed;
         T.keys = keys.as<unsigned long long>();
         T.fp_mask = ~0ull;
@@ -691,6 +705,8 @@ uint64_t dedup_pairs(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, const 
     const uint64_t max_cap = next_pow2(2 * bound + 1024);
     if (cap > max_cap) cap = max_cap;
     int retries = 0;
+    uint64_t retry_cap = 1u << 14;  // tile-local overflow pairs (grows x8 when exceeded)
+    bool retry_grow = false;
     std::vector<DevBuf> level_reps;  // per level: reps
     std::vector<uint64_t> level_counts;
     uint64_t collisions_total = 0;
@@ -705,7 +721,8 @@ uint64_t dedup_pairs(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, const 
             TableMem tm;
             const uint64_t lcap = level == 0 ? cap : next_pow2(4 * n_pending + 1024);
             const uint64_t ovf_cap = level == 0 ? std::max<uint64_t>(1u << 20, cap / 64) : n_pending + 1;
-            Table T = tm.make(ctx, lcap, ovf_cap, 0x2545f4914f6cdd1dull * (uint64_t)(level + 1), k);
+            Table T = tm.make(ctx, lcap, ovf_cap, 0x2545f4914f6cdd1dull * (uint64_t)(level + 1), k,
+                              level == 0 && !src.list ? retry_cap : 1);
             if (level == 0 && src.list) {
                 if (src.n_list)
                     IGB_LAUNCH(ctx, pair_insert_list, grid_for(ctx, src.n_list, 256), 256, 0, d_rows, (int)k, src.list,
@@ -751,8 +768,19 @@ uint64_t dedup_pairs(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, const 
                            pending.as<uint2>(), n_pending, T);
             }
             if (ctx.progress) poll_progress(ctx);
-            unsigned long long h[4];
+            unsigned long long h[5];
             read_back(ctx, h, tm.ctr.p, sizeof(h));
+            if ((h[3] & 4u) && !(h[3] & 3u)) {  // retry list too small: grow it, redo the level
+                retry_cap = std::max<uint64_t>(retry_cap * 8, h[4]);
+                ok = false;
+                retry_grow = true;
+                break;
+            }
+            if (h[4] && !(h[3] & 0xffffffffu)) {  // pairs the tile-local tables could not place
+                IGB_LAUNCH(ctx, pair_insert_list, grid_for(ctx, h[4], 256), 256, 0, d_rows, (int)k, tm.retry.as<uint2>(),
+                           h[4], T);
+                read_back(ctx, h, tm.ctr.p, sizeof(h));
+            }
             const int failbits = (int)(h[3] & 0xffffffffu);
             if (failbits) {
                 ok = false;
@@ -767,6 +795,10 @@ uint64_t dedup_pairs(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, const 
             if (level > 64) fail(IG_E_CUDA, "enumerate: fingerprint collision levels did not converge");
         }
         if (ok) break;
+        if (retry_grow) {
+            retry_grow = false;
+            continue;
+        }
         if (cap >= max_cap) fail(IG_E_OOM, "enumerate: candidate table cannot grow further");
         cap = std::min<uint64_t>(cap * 4, max_cap);
         ++retries;
