@@ -319,11 +319,15 @@ pair_enum(const int64_t* __restrict__ X, uint32_t n, int k_rt, int stride, uint6
         }
         __syncthreads();
         const int nI = diag ? TILE : s_cnt[0], nJ = diag ? TILE : s_cnt[1];
-        for (int q = threadIdx.x; q < nI * nJ; q += kPairThreads) {
-            // every lane runs the same trip count: re-converge the warp each
-            // pair so the AND + fingerprint work runs on full warps (lanes
-            // otherwise drift apart after the data-dependent probe paths)
+        const int npairs = nI * nJ;
+        for (int q0 = 0; q0 < npairs; q0 += kPairThreads) {
+            // every lane runs the same trip count (npairs need not be a multiple
+            // of the block): re-converge the warp each pair so the AND +
+            // fingerprint work runs on full warps (lanes otherwise drift apart
+            // after the data-dependent probe paths)
             __syncwarp();
+            const int q = q0 + (int)threadIdx.x;
+            if (q >= npairs) continue;
             const int r = diag ? q / TILE : s_list[0][q / nJ], c = diag ? q % TILE : s_list[1][q % nJ];
             const uint32_t u = i0 + r, v = j0 + c;
             if (u >= n || v >= n || u > v) continue;
