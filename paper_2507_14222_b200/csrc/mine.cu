@@ -361,9 +361,9 @@ pair_enum(const int64_t* __restrict__ X, uint32_t n, int k_rt, int stride, uint6
                     }
                 }
                 if ((cur >> 12) != (entry >> 12)) continue;
-                const int q2 = (int)(cur & 0xfffu);
-                const int64_t* a2 = sI + (q2 / TILE) * stride;
-                const int64_t* b2 = sJ + (q2 % TILE) * stride;
+                const int q2 = (int)(cur & 0xfffu);  // in this tile's pair numbering (projected lists)
+                const int64_t* a2 = sI + (diag ? q2 / TILE : s_list[0][q2 / nJ]) * stride;
+                const int64_t* b2 = sJ + (diag ? q2 % TILE : s_list[1][q2 % nJ]) * stride;
                 bool same = true;
                 if constexpr (kRegs) {
 #pragma unroll
