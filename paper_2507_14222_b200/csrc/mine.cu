@@ -269,13 +269,15 @@ pair_enum(const int64_t* __restrict__ X, uint32_t n, int k_rt, int stride, uint6
             // intersections is unchanged (exact), and rows that differ only in
             // tokens the other block never holds (prototype mutations) collapse.
             __syncthreads();
-            for (int q = threadIdx.x; q < 2 * k; q += kPairThreads) {
-                const int side = q >= k, w = side ? q - k : q;
+            // ORs: a warp per word, two rows per lane, shuffle reduction
+            for (int q = threadIdx.x >> 5; q < 2 * k; q += kPairThreads / 32) {
+                const int side = q >= k, w = side ? q - k : q, lane = threadIdx.x & 31;
                 const int64_t* src = side ? sJ : sI;
                 const int nr = side ? nrJ : nrI;
                 unsigned long long acc = 0;
-                for (int r = 0; r < nr; ++r) acc |= (unsigned long long)src[r * stride + w];
-                sOr[q] = acc;
+                for (int r = lane; r < nr; r += 32) acc |= (unsigned long long)src[r * stride + w];
+                for (int o = 16; o; o >>= 1) acc |= __shfl_xor_sync(0xffffffffu, acc, o);
+                if (lane == 0) sOr[q] = acc;
             }
             __syncthreads();
             for (int q = threadIdx.x; q < TILE * k; q += kPairThreads) {
