@@ -167,6 +167,27 @@ __device__ void table_insert(const Table& T, const int64_t* __restrict__ X, int 
     atomicOr(T.fail, 1);
 }
 
+// TMA (bulk async copy) of a row block into shared memory, completion tracked
+// by an mbarrier's transaction count (sm_90+ cp.async.bulk)
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_load_rows(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)), "r"(phase) : "memory");
+}
+
 __device__ __forceinline__ void tile_of(uint64_t t, uint32_t& bi, uint32_t& bj) {
     // t enumerates (bi <= bj) column by column: t = bj(bj+1)/2 + bi
     uint64_t j = (uint64_t)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
@@ -191,7 +212,7 @@ template <int TILE, int KC>
 __global__ void __launch_bounds__(kPairThreads, KC == 17 ? 4 : KC > 0 && KC <= 16 ? 5 : 6)
 pair_enum(const int64_t* __restrict__ X, uint32_t n, int k_rt, int stride, uint64_t n_tiles, Table T,
           uint64_t tile_begin, uint64_t tile_step, unsigned long long* __restrict__ prog_ctr,
-          unsigned long long* __restrict__ prog_host, int project) {
+          unsigned long long* __restrict__ prog_host, int project, int use_tma) {
     const int k = KC > 0 ? KC : k_rt;
     constexpr bool kRegs = KC > 0 && KC <= 17;
     extern __shared__ int64_t sm[];
@@ -208,6 +229,15 @@ pair_enum(const int64_t* __restrict__ X, uint32_t n, int k_rt, int stride, uint6
     __shared__ unsigned long long s_base;
     __shared__ int s_stop;
     __shared__ unsigned long long s_pairs;  // pairs of the tile just finished (progress)
+    __shared__ alignas(8) uint64_t s_bar;   // TMA row-block arrival
+    // row blocks arrive by TMA when the shared layout is the global one (odd K:
+    // the conflict-free odd stride is K itself) and the block is full
+    const bool tma = use_tma && (k & 1) && stride == k;
+    unsigned phase = 0;
+    if (tma && threadIdx.x == 0) {
+        mbar_init(&s_bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     const RepStage stage{s_reps, &s_nrep};
     for (int w = threadIdx.x; w < k; w += kPairThreads) sKey[w] = T.keys[w];
     if (threadIdx.x == 0) {
@@ -254,12 +284,27 @@ pair_enum(const int64_t* __restrict__ X, uint32_t n, int k_rt, int stride, uint6
             const unsigned long long ri = min((uint32_t)TILE, n - i0), rj = min((uint32_t)TILE, n - j0);
             s_pairs = bi == bj ? ri * (ri + 1) / 2 : ri * rj;
         }
-        for (int q = threadIdx.x; q < TILE * k; q += kPairThreads) {
-            const int r = q / k, w = q % k;
-            sI[r * stride + w] = (i0 + r < n) ? X[(size_t)(i0 + r) * k + w] : 0;
-            sJ[r * stride + w] = (j0 + r < n) ? X[(size_t)(j0 + r) * k + w] : 0;
+        const bool tI = tma && i0 + TILE <= n, tJ = tma && j0 + TILE <= n;
+        if ((tI || tJ) && threadIdx.x == 0) {
+            // the previous tile's generic-proxy writes (projection) are complete
+            // (barrier above); order them before the async-proxy overwrite
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            const unsigned bytes = (unsigned)(TILE * k * 8);
+            mbar_expect_tx(&s_bar, (tI ? bytes : 0u) + (tJ ? bytes : 0u));
+            if (tI) tma_load_rows(sI, X + (size_t)i0 * k, bytes, &s_bar);
+            if (tJ) tma_load_rows(sJ, X + (size_t)j0 * k, bytes, &s_bar);
         }
+        if (!tI || !tJ)
+            for (int q = threadIdx.x; q < TILE * k; q += kPairThreads) {
+                const int r = q / k, w = q % k;
+                if (!tI) sI[r * stride + w] = (i0 + r < n) ? X[(size_t)(i0 + r) * k + w] : 0;
+                if (!tJ) sJ[r * stride + w] = (j0 + r < n) ? X[(size_t)(j0 + r) * k + w] : 0;
+            }
         for (int q = threadIdx.x; q < kLocalSlots; q += kPairThreads) local[q] = 0u;
+        if (tI || tJ) {
+            mbar_wait(&s_bar, phase);
+            phase ^= 1u;
+        }
         // plain: pairs numbered q = r * TILE + c over the whole tile (diagonal
         // tiles, or projection off); else over the blocks' distinct projections
         const bool plain = bi == bj || !project;
@@ -743,24 +788,25 @@ uint64_t dedup_pairs(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, const 
                 // prototype (C4: 1.16x faster), not on small classes (C3: 1.13x
                 // slower); the results are identical either way
                 const int project = n >= kProjectRows ? 1 : 0;
+                static const int use_tma = getenv("IG_TMA") ? atoi(getenv("IG_TMA")) : 1;  // A/B
                 unsigned long long* pc = ctx.progress ? ctx.progress->ctr : nullptr;
                 unsigned long long* ph = ctx.progress ? ctx.progress->dev : nullptr;
                 if (my_tiles) {
                     if (tile == 64 && k == 14)
                         IGB_LAUNCH(ctx, (pair_enum<64, 14>), grid, kPairThreads, smem, d_rows, (uint32_t)n, (int)k,
-                                   stride, n_tiles, T, src.tile_begin, src.tile_step, pc, ph, project);
+                                   stride, n_tiles, T, src.tile_begin, src.tile_step, pc, ph, project, use_tma);
                     else if (tile == 64 && k == 17)
                         IGB_LAUNCH(ctx, (pair_enum<64, 17>), grid, kPairThreads, smem, d_rows, (uint32_t)n, (int)k,
-                                   stride, n_tiles, T, src.tile_begin, src.tile_step, pc, ph, project);
+                                   stride, n_tiles, T, src.tile_begin, src.tile_step, pc, ph, project, use_tma);
                     else if (tile == 64)
                         IGB_LAUNCH(ctx, (pair_enum<64, 0>), grid, kPairThreads, smem, d_rows, (uint32_t)n, (int)k,
-                                   stride, n_tiles, T, src.tile_begin, src.tile_step, pc, ph, project);
+                                   stride, n_tiles, T, src.tile_begin, src.tile_step, pc, ph, project, use_tma);
                     else if (tile == 32)
                         IGB_LAUNCH(ctx, (pair_enum<32, 0>), grid, kPairThreads, smem, d_rows, (uint32_t)n, (int)k,
-                                   stride, n_tiles, T, src.tile_begin, src.tile_step, pc, ph, project);
+                                   stride, n_tiles, T, src.tile_begin, src.tile_step, pc, ph, project, use_tma);
                     else
                         IGB_LAUNCH(ctx, (pair_enum<16, 0>), grid, kPairThreads, smem, d_rows, (uint32_t)n, (int)k,
-                                   stride, n_tiles, T, src.tile_begin, src.tile_step, pc, ph, project);
+                                   stride, n_tiles, T, src.tile_begin, src.tile_step, pc, ph, project, use_tma);
                 }
                 if (ctx.diag) {
                     // useful work: K word-ANDs per pair (u <= v) of this launch's tiles

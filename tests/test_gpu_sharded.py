@@ -24,16 +24,20 @@ def _union(dicts, k):
     return w[order], s[order], sc[order]
 
 
-@pytest.mark.parametrize("rows,ratio", [(2500, 8), (20000, 1)])
-def test_emulated_world_matches_single_device(mods, rows, ratio):
+@pytest.mark.parametrize("shape,rows,ratio", [("nsl", 2500, 8), ("nsl", 20000, 1), ("cicids", 12000, 8)])
+def test_emulated_world_matches_single_device(mods, shape, rows, ratio):
+    """cicids: configs[4]'s shape (p = 2, K ~ 70 wide rows, 80/20) on a sample
+    that fits one device — the 1-GPU vs N-GPU identity C5 relies on."""
     import torch
     api, sharded = mods
-    csv = synth.nsl_csv(rows, seed=77)
+    cic = shape == "cicids"
+    csv = synth.cicids_csv(rows, seed=77) if cic else synth.nsl_csv(rows, seed=77)
     ctx = api.default_context()
     table = api.read_csv(csv)
     ntr = ratio * table.rows // 10
     tr, te = table.slice(0, ntr), table.slice(ntr, table.rows)
-    schema = api.infer_schema(tr, "label", decimals=1)
+    schema = api.infer_schema(tr, "Label" if cic else "label", normal_values=["BENIGN"] if cic else [],
+                              decimals=2 if cic else 1)
     enc = api.encode_training(api.Columns(tr, schema, True), ctx)
     tenc = api.encode_rows(api.Columns(te, schema, False), enc, ctx)
     single = api.fit_encoded(enc)
