@@ -208,11 +208,11 @@ constexpr size_t kProjectRows = 16384;  // distinct class rows from which off-di
 // KC > 0: the row width K is a compile-time constant (the common NSL shapes),
 // so the word loops unroll; KC <= 16 also keeps the pair's AND in registers
 // for the duplicate check.
-template <int TILE, int KC>
+template <int TILE, int KC, bool PROJ>
 __global__ void __launch_bounds__(kPairThreads, KC == 17 ? 4 : KC > 0 && KC <= 16 ? 5 : 6)
 pair_enum(const int64_t* __restrict__ X, uint32_t n, int k_rt, int stride, uint64_t n_tiles, Table T,
           uint64_t tile_begin, uint64_t tile_step, unsigned long long* __restrict__ prog_ctr,
-          unsigned long long* __restrict__ prog_host, int project, int use_tma) {
+          unsigned long long* __restrict__ prog_host, int use_tma) {
     const int k = KC > 0 ? KC : k_rt;
     constexpr bool kRegs = KC > 0 && KC <= 17;
     extern __shared__ int64_t sm[];
@@ -307,7 +307,7 @@ pair_enum(const int64_t* __restrict__ X, uint32_t n, int k_rt, int stride, uint6
         }
         // plain: pairs numbered q = r * TILE + c over the whole tile (diagonal
         // tiles, or projection off); else over the blocks' distinct projections
-        const bool plain = bi == bj || !project;
+        const bool plain = !PROJ || bi == bj;
         const int nrI = (int)min((uint32_t)TILE, n - i0), nrJ = plain ? 0 : (int)min((uint32_t)TILE, n - j0);
         if (!plain) {
             // Row equivalence within an off-diagonal tile: with OR_J the OR of
@@ -742,11 +742,15 @@ uint64_t dedup_pairs(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, const 
     const int tile = tile_rows;
     const size_t smem = (size_t)kLocalSlots * 4 + 2 * (size_t)tile * stride * 8 + 3 * k * 8;  // + keys, ORs
     if (smem > 190 * 1024) fail(IG_E_INVALID_ARG, "enumerate: rows wider than the shared-memory tile (K > 700)");
-    IGB_CUDA(cudaFuncSetAttribute(pair_enum<64, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    IGB_CUDA(cudaFuncSetAttribute(pair_enum<64, 14>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    IGB_CUDA(cudaFuncSetAttribute(pair_enum<64, 17>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    IGB_CUDA(cudaFuncSetAttribute(pair_enum<32, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    IGB_CUDA(cudaFuncSetAttribute(pair_enum<16, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+#define IGB_PAIR_ATTR(T_, K_)                                                                                 \
+    IGB_CUDA(cudaFuncSetAttribute(pair_enum<T_, K_, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    IGB_CUDA(cudaFuncSetAttribute(pair_enum<T_, K_, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))
+    IGB_PAIR_ATTR(64, 0);
+    IGB_PAIR_ATTR(64, 14);
+    IGB_PAIR_ATTR(64, 17);
+    IGB_PAIR_ATTR(32, 0);
+    IGB_PAIR_ATTR(16, 0);
+#undef IGB_PAIR_ATTR
 
     // Initial capacity from a sub-linear guess of the distinct count; doubled
     // (x4) and rerun if the table fills.  Results never depend on capacity.
@@ -792,21 +796,27 @@ uint64_t dedup_pairs(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, const 
                 unsigned long long* pc = ctx.progress ? ctx.progress->ctr : nullptr;
                 unsigned long long* ph = ctx.progress ? ctx.progress->dev : nullptr;
                 if (my_tiles) {
-                    if (tile == 64 && k == 14)
-                        IGB_LAUNCH(ctx, (pair_enum<64, 14>), grid, kPairThreads, smem, d_rows, (uint32_t)n, (int)k,
-                                   stride, n_tiles, T, src.tile_begin, src.tile_step, pc, ph, project, use_tma);
-                    else if (tile == 64 && k == 17)
-                        IGB_LAUNCH(ctx, (pair_enum<64, 17>), grid, kPairThreads, smem, d_rows, (uint32_t)n, (int)k,
-                                   stride, n_tiles, T, src.tile_begin, src.tile_step, pc, ph, project, use_tma);
-                    else if (tile == 64)
-                        IGB_LAUNCH(ctx, (pair_enum<64, 0>), grid, kPairThreads, smem, d_rows, (uint32_t)n, (int)k,
-                                   stride, n_tiles, T, src.tile_begin, src.tile_step, pc, ph, project, use_tma);
-                    else if (tile == 32)
-                        IGB_LAUNCH(ctx, (pair_enum<32, 0>), grid, kPairThreads, smem, d_rows, (uint32_t)n, (int)k,
-                                   stride, n_tiles, T, src.tile_begin, src.tile_step, pc, ph, project, use_tma);
-                    else
-                        IGB_LAUNCH(ctx, (pair_enum<16, 0>), grid, kPairThreads, smem, d_rows, (uint32_t)n, (int)k,
-                                   stride, n_tiles, T, src.tile_begin, src.tile_step, pc, ph, project, use_tma);
+#define IGB_PAIR_ENUM(T_, K_, P_)                                                                             \
+    IGB_LAUNCH(ctx, (pair_enum<T_, K_, P_>), grid, kPairThreads, smem, d_rows, (uint32_t)n, (int)k, stride,   \
+               n_tiles, T, src.tile_begin, src.tile_step, pc, ph, use_tma)
+#define IGB_PAIR_ENUM_P(T_, K_)          \
+    if (project)                         \
+        IGB_PAIR_ENUM(T_, K_, true);     \
+    else                                 \
+        IGB_PAIR_ENUM(T_, K_, false)
+                    if (tile == 64 && k == 14) {
+                        IGB_PAIR_ENUM_P(64, 14);
+                    } else if (tile == 64 && k == 17) {
+                        IGB_PAIR_ENUM_P(64, 17);
+                    } else if (tile == 64) {
+                        IGB_PAIR_ENUM_P(64, 0);
+                    } else if (tile == 32) {
+                        IGB_PAIR_ENUM_P(32, 0);
+                    } else {
+                        IGB_PAIR_ENUM_P(16, 0);
+                    }
+#undef IGB_PAIR_ENUM_P
+#undef IGB_PAIR_ENUM
                 }
                 if (ctx.diag) {
                     // useful work: K word-ANDs per pair (u <= v) of this launch's tiles
