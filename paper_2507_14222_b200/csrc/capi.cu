@@ -260,10 +260,10 @@ void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m, bool enumerate 
             m.cand[c].ordered = false;
         }
         tr.mark("enumerate");
-        // one posting row per distinct training row, with its multiplicity:
-        // coverage ignores it, support weights by it (C4: 37 % of the rows
-        // are repeats, so the scans walk 37 % fewer posting words)
-        if (vertical) igb::build_postings(cx, X[c].p, X[c].n, k, L, PX[c], true, true, pc, true);
+        // every training row (support counts identical rows);
+        // distinct rows weighted by their multiplicity measured slower
+        //
+        if (vertical) igb::build_postings(cx, X[c].p, X[c].n, k, L, PX[c], true, false, pc);
         tr.mark("postings");
     }, concurrent);
     // one token rank space for every scan of this fit: frequencies over all
