@@ -315,11 +315,6 @@ __global__ void row_heads(const int64_t* __restrict__ rows, const uint32_t* __re
 }
 
 // exclusive sum of heads -> group index of each position (heads start a new group)
-__global__ void count_groups(const uint32_t* __restrict__ group, size_t n, uint32_t* __restrict__ mult) {
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
-        atomicAdd(mult + group[i], 1u);
-}
-
 __global__ void fix_group(const uint32_t* __restrict__ head, size_t n, uint32_t* __restrict__ group) {
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
         group[i] = group[i] + head[i] - 1;
@@ -591,7 +586,7 @@ grouped_scan(const unsigned long long* __restrict__ dense, size_t W, size_t n_ro
              const uint32_t* __restrict__ ew, const unsigned long long* __restrict__ em,
              const int64_t* __restrict__ scores, unsigned long long* __restrict__ acc,
              int64_t* __restrict__ support_out, uint8_t* __restrict__ cover_out, int* __restrict__ flags,
-             unsigned long long* __restrict__ work, const uint32_t* __restrict__ mult) {
+             unsigned long long* __restrict__ work) {
     const int lane = threadIdx.x & 31;
     const size_t warps = ((size_t)gridDim.x * blockDim.x) >> 5;
     bool ovf = false;
@@ -639,16 +634,7 @@ grouped_scan(const unsigned long long* __restrict__ dense, size_t W, size_t n_ro
                 if (mw) mw &= col[tt * Wu];
             }
             if (MODE == kSupport) {
-                if (mult) {
-                    // distinct posting rows: each stands for mult[row] identical rows
-                    const uint32_t* mr = mult + (size_t)w * 64;
-                    while (mw) {
-                        cnt += __ldg(mr + (__ffsll((long long)mw) - 1));
-                        mw &= mw - 1;
-                    }
-                } else {
-                    cnt += __popcll(mw);
-                }
+                cnt += __popcll(mw);
             } else if (MODE == kCover) {
                 if (__any_sync(kFull, mw != 0ull)) {
                     hit = true;
@@ -792,7 +778,7 @@ void launch_scan(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Post
                    P.n, I->beg.as<uint32_t>(), I->len.as<uint32_t>(), I->toks->as<uint16_t>(), np,
                    I->order.as<uint32_t>(), I->gid.as<uint32_t>(), goff.as<unsigned long long>(),
                    glen.as<uint32_t>(), ew.as<uint32_t>(), em.as<unsigned long long>(), scores, acc, support,
-                   cover, flags, work, MODE == kSupport ? P.mult.as<uint32_t>() : nullptr);
+                   cover, flags, work);
     };
     launch(std::false_type{}, nullptr);
     tr.mark("grouped_scan");
@@ -1082,14 +1068,13 @@ bool postings_supported(uint32_t L, size_t n) {
 }
 
 void build_postings(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, uint32_t /*logical_len*/, Postings& P,
-                    bool canonical, bool distinct, const uint32_t* d_perm, bool weights) {
+                    bool canonical, bool distinct, const uint32_t* d_perm) {
     const uint32_t L = (uint32_t)(64 * k);  // every bit position, padding included
     P.L = L;
     P.n_src = n;
     P.perm.release();
     P.group.release();
     P.rep.release();
-    P.mult.release();
     if ((canonical || distinct) && n > 1) {
         P.perm.alloc(n * 4, ctx.stream);
         if (d_perm)
@@ -1123,12 +1108,6 @@ void build_postings(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, uint32_
         read_back(ctx, &m, nsel.p, 8);
         nd = (size_t)m;
         rows_of = P.rep.as<uint32_t>();
-        if (weights) {
-            P.mult.alloc(std::max<size_t>(nd, 1) * 4, ctx.stream);
-            IGB_CUDA(cudaMemsetAsync(P.mult.p, 0, std::max<size_t>(nd, 1) * 4, ctx.stream));
-            IGB_LAUNCH(ctx, count_groups, grid_for(ctx, n, 256), 256, 0, P.group.as<uint32_t>(), n,
-                       P.mult.as<uint32_t>());
-        }
     }
     P.n = nd;
     P.W = (nd + 63) / 64;

@@ -22,7 +22,6 @@ struct Postings {
     DevBuf perm;         // canonical position i = source row perm[i]; empty = identity
     DevBuf group;        // canonical position i -> posting row (distinct builds only)
     DevBuf rep;          // posting row -> source row (distinct builds only)
-    DevBuf mult;         // posting row -> number of identical source rows (weighted builds only)
 };
 
 // Token rank space: tokens ordered by (document frequency, id), rarest first.
@@ -70,12 +69,8 @@ bool postings_supported(uint32_t L, size_t n);
 // canonical: index rows in words::less order (clusters rows that share tokens).
 // distinct: one posting row per distinct row (for coverage / evidence, where
 // multiplicity does not matter or is restored by `group`); never for support.
-// weights (with distinct): keep each distinct row's multiplicity, so that
-// support counts (which count identical rows) can run on the
-// distinct rows: a posting row contributes its multiplicity instead of 1.
 void build_postings(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, uint32_t L, Postings& P,
-                    bool canonical = true, bool distinct = false, const uint32_t* d_perm = nullptr,
-                    bool weights = false);
+                    bool canonical = true, bool distinct = false, const uint32_t* d_perm = nullptr);
 // I: the patterns' scan index (nullptr: built here, ranked by P's frequencies)
 void posting_support(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Postings& P, int64_t* d_support,
                      const PatternIndex* I = nullptr);
