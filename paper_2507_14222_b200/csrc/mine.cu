@@ -188,6 +188,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
         "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)), "r"(phase) : "memory");
 }
 
+// x[w] = a[w] & b[w] for w < KC, two words per shared-memory load
+template <int KC>
+__device__ __forceinline__ void load_and_x2(const int64_t* a, const int64_t* b, uint64_t* x) {
+#pragma unroll
+    for (int w = 0; w + 1 < KC; w += 2) {
+        const ulonglong2 va = *reinterpret_cast<const ulonglong2*>(a + w);
+        const ulonglong2 vb = *reinterpret_cast<const ulonglong2*>(b + w);
+        x[w] = va.x & vb.x;
+        x[w + 1] = va.y & vb.y;
+    }
+    if (KC & 1) x[KC - 1] = (uint64_t)(a[KC - 1] & b[KC - 1]);
+}
+
 __device__ __forceinline__ void tile_of(uint64_t t, uint32_t& bi, uint32_t& bj) {
     // t enumerates (bi <= bj) column by column: t = bj(bj+1)/2 + bi
     uint64_t j = (uint64_t)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
@@ -230,9 +243,10 @@ pair_enum(const int64_t* __restrict__ X, uint32_t n, int k_rt, int stride, uint6
     __shared__ int s_stop;
     __shared__ unsigned long long s_pairs;  // pairs of the tile just finished (progress)
     __shared__ alignas(8) uint64_t s_bar;   // TMA row-block arrival
-    // row blocks arrive by TMA when the shared layout is the global one (odd K:
-    // the conflict-free odd stride is K itself) and the block is full
-    const bool tma = use_tma && (k & 1) && stride == k;
+    // row blocks arrive by TMA when the shared layout is the global one (the
+    // stride is K itself: K = 14, or odd K in the generic kernels) and the
+    // block is full
+    const bool tma = use_tma && stride == k;
     unsigned phase = 0;
     if (tma && threadIdx.x == 0) {
         mbar_init(&s_bar, 1);
@@ -386,12 +400,22 @@ pair_enum(const int64_t* __restrict__ X, uint32_t n, int k_rt, int stride, uint6
             Fp fp;
             uint64_t nz = 0;
             uint64_t xr[kRegs ? KC : 1];
+            if constexpr (kRegs) {
+                // 128-bit shared loads: the row stride is 2 (mod 4) words
+                // (host, dedup_pairs), so rows are 16-byte aligned and the 8
+                // lanes of a quarter-warp hit 8 distinct 4-bank groups
+                load_and_x2<KC>(a, b, xr);
 #pragma unroll
-            for (int w = 0; w < k; ++w) {
-                const uint64_t x = (uint64_t)(a[w] & b[w]);
-                if constexpr (kRegs) xr[w] = x;
-                nz |= x;
-                fp.add(x, sKey[w]);
+                for (int w = 0; w < KC; ++w) {
+                    nz |= xr[w];
+                    fp.add(xr[w], sKey[w]);
+                }
+            } else {
+                for (int w = 0; w < k; ++w) {
+                    const uint64_t x = (uint64_t)(a[w] & b[w]);
+                    nz |= x;
+                    fp.add(x, sKey[w]);
+                }
             }
             if (!nz) continue;  // SPEC.md:338 empty intersections dropped at the source
             const uint64_t f = (fp.final(k) & T.fp_mask) | 1ull;
@@ -416,8 +440,10 @@ pair_enum(const int64_t* __restrict__ X, uint32_t n, int k_rt, int stride, uint6
                 const int64_t* b2 = sJ + (plain ? q2 % TILE : s_list[1][q2 % nJ]) * stride;
                 bool same = true;
                 if constexpr (kRegs) {
+                    uint64_t y[KC];
+                    load_and_x2<KC>(a2, b2, y);
 #pragma unroll
-                    for (int w = 0; w < KC; ++w) same &= ((uint64_t)(a2[w] & b2[w]) == xr[w]);
+                    for (int w = 0; w < KC; ++w) same &= y[w] == xr[w];
                 } else {
                     for (int w = 0; w < k && same; ++w) same = ((a2[w] & b2[w]) == (a[w] & b[w]));
                 }
@@ -729,7 +755,14 @@ uint64_t dedup_pairs(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, const 
     reps_out.alloc(8, ctx.stream);
     if (n == 0) return 0;
     if (n > 0xffffffffull) fail(IG_E_INVALID_ARG, "enumerate: more than 2^32 rows");
-    const int stride = (int)(k | 1);
+    // shared row stride: the K = 14 / 17 kernels read rows as 16-byte words,
+    // conflict-free when the stride is 2 (mod 4) words; others read 8-byte
+    // words, conflict-free with an odd stride
+    int stride = (int)(k | 1);
+    if (k == 14 || k == 17) {
+        stride = (int)k;
+        while (stride % 4 != 2) ++stride;
+    }
     int tile_rows = 64;
     while (tile_rows > 16 && (size_t)kLocalSlots * 4 + 2 * (size_t)tile_rows * stride * 8 + 3 * k * 8 > 190 * 1024)
         tile_rows /= 2;
