@@ -188,9 +188,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
         "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)), "r"(phase) : "memory");
 }
 
-// x[w] = a[w] & b[w] for w < KC, two words per shared-memory load
+// x[w] = a[w] & b[w] for w < KC; two words per shared-memory load for K = 14
 template <int KC>
-__device__ __forceinline__ void load_and_x2(const int64_t* a, const int64_t* b, uint64_t* x) {
+__device__ __forceinline__ void load_and_x(const int64_t* a, const int64_t* b, uint64_t* x) {
+    if (KC != 14) {
+#pragma unroll
+        for (int w = 0; w < KC; ++w) x[w] = (uint64_t)(a[w] & b[w]);
+        return;
+    }
 #pragma unroll
     for (int w = 0; w + 1 < KC; w += 2) {
         const ulonglong2 va = *reinterpret_cast<const ulonglong2*>(a + w);
@@ -401,10 +406,10 @@ pair_enum(const int64_t* __restrict__ X, uint32_t n, int k_rt, int stride, uint6
             uint64_t nz = 0;
             uint64_t xr[kRegs ? KC : 1];
             if constexpr (kRegs) {
-                // 128-bit shared loads: the row stride is 2 (mod 4) words
-                // (host, dedup_pairs), so rows are 16-byte aligned and the 8
-                // lanes of a quarter-warp hit 8 distinct 4-bank groups
-                load_and_x2<KC>(a, b, xr);
+                // K = 14: 128-bit shared loads (the row stride is 14 = 2 mod 4
+                // words, so rows are 16-byte aligned and the 8 lanes of a
+                // quarter-warp hit 8 distinct 4-bank groups); K = 17: 64-bit
+                load_and_x<KC>(a, b, xr);
 #pragma unroll
                 for (int w = 0; w < KC; ++w) {
                     nz |= xr[w];
@@ -441,7 +446,7 @@ pair_enum(const int64_t* __restrict__ X, uint32_t n, int k_rt, int stride, uint6
                 bool same = true;
                 if constexpr (kRegs) {
                     uint64_t y[KC];
-                    load_and_x2<KC>(a2, b2, y);
+                    load_and_x<KC>(a2, b2, y);
 #pragma unroll
                     for (int w = 0; w < KC; ++w) same &= y[w] == xr[w];
                 } else {
@@ -755,14 +760,12 @@ uint64_t dedup_pairs(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, const 
     reps_out.alloc(8, ctx.stream);
     if (n == 0) return 0;
     if (n > 0xffffffffull) fail(IG_E_INVALID_ARG, "enumerate: more than 2^32 rows");
-    // shared row stride: the K = 14 / 17 kernels read rows as 16-byte words,
-    // conflict-free when the stride is 2 (mod 4) words; others read 8-byte
-    // words, conflict-free with an odd stride
+    // shared row stride: the K = 14 kernel reads rows as 16-byte words,
+    // conflict-free when the stride is 2 (mod 4) words; the others read 8-byte
+    // words, conflict-free with an odd stride (K = 17 with 16-byte words and
+    // stride 18 measured slower: more spills)
     int stride = (int)(k | 1);
-    if (k == 14 || k == 17) {
-        stride = (int)k;
-        while (stride % 4 != 2) ++stride;
-    }
+    if (k == 14) stride = 14;  // the K = 14 kernel's 16-byte loads (14 = 2 mod 4)
     int tile_rows = 64;
     while (tile_rows > 16 && (size_t)kLocalSlots * 4 + 2 * (size_t)tile_rows * stride * 8 + 3 * k * 8 > 190 * 1024)
         tile_rows /= 2;
