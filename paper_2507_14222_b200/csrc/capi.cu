@@ -290,11 +290,10 @@ void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m, bool enumerate 
             igb::count_support_dev(cx, C.rows.data(), np, X[c].p, X[c].n, k, C.support.as<int64_t>());
         }
         tr.mark("support");
-        if (igb::score_dev(cx, C.rows.data(), np, k, C.support.as<int64_t>(), C.score.as<int64_t>()) != IG_OK)
-            fail(IG_E_OVERFLOW, "pattern score overflows int64");
         int64_t total = 0;
-        if (igb::total_score_dev(cx, C.score.as<int64_t>(), np, &total) != IG_OK)
-            fail(IG_E_OVERFLOW, "total score overflows int64");
+        if (igb::score_total_dev(cx, C.rows.data(), np, k, C.support.as<int64_t>(), C.score.as<int64_t>(), &total) !=
+            IG_OK)
+            fail(IG_E_OVERFLOW, "pattern score or total score overflows int64");
         m.partial_total[c] = (uint64_t)total;
         C.has_support = C.has_score = true;
         tr.mark("score+total");

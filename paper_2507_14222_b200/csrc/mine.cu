@@ -992,18 +992,41 @@ int score_dev(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const int64_t
     return h ? IG_E_OVERFLOW : IG_OK;
 }
 
+// score_patterns then total_score (mine.hpp:46-51) with one read-back: the
+// score overflow flag and the per-block 128-bit partial sums come back together.
+int score_total_dev(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const int64_t* d_support, int64_t* d_score,
+                    int64_t* total) {
+    *total = 0;
+    if (np == 0) return IG_OK;
+    const unsigned g = std::min<unsigned>(grid_for(ctx, np, 256), 1024);
+    DevBuf buf((2 * (size_t)g + 1) * 8, ctx.stream);
+    unsigned long long* lo = buf.as<unsigned long long>();
+    long long* hi = reinterpret_cast<long long*>(lo + g);
+    int* flag = reinterpret_cast<int*>(lo + 2 * g);
+    IGB_CUDA(cudaMemsetAsync(flag, 0, 8, ctx.stream));
+    IGB_LAUNCH(ctx, score_k, grid_for(ctx, np, 256), 256, 0, d_pat, np, (int)k, d_support, d_score, flag);
+    IGB_LAUNCH(ctx, sum128, g, 256, 0, d_score, np, lo, hi);
+    std::vector<unsigned long long> h(2 * (size_t)g + 1);
+    read_back(ctx, h.data(), buf.p, h.size() * 8);
+    if (*reinterpret_cast<const int*>(&h[2 * g])) return IG_E_OVERFLOW;
+    __int128 acc = 0;
+    for (unsigned i = 0; i < g; ++i) acc += ((__int128)(long long)h[g + i] << 32) + (__int128)h[i];
+    if (acc > (__int128)INT64_MAX || acc < (__int128)INT64_MIN) return IG_E_OVERFLOW;
+    *total = (int64_t)acc;
+    return IG_OK;
+}
+
 int total_score_dev(Ctx& ctx, const int64_t* d_score, size_t np, int64_t* total) {
     *total = 0;
     if (np == 0) return IG_OK;
     const unsigned g = std::min<unsigned>(grid_for(ctx, np, 256), 1024);
     DevBuf lo(g * 8, ctx.stream), hi(g * 8, ctx.stream);
     IGB_LAUNCH(ctx, sum128, g, 256, 0, d_score, np, lo.as<unsigned long long>(), hi.as<long long>());
-    std::vector<unsigned long long> hl(g);
-    std::vector<long long> hh(g);
+    std::vector<unsigned long long> hl(2 * (size_t)g);
     read_back(ctx, hl.data(), lo.p, g * 8);
-    read_back(ctx, hh.data(), hi.p, g * 8);
+    read_back(ctx, hl.data() + g, hi.p, g * 8);
     __int128 acc = 0;
-    for (unsigned i = 0; i < g; ++i) acc += ((__int128)hh[i] << 32) + (__int128)hl[i];
+    for (unsigned i = 0; i < g; ++i) acc += ((__int128)(long long)hl[g + i] << 32) + (__int128)hl[i];
     // Scores are non-negative (support >= 0), so the running-sum overflow of
     // total_score (mine.hpp:50-51) happens iff the exact total exceeds INT64_MAX.
     if (acc > (__int128)INT64_MAX || acc < (__int128)INT64_MIN) return IG_E_OVERFLOW;

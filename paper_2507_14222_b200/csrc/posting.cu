@@ -420,11 +420,11 @@ __global__ void parent_keys(const unsigned long long* __restrict__ gkey, size_t 
         pk[g] = (uint32_t)(gkey[g] >> 16);
 }
 
-// upper bound of a 3-group's list: its parent's list length
-__global__ void child_bound(const uint32_t* __restrict__ pid, size_t G, const uint32_t* __restrict__ plen,
+// upper bound of a 3-group's list: its parent's upper bound
+__global__ void child_bound(const uint32_t* __restrict__ pid, size_t G, const unsigned long long* __restrict__ pub,
                             unsigned long long* __restrict__ ub) {
     for (size_t g = (size_t)blockIdx.x * blockDim.x + threadIdx.x; g < G; g += (size_t)gridDim.x * blockDim.x)
-        ub[g] = plen[pid[g]];
+        ub[g] = pub[pid[g]];
 }
 
 // Warp per (t1, t2, t3) group: its parent (t1, t2) list filtered by post[t3].
@@ -735,33 +735,41 @@ void launch_scan(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Post
     const size_t G = I->G, G2 = I->G2;
     // parent (t1, t2) lists S2 = non-zero (w, post[t1][w] & post[t2][w]) in P,
     // then each (t1, t2, t3) group's list S = S2 filtered by post[t3]
+    // Both list levels are sized before either is built, with one read-back:
+    // a parent list holds at most nnz(post[t1]) words (its upper bound), and a
+    // child list at most its parent's bound.
     DevBuf ub((G2 + 1) * 8, ctx.stream), poff((G2 + 1) * 8, ctx.stream), plen(G2 * 4 + 4, ctx.stream);
+    DevBuf ub3((G + 1) * 8, ctx.stream), goff((G + 1) * 8, ctx.stream), glen(G * 4 + 4, ctx.stream);
     if (G2)
         IGB_LAUNCH(ctx, group_bound, grid_for(ctx, G2, 256), 256, 0, I->pkey.as<uint32_t>(), G2,
                    P.nz_off.as<uint32_t>(), P.W, ub.as<unsigned long long>());
     IGB_CUDA(cudaMemsetAsync(ub.as<unsigned long long>() + G2, 0, 8, ctx.stream));
+    if (G)
+        IGB_LAUNCH(ctx, child_bound, grid_for(ctx, G, 256), 256, 0, I->pid.as<uint32_t>(), G, ub.as<unsigned long long>(),
+                   ub3.as<unsigned long long>());
+    IGB_CUDA(cudaMemsetAsync(ub3.as<unsigned long long>() + G, 0, 8, ctx.stream));
     size_t tb4 = 0;
     IGB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb4, ub.as<unsigned long long>(), poff.as<unsigned long long>(),
                                            (int64_t)std::max(G, G2) + 1, ctx.stream));
     DevBuf temp4(tb4, ctx.stream);
     IGB_CUDA(cub::DeviceScan::ExclusiveSum(temp4.p, tb4, ub.as<unsigned long long>(), poff.as<unsigned long long>(),
                                            (int64_t)G2 + 1, ctx.stream));
-    unsigned long long E2 = 0;
-    read_back(ctx, &E2, poff.as<unsigned long long>() + G2, 8);
+    IGB_CUDA(cub::DeviceScan::ExclusiveSum(temp4.p, tb4, ub3.as<unsigned long long>(), goff.as<unsigned long long>(),
+                                           (int64_t)G + 1, ctx.stream));
+    unsigned long long E2E[2] = {0, 0};
+    {
+        DevBuf both(16, ctx.stream);
+        IGB_CUDA(cudaMemcpyAsync(both.p, poff.as<unsigned long long>() + G2, 8, cudaMemcpyDeviceToDevice, ctx.stream));
+        IGB_CUDA(cudaMemcpyAsync(both.as<unsigned long long>() + 1, goff.as<unsigned long long>() + G, 8,
+                                 cudaMemcpyDeviceToDevice, ctx.stream));
+        read_back(ctx, E2E, both.p, 16);
+    }
+    const unsigned long long E2 = E2E[0], E = E2E[1];
     DevBuf pw(std::max<unsigned long long>(E2, 1) * 4, ctx.stream), pm(std::max<unsigned long long>(E2, 1) * 8, ctx.stream);
     if (G2)
         IGB_LAUNCH(ctx, group_lists, grid_for(ctx, G2 * 32, 256), 256, 0, I->pkey.as<uint32_t>(), G2,
                    P.dense.as<unsigned long long>(), P.W, P.n, P.nz_off.as<uint32_t>(), P.nz_idx.as<uint32_t>(),
                    poff.as<unsigned long long>(), plen.as<uint32_t>(), pw.as<uint32_t>(), pm.as<unsigned long long>());
-    DevBuf ub3((G + 1) * 8, ctx.stream), goff((G + 1) * 8, ctx.stream), glen(G * 4 + 4, ctx.stream);
-    if (G)
-        IGB_LAUNCH(ctx, child_bound, grid_for(ctx, G, 256), 256, 0, I->pid.as<uint32_t>(), G, plen.as<uint32_t>(),
-                   ub3.as<unsigned long long>());
-    IGB_CUDA(cudaMemsetAsync(ub3.as<unsigned long long>() + G, 0, 8, ctx.stream));
-    IGB_CUDA(cub::DeviceScan::ExclusiveSum(temp4.p, tb4, ub3.as<unsigned long long>(), goff.as<unsigned long long>(),
-                                           (int64_t)G + 1, ctx.stream));
-    unsigned long long E = 0;
-    read_back(ctx, &E, goff.as<unsigned long long>() + G, 8);
     DevBuf ew(std::max<unsigned long long>(E, 1) * 4, ctx.stream), em(std::max<unsigned long long>(E, 1) * 8, ctx.stream);
     if (G)
         IGB_LAUNCH(ctx, child_lists, grid_for(ctx, G * 32, 256), 256, 0, I->gkey.as<unsigned long long>(),

@@ -313,8 +313,8 @@ void sort_rows_canonical(Ctx& ctx, const int64_t* d_words, size_t n, size_t k, u
     // Per-column hash sets; start small (columns usually hold a few thousand
     // distinct words) and grow x16 when a column passes half load.
     uint32_t slots = next_pow2_u32(std::min<uint64_t>(2 * n + 16, 1ull << 16));
-    DevBuf tables, counts((k + 1) * 4, ctx.stream), full(4, ctx.stream);
-    std::vector<unsigned int> hc(k + 1);
+    DevBuf tables, counts((k + 2) * 4, ctx.stream);  // per column counts, then the full flag
+    std::vector<unsigned int> hc(k + 2);
     for (;;) {
         if ((uint64_t)slots * k * 16 > (1ull << 31) || k > 512) {
             sort_rows_canonical_lsd(ctx, d_words, n, k, d_perm);
@@ -322,13 +322,11 @@ void sort_rows_canonical(Ctx& ctx, const int64_t* d_words, size_t n, size_t k, u
         }
         tables.alloc((size_t)slots * k * 16, ctx.stream);
         IGB_CUDA(cudaMemsetAsync(tables.p, 0, (size_t)slots * k * 16, ctx.stream));
-        IGB_CUDA(cudaMemsetAsync(counts.p, 0, (k + 1) * 4, ctx.stream));
-        IGB_CUDA(cudaMemsetAsync(full.p, 0, 4, ctx.stream));
+        IGB_CUDA(cudaMemsetAsync(counts.p, 0, (k + 2) * 4, ctx.stream));
         IGB_LAUNCH(ctx, column_insert, grid_for(ctx, n * k, 256), 256, 0, d_words, n, (int)k, tables.as<ulonglong2>(),
-                   slots, counts.as<unsigned int>(), full.as<int>());
-        int hfull = 0;
-        read_back(ctx, hc.data(), counts.p, k * 4);
-        read_back(ctx, &hfull, full.p, 4);
+                   slots, counts.as<unsigned int>(), reinterpret_cast<int*>(counts.as<unsigned int>() + k + 1));
+        read_back(ctx, hc.data(), counts.p, (k + 2) * 4);  // counts and the full flag in one read-back
+        const int hfull = (int)hc[k + 1];
         if (!hfull) break;
         if (slots >= (1u << 20) || slots >= 2 * n + 16) {
             sort_rows_canonical_lsd(ctx, d_words, n, k, d_perm);

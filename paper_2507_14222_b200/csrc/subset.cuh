@@ -62,6 +62,9 @@ int score_dev(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const int64_t
               int64_t* d_score);
 // Checked Σ scores (mine.hpp:50-51) -> IG_OK / IG_E_OVERFLOW.
 int total_score_dev(Ctx& ctx, const int64_t* d_score, size_t np, int64_t* total);
+// both, with one read-back (IG_E_OVERFLOW if either overflows)
+int score_total_dev(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const int64_t* d_support, int64_t* d_score,
+                    int64_t* total);
 
 // Keep rows whose flag is 0 (stable), with their supports/scores.
 size_t compact_unflagged(Ctx& ctx, const int64_t* d_words, const int64_t* d_sup, const int64_t* d_sc,
