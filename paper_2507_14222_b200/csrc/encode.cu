@@ -777,7 +777,7 @@ bool device_vocab(Ctx& ctx, const ig_columns& c, const DeviceCols& d, const Voca
     uint64_t pow10p = 1;
     for (int i = 0; i < c.decimals; ++i) pow10p *= 10;
     const int smem = kVocabMax * 18;
-    IGB_CUDA(cudaFuncSetAttribute(vocab_build, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    IGB_SMEM_ATTR(ctx, vocab_build, smem);
     IGB_LAUNCH(ctx, vocab_build, 1, 1024, smem, u_code.as<int64_t>(), u_feat.as<int32_t>(),
                u_count.as<unsigned int>(), ddesc.as<FeatDesc>(), nf, dcrank.as<int32_t>(), cat_total, pow10p,
                dv.lut.as<Lut>(), dv.lcodes.as<int64_t>(), dv.lbits.as<int32_t>(), dv.cbits.as<int32_t>(),
@@ -902,8 +902,7 @@ void encode_training_dev(Ctx& ctx, const ig_columns& c, ig_encoding& e) {
     DevBuf lcode(cap * 8, ctx.stream), lcol(cap * 4, ctx.stream), lcnt(8, ctx.stream);
     IGB_CUDA(cudaMemsetAsync(lcnt.p, 0, 8, ctx.stream));
     if (d.n && d.n_feat)
-        IGB_CUDA(cudaFuncSetAttribute(distinct_codes, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      kDistinctSlots * (int)sizeof(int64_t)));
+        IGB_SMEM_ATTR(ctx, distinct_codes, kDistinctSlots * (int)sizeof(int64_t));
     if (d.n && d.n_feat)
         IGB_LAUNCH(ctx, distinct_codes, dim3((unsigned)chunks, (unsigned)d.n_feat), 256,
                    kDistinctSlots * sizeof(int64_t), d.codes.as<int64_t>(), d.n,
@@ -955,7 +954,10 @@ void encode_training_dev(Ctx& ctx, const ig_columns& c, ig_encoding& e) {
             IGB_LAUNCH(ctx, gather_rows_idx, grid_for(ctx, mrows * k, 256), 256, 0, all.data(),
                        (cls == 0 ? idx_a : idx_n).as<uint32_t>(), mrows, (int)k, dst.data());
     }
-    IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+    // no final synchronisation: every consumer of the rows is ordered on this
+    // stream (or waits for an event recorded on it), and the queued work reads
+    // no host memory (the columns' copies finished before the read-backs
+    // above), so the caller's next host work overlaps the gathers
 }
 
 void encode_rows_dev(Ctx& ctx, const ig_columns& c, const ig_encoding& train, ig_encoding& e, bool queue_only) {

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 
 #include <cstdint>
@@ -236,6 +237,18 @@ struct Trace {
 };
 
 inline size_t words_for(uint32_t L) { return (static_cast<size_t>(L) + 63) / 64; }
+
+// Raise a kernel's dynamic shared-memory limit once per device and size (the
+// attribute call costs a few microseconds of host time on every launch site).
+#define IGB_SMEM_ATTR(ctx, kernel, bytes)                                                           \
+    do {                                                                                            \
+        static std::atomic<int> igb_smem_set_[64];                                                  \
+        const int igb_dev_ = (ctx).device & 63, igb_b_ = (int)(bytes);                              \
+        if (igb_smem_set_[igb_dev_].load(std::memory_order_relaxed) < igb_b_) {                     \
+            IGB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, igb_b_)); \
+            igb_smem_set_[igb_dev_].store(igb_b_, std::memory_order_relaxed);                       \
+        }                                                                                           \
+    } while (0)
 
 // Every kernel launch goes through this so the context can report how many of
 // its own kernels ran (bench `gpu_launches`) and catch launch errors at once.

@@ -779,8 +779,8 @@ uint64_t dedup_pairs(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, const 
     const size_t smem = (size_t)kLocalSlots * 4 + 2 * (size_t)tile * stride * 8 + 3 * k * 8;  // + keys, ORs
     if (smem > 190 * 1024) fail(IG_E_INVALID_ARG, "enumerate: rows wider than the shared-memory tile (K > 700)");
 #define IGB_PAIR_ATTR(T_, K_)                                                                                 \
-    IGB_CUDA(cudaFuncSetAttribute(pair_enum<T_, K_, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    IGB_CUDA(cudaFuncSetAttribute(pair_enum<T_, K_, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))
+    IGB_SMEM_ATTR(ctx, (pair_enum<T_, K_, false>), smem);                                                 \
+    IGB_SMEM_ATTR(ctx, (pair_enum<T_, K_, true>), smem)
     IGB_PAIR_ATTR(64, 0);
     IGB_PAIR_ATTR(64, 14);
     IGB_PAIR_ATTR(64, 17);

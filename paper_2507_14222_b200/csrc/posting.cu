@@ -866,8 +866,7 @@ void build_pattern_index(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, co
     {                                                                                                              \
         const size_t smem = (size_t)L * 4 + (size_t)2 * KW * kFillThreads * 4;                                    \
         if (smem > 48 * 1024)                                                                                      \
-            IGB_CUDA(cudaFuncSetAttribute(pattern_token_fill_rank<KW>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                          (int)smem));                                                             \
+            IGB_SMEM_ATTR(ctx, pattern_token_fill_rank<KW>, (int)smem);                                           \
         IGB_LAUNCH(ctx, pattern_token_fill_rank<KW>, grid_for(ctx, np, kFillThreads), kFillThreads, smem, d_pat,   \
                    np, (int)k,                                                                                     \
                    R.rank.as<uint16_t>(), R.byrank.as<uint16_t>(), L, I.beg.as<uint32_t>(), I.toks->as<uint16_t>()); \
@@ -882,7 +881,7 @@ void build_pattern_index(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, co
     } else {
         const size_t smem = (size_t)L * 4;
         if (smem > 48 * 1024)
-            IGB_CUDA(cudaFuncSetAttribute(pattern_token_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            IGB_SMEM_ATTR(ctx, pattern_token_fill, smem);
         IGB_LAUNCH(ctx, pattern_token_fill, grid_for(ctx, np, 128), 128, smem, d_pat, np, (int)k,
                    R.df.as<uint32_t>(), L, I.beg.as<uint32_t>(), I.toks->as<uint16_t>());
     }
@@ -1057,7 +1056,7 @@ void cluster_order(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, uint32_t
         return;
     }
     if ((size_t)L * 4 > 48 * 1024)
-        IGB_CUDA(cudaFuncSetAttribute(row_token_df, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L * 4));
+        IGB_SMEM_ATTR(ctx, row_token_df, (int)L * 4);
     DevBuf df((size_t)L * 4, ctx.stream), prow(n * k * 8, ctx.stream);
     IGB_CUDA(cudaMemsetAsync(df.p, 0, (size_t)L * 4, ctx.stream));
     IGB_LAUNCH(ctx, row_token_df, std::max(1, ctx.sm_count * 2), 256, (size_t)L * 4, d_rows, n, (int)k,
