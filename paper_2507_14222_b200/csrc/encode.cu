@@ -665,11 +665,9 @@ struct HostVocabJob {
     std::mutex mu;
     bool joined = false;
     std::exception_ptr err;
-    void* pinned = nullptr;
-    cudaEvent_t ready = nullptr;
+    void* pinned = nullptr;  // codes [kVocabMax] int64, features [kVocabMax] int32, L (the library's pool)
     ~HostVocabJob() {
         if (th.joinable()) th.join();
-        if (ready) cudaEventDestroy(ready);
         if (pinned) ig_host_free(pinned);
     }
 };
@@ -750,68 +748,81 @@ bool device_vocab(Ctx& ctx, const ig_columns& c, const DeviceCols& d, const Voca
     if (!vp.ok || vp.nf != nf) return false;
     const int cat_total = vp.cat_total;
     e.dv.cat_off = vp.cat_off;
-    DevBuf ddesc(nf * sizeof(FeatDesc), ctx.stream), dcrank(std::max(cat_total, 1) * 4, ctx.stream);
-    IGB_CUDA(cudaMemcpyAsync(ddesc.p, vp.pinned, nf * sizeof(FeatDesc), cudaMemcpyHostToDevice, ctx.stream));
+    // scratch in one block: descriptors, crank | dedup slots, counter | unique
+    // (code, feature) | their bits | token list in bit order + L
+    auto up16 = [](size_t b) { return (b + 15) & ~size_t{15}; };
+    const size_t o_desc = 0, o_crank = o_desc + up16(nf * sizeof(FeatDesc)),
+                 o_slots = o_crank + up16(std::max(cat_total, 1) * 4),
+                 o_ucount = o_slots + (size_t)kVocabSlots * sizeof(ulonglong2), o_ucode = o_ucount + 16,
+                 o_ufeat = o_ucode + kVocabMax * 8, o_ubits = o_ufeat + kVocabMax * 4, o_list = o_ubits + kVocabMax * 4,
+                 list_bytes = (size_t)kVocabMax * 12 + 8, total = o_list + list_bytes;
+    DevBuf scratch(total, ctx.stream);
+    char* sp = scratch.as<char>();
+    IGB_CUDA(cudaMemcpyAsync(sp + o_desc, vp.pinned, nf * sizeof(FeatDesc), cudaMemcpyHostToDevice, ctx.stream));
     if (cat_total)
-        IGB_CUDA(cudaMemcpyAsync(dcrank.p, static_cast<const char*>(vp.pinned) + nf * sizeof(FeatDesc),
+        IGB_CUDA(cudaMemcpyAsync(sp + o_crank, static_cast<const char*>(vp.pinned) + nf * sizeof(FeatDesc),
                                  (size_t)cat_total * 4, cudaMemcpyHostToDevice, ctx.stream));
-    // exact distinct (feature, code), then the ranking and the pack tables
-    DevBuf slots((size_t)kVocabSlots * sizeof(ulonglong2), ctx.stream), u_code(kVocabMax * 8, ctx.stream),
-        u_feat(kVocabMax * 4, ctx.stream), u_count(8, ctx.stream);
-    IGB_CUDA(cudaMemsetAsync(slots.p, 0, (size_t)kVocabSlots * sizeof(ulonglong2), ctx.stream));
-    IGB_CUDA(cudaMemsetAsync(u_count.p, 0, 8, ctx.stream));
+    IGB_CUDA(cudaMemsetAsync(sp + o_slots, 0, o_ucode - o_slots, ctx.stream));  // slots + counter
+    unsigned int* u_count = reinterpret_cast<unsigned int*>(sp + o_ucount);
+    int64_t* u_code = reinterpret_cast<int64_t*>(sp + o_ucode);
+    int32_t* u_feat = reinterpret_cast<int32_t*>(sp + o_ufeat);
     IGB_LAUNCH(ctx, vocab_unique, (unsigned)ctx.sm_count, 256, 0, lcode.as<int64_t>(), lcol.as<int32_t>(),
-               lcnt.as<unsigned long long>(), slots.as<ulonglong2>(), u_code.as<int64_t>(), u_feat.as<int32_t>(),
-               u_count.as<unsigned int>());
+               lcnt.as<unsigned long long>(), reinterpret_cast<ulonglong2*>(sp + o_slots), u_code, u_feat, u_count);
     DeviceVocab& dv = e.dv;
     dv.n_feat = nf;
     dv.feat_col = d.feat_col;
-    dv.lut.alloc(nf * sizeof(Lut), ctx.stream);
-    dv.lcodes.alloc(kVocabMax * 8, ctx.stream);
-    dv.lbits.alloc(kVocabMax * 4, ctx.stream);
-    dv.cbits.alloc(std::max(cat_total, 1) * 4, ctx.stream);
-    DevBuf ubits(kVocabMax * 4, ctx.stream), list(kVocabMax * 12 + 8, ctx.stream);
-    int64_t* list_code = list.as<int64_t>();
-    int32_t* list_feat = reinterpret_cast<int32_t*>(list.as<char>() + kVocabMax * 8);
-    unsigned int* out_L = reinterpret_cast<unsigned int*>(list.as<char>() + kVocabMax * 12);
+    const size_t p_lut = 0, p_lcodes = up16(nf * sizeof(Lut)), p_lbits = p_lcodes + kVocabMax * 8,
+                 p_cbits = p_lbits + kVocabMax * 4;
+    dv.mem.alloc(p_cbits + std::max(cat_total, 1) * 4, ctx.stream);
+    char* mp = dv.mem.as<char>();
+    dv.lut = mp + p_lut;
+    dv.lcodes = reinterpret_cast<int64_t*>(mp + p_lcodes);
+    dv.lbits = reinterpret_cast<int32_t*>(mp + p_lbits);
+    dv.cbits = reinterpret_cast<int32_t*>(mp + p_cbits);
+    int64_t* list_code = reinterpret_cast<int64_t*>(sp + o_list);
+    int32_t* list_feat = reinterpret_cast<int32_t*>(sp + o_list + kVocabMax * 8);
+    unsigned int* out_L = reinterpret_cast<unsigned int*>(sp + o_list + kVocabMax * 12);
     uint64_t pow10p = 1;
     for (int i = 0; i < c.decimals; ++i) pow10p *= 10;
     const int smem = kVocabMax * 18;
     IGB_SMEM_ATTR(ctx, vocab_build, smem);
-    IGB_LAUNCH(ctx, vocab_build, 1, 1024, smem, u_code.as<int64_t>(), u_feat.as<int32_t>(),
-               u_count.as<unsigned int>(), ddesc.as<FeatDesc>(), nf, dcrank.as<int32_t>(), cat_total, pow10p,
-               dv.lut.as<Lut>(), dv.lcodes.as<int64_t>(), dv.lbits.as<int32_t>(), dv.cbits.as<int32_t>(),
-               ubits.as<int32_t>(), list_code, list_feat, out_L);
-    unsigned int L = 0;
-    read_back(ctx, &L, out_L, 4);
+    IGB_LAUNCH(ctx, vocab_build, 1, 1024, smem, u_code, u_feat, u_count,
+               reinterpret_cast<const FeatDesc*>(sp + o_desc), nf, reinterpret_cast<const int32_t*>(sp + o_crank),
+               cat_total, pow10p, static_cast<Lut*>(dv.lut), dv.lcodes, dv.lbits, dv.cbits,
+               reinterpret_cast<int32_t*>(sp + o_ubits), list_code, list_feat, out_L);
+    // the token list (for the host text) and L come back in one copy
+    auto job = std::make_shared<HostVocabJob>();
+    if (ig_host_alloc(list_bytes, &job->pinned) != IG_OK) fail(IG_E_OOM, "page-locked host memory");
+    IGB_CUDA(cudaMemcpyAsync(job->pinned, list_code, list_bytes, cudaMemcpyDeviceToHost, ctx.stream));
+    IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+    const unsigned int L = *reinterpret_cast<const unsigned int*>(static_cast<const char*>(job->pinned) +
+                                                                  (size_t)kVocabMax * 12);
     if (L > (unsigned)kVocabMax) {
         dv = DeviceVocab{};
         return false;
     }
     e.L = L;
     dv.valid = true;
-    for (DevBuf* b : {&dv.lut, &dv.lcodes, &dv.lbits, &dv.cbits}) b->persist();
-    // the host text: tokens in bit order, copied back behind the tables
-    auto job = std::make_shared<HostVocabJob>();
-    const size_t bytes = (size_t)L * 12;
-    if (ig_host_alloc(std::max<size_t>(bytes, 16), &job->pinned) != IG_OK) fail(IG_E_OOM, "page-locked host memory");
-    if (L) {
-        IGB_CUDA(cudaMemcpyAsync(job->pinned, list_code, (size_t)L * 8, cudaMemcpyDeviceToHost, ctx.stream));
-        IGB_CUDA(cudaMemcpyAsync(static_cast<char*>(job->pinned) + (size_t)L * 8, list_feat, (size_t)L * 4,
-                                 cudaMemcpyDeviceToHost, ctx.stream));
-    }
-    IGB_CUDA(cudaEventCreateWithFlags(&job->ready, cudaEventDisableTiming));
-    IGB_CUDA(cudaEventRecord(job->ready, ctx.stream));
+    dv.mem.persist();
+    e.hv = job;  // text built by start_host_vocab once the rows are queued
+    return true;
+}
+
+// The host fields of a device-built vocabulary, on a host thread (the token
+// list is already in page-locked memory).
+void start_host_vocab(const ig_columns& c, const DeviceCols& d, ig_encoding& e) {
+    HostVocabJob* jp = e.hv.get();
+    if (!jp) return;
+    const uint32_t L = e.L;
     const int ncols = (int)c.n_cols, decimals = c.decimals;
     std::vector<int> kind = c.kind, fcol = d.feat_col;
-    HostVocabJob* jp = job.get();
     ig_encoding* ep = &e;
     const auto* dict = &e.dict;  // e.dict = c.dict (copied before this call)
-    job->th = std::thread([jp, ep, dict, ncols, decimals, kind, fcol, L] {
+    jp->th = std::thread([jp, ep, dict, ncols, decimals, kind, fcol, L] {
         try {
-            IGB_CUDA(cudaEventSynchronize(jp->ready));
             const int64_t* code = static_cast<const int64_t*>(jp->pinned);
-            const int32_t* feat = reinterpret_cast<const int32_t*>(static_cast<const char*>(jp->pinned) + (size_t)L * 8);
+            const int32_t* feat =
+                reinterpret_cast<const int32_t*>(static_cast<const char*>(jp->pinned) + (size_t)kVocabMax * 8);
             ig_encoding& E = *ep;
             E.num_codes.assign(ncols, {});
             E.num_bits.assign(ncols, {});
@@ -853,8 +864,6 @@ bool device_vocab(Ctx& ctx, const ig_columns& c, const DeviceCols& d, const Voca
             jp->err = std::current_exception();
         }
     });
-    e.hv = std::move(job);
-    return true;
 }
 
 }  // namespace
@@ -909,9 +918,9 @@ void encode_training_dev(Ctx& ctx, const ig_columns& c, ig_encoding& e) {
                    lcode.as<int64_t>(), lcol.as<int32_t>(), lcnt.as<unsigned long long>());
     DevRows all;
     if (device_vocab(ctx, c, d, vp, lcode, lcol, lcnt, e)) {
-        // (1c) pack every training row with the device tables
-        pack_tables(ctx, e.L, d, e.dv.lut.as<Lut>(), e.dv.lcodes.as<int64_t>(), e.dv.lbits.as<int32_t>(),
-                    e.dv.cbits.as<int32_t>(), all);
+        // (1c) pack every training row with the device tables, then the host text
+        pack_tables(ctx, e.L, d, static_cast<const Lut*>(e.dv.lut), e.dv.lcodes, e.dv.lbits, e.dv.cbits, all);
+        start_host_vocab(c, d, e);
     } else {
         host_vocab_build(ctx, c, d, lcode, lcol, lcnt, e, all);
     }
@@ -992,7 +1001,7 @@ void encode_rows_dev(Ctx& ctx, const ig_columns& c, const ig_encoding& train, ig
             }
         }
         DevBuf lut(d.n_feat * sizeof(Lut), ctx.stream), cb(std::max<size_t>(remap.size(), 1) * 4, ctx.stream);
-        IGB_CUDA(cudaMemcpyAsync(lut.p, dv.lut.p, d.n_feat * sizeof(Lut), cudaMemcpyDeviceToDevice, ctx.stream));
+        IGB_CUDA(cudaMemcpyAsync(lut.p, dv.lut, d.n_feat * sizeof(Lut), cudaMemcpyDeviceToDevice, ctx.stream));
         if (!cfeat.empty()) {
             DevBuf rm(remap.size() * 4 + train_off.size() * 4 + cfeat.size() * 12, ctx.stream);
             std::vector<int32_t> host(remap);
@@ -1006,11 +1015,10 @@ void encode_rows_dev(Ctx& ctx, const ig_columns& c, const ig_encoding& train, ig
             const int32_t* rmp = rm.as<int32_t>();
             if (!remap.empty())
                 IGB_LAUNCH(ctx, remap_cat, grid_for(ctx, remap.size(), 256), 256, 0, rmp, (int)remap.size(),
-                           dv.cbits.as<int32_t>(), rmp + remap.size(), cb.as<int32_t>());
+                           dv.cbits, rmp + remap.size(), cb.as<int32_t>());
             IGB_LAUNCH(ctx, patch_cat_lut, 1, 256, 0, rmp + 2 * remap.size(), (int)cfeat.size(), lut.as<Lut>());
         }
-        pack_tables(ctx, train.L, d, lut.as<Lut>(), dv.lcodes.as<int64_t>(), dv.lbits.as<int32_t>(), cb.as<int32_t>(),
-                    e.all);
+        pack_tables(ctx, train.L, d, lut.as<Lut>(), dv.lcodes, dv.lbits, cb.as<int32_t>(), e.all);
         if (host_read || !queue_only) IGB_CUDA(cudaStreamSynchronize(ctx.stream));
         return;
     }

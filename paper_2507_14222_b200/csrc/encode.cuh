@@ -20,9 +20,11 @@ struct DeviceVocab {
     int n_feat = 0;
     std::vector<int> feat_col;      // feature -> table column
     std::vector<int> cat_off;       // per feature: offset of its dictionary in cbits (categorical)
-    igb::DevBuf lut;                // n_feat Lut (encode.cu)
-    igb::DevBuf lcodes, lbits;      // numeric (feature, code) sorted -> bit
-    igb::DevBuf cbits;              // categorical (feature, training id) -> bit
+    igb::DevBuf mem;                // one block holding the four tables below
+    void* lut = nullptr;            // n_feat Lut (encode.cu)
+    int64_t* lcodes = nullptr;      // numeric (feature, code) sorted ...
+    int32_t* lbits = nullptr;       // ... -> bit
+    int32_t* cbits = nullptr;       // categorical (feature, training id) -> bit
 };
 
 struct ig_encoding {
