@@ -29,6 +29,7 @@
 // an entry point may call another.
 struct ig_ctx : igb::Ctx {
     std::recursive_mutex mu;
+    std::unique_ptr<igb::Worker> class_worker;  // igb::Ctx::worker
 };
 
 struct ig_candidates {
@@ -184,20 +185,29 @@ void for_both_classes(igb::Ctx& ctx, F&& fn, bool concurrent = true) {
     c1.launches = 0;
     for (auto& d : c1.diag_k) d = igb::DiagStat{};
     std::exception_ptr e0, e1;
-    std::thread th([&] {
+    auto run1 = [&] {
         try {
             IGB_CUDA(cudaSetDevice(ctx.device));
             fn(c1, 1);
         } catch (...) {
             e1 = std::current_exception();
         }
-    });
+    };
+    std::thread th;
+    std::future<void> done;
+    if (ctx.worker)
+        done = ctx.worker->submit(run1);
+    else
+        th = std::thread(run1);
     try {
         fn(ctx, 0);
     } catch (...) {
         e0 = std::current_exception();
     }
-    th.join();
+    if (ctx.worker)
+        done.wait();
+    else
+        th.join();
     cudaEventRecord(join, c1.stream);
     cudaStreamWaitEvent(ctx.stream, join, 0);
     cudaEventDestroy(fork);
@@ -448,6 +458,8 @@ int ig_ctx_create(int device, ig_ctx** out) {
     auto c = std::make_unique<ig_ctx>();
     c->device = device;
     int st = guard(c.get(), [&] {
+        c->class_worker = std::make_unique<igb::Worker>(device);
+        c->worker = c->class_worker.get();
         IGB_CUDA(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
         IGB_CUDA(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
         IGB_CUDA(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));

@@ -5,6 +5,12 @@
 
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
+#include <deque>
+#include <functional>
+#include <future>
+#include <mutex>
+#include <thread>
 #include <cstring>
 
 #include <cstdint>
@@ -110,6 +116,54 @@ struct ProgressHook {
     uint64_t seen[2] = {0, 0};
 };
 
+// A persistent host thread running submitted tasks in order (the second class
+// of a fit, the test index build): thread creation on every step cost tens of
+// microseconds of idle GPU.
+class Worker {
+public:
+    explicit Worker(int device) : th_([this, device] {
+        cudaSetDevice(device);
+        for (;;) {
+            std::function<void()> task;
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [this] { return stop_ || !q_.empty(); });
+                if (q_.empty()) return;  // stopping
+                task = std::move(q_.front());
+                q_.pop_front();
+            }
+            task();
+        }
+    }) {}
+    Worker(const Worker&) = delete;
+    ~Worker() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        th_.join();
+    }
+    // run fn on the worker; the future completes when it returned (fn must not throw)
+    std::future<void> submit(std::function<void()> fn) {
+        auto task = std::make_shared<std::packaged_task<void()>>(std::move(fn));
+        std::future<void> f = task->get_future();
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            q_.emplace_back([task] { (*task)(); });
+        }
+        cv_.notify_one();
+        return f;
+    }
+
+private:
+    std::mutex mu_;
+    std::condition_variable cv_;
+    std::deque<std::function<void()>> q_;
+    bool stop_ = false;
+    std::thread th_;  // last: started once the queue exists
+};
+
 struct Ctx {
     int device = 0;
     cudaStream_t own = nullptr;
@@ -125,6 +179,7 @@ struct Ctx {
     bool diag = false;
     DiagStat diag_k[kDiagKinds];
     ProgressHook* progress = nullptr;  // set by ig_enumerate_candidates for one call
+    Worker* worker = nullptr;          // owned by the ABI context; copies share it (may be null)
     void diag_merge(const Ctx& o) {
         for (int i = 0; i < kDiagKinds; ++i) {
             diag_k[i].ms += o.diag_k[i].ms;
