@@ -12,6 +12,8 @@
 #include <map>
 #include <mutex>
 #include <exception>
+#include <future>
+#include <utility>
 #include <string>
 #include <thread>
 #include <vector>
@@ -234,8 +236,10 @@ struct FusedEvidence {
 
 // row_perm (optional): each class's canonical row permutation, already known
 // (a shard computed it for its distinct rows).
+// pre (optional): each class's training postings, already built on the
+// context's aux stream (a shard builds them while its records travel).
 void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m, bool enumerate = true, FusedEvidence* ev = nullptr,
-              const uint32_t* const* row_perm = nullptr) {
+              const uint32_t* const* row_perm = nullptr, igb::Postings* pre = nullptr) {
     m.L = L;
     const size_t k = igb::words_for(L);
     for (int c = 0; c < 2; ++c)
@@ -273,7 +277,10 @@ void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m, bool enumerate 
         // every training row (support counts identical rows);
         // distinct rows weighted by their multiplicity measured slower
         //
-        if (vertical) igb::build_postings(cx, X[c].p, X[c].n, k, L, PX[c], true, false, pc);
+        if (vertical && pre && pre[c].L)
+            PX[c] = std::move(pre[c]);
+        else if (vertical)
+            igb::build_postings(cx, X[c].p, X[c].n, k, L, PX[c], true, false, pc);
         tr.mark("postings");
     }, concurrent);
     // one token rank space for every scan of this fit: frequencies over all
@@ -1195,6 +1202,29 @@ struct ig_shard {
     std::vector<uint64_t> counts[2];
     bool received[2] = {false, false};
     ig_model model;
+    // each class's training postings (replicated work: every rank scans its own
+    // candidates against all training rows), built on the context's aux stream
+    // by its worker while the class's records travel; finish() takes them
+    igb::Postings PX[2];
+    std::unique_ptr<igb::Ctx> px_ctx[2];
+    std::future<void> px_done[2];
+    std::exception_ptr px_err[2];
+    void wait_postings(igb::Ctx& ctx) {
+        for (int c = 0; c < 2; ++c) {
+            if (!px_done[c].valid()) continue;
+            px_done[c].wait();
+            px_done[c] = {};
+            ctx.launches += px_ctx[c]->launches;
+            ctx.diag_merge(*px_ctx[c]);
+            px_ctx[c].reset();
+        }
+        for (auto& e : px_err)
+            if (e) std::rethrow_exception(std::exchange(e, nullptr));
+    }
+    ~ig_shard() {
+        for (auto& f : px_done)
+            if (f.valid()) f.wait();
+    }
 };
 
 int ig_shard_create(ig_ctx* ctx, const ig_encoding* train, int rank, int world, const ig_kernel_config* cfg,
@@ -1229,14 +1259,43 @@ int ig_shard_enumerate(ig_ctx* ctx, ig_shard* s, int cls, uint64_t* counts, cons
         src.tile_step = (uint64_t)s->world;
         igb::DevBuf reps;
         igb::Trace tr(*ctx, "shard_enumerate", cls);
-        const uint64_t c = igb::dedup_pairs(*ctx, s->U[cls].as<int64_t>(), s->m[cls], s->k, src, reps, nullptr);
+        // one rank: its deduplicated records are the whole class's, all owned here
+        const bool solo = s->world == 1;
+        const uint64_t c = igb::dedup_pairs(*ctx, s->U[cls].as<int64_t>(), s->m[cls], s->k, src, reps,
+                                            solo ? &s->model.stats[cls] : nullptr);
         tr.mark("dedup");
-        igb::bucket_by_owner(*ctx, s->U[cls].as<int64_t>(), s->k, reps.as<uint2>(), c, s->world, s->send[cls],
-                             s->counts[cls]);
+        if (solo) {
+            s->send[cls] = std::move(reps);
+            s->counts[cls].assign(1, c);
+        } else {
+            igb::bucket_by_owner(*ctx, s->U[cls].as<int64_t>(), s->k, reps.as<uint2>(), c, s->world, s->send[cls],
+                                 s->counts[cls]);
+        }
         tr.mark("bucket");
         s->send[cls].persist();
         for (int r = 0; r < s->world; ++r) counts[r] = s->counts[cls][r];
         *d_send = s->send[cls].p;
+        // this class's training postings, off the caller's thread and stream
+        const igb::DevRows& X = cls == 0 ? s->train->attack : s->train->normal;
+        const size_t nmax = std::max(s->train->attack.n, s->train->normal.n);
+        if (ctx->worker && !s->px_done[cls].valid() && !s->PX[cls].L && igb::postings_supported(s->L, nmax)) {
+            s->px_ctx[cls] = std::make_unique<igb::Ctx>(*ctx);
+            igb::Ctx* cx = s->px_ctx[cls].get();
+            cx->stream = ctx->aux;
+            cx->launches = 0;
+            cx->progress = nullptr;
+            for (auto& d : cx->diag_k) d = igb::DiagStat{};
+            ig_shard* sh = s;
+            s->px_done[cls] = ctx->worker->submit([sh, cx, cls, &X] {
+                try {
+                    IGB_CUDA(cudaSetDevice(cx->device));
+                    igb::build_postings(*cx, X.data(), X.n, sh->k, sh->L, sh->PX[cls], true, false,
+                                        sh->perm[cls].as<uint32_t>());
+                } catch (...) {
+                    sh->px_err[cls] = std::current_exception();
+                }
+            });
+        }
     });
 }
 
@@ -1247,10 +1306,15 @@ int ig_shard_receive(ig_ctx* ctx, ig_shard* s, int cls, const void* d_recv, uint
         src.list = static_cast<const uint2*>(d_recv);
         src.n_list = n_records;
         igb::DevBuf reps;
-        const uint64_t c = igb::dedup_pairs(*ctx, s->U[cls].as<int64_t>(), s->m[cls], s->k, src, reps,
-                                            &s->model.stats[cls]);
         ig_candidates& C = s->model.cand[cls];
-        igb::materialize_pairs(*ctx, s->U[cls].as<int64_t>(), s->k, reps.as<uint2>(), c, s->L, C.rows);
+        if (s->world == 1) {
+            // a single sender's records are already distinct (its own dedup)
+            igb::materialize_pairs(*ctx, s->U[cls].as<int64_t>(), s->k, src.list, n_records, s->L, C.rows);
+        } else {
+            const uint64_t c = igb::dedup_pairs(*ctx, s->U[cls].as<int64_t>(), s->m[cls], s->k, src, reps,
+                                                &s->model.stats[cls]);
+            igb::materialize_pairs(*ctx, s->U[cls].as<int64_t>(), s->k, reps.as<uint2>(), c, s->L, C.rows);
+        }
         C.ordered = false;
         IGB_CUDA(cudaStreamSynchronize(ctx->stream));
         s->received[cls] = true;
@@ -1264,7 +1328,13 @@ int ig_shard_finish(ig_ctx* ctx, ig_shard* s, uint64_t* partial_totals) {
                      {s->train->normal.data(), s->train->normal.n, s->train->normal.k}};
         const uint32_t* rp[2] = {s->perm[0].p ? s->perm[0].as<uint32_t>() : nullptr,
                                  s->perm[1].p ? s->perm[1].as<uint32_t>() : nullptr};
-        fit_impl(*ctx, X, s->L, s->model, /*enumerate=*/false, nullptr, rp);
+        s->wait_postings(*ctx);
+        cudaEvent_t built;
+        IGB_CUDA(cudaEventCreateWithFlags(&built, cudaEventDisableTiming));
+        IGB_CUDA(cudaEventRecord(built, ctx->aux));
+        IGB_CUDA(cudaStreamWaitEvent(ctx->stream, built, 0));
+        cudaEventDestroy(built);
+        fit_impl(*ctx, X, s->L, s->model, /*enumerate=*/false, nullptr, rp, s->PX);
         partial_totals[0] = s->model.partial_total[0];
         partial_totals[1] = s->model.partial_total[1];
     });

@@ -701,6 +701,47 @@ void scan_stats(Ctx& ctx, int mode, const PatternIndex& I, const DevBuf& glen, s
         ++hist[l == 0 ? 0 : std::min(b + 1, 7)];
         toks += len[order[i]];
     }
+    {
+        // staging estimate: words a group-shared SMEM tile of every token of the
+        // group (tokens 3..) would load, against the dense per-pattern ANDs
+        std::vector<uint32_t> beg(np);
+        read_back(ctx, beg.data(), I.beg.p, np * 4);
+        uint32_t tmax = 0;
+        for (size_t p = 0; p < np; ++p) tmax = std::max(tmax, beg[p] + len[p]);
+        std::vector<uint16_t> toks(tmax);
+        read_back(ctx, toks.data(), I.toks->p, (size_t)tmax * 2);
+        std::vector<uint32_t> seen(65536, 0xffffffffu);
+        uint64_t staged = 0, dense_ands = 0, ucnt = 0, uhist[6] = {0, 0, 0, 0, 0, 0};
+        size_t i = 0;
+        while (i < np) {
+            const uint32_t g = gid[i];
+            uint32_t u = 0;
+            size_t j = i;
+            for (; j < np && gid[j] == g; ++j) {
+                const uint32_t p = order[j];
+                for (uint32_t t = 3; t < len[p]; ++t) {
+                    const uint16_t tk = toks[beg[p] + t];
+                    if (seen[tk] != g) {
+                        seen[tk] = g;
+                        ++u;
+                    }
+                }
+                dense_ands += (uint64_t)(len[p] > 3 ? len[p] - 3 : 0) * gl[g];
+            }
+            staged += (uint64_t)u * gl[g];
+            ucnt += u;
+            uhist[u <= 16 ? 0 : u <= 32 ? 1 : u <= 64 ? 2 : u <= 128 ? 3 : u <= 256 ? 4 : 5] += j - i;
+            i = j;
+        }
+        fprintf(stderr,
+                "[ig scan] mode %d staging: union tokens/group %.1f, staged words %.3g vs dense pattern ANDs %.3g "
+                "(x%.2f) | patterns in groups with union <=16:%llu <=32:%llu <=64:%llu <=128:%llu <=256:%llu "
+                ">256:%llu\n",
+                mode, (double)ucnt / G, (double)staged, (double)dense_ands,
+                staged ? (double)dense_ands / staged : 0.0, (unsigned long long)uhist[0],
+                (unsigned long long)uhist[1], (unsigned long long)uhist[2], (unsigned long long)uhist[3],
+                (unsigned long long)uhist[4], (unsigned long long)uhist[5]);
+    }
     uint64_t pgh[6] = {0, 0, 0, 0, 0, 0};
     for (size_t g = 0; g < G; ++g) {
         const uint64_t c = pg[g];
