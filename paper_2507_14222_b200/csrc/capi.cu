@@ -289,9 +289,9 @@ void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m, bool enumerate 
     igb::RankSpace R;
     igb::PatternIndex CI[2];
     if (vertical) igb::combined_rank_space(ctx, PX[0], PX[1], R);
+    // the test index keeps building on its own stream through phase B; the
+    // matchers (phase C) wait for it
     const bool fuse = ev && ev->job && vertical;
-    if (fuse) ev->job->wait(&ctx);  // the test index was built during phase A
-    const bool fused = fuse && ev->job->has_postings && ev->job->P.L == (uint32_t)(64 * k);
     tm.mark();  // 1
     // phase B (per class): candidate index, support, score, checked total, purify
     for_both_classes(ctx, [&](igb::Ctx& cx, int c) {
@@ -350,17 +350,29 @@ void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m, bool enumerate 
                               &m.pidx[c].gkey, &m.pidx[c].pid, &m.pidx[c].pkey})
                 b->persist();
             tr.mark("pure_index");
-            if (fused) {
-                // Σ scores <= Σ candidate scores, checked <= INT64_MAX above: unchecked sums
-                IGB_CUDA(cudaStreamWaitEvent(cx.stream, ev->job->done, 0));
-                igb::posting_match(cx, P.rows.data(), P.rows.n, k, P.score.as<int64_t>(), ev->job->P, ev->out[c],
-                                   nullptr, true, &m.pidx[c]);
-                tr.mark("evidence");
-            }
         }
         IGB_CUDA(cudaStreamSynchronize(cx.stream));
     }, concurrent);
     m.has_pidx = vertical;
+    // phase C (per class): evidence of the test encoding, once both classes'
+    // pure dictionaries are indexed — the matchers fill the GPU, and a class's
+    // small index kernels queued behind the other class's matcher would stall
+    bool fused = false;
+    if (fuse) {
+        ev->job->wait(&ctx);  // (built during phases A and B)
+        fused = ev->job->has_postings && ev->job->P.L == (uint32_t)(64 * k);
+    }
+    if (fused) {
+        for_both_classes(ctx, [&](igb::Ctx& cx, int c) {
+            igb::Trace tr(cx, "fitC", c);
+            const ig_candidates& P = m.pure[c];
+            // Σ scores <= Σ candidate scores, checked <= INT64_MAX above: unchecked sums
+            IGB_CUDA(cudaStreamWaitEvent(cx.stream, ev->job->done, 0));
+            igb::posting_match(cx, P.rows.data(), P.rows.n, k, P.score.as<int64_t>(), ev->job->P, ev->out[c],
+                               nullptr, true, &m.pidx[c]);
+            tr.mark("evidence");
+        }, concurrent);
+    }
     if (ev) ev->done = fused;
     tm.mark();  // 2
     IGB_CUDA(cudaStreamSynchronize(ctx.stream));

@@ -710,6 +710,60 @@ void scan_stats(Ctx& ctx, int mode, const PatternIndex& I, const DevBuf& glen, s
         for (size_t p = 0; p < np; ++p) tmax = std::max(tmax, beg[p] + len[p]);
         std::vector<uint16_t> toks(tmax);
         read_back(ctx, toks.data(), I.toks->p, (size_t)tmax * 2);
+        {
+            // per task (<= 64 patterns of one group of >= 4): tokens common to
+            // all its patterns (ANDed once per task), residual tokens per pattern
+            std::vector<uint32_t> cntt(65536, 0);
+            uint64_t base_ands = 0, resid_ands = 0, resid_union = 0, small_ands = 0, ntask = 0, csum = 0;
+            size_t i = 0;
+            while (i < np) {
+                size_t e = i;
+                while (e < np && gid[e] == gid[i]) ++e;
+                const uint32_t g = gid[i];
+                if (e - i < 4) {
+                    for (size_t j = i; j < e; ++j) {
+                        const uint32_t p = order[j];
+                        small_ands += (uint64_t)(len[p] > 3 ? len[p] - 3 : 0) * gl[g];
+                    }
+                    i = e;
+                    continue;
+                }
+                for (size_t t0 = i; t0 < e; t0 += 64) {
+                    const size_t t1 = std::min(e, t0 + 64), n = t1 - t0;
+                    std::vector<uint16_t> used;
+                    for (size_t j = t0; j < t1; ++j) {
+                        const uint32_t p = order[j];
+                        for (uint32_t t = 3; t < len[p]; ++t) {
+                            const uint16_t tk = toks[beg[p] + t];
+                            if (cntt[tk]++ == 0) used.push_back(tk);
+                        }
+                    }
+                    uint32_t c = 0, ru = 0;
+                    for (uint16_t tk : used) {
+                        if (cntt[tk] == n)
+                            ++c;
+                        else
+                            ++ru;
+                    }
+                    for (size_t j = t0; j < t1; ++j) {
+                        const uint32_t p = order[j];
+                        const uint32_t m3 = len[p] > 3 ? len[p] - 3 : 0;
+                        resid_ands += (uint64_t)(m3 - c) * gl[g];
+                    }
+                    for (uint16_t tk : used) cntt[tk] = 0;
+                    base_ands += (uint64_t)c * gl[g];
+                    resid_union += (uint64_t)ru * gl[g];
+                    csum += c;
+                    ++ntask;
+                }
+                i = e;
+            }
+            fprintf(stderr,
+                    "[ig scan] mode %d tasks %llu: common tokens/task %.1f, base ANDs %.3g, residual ANDs %.3g (dense), "
+                    "residual rows staged %.3g, small-group ANDs %.3g (dense)\n",
+                    mode, (unsigned long long)ntask, ntask ? (double)csum / ntask : 0.0, (double)base_ands,
+                    (double)resid_ands, (double)resid_union, (double)small_ands);
+        }
         std::vector<uint32_t> seen(65536, 0xffffffffu);
         uint64_t staged = 0, dense_ands = 0, ucnt = 0, uhist[6] = {0, 0, 0, 0, 0, 0};
         size_t i = 0;

@@ -30,6 +30,8 @@ torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
     step()
     torch.cuda.synchronize()
+if os.environ.get("TRACE"):
+    prof.export_chrome_trace(os.environ["TRACE"])
 ev = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA and "memcpy" not in e.name.lower()
       and "memset" not in e.name.lower()]
 iv = sorted((e.time_range.start, e.time_range.end, e.name) for e in ev)
