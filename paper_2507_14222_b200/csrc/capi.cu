@@ -238,8 +238,11 @@ struct FusedEvidence {
 // (a shard computed it for its distinct rows).
 // pre (optional): each class's training postings, already built on the
 // context's aux stream (a shard builds them while its records travel).
+// max_row_tokens (optional): an upper bound on the set bits of a training row
+// (an encoding's feature count: one token per column), which bounds every
+// pattern's token list and spares the index build a read-back.
 void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m, bool enumerate = true, FusedEvidence* ev = nullptr,
-              const uint32_t* const* row_perm = nullptr, igb::Postings* pre = nullptr) {
+              const uint32_t* const* row_perm = nullptr, igb::Postings* pre = nullptr, uint32_t max_row_tokens = 0) {
     m.L = L;
     const size_t k = igb::words_for(L);
     for (int c = 0; c < 2; ++c)
@@ -294,6 +297,8 @@ void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m, bool enumerate 
     const bool fuse = ev && ev->job && vertical;
     tm.mark();  // 1
     // phase B (per class): candidate index, support, score, checked total, purify
+    DevBuf tot_buf[2];
+    unsigned tot_g[2] = {0, 0};
     for_both_classes(ctx, [&](igb::Ctx& cx, int c) {
         igb::Trace tr(cx, "fitA", c);
         ig_candidates& C = m.cand[c];
@@ -301,17 +306,15 @@ void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m, bool enumerate 
         C.support.alloc(std::max<size_t>(np, 1) * 8, cx.stream);
         C.score.alloc(std::max<size_t>(np, 1) * 8, cx.stream);
         if (vertical) {
-            igb::build_pattern_index(cx, C.rows.data(), np, k, R, CI[c]);
+            igb::build_pattern_index(cx, C.rows.data(), np, k, R, CI[c], max_row_tokens);
             igb::posting_support(cx, C.rows.data(), np, k, PX[c], C.support.as<int64_t>(), &CI[c]);
         } else {
             igb::count_support_dev(cx, C.rows.data(), np, X[c].p, X[c].n, k, C.support.as<int64_t>());
         }
         tr.mark("support");
-        int64_t total = 0;
-        if (igb::score_total_dev(cx, C.rows.data(), np, k, C.support.as<int64_t>(), C.score.as<int64_t>(), &total) !=
-            IG_OK)
-            fail(IG_E_OVERFLOW, "pattern score or total score overflows int64");
-        m.partial_total[c] = (uint64_t)total;
+        // (the total and the overflow checks are collected at the end of the fit)
+        tot_g[c] = igb::score_total_launch(cx, C.rows.data(), np, k, C.support.as<int64_t>(), C.score.as<int64_t>(),
+                                           tot_buf[c]);
         C.has_support = C.has_score = true;
         tr.mark("score+total");
         // then (same class, no wait for the other class's support): reject_covered
@@ -377,6 +380,12 @@ void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m, bool enumerate 
     tm.mark();  // 2
     IGB_CUDA(cudaStreamSynchronize(ctx.stream));
     IGB_CUDA(cudaStreamSynchronize(ctx.aux));
+    for (int c = 0; c < 2; ++c) {
+        int64_t total = 0;
+        if (igb::score_total_collect(ctx, tot_buf[c], tot_g[c], &total) != IG_OK)
+            fail(IG_E_OVERFLOW, "pattern score or total score overflows int64");
+        m.partial_total[c] = (uint64_t)total;
+    }
     m.ms[0] = 0;
     m.ms[1] = tm.ms(0, 1);  // canonical rows + enumerate + postings (both classes, concurrent)
     m.ms[2] = 0;
@@ -1121,7 +1130,7 @@ int ig_fit_encoded(ig_ctx* ctx, const ig_encoding* train, const ig_kernel_config
         View X[2] = {{train->attack.data(), train->attack.n, train->attack.k},
                      {train->normal.data(), train->normal.n, train->normal.k}};
         auto m = std::make_unique<ig_model>();
-        fit_impl(*ctx, X, train->L, *m);
+        fit_impl(*ctx, X, train->L, *m, true, nullptr, nullptr, nullptr, (uint32_t)train->n_cols);
         *out = m.release();
     });
 }
@@ -1164,7 +1173,7 @@ int ig_fit_evidence_encoded(ig_ctx* ctx, const ig_encoding* train, const ig_enco
         ev.out[0] = d_A;
         ev.out[1] = d_N;
         if (tests->all.n == 0) ev.job = nullptr;
-        fit_impl(*ctx, X, train->L, *m, true, &ev);
+        fit_impl(*ctx, X, train->L, *m, true, &ev, nullptr, nullptr, (uint32_t)train->n_cols);
         if (!ev.done && tests->all.n) evidence_of_encoding(ctx, m.get(), tests, d_A, d_N);
         *out = m.release();
     });
@@ -1346,7 +1355,7 @@ int ig_shard_finish(ig_ctx* ctx, ig_shard* s, uint64_t* partial_totals) {
         IGB_CUDA(cudaEventRecord(built, ctx->aux));
         IGB_CUDA(cudaStreamWaitEvent(ctx->stream, built, 0));
         cudaEventDestroy(built);
-        fit_impl(*ctx, X, s->L, s->model, /*enumerate=*/false, nullptr, rp, s->PX);
+        fit_impl(*ctx, X, s->L, s->model, /*enumerate=*/false, nullptr, rp, s->PX, (uint32_t)s->train->n_cols);
         partial_totals[0] = s->model.partial_total[0];
         partial_totals[1] = s->model.partial_total[1];
     });

@@ -992,20 +992,28 @@ int score_dev(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const int64_t
     return h ? IG_E_OVERFLOW : IG_OK;
 }
 
-// score_patterns then total_score (mine.hpp:46-51) with one read-back: the
-// score overflow flag and the per-block 128-bit partial sums come back together.
-int score_total_dev(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const int64_t* d_support, int64_t* d_score,
-                    int64_t* total) {
-    *total = 0;
-    if (np == 0) return IG_OK;
+// score_patterns then total_score (mine.hpp:46-51): the score kernel and the
+// per-block 128-bit partial sums (plus the score overflow flag) are left in
+// `buf`; score_total_collect reads them back once, when the caller's stream
+// has drained anyway (the fit defers it to its end: nothing downstream needs
+// the total on the host).
+unsigned score_total_launch(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const int64_t* d_support,
+                            int64_t* d_score, DevBuf& buf) {
+    if (np == 0) return 0;
     const unsigned g = std::min<unsigned>(grid_for(ctx, np, 256), 1024);
-    DevBuf buf((2 * (size_t)g + 1) * 8, ctx.stream);
+    buf.alloc((2 * (size_t)g + 1) * 8, ctx.stream);
     unsigned long long* lo = buf.as<unsigned long long>();
     long long* hi = reinterpret_cast<long long*>(lo + g);
     int* flag = reinterpret_cast<int*>(lo + 2 * g);
     IGB_CUDA(cudaMemsetAsync(flag, 0, 8, ctx.stream));
     IGB_LAUNCH(ctx, score_k, grid_for(ctx, np, 256), 256, 0, d_pat, np, (int)k, d_support, d_score, flag);
     IGB_LAUNCH(ctx, sum128, g, 256, 0, d_score, np, lo, hi);
+    return g;
+}
+
+int score_total_collect(Ctx& ctx, const DevBuf& buf, unsigned g, int64_t* total) {
+    *total = 0;
+    if (g == 0) return IG_OK;
     std::vector<unsigned long long> h(2 * (size_t)g + 1);
     read_back(ctx, h.data(), buf.p, h.size() * 8);
     if (*reinterpret_cast<const int*>(&h[2 * g])) return IG_E_OVERFLOW;
@@ -1014,6 +1022,13 @@ int score_total_dev(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const i
     if (acc > (__int128)INT64_MAX || acc < (__int128)INT64_MIN) return IG_E_OVERFLOW;
     *total = (int64_t)acc;
     return IG_OK;
+}
+
+int score_total_dev(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const int64_t* d_support, int64_t* d_score,
+                    int64_t* total) {
+    DevBuf buf;
+    const unsigned g = score_total_launch(ctx, d_pat, np, k, d_support, d_score, buf);
+    return score_total_collect(ctx, buf, g, total);
 }
 
 int total_score_dev(Ctx& ctx, const int64_t* d_score, size_t np, int64_t* total) {

@@ -813,6 +813,8 @@ void scan_stats(Ctx& ctx, int mode, const PatternIndex& I, const DevBuf& glen, s
             (unsigned long long)pgh[4], (unsigned long long)pgh[5], (double)toks / np);
 }
 
+constexpr unsigned long long kListBudget = 3ull << 30;  // bytes of scan lists allocated from bounds
+
 template <int MODE>
 void launch_scan(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Postings& P, const PatternIndex* I,
                  const int64_t* scores, unsigned long long* acc, int64_t* support, uint8_t* cover, int* flags) {
@@ -851,8 +853,14 @@ void launch_scan(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Post
                                            (int64_t)G2 + 1, ctx.stream));
     IGB_CUDA(cub::DeviceScan::ExclusiveSum(temp4.p, tb4, ub3.as<unsigned long long>(), goff.as<unsigned long long>(),
                                            (int64_t)G + 1, ctx.stream));
-    unsigned long long E2E[2] = {0, 0};
-    {
+    // Every list is at most W words long, so G2·W and G·W entries bound both
+    // levels: when that fits kListBudget, allocate the bound (the pool keeps
+    // the pages mapped; only the written entries are touched) and skip the
+    // read-back of the exact sizes — one host round trip less per scan.
+    const unsigned long long Wl = std::max<unsigned long long>(P.W, 1);
+    unsigned long long E2E[2] = {(unsigned long long)G2 * Wl, (unsigned long long)G * Wl};
+    static const bool exact_sizes = getenv("IG_SCAN_EXACT_SIZES") != nullptr;  // A/B
+    if (exact_sizes || (E2E[0] + E2E[1]) * 12 > kListBudget) {
         DevBuf both(16, ctx.stream);
         IGB_CUDA(cudaMemcpyAsync(both.p, poff.as<unsigned long long>() + G2, 8, cudaMemcpyDeviceToDevice, ctx.stream));
         IGB_CUDA(cudaMemcpyAsync(both.as<unsigned long long>() + 1, goff.as<unsigned long long>() + G, 8,
@@ -931,7 +939,8 @@ void combined_rank_space(Ctx& ctx, const Postings& A, const Postings& B, RankSpa
     make_rank_space(ctx, df.as<uint32_t>(), A.L, R);
 }
 
-void build_pattern_index(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const RankSpace& R, PatternIndex& I) {
+void build_pattern_index(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const RankSpace& R, PatternIndex& I,
+                         uint32_t max_tokens) {
     Trace tr(ctx, "pattern_index", -1);
     I.np = np;
     I.G = 0;
@@ -950,8 +959,14 @@ void build_pattern_index(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, co
     DevBuf temp(tb, ctx.stream);
     IGB_CUDA(cub::DeviceScan::ExclusiveSum(temp.p, tb, I.len.as<uint32_t>(), I.beg.as<uint32_t>(), (int64_t)np + 1,
                                            ctx.stream));
-    uint32_t total = 0;
-    read_back(ctx, &total, I.beg.as<uint32_t>() + np, 4);
+    // token list space: np * max_tokens when the caller bounds a pattern's
+    // tokens (no read-back), else the exact total
+    uint64_t total = (uint64_t)np * std::min<uint32_t>(max_tokens, (uint32_t)(64 * k));
+    if (!max_tokens || total > 0xffffffffull) {
+        uint32_t t32 = 0;
+        read_back(ctx, &t32, I.beg.as<uint32_t>() + np, 4);
+        total = t32;
+    }
     I.toks = std::make_shared<DevBuf>();
     I.toks->alloc(std::max<size_t>(total, 1) * 2, ctx.stream);
     if (np == 0) return;
@@ -1233,10 +1248,8 @@ void build_postings(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, uint32_
     DevBuf temp(tb, ctx.stream);
     IGB_CUDA(cub::DeviceScan::ExclusiveSum(temp.p, tb, nzc.as<uint32_t>(), P.nz_off.as<uint32_t>(), (int64_t)L + 1,
                                            ctx.stream));
-    uint32_t total = 0;
-    read_back(ctx, &total, P.nz_off.as<uint32_t>() + L, 4);
-    P.nz_total = total;
-    P.nz_idx.alloc(std::max<size_t>(total, 1) * 4, ctx.stream);
+    // (sized for every word non-zero: half the dense bytes, no read-back)
+    P.nz_idx.alloc(std::max<size_t>((size_t)L * P.W, 1) * 4, ctx.stream);
     IGB_LAUNCH(ctx, fill_nonzero, grid_for(ctx, (size_t)L * 32, 256), 256, 0, P.dense.as<unsigned long long>(), L,
                P.W, P.nz_off.as<uint32_t>(), P.nz_idx.as<uint32_t>());
 }

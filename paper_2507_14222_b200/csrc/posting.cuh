@@ -14,7 +14,6 @@ struct Postings {
     size_t n = 0;        // posting rows (distinct rows when built with distinct = true)
     size_t n_src = 0;    // source rows
     size_t W = 0;        // words per posting = ceil(n / 64)
-    uint32_t nz_total = 0;
     DevBuf dense;        // L x W u64
     DevBuf df;           // L u32: rows containing the bit
     DevBuf nz_off;       // L+1 u32: CSR offsets of non-zero words
@@ -59,7 +58,9 @@ void make_rank_space(Ctx& ctx, const uint32_t* d_df, uint32_t L, RankSpace& R, b
 void cluster_order(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, uint32_t* d_perm);
 // df = A.df + B.df (postings of the two training classes)
 void combined_rank_space(Ctx& ctx, const Postings& A, const Postings& B, RankSpace& R);
-void build_pattern_index(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const RankSpace& R, PatternIndex& I);
+// max_tokens: an upper bound on a pattern's token count (0: unknown)
+void build_pattern_index(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const RankSpace& R, PatternIndex& I,
+                         uint32_t max_tokens = 0);
 void group_ids(Ctx& ctx, const unsigned long long* d_sorted_key, size_t np, PatternIndex& I);
 // index of the patterns S.pattern[d_src_of[i]], i < n (a subset, e.g. the pure
 // patterns among the candidates), without re-ranking or re-sorting

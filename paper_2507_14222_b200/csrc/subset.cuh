@@ -65,6 +65,9 @@ int total_score_dev(Ctx& ctx, const int64_t* d_score, size_t np, int64_t* total)
 // both, with one read-back (IG_E_OVERFLOW if either overflows)
 int score_total_dev(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const int64_t* d_support, int64_t* d_score,
                     int64_t* total);
+unsigned score_total_launch(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const int64_t* d_support,
+                            int64_t* d_score, DevBuf& buf);
+int score_total_collect(Ctx& ctx, const DevBuf& buf, unsigned g, int64_t* total);
 
 // Keep rows whose flag is 0 (stable), with their supports/scores.
 size_t compact_unflagged(Ctx& ctx, const int64_t* d_words, const int64_t* d_sup, const int64_t* d_sc,
