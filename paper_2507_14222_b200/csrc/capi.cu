@@ -506,7 +506,9 @@ int ig_ctx_create(int device, ig_ctx** out) {
         // costs ~100 ms per first-time allocation pattern inside a fit.
         size_t free_b = 0, total_b = 0;
         IGB_CUDA(cudaMemGetInfo(&free_b, &total_b));
-        size_t reserve = std::min<size_t>(free_b / 4, size_t{24} << 30);
+        // (C4 alone measured 370 ms per step with 24 GB — the pool kept growing —
+        // and 136 ms with 60 GB)
+        size_t reserve = std::min<size_t>(free_b / 2, size_t{64} << 30);
         if (const char* e = getenv("IG_POOL_RESERVE_GB")) reserve = (size_t)(atof(e) * (1ull << 30));
         if (reserve) {
             void* p = nullptr;
