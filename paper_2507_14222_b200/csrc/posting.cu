@@ -589,6 +589,12 @@ grouped_scan(const unsigned long long* __restrict__ dense, size_t W, size_t n_ro
              unsigned long long* __restrict__ work) {
     const int lane = threadIdx.x & 31;
     const size_t warps = ((size_t)gridDim.x * blockDim.x) >> 5;
+    // matcher: per warp, the current pattern's tokens 3..34, read four at a
+    // time as one 16-byte broadcast instead of four shuffles (C3 matcher -3 %;
+    // support and coverage patterns are too short to repay the store)
+    constexpr bool kSmemTok = MODE == kMatch || MODE == kMatchChecked;
+    __shared__ __align__(16) uint32_t s_off[8][32];
+    uint32_t* so = s_off[(threadIdx.x >> 5) & 7];
     bool ovf = false;
     unsigned long long nand = 0;  // COUNT only
     for (size_t i = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < np; i += warps) {
@@ -601,7 +607,12 @@ grouped_scan(const unsigned long long* __restrict__ dense, size_t W, size_t n_ro
         // whose posting already contains every surviving word of the group
         // list, so ANDing it again is a no-op
         const uint32_t t0 = m ? (uint32_t)toks[o] : 0u;
-        const uint32_t toff = lane < m ? (uint32_t)toks[o + lane] : t0;
+        const uint32_t tl = lane < m ? (uint32_t)toks[o + lane] : t0;
+        if (kSmemTok) {
+            __syncwarp();  // the previous pattern's tokens are read
+            so[lane >= 3 ? lane - 3 : 29 + lane] = lane >= 3 ? tl : t0;
+            __syncwarp();
+        }
         const unsigned long long base = goff[g];
         const uint32_t len = glen[g];
         unsigned long long s = 0;
@@ -613,25 +624,32 @@ grouped_scan(const unsigned long long* __restrict__ dense, size_t W, size_t n_ro
             const uint32_t w = j < len ? ew[base + j] : 0u;
             unsigned long long mw = j < len ? em[base + j] : 0ull;
             const unsigned long long* col = dense + w;
-            // tokens 3..31 from the lanes' registers (0..2 are the group key,
-            // already applied in the list), four per round, with compile-time
-            // shuffle lanes (lanes 32..34 of the last round wrap to tokens
-            // 0..2: no-ops); the rare tail past 32 is read from memory
+            // tokens 3..31 (0..2 are the group key, already applied in the
+            // list), four per round; offsets past the pattern are token 0's
+            // (no-ops); the rare tail past 32 is read from memory
 #pragma unroll
-            for (int t = 3; t < 32; t += 4) {
+            for (int q = 0; q < 8; ++q) {
+                const int t = 3 + 4 * q;
                 if ((uint32_t)t >= m) break;
                 const bool live = mw != 0ull;
                 if (!__any_sync(kFull, live)) break;
-                const uint32_t o0 = __shfl_sync(kFull, toff, t), o1 = __shfl_sync(kFull, toff, (t + 1) & 31);
-                const uint32_t o2 = __shfl_sync(kFull, toff, (t + 2) & 31), o3 = __shfl_sync(kFull, toff, (t + 3) & 31);
+                uint4 tw;
+                if (kSmemTok) {
+                    tw = reinterpret_cast<const uint4*>(so)[q];
+                } else {  // compile-time shuffle lanes; 32..34 wrap to tokens 0..2 (no-ops)
+                    tw.x = __shfl_sync(kFull, tl, t);
+                    tw.y = __shfl_sync(kFull, tl, (t + 1) & 31);
+                    tw.z = __shfl_sync(kFull, tl, (t + 2) & 31);
+                    tw.w = __shfl_sync(kFull, tl, (t + 3) & 31);
+                }
                 if (COUNT && live) nand += min(4u, m - (uint32_t)t);
-                if (live) mw &= (ld_tok(col, o0, wb) & ld_tok(col, o1, wb)) & (ld_tok(col, o2, wb) & ld_tok(col, o3, wb));
+                if (live) mw &= (ld_tok(col, tw.x, wb) & ld_tok(col, tw.y, wb)) & (ld_tok(col, tw.z, wb) & ld_tok(col, tw.w, wb));
             }
             for (uint32_t t = 32; t < m; ++t) {
                 if (!__any_sync(kFull, mw != 0ull)) break;
                 const uint32_t tt = toks[o + t];
                 if (COUNT && mw) ++nand;
-                if (mw) mw &= col[tt * Wu];
+                if (mw) mw &= ld_tok(col, tt, wb);
             }
             if (MODE == kSupport) {
                 cnt += __popcll(mw);
@@ -1180,8 +1198,9 @@ void cluster_order(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, uint32_t
 }
 
 bool postings_supported(uint32_t L, size_t n) {
-    // token ids fit u16 (and W * 8 fits u32)
-    return words_for(L) * 64 < 65535 && n < 0xffffffffull;
+    // token ids fit u16, and every posting's word offset (token * W) fits u32
+    return words_for(L) * 64 < 65535 && n < 0xffffffffull &&
+           (uint64_t)words_for(L) * 64 * ((n + 63) / 64) < 0xffffffffull;
 }
 
 void build_postings(Ctx& ctx, const int64_t* d_rows, size_t n, size_t k, uint32_t /*logical_len*/, Postings& P,
