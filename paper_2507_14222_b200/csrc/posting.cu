@@ -212,17 +212,24 @@ pattern_token_fill_rank(const int64_t* __restrict__ pat, size_t np, int k, const
         byrank[i] = gbyrank[i];
     }
     __syncthreads();
+    // this thread's rank bitmap: a column of rb only it touches (plain
+    // read-modify-writes, conflict-free across the warp), cleared as it is read
     uint32_t* my = rb + threadIdx.x;
     const int nw = 2 * k;  // 32-bit rank words
+    for (int q = 0; q < nw; ++q) my[q * kFillThreads] = 0u;
     for (size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += (size_t)gridDim.x * blockDim.x) {
-        for (int q = 0; q < nw; ++q) my[q * kFillThreads] = 0u;
-        for (int w = 0; w < k; ++w) {
-            uint64_t x = (uint64_t)pat[p * k + w];
+        // the row's words first, all loads in flight at once (KW >= k)
+        uint64_t row[KW];
+#pragma unroll
+        for (int w = 0; w < KW; ++w) row[w] = w < k ? (uint64_t)__ldg(pat + p * k + w) : 0ull;
+#pragma unroll
+        for (int w = 0; w < KW; ++w) {
+            uint64_t x = row[w];
             while (x) {
                 const int b = __ffsll((long long)x) - 1;
                 x &= x - 1;
                 const uint32_t r = rank[w * 64 + b];
-                atomicOr(my + (r >> 5) * kFillThreads, 1u << (r & 31));
+                my[(r >> 5) * kFillThreads] |= 1u << (r & 31);
             }
         }
         // tokens out four at a time (one 8-byte store instead of four 2-byte
@@ -231,7 +238,8 @@ pattern_token_fill_rank(const int64_t* __restrict__ pat, size_t np, int k, const
         unsigned long long buf = 0;
         uint32_t nb = 0;
         for (int q = 0; q < nw; ++q) {
-            uint32_t y = atomicOr(my + q * kFillThreads, 0u);  // ordered after this thread's ORs
+            uint32_t y = my[q * kFillThreads];
+            if (y) my[q * kFillThreads] = 0u;
             while (y) {
                 const int b = __ffs((int)y) - 1;
                 y &= y - 1;
