@@ -706,6 +706,135 @@ grouped_scan(const unsigned long long* __restrict__ dense, size_t W, size_t n_ro
     if (MODE == kMatchChecked && ovf) atomicOr(flags, 1);
 }
 
+// Support and coverage lists are short (C3: 10-20 words per pattern, half of
+// a warp's lanes idle): a warp takes two neighbouring patterns, each on a
+// half-warp, whenever both lists fit 16 words; otherwise it runs them one
+// after the other on the full warp, as grouped_scan does.
+template <int MODE, bool COUNT = false>
+__global__ void __launch_bounds__(256)
+half_scan(const unsigned long long* __restrict__ dense, size_t W, const uint32_t* __restrict__ tok_beg,
+          const uint32_t* __restrict__ tok_len, const uint16_t* __restrict__ toks, size_t np,
+          const uint32_t* __restrict__ order, const uint32_t* __restrict__ gid,
+          const unsigned long long* __restrict__ goff, const uint32_t* __restrict__ glen,
+          const uint32_t* __restrict__ ew, const unsigned long long* __restrict__ em,
+          int64_t* __restrict__ support_out, uint8_t* __restrict__ cover_out, unsigned long long* __restrict__ work) {
+    static_assert(MODE == kSupport || MODE == kCover, "half_scan: support or coverage");
+    const int lane = threadIdx.x & 31, half = lane >> 4, hl = lane & 15;
+    const unsigned hmask = half ? 0xffff0000u : 0x0000ffffu;
+    const uint32_t Wu = (uint32_t)W, wb = Wu * 8u;
+    // per warp and half: tokens 3..34 of the half's pattern (past it: token 0)
+    __shared__ __align__(16) uint32_t s_tok[8][2][32];
+    uint32_t(*st)[32] = s_tok[(threadIdx.x >> 5) & 7];
+    const size_t warps = ((size_t)gridDim.x * blockDim.x) >> 5;
+    const size_t npairs = (np + 1) / 2;
+    unsigned long long nand = 0;
+    for (size_t pi = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; pi < npairs; pi += warps) {
+        const size_t ih = 2 * pi + (size_t)half;
+        const bool has = ih < np;
+        uint32_t p = 0, o = 0, m = 0, len = 0;
+        unsigned long long base = 0;
+        if (has) {
+            p = order[ih];
+            const uint32_t g = gid[ih];
+            o = tok_beg[p];
+            m = tok_len[p];
+            len = glen[g];
+            base = goff[g];
+        }
+        const uint32_t lenA = __shfl_sync(kFull, len, 0), lenB = __shfl_sync(kFull, len, 16);
+        if (lenA <= 16 && lenB <= 16) {
+            const uint32_t t0 = m ? (uint32_t)toks[o] : 0u;
+            __syncwarp();  // the previous pair's tokens are read
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const uint32_t t = (uint32_t)hl + 16u * r;
+                st[half][t >= 3 ? t - 3 : 29 + t] = (t < m && t >= 3) ? (uint32_t)toks[o + t] : t0;
+            }
+            __syncwarp();
+            const uint32_t w = (uint32_t)hl < len ? ew[base + hl] : 0u;
+            unsigned long long mw = (uint32_t)hl < len ? em[base + hl] : 0ull;
+            const unsigned long long* col = dense + w;
+            const uint32_t mmax = max(__shfl_sync(kFull, m, 0), __shfl_sync(kFull, m, 16));
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const uint32_t t = 3u + 4u * q;
+                if (t >= mmax) break;
+                const bool live = mw != 0ull && t < m;
+                if (!__any_sync(kFull, live)) break;
+                const uint4 tw = reinterpret_cast<const uint4*>(st[half])[q];
+                if (COUNT && live) nand += min(4u, m - t);
+                if (live) mw &= (ld_tok(col, tw.x, wb) & ld_tok(col, tw.y, wb)) & (ld_tok(col, tw.z, wb) & ld_tok(col, tw.w, wb));
+            }
+            for (uint32_t t = 32; t < mmax; ++t) {  // rare tail
+                const bool live = mw != 0ull && t < m;
+                if (!__any_sync(kFull, live)) break;
+                if (COUNT && live) ++nand;
+                if (live) mw &= ld_tok(col, toks[o + t], wb);
+            }
+            if (COUNT) continue;
+            if (MODE == kSupport) {
+                uint32_t cnt = __popcll(mw);
+                for (int o2 = 8; o2; o2 >>= 1) cnt += __shfl_xor_sync(kFull, cnt, o2);
+                if (hl == 0 && has) support_out[p] = (int64_t)cnt;
+            } else {
+                const unsigned hit = __ballot_sync(kFull, mw != 0ull) & hmask;
+                if (hl == 0 && has) cover_out[p] = hit ? 1 : 0;
+            }
+            continue;
+        }
+        // full warp, one pattern after the other
+        for (int h = 0; h < 2; ++h) {
+            const size_t i = 2 * pi + (size_t)h;
+            if (i >= np) break;
+            const uint32_t pp = __shfl_sync(kFull, p, 16 * h), oo = __shfl_sync(kFull, o, 16 * h);
+            const uint32_t mm = __shfl_sync(kFull, m, 16 * h), ll = h ? lenB : lenA;
+            const unsigned long long bb = __shfl_sync(kFull, base, 16 * h);
+            const uint32_t t0 = mm ? (uint32_t)toks[oo] : 0u;
+            const uint32_t tl = (uint32_t)lane < mm ? (uint32_t)toks[oo + lane] : t0;
+            uint32_t cnt = 0;
+            bool hit = false;
+            for (uint32_t j0 = 0; j0 < ll; j0 += 32) {
+                const uint32_t j = j0 + lane;
+                const uint32_t w = j < ll ? ew[bb + j] : 0u;
+                unsigned long long mw = j < ll ? em[bb + j] : 0ull;
+                const unsigned long long* col = dense + w;
+#pragma unroll
+                for (int t = 3; t < 32; t += 4) {
+                    if ((uint32_t)t >= mm) break;
+                    const bool live = mw != 0ull;
+                    if (!__any_sync(kFull, live)) break;
+                    const uint32_t o0 = __shfl_sync(kFull, tl, t), o1 = __shfl_sync(kFull, tl, (t + 1) & 31);
+                    const uint32_t o2 = __shfl_sync(kFull, tl, (t + 2) & 31), o3 = __shfl_sync(kFull, tl, (t + 3) & 31);
+                    if (COUNT && live) nand += min(4u, mm - (uint32_t)t);
+                    if (live) mw &= (ld_tok(col, o0, wb) & ld_tok(col, o1, wb)) & (ld_tok(col, o2, wb) & ld_tok(col, o3, wb));
+                }
+                for (uint32_t t = 32; t < mm; ++t) {
+                    if (!__any_sync(kFull, mw != 0ull)) break;
+                    if (COUNT && mw) ++nand;
+                    if (mw) mw &= ld_tok(col, toks[oo + t], wb);
+                }
+                if (MODE == kSupport) {
+                    cnt += __popcll(mw);
+                } else if (__any_sync(kFull, mw != 0ull)) {
+                    hit = true;
+                    break;
+                }
+            }
+            if (COUNT) continue;
+            if (MODE == kSupport) {
+                for (int o2 = 16; o2; o2 >>= 1) cnt += __shfl_xor_sync(kFull, cnt, o2);
+                if (lane == 0) support_out[pp] = (int64_t)cnt;
+            } else if (lane == 0) {
+                cover_out[pp] = hit ? 1 : 0;
+            }
+        }
+    }
+    if (COUNT) {
+        for (int o2 = 16; o2; o2 >>= 1) nand += __shfl_xor_sync(kFull, nand, o2);
+        if (lane == 0 && nand) atomicAdd(work, nand);
+    }
+}
+
 // IG_SCAN_STATS=1 (development): shape of one scan on stderr — patterns per
 // group, list words per pattern (lane occupancy of a warp per pattern), tokens
 // per pattern.
@@ -909,8 +1038,19 @@ void launch_scan(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Post
     if (getenv("IG_SCAN_STATS")) scan_stats(ctx, MODE, *I, glen, G, np);
     const size_t blocks = std::min<size_t>((np + 7) / 8, (size_t)ctx.sm_count * 64);
     DiagSpan dspan(ctx, MODE == kSupport ? kDiagSupport : MODE == kCover ? kDiagCover : kDiagMatch);
+    static const int half_env = getenv("IG_HALF_SCAN") ? atoi(getenv("IG_HALF_SCAN")) : 1;  // A/B
     auto launch = [&](auto count_tag, unsigned long long* work) {
         constexpr bool C = decltype(count_tag)::value;
+        if constexpr (MODE == kSupport || MODE == kCover) {
+            if (half_env) {
+                const size_t hblocks = std::min<size_t>((np + 15) / 16, (size_t)ctx.sm_count * 64);
+                IGB_LAUNCH(ctx, (half_scan<MODE, C>), (unsigned)hblocks, 256, 0, P.dense.as<unsigned long long>(), P.W,
+                           I->beg.as<uint32_t>(), I->len.as<uint32_t>(), I->toks->as<uint16_t>(), np,
+                           I->order.as<uint32_t>(), I->gid.as<uint32_t>(), goff.as<unsigned long long>(),
+                           glen.as<uint32_t>(), ew.as<uint32_t>(), em.as<unsigned long long>(), support, cover, work);
+                return;
+            }
+        }
         IGB_LAUNCH(ctx, (grouped_scan<MODE, C>), (unsigned)blocks, 256, 0, P.dense.as<unsigned long long>(), P.W,
                    P.n, I->beg.as<uint32_t>(), I->len.as<uint32_t>(), I->toks->as<uint16_t>(), np,
                    I->order.as<uint32_t>(), I->gid.as<uint32_t>(), goff.as<unsigned long long>(),
