@@ -137,12 +137,13 @@ KERNEL_INFO = {
     "pair_enum": ("pair_enum (kernels 2+3: pair AND + fingerprint + tile/device dedup)",
                   "SURVEY.md §8(d) (2): K word-ANDs per pair u <= v of the class's distinct canonical rows",
                   "r02_ncu_raw_pair_enum.csv"),
-    "support": ("grouped_scan<kSupport> (kernel 5: f_c(b) by posting AND + POPC)",
+    "support": ("half_scan<kSupport> (kernel 5: f_c(b) by posting AND + POPC, two short-list patterns per warp)",
                 "posting word-ANDs on live list words (counted exactly by a counting re-run)",
-                "r02_ncu_raw_grouped_scan_support.csv"),
-    "cover": ("grouped_scan<kCover> (kernel 4: opposite-class subset filter, warp-vote early exit)",
+                "r02_ncu_raw_half_scan_support.csv"),
+    "cover": ("half_scan<kCover> (kernel 4: opposite-class subset filter, vote early exit, two short-list "
+              "patterns per warp)",
               "posting word-ANDs on live list words up to the first covering word (counted exactly)",
-              "r02_ncu_raw_grouped_scan_cover.csv"),
+              "r02_ncu_raw_half_scan_cover.csv"),
     "match": ("grouped_scan<kMatch> (kernel 6: matcher, difference-array runs)",
               "posting word-ANDs on live list words (counted exactly)",
               "r02_ncu_raw_grouped_scan_match.csv"),
