@@ -32,6 +32,7 @@
 struct ig_ctx : igb::Ctx {
     std::recursive_mutex mu;
     std::unique_ptr<igb::Worker> class_worker;  // igb::Ctx::worker
+    std::unique_ptr<igb::Worker> index_bg, vocab_bg;  // igb::Ctx::index_worker, vocab_worker
 };
 
 struct ig_candidates {
@@ -61,7 +62,7 @@ struct ig_model {
 // index stream (rows_ready) and a host thread builds their postings there
 // (done), so a fit issued meanwhile on the other streams overlaps both.
 struct RowIndexJob {
-    std::thread th;
+    igb::BgTask task;
     igb::Postings P;
     bool has_postings = false;
     cudaEvent_t rows_ready = nullptr, done = nullptr;
@@ -73,14 +74,14 @@ struct RowIndexJob {
     void wait(igb::Ctx* ctx) {
         std::lock_guard<std::mutex> lock(mu);
         if (!joined) {
-            if (th.joinable()) th.join();
+            task.join();
             joined = true;
             if (ctx) ctx->launches += launches;
         }
         if (err) std::rethrow_exception(err);
     }
     ~RowIndexJob() {
-        if (th.joinable()) th.join();
+        task.join();
         if (rows_ready) cudaEventDestroy(rows_ready);
         if (done) cudaEventDestroy(done);
     }
@@ -488,6 +489,10 @@ int ig_ctx_create(int device, ig_ctx** out) {
     int st = guard(c.get(), [&] {
         c->class_worker = std::make_unique<igb::Worker>(device);
         c->worker = c->class_worker.get();
+        c->index_bg = std::make_unique<igb::Worker>(device);
+        c->index_worker = c->index_bg.get();
+        c->vocab_bg = std::make_unique<igb::Worker>(device);
+        c->vocab_worker = c->vocab_bg.get();
         IGB_CUDA(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
         IGB_CUDA(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
         IGB_CUDA(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
@@ -1062,7 +1067,7 @@ int ig_encode_rows(ig_ctx* ctx, const ig_columns* cols, const ig_encoding* train
             cx.launches = 0;
             const int64_t* rows = e->all.data();
             RowIndexJob* j = job.get();
-            job->th = std::thread([j, cx, rows, n, k, L]() mutable {
+            job->task.start(ctx->index_worker, [j, cx, rows, n, k, L]() mutable {
                 try {
                     IGB_CUDA(cudaSetDevice(cx.device));
                     igb::build_postings(cx, rows, n, k, L, j->P, true, true);

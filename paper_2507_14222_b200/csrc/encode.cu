@@ -661,13 +661,13 @@ void host_vocab_build(Ctx& ctx, const ig_columns& c, const DeviceCols& d, const 
 // waits for them and fills the host fields.  It also checks that the tokens'
 // text is strictly increasing in byte order — the device keys' contract.
 struct HostVocabJob {
-    std::thread th;
+    igb::BgTask task;
     std::mutex mu;
     bool joined = false;
     std::exception_ptr err;
     void* pinned = nullptr;  // codes [kVocabMax] int64, features [kVocabMax] int32, L (the library's pool)
     ~HostVocabJob() {
-        if (th.joinable()) th.join();
+        task.join();
         if (pinned) ig_host_free(pinned);
     }
 };
@@ -676,7 +676,7 @@ const ig_encoding& ig_encoding::host_vocab() const {
     if (hv) {
         std::lock_guard<std::mutex> lock(hv->mu);
         if (!hv->joined) {
-            if (hv->th.joinable()) hv->th.join();
+            hv->task.join();
             hv->joined = true;
         }
         if (hv->err) std::rethrow_exception(hv->err);
@@ -810,7 +810,7 @@ bool device_vocab(Ctx& ctx, const ig_columns& c, const DeviceCols& d, const Voca
 
 // The host fields of a device-built vocabulary, on a host thread (the token
 // list is already in page-locked memory).
-void start_host_vocab(const ig_columns& c, const DeviceCols& d, ig_encoding& e) {
+void start_host_vocab(Ctx& ctx, const ig_columns& c, const DeviceCols& d, ig_encoding& e) {
     HostVocabJob* jp = e.hv.get();
     if (!jp) return;
     const uint32_t L = e.L;
@@ -818,7 +818,7 @@ void start_host_vocab(const ig_columns& c, const DeviceCols& d, ig_encoding& e) 
     std::vector<int> kind = c.kind, fcol = d.feat_col;
     ig_encoding* ep = &e;
     const auto* dict = &e.dict;  // e.dict = c.dict (copied before this call)
-    jp->th = std::thread([jp, ep, dict, ncols, decimals, kind, fcol, L] {
+    jp->task.start(ctx.vocab_worker, [jp, ep, dict, ncols, decimals, kind, fcol, L] {
         try {
             const int64_t* code = static_cast<const int64_t*>(jp->pinned);
             const int32_t* feat =
@@ -920,7 +920,7 @@ void encode_training_dev(Ctx& ctx, const ig_columns& c, ig_encoding& e) {
     if (device_vocab(ctx, c, d, vp, lcode, lcol, lcnt, e)) {
         // (1c) pack every training row with the device tables, then the host text
         pack_tables(ctx, e.L, d, static_cast<const Lut*>(e.dv.lut), e.dv.lcodes, e.dv.lbits, e.dv.cbits, all);
-        start_host_vocab(c, d, e);
+        start_host_vocab(ctx, c, d, e);
     } else {
         host_vocab_build(ctx, c, d, lcode, lcol, lcnt, e, all);
     }

@@ -164,6 +164,23 @@ private:
     std::thread th_;  // last: started once the queue exists
 };
 
+// A background job: on a persistent worker when there is one (no thread
+// start per call), else on its own thread.
+struct BgTask {
+    std::thread th;
+    std::future<void> fut;
+    void start(Worker* w, std::function<void()> fn) {
+        if (w)
+            fut = w->submit(std::move(fn));
+        else
+            th = std::thread(std::move(fn));
+    }
+    void join() {
+        if (th.joinable()) th.join();
+        if (fut.valid()) fut.wait();
+    }
+};
+
 struct Ctx {
     int device = 0;
     cudaStream_t own = nullptr;
@@ -180,6 +197,10 @@ struct Ctx {
     DiagStat diag_k[kDiagKinds];
     ProgressHook* progress = nullptr;  // set by ig_enumerate_candidates for one call
     Worker* worker = nullptr;          // owned by the ABI context; copies share it (may be null)
+    // background jobs of an encode (owned by the ABI context, may be null): the
+    // test rows' index, the training vocabulary's host text
+    Worker* index_worker = nullptr;
+    Worker* vocab_worker = nullptr;
     void diag_merge(const Ctx& o) {
         for (int i = 0; i < kDiagKinds; ++i) {
             diag_k[i].ms += o.diag_k[i].ms;
@@ -228,26 +249,22 @@ struct DiagSpan {
 // for it, through a per-thread page-locked bounce buffer: a pageable
 // destination is staged by the driver and can queue behind a large in-flight
 // host->device copy (e.g. a columns prefetch) on the copy engines.
+// page-locked bounce buffer from the library's host pool (ig_host_alloc): no
+// per-thread cudaMallocHost / cudaFreeHost in the short-lived encode jobs
 inline void read_back(const Ctx& ctx, void* host_dst, const void* d_src, size_t bytes) {
-    struct Pinned {
-        void* p = nullptr;
-        size_t cap = 0;
-        ~Pinned() {
-            if (p) cudaFreeHost(p);
-        }
-    };
-    thread_local Pinned buf;
-    if (bytes > buf.cap) {
-        if (buf.p) cudaFreeHost(buf.p);
-        buf.p = nullptr;
-        buf.cap = 0;
-        const size_t cap = std::max<size_t>(bytes, 64 << 10);
-        IGB_CUDA(cudaMallocHost(&buf.p, cap));
-        buf.cap = cap;
+    if (!bytes) {
+        IGB_CUDA(cudaStreamSynchronize(ctx.stream));
+        return;
     }
-    if (bytes) IGB_CUDA(cudaMemcpyAsync(buf.p, d_src, bytes, cudaMemcpyDeviceToHost, ctx.stream));
+    void* buf = nullptr;
+    if (ig_host_alloc(std::max<size_t>(bytes, 4096), &buf) != IG_OK) fail(IG_E_OOM, "page-locked read-back buffer");
+    struct Back {
+        void* p;
+        ~Back() { ig_host_free(p); }
+    } back{buf};
+    IGB_CUDA(cudaMemcpyAsync(buf, d_src, bytes, cudaMemcpyDeviceToHost, ctx.stream));
     IGB_CUDA(cudaStreamSynchronize(ctx.stream));
-    if (bytes) std::memcpy(host_dst, buf.p, bytes);
+    std::memcpy(host_dst, buf, bytes);
 }
 
 // Device -> host result copy: straight into page-locked destinations (the
