@@ -220,6 +220,11 @@ int ig_ingest_csv(ig_ctx* ctx, const char* bytes, size_t len, const char* label_
                   const char* normal_values, int decimals, long long train_rows, int ratio_k, ig_schema** schema,
                   ig_columns** train, ig_columns** test);
 size_t ig_columns_rows(const ig_columns* c);
+/* Bytes a host->device copy of the columns moves: the numeric block in its
+ * narrow exact form (per column the first decimal scale whose integer codes
+ * reproduce every parsed double bitwise under IEEE division, in the smallest
+ * integer type; else the raw doubles; built by ig_columns_build), the
+ * categorical ids and the labels. */
 size_t ig_columns_bytes(const ig_columns* c);
 void ig_columns_free(ig_columns* c);
 

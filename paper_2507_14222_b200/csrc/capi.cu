@@ -958,6 +958,7 @@ int ig_columns_build(const ig_table* t, const ig_schema* s, int with_labels, ig_
     return guard(nullptr, [&] {
         auto c = std::make_unique<ig_columns>();
         igb::build_columns(*t, *s, with_labels != 0, *c);
+        igb::build_narrow(*c);
         // Page-lock the typed arrays once so every encode's H2D runs at full PCIe/C2C
         // speed; best effort (no GPU here -> plain pageable copies).
         auto pin = [&](void* p, size_t bytes) {
@@ -967,6 +968,7 @@ int ig_columns_build(const ig_table* t, const ig_schema* s, int with_labels, ig_
                 cudaGetLastError();
         };
         pin(c->values.data(), c->values.size() * 8);
+        pin(c->narrow.data(), c->narrow.size());
         pin(c->cat.data(), c->cat.size() * 4);
         pin(c->is_attack.data(), c->is_attack.size());
         *out = c.release();
@@ -1023,7 +1025,9 @@ int ig_columns_prefetch(ig_ctx* ctx, ig_columns* c) {
 }
 size_t ig_columns_rows(const ig_columns* c) { return c ? c->n_rows : 0; }
 size_t ig_columns_bytes(const ig_columns* c) {
-    return c ? c->values.size() * 8 + c->cat.size() * 4 + c->is_attack.size() : 0;
+    if (!c) return 0;
+    const size_t num = c->narrow.empty() ? c->values.size() * 8 : c->narrow.size();
+    return num + c->cat.size() * 4 + c->is_attack.size();
 }
 void ig_columns_free(ig_columns* c) {
     if (!c) return;

@@ -5,6 +5,8 @@
 #include <algorithm>
 #include <charconv>
 #include <cmath>
+#include <cstdint>
+#include <cstring>
 #include <limits>
 #include <string>
 #include <unordered_map>
@@ -190,6 +192,82 @@ void infer_schema(const ig_table& t, const std::string& label, const std::vector
 // Typed columns of `t` under `s`: the "parsed columns" a fit starts from.
 // Row-count mismatch and unparsable numeric cells raise DataError exactly as
 // tokenize_row does (pipeline.cpp:173-193).
+// The narrow copy form of the numeric block (host_pipeline.hpp): per column
+// the first decimal scale whose codes reproduce every parsed value bitwise,
+// in the smallest integer type holding them; else the raw doubles.
+void build_narrow(ig_columns& c) {
+    c.narrow.clear();
+    const size_t n = c.n_rows, nn = c.n_num;
+    if (!nn || !n) return;
+    static const double kScales[] = {1.0, 10.0, 100.0, 1000.0, 1e4, 1e5, 1e6};
+    std::vector<NarrowHead> head(nn);
+    std::vector<int64_t> q(n);
+    size_t off = (nn * sizeof(NarrowHead) + 15) & ~size_t{15};
+    std::vector<std::vector<uint8_t>> data(nn);
+    for (size_t j = 0; j < nn; ++j) {
+        const double* v = c.values.data() + j * n;
+        NarrowHead h{0, 0, 0, 1.0};
+        for (double sc : kScales) {
+            bool ok = true;
+            int64_t lo = 0, hi = 0;
+            for (size_t r = 0; r < n && ok; ++r) {
+                const double x = v[r];
+                if (std::isnan(x)) {
+                    q[r] = INT64_MIN;
+                    continue;
+                }
+                const double y = x * sc;
+                if (!(std::fabs(y) < 2.0e9)) {
+                    ok = false;
+                    break;
+                }
+                const int64_t k = std::llround(y);
+                const double back = (double)k / sc;
+                if (std::memcmp(&back, &x, sizeof(double)) != 0) {
+                    ok = false;
+                    break;
+                }
+                q[r] = k;
+                lo = std::min(lo, k);
+                hi = std::max(hi, k);
+            }
+            if (!ok) continue;
+            // the type's minimum is the empty-cell code
+            h.type = (lo > INT8_MIN && hi <= INT8_MAX) ? 1u : (lo > INT16_MIN && hi <= INT16_MAX) ? 2u
+                     : (lo > INT32_MIN && hi <= INT32_MAX) ? 3u : 0u;
+            h.scale = sc;
+            break;
+        }
+        auto& d = data[j];
+        if (h.type == 0) {
+            d.resize(n * 8);
+            std::memcpy(d.data(), v, n * 8);
+        } else {
+            const size_t w = h.type == 1 ? 1 : h.type == 2 ? 2 : 4;
+            d.resize(n * w);
+            for (size_t r = 0; r < n; ++r) {
+                const int64_t k = q[r];
+                if (h.type == 1) {
+                    const int8_t x = k == INT64_MIN ? INT8_MIN : (int8_t)k;
+                    std::memcpy(d.data() + r, &x, 1);
+                } else if (h.type == 2) {
+                    const int16_t x = k == INT64_MIN ? INT16_MIN : (int16_t)k;
+                    std::memcpy(d.data() + 2 * r, &x, 2);
+                } else {
+                    const int32_t x = k == INT64_MIN ? INT32_MIN : (int32_t)k;
+                    std::memcpy(d.data() + 4 * r, &x, 4);
+                }
+            }
+        }
+        h.off = off;
+        head[j] = h;
+        off = (off + d.size() + 15) & ~size_t{15};
+    }
+    c.narrow.assign(off, 0);
+    std::memcpy(c.narrow.data(), head.data(), nn * sizeof(NarrowHead));
+    for (size_t j = 0; j < nn; ++j) std::memcpy(c.narrow.data() + head[j].off, data[j].data(), data[j].size());
+}
+
 void build_columns(const ig_table& t, const ig_schema& s, bool with_labels, ig_columns& c) {
     if (t.header.size() != s.names.size())
         throw Error{IG_E_DATA, "row 0: expected " + std::to_string(s.names.size()) + " columns, got " +

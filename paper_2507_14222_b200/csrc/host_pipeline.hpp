@@ -52,6 +52,12 @@ struct ig_columns {
     std::vector<std::vector<std::string>> dict;  // per table column: categorical id -> text
     std::vector<uint8_t> is_attack;     // [n_rows] when built with labels
     size_t n_num = 0, n_cat = 0;
+    // The numeric block in its narrowest exact form, what a host->device copy
+    // (ig_columns_prefetch) moves: n_num NarrowHead records, then each
+    // column's codes (16-byte aligned); value = code / scale in IEEE double
+    // division, checked equal (bitwise) to the parsed value for every cell when
+    // built; the type's minimum marks an empty cell; type 0 = the raw doubles.
+    std::vector<uint8_t> narrow;
     // Device-resident copies after ig_columns_upload (values, cat, is_attack),
     // owned with a cudaFree deleter; null until uploaded.
     std::shared_ptr<void> d_values, d_cat, d_attack;
@@ -62,9 +68,17 @@ struct ig_columns {
     mutable std::shared_ptr<void> prefetch;
 };
 
+struct NarrowHead {
+    uint32_t type;  // 0 raw f64, 1 int8, 2 int16, 3 int32 codes
+    uint32_t pad;
+    uint64_t off;   // byte offset of the column's data in ig_columns::narrow
+    double scale;
+};
+
 namespace igb {
 
 std::optional<double> parse_double_strict(std::string_view s);
+void build_narrow(ig_columns& c);
 void read_csv(const char* bytes, size_t len, ig_table& out);
 bool is_attack(const ig_schema& s, std::string_view label);
 void infer_schema(const ig_table& t, const std::string& label, const std::vector<std::string>& attack,

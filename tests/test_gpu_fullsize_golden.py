@@ -100,11 +100,14 @@ def api():
     return a
 
 
-@pytest.mark.parametrize("name", ["c3", "c4", "c5s"])
-def test_fullsize_host_pipeline_vs_reference(api, golden_dir, name):
-    """Host CSV reader + schema -> device encode -> fused fit + evidence (the
-    bench's e2e path), every output against the reference's digests.  c5s:
-    configs[4]'s CICIDS shape (p = 2, wide rows) on a 25,000-record sample."""
+@pytest.mark.parametrize("name,prefetch", [("c3", False), ("c4", False), ("c5s", False), ("c3", True),
+                                           ("c5s", True)])
+def test_fullsize_host_pipeline_vs_reference(api, golden_dir, name, prefetch):
+    """Host CSV reader + schema -> device encode -> fused fit + evidence, every
+    output against the reference's digests.  prefetch: the columns go over in
+    their narrow exact form (ig_columns_prefetch; code / scale per column,
+    decoded on the device) — the bench's e2e path.  c5s: configs[4]'s CICIDS
+    shape (p = 2, wide rows) on a 25,000-record sample."""
     g = _golden(golden_dir, name)
     gen = synth.cicids_csv if g.get("shape") == "cicids" else synth.nsl_csv
     csv = gen(g["rows"], seed=g["seed"])
@@ -117,8 +120,12 @@ def test_fullsize_host_pipeline_vs_reference(api, golden_dir, name):
     normal = [g["normal_values"]] if g.get("normal_values") else []
     schema = api.infer_schema(tr, g.get("label", "label"), normal_values=normal, decimals=g["decimals"])
     assert _schema_digest(schema, table.columns) == g["schema_digest"]
-    enc = api.encode_training(api.Columns(tr, schema, True), ctx)
-    tenc = api.encode_rows(api.Columns(te, schema, False), enc, ctx)
+    ctr, cte = api.Columns(tr, schema, True), api.Columns(te, schema, False)
+    if prefetch:
+        ctr.prefetch(ctx)
+        cte.prefetch(ctx)
+    enc = api.encode_training(ctr, ctx)
+    tenc = api.encode_rows(cte, enc, ctx)
     _check_encoding(g, enc, tenc)
     model, A, N = api.fit_evidence_encoded(enc, tenc)
     _check_evidence(g, A, N, api)
