@@ -281,6 +281,48 @@ __device__ void block_bitonic(unsigned long long* hi, unsigned long long* lo, ui
         }
 }
 
+// The same for n2 <= 1024 with a 1024-thread block, one element per thread
+// (padded with all-ones keys): the exchanges with partners in the same warp
+// (j < 32, 40 of the 55 stages) go through shuffles, the rest through shared
+// memory — 15 block barriers instead of 55.
+__device__ void block_bitonic_1024(unsigned long long* hi, unsigned long long* lo, uint16_t* idx, int n2) {
+    const int i = threadIdx.x;
+    unsigned long long h = i < n2 ? hi[i] : ~0ull, l = i < n2 ? lo[i] : ~0ull;
+    uint32_t x = i < n2 ? idx[i] : 0xffffu;
+    __syncthreads();
+    for (int k = 2; k <= 1024; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            unsigned long long ph, pl;
+            uint32_t px;
+            if (j < 32) {
+                ph = __shfl_xor_sync(0xffffffffu, h, j);
+                pl = __shfl_xor_sync(0xffffffffu, l, j);
+                px = __shfl_xor_sync(0xffffffffu, x, j);
+            } else {
+                hi[i] = h;
+                lo[i] = l;
+                idx[i] = (uint16_t)x;
+                __syncthreads();
+                ph = hi[i ^ j];
+                pl = lo[i ^ j];
+                px = idx[i ^ j];
+                __syncthreads();
+            }
+            // ascending where (i & k) == 0: the lower index keeps the smaller key
+            const bool up = (i & k) == 0, lower = (i & j) == 0;
+            const bool mine_gt = key_gt(h, l, ph, pl);
+            if (mine_gt == (up == lower)) {
+                h = ph;
+                l = pl;
+                x = px;
+            }
+        }
+    hi[i] = h;
+    lo[i] = l;
+    idx[i] = (uint16_t)x;
+    __syncthreads();
+}
+
 // One block: rank the distinct tokens in byte order (bit = rank), then the pack
 // tables — numeric (feature, code) sorted with their bits, categorical id ->
 // bit, the empty token's bit per feature — and the token list in bit order for
@@ -316,7 +358,10 @@ vocab_build(const int64_t* __restrict__ u_code, const int32_t* __restrict__ u_fe
         idx[i] = (uint16_t)i;
     }
     __syncthreads();
-    block_bitonic(hi, lo, idx, n2);
+    if (n2 <= 1024 && blockDim.x == 1024)
+        block_bitonic_1024(hi, lo, idx, n2);
+    else
+        block_bitonic(hi, lo, idx, n2);
     for (int pos = threadIdx.x; pos < (int)U; pos += blockDim.x) {
         const int i = idx[pos];
         const int f = u_feat[i];
@@ -342,7 +387,10 @@ vocab_build(const int64_t* __restrict__ u_code, const int32_t* __restrict__ u_fe
         idx[i] = (uint16_t)i;
     }
     __syncthreads();
-    block_bitonic(hi, lo, idx, n2);
+    if (n2 <= 1024 && blockDim.x == 1024)
+        block_bitonic_1024(hi, lo, idx, n2);
+    else
+        block_bitonic(hi, lo, idx, n2);
     for (int pos = threadIdx.x; pos < (int)U; pos += blockDim.x) {
         const int i = idx[pos];
         lcodes[pos] = u_code[i];
