@@ -706,10 +706,26 @@ grouped_scan(const unsigned long long* __restrict__ dense, size_t W, size_t n_ro
     if (MODE == kMatchChecked && ovf) atomicOr(flags, 1);
 }
 
-// Support and coverage lists are short (C3: 10-20 words per pattern, half of
-// a warp's lanes idle): a warp takes two neighbouring patterns, each on a
-// half-warp, whenever both lists fit 16 words; otherwise it runs them one
-// after the other on the full warp, as grouped_scan does.
+// difference array of one mask: +s at each run start, -s after each run end
+// (ctz(x) = popc(~x & (x - 1)) avoids the 64-bit find-first sequence)
+__device__ __forceinline__ void scatter_runs(unsigned long long mw, unsigned long long s, unsigned long long* row) {
+    unsigned long long st = mw & ~(mw << 1), en = mw & ~(mw >> 1);
+    while (st) {
+        __builtin_assume(en != 0ull);
+        const unsigned long long st1 = st - 1, en1 = en - 1;
+        atomicAdd(row + __popcll(~st & st1), s);
+        atomicAdd(row + 1 + __popcll(~en & en1), 0ull - s);
+        st &= st1;
+        en &= en1;
+    }
+}
+
+// Short lists (support and coverage at C3: 10-20 words per pattern; the
+// matcher at C4: 20-22) leave half of a warp's lanes idle: a warp takes two
+// neighbouring patterns, each on a half-warp, whenever both group lists fit 16
+// words; otherwise it runs them one after the other on the full warp, as
+// grouped_scan does (the matcher's full-warp path reads the pattern's tokens
+// from a per-warp shared-memory row, support / coverage from shuffles).
 template <int MODE, bool COUNT = false>
 __global__ void __launch_bounds__(256)
 half_scan(const unsigned long long* __restrict__ dense, size_t W, const uint32_t* __restrict__ tok_beg,
@@ -717,8 +733,10 @@ half_scan(const unsigned long long* __restrict__ dense, size_t W, const uint32_t
           const uint32_t* __restrict__ order, const uint32_t* __restrict__ gid,
           const unsigned long long* __restrict__ goff, const uint32_t* __restrict__ glen,
           const uint32_t* __restrict__ ew, const unsigned long long* __restrict__ em,
+          const int64_t* __restrict__ scores, unsigned long long* __restrict__ acc,
           int64_t* __restrict__ support_out, uint8_t* __restrict__ cover_out, unsigned long long* __restrict__ work) {
-    static_assert(MODE == kSupport || MODE == kCover, "half_scan: support or coverage");
+    static_assert(MODE == kSupport || MODE == kCover || MODE == kMatch, "half_scan: support, coverage or match");
+    constexpr bool kSmemTok = MODE == kMatch;
     const int lane = threadIdx.x & 31, half = lane >> 4, hl = lane & 15;
     const unsigned hmask = half ? 0xffff0000u : 0x0000ffffu;
     const uint32_t Wu = (uint32_t)W, wb = Wu * 8u;
@@ -732,7 +750,7 @@ half_scan(const unsigned long long* __restrict__ dense, size_t W, const uint32_t
         const size_t ih = 2 * pi + (size_t)half;
         const bool has = ih < np;
         uint32_t p = 0, o = 0, m = 0, len = 0;
-        unsigned long long base = 0;
+        unsigned long long base = 0, sc = 0;
         if (has) {
             p = order[ih];
             const uint32_t g = gid[ih];
@@ -740,6 +758,7 @@ half_scan(const unsigned long long* __restrict__ dense, size_t W, const uint32_t
             m = tok_len[p];
             len = glen[g];
             base = goff[g];
+            if (MODE == kMatch) sc = (unsigned long long)scores[p];
         }
         const uint32_t lenA = __shfl_sync(kFull, len, 0), lenB = __shfl_sync(kFull, len, 16);
         if (lenA <= 16 && lenB <= 16) {
@@ -776,9 +795,11 @@ half_scan(const unsigned long long* __restrict__ dense, size_t W, const uint32_t
                 uint32_t cnt = __popcll(mw);
                 for (int o2 = 8; o2; o2 >>= 1) cnt += __shfl_xor_sync(kFull, cnt, o2);
                 if (hl == 0 && has) support_out[p] = (int64_t)cnt;
-            } else {
+            } else if (MODE == kCover) {
                 const unsigned hit = __ballot_sync(kFull, mw != 0ull) & hmask;
                 if (hl == 0 && has) cover_out[p] = hit ? 1 : 0;
+            } else if (mw) {
+                scatter_runs(mw, sc, acc + (size_t)w * 64);
             }
             continue;
         }
@@ -789,8 +810,14 @@ half_scan(const unsigned long long* __restrict__ dense, size_t W, const uint32_t
             const uint32_t pp = __shfl_sync(kFull, p, 16 * h), oo = __shfl_sync(kFull, o, 16 * h);
             const uint32_t mm = __shfl_sync(kFull, m, 16 * h), ll = h ? lenB : lenA;
             const unsigned long long bb = __shfl_sync(kFull, base, 16 * h);
+            const unsigned long long ss = __shfl_sync(kFull, sc, 16 * h);
             const uint32_t t0 = mm ? (uint32_t)toks[oo] : 0u;
             const uint32_t tl = (uint32_t)lane < mm ? (uint32_t)toks[oo + lane] : t0;
+            if (kSmemTok) {
+                __syncwarp();  // the previous pattern's tokens are read
+                st[0][lane >= 3 ? lane - 3 : 29 + lane] = lane >= 3 ? tl : t0;
+                __syncwarp();
+            }
             uint32_t cnt = 0;
             bool hit = false;
             for (uint32_t j0 = 0; j0 < ll; j0 += 32) {
@@ -799,14 +826,22 @@ half_scan(const unsigned long long* __restrict__ dense, size_t W, const uint32_t
                 unsigned long long mw = j < ll ? em[bb + j] : 0ull;
                 const unsigned long long* col = dense + w;
 #pragma unroll
-                for (int t = 3; t < 32; t += 4) {
+                for (int q = 0; q < 8; ++q) {
+                    const int t = 3 + 4 * q;
                     if ((uint32_t)t >= mm) break;
                     const bool live = mw != 0ull;
                     if (!__any_sync(kFull, live)) break;
-                    const uint32_t o0 = __shfl_sync(kFull, tl, t), o1 = __shfl_sync(kFull, tl, (t + 1) & 31);
-                    const uint32_t o2 = __shfl_sync(kFull, tl, (t + 2) & 31), o3 = __shfl_sync(kFull, tl, (t + 3) & 31);
+                    uint4 tw;
+                    if (kSmemTok) {
+                        tw = reinterpret_cast<const uint4*>(st[0])[q];
+                    } else {  // compile-time shuffle lanes; 32..34 wrap to tokens 0..2 (no-ops)
+                        tw.x = __shfl_sync(kFull, tl, t);
+                        tw.y = __shfl_sync(kFull, tl, (t + 1) & 31);
+                        tw.z = __shfl_sync(kFull, tl, (t + 2) & 31);
+                        tw.w = __shfl_sync(kFull, tl, (t + 3) & 31);
+                    }
                     if (COUNT && live) nand += min(4u, mm - (uint32_t)t);
-                    if (live) mw &= (ld_tok(col, o0, wb) & ld_tok(col, o1, wb)) & (ld_tok(col, o2, wb) & ld_tok(col, o3, wb));
+                    if (live) mw &= (ld_tok(col, tw.x, wb) & ld_tok(col, tw.y, wb)) & (ld_tok(col, tw.z, wb) & ld_tok(col, tw.w, wb));
                 }
                 for (uint32_t t = 32; t < mm; ++t) {
                     if (!__any_sync(kFull, mw != 0ull)) break;
@@ -815,16 +850,20 @@ half_scan(const unsigned long long* __restrict__ dense, size_t W, const uint32_t
                 }
                 if (MODE == kSupport) {
                     cnt += __popcll(mw);
-                } else if (__any_sync(kFull, mw != 0ull)) {
-                    hit = true;
-                    break;
+                } else if (MODE == kCover) {
+                    if (__any_sync(kFull, mw != 0ull)) {
+                        hit = true;
+                        break;
+                    }
+                } else if (!COUNT && mw) {
+                    scatter_runs(mw, ss, acc + (size_t)w * 64);
                 }
             }
             if (COUNT) continue;
             if (MODE == kSupport) {
                 for (int o2 = 16; o2; o2 >>= 1) cnt += __shfl_xor_sync(kFull, cnt, o2);
                 if (lane == 0) support_out[pp] = (int64_t)cnt;
-            } else if (lane == 0) {
+            } else if (MODE == kCover && lane == 0) {
                 cover_out[pp] = hit ? 1 : 0;
             }
         }
@@ -969,6 +1008,10 @@ void scan_stats(Ctx& ctx, int mode, const PatternIndex& I, const DevBuf& glen, s
 }
 
 constexpr unsigned long long kListBudget = 3ull << 30;  // bytes of scan lists allocated from bounds
+#ifndef IG_HALF_MATCH_MAX_W
+#define IG_HALF_MATCH_MAX_W 1024
+#endif
+constexpr size_t kHalfMatchMaxW = IG_HALF_MATCH_MAX_W;  // the matcher pairs short lists when W <= this
 
 template <int MODE>
 void launch_scan(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Postings& P, const PatternIndex* I,
@@ -1041,13 +1084,17 @@ void launch_scan(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Post
     static const int half_env = getenv("IG_HALF_SCAN") ? atoi(getenv("IG_HALF_SCAN")) : 1;  // A/B
     auto launch = [&](auto count_tag, unsigned long long* work) {
         constexpr bool C = decltype(count_tag)::value;
-        if constexpr (MODE == kSupport || MODE == kCover) {
-            if (half_env) {
+        if constexpr (MODE == kSupport || MODE == kCover || MODE == kMatch) {
+            // (the matcher: only where its lists are short — the test
+            // postings' width bounds every list; C3's 1,513-word postings give
+            // 80-90-word matcher lists, C4's 464-word ones 20-22)
+            if (half_env && (MODE != kMatch || P.W <= kHalfMatchMaxW)) {
                 const size_t hblocks = std::min<size_t>((np + 15) / 16, (size_t)ctx.sm_count * 64);
                 IGB_LAUNCH(ctx, (half_scan<MODE, C>), (unsigned)hblocks, 256, 0, P.dense.as<unsigned long long>(), P.W,
                            I->beg.as<uint32_t>(), I->len.as<uint32_t>(), I->toks->as<uint16_t>(), np,
                            I->order.as<uint32_t>(), I->gid.as<uint32_t>(), goff.as<unsigned long long>(),
-                           glen.as<uint32_t>(), ew.as<uint32_t>(), em.as<unsigned long long>(), support, cover, work);
+                           glen.as<uint32_t>(), ew.as<uint32_t>(), em.as<unsigned long long>(), scores, acc, support,
+                           cover, work);
                 return;
             }
         }
