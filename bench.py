@@ -442,8 +442,13 @@ def run_b200(args):
     # schema, typed columns) -> encode -> fit -> evidence -> A/N on the host
     csv_leg = None
     if not sharded_mode:
+        # the CSV bytes in page-locked host memory, like the e2e columns
+        import numpy as np
+        csv_pinned = api.pinned_array(len(csv), np.uint8)
+        csv_pinned[:] = np.frombuffer(csv, np.uint8)
+
         def step_csv():
-            _, ctr_, cte_ = api.ingest_csv(csv, decimals=args.decimals, ratio_k=args.ratio, ctx=ctx)
+            _, ctr_, cte_ = api.ingest_csv(csv_pinned, decimals=args.decimals, ratio_k=args.ratio, ctx=ctx)
             enc_ = api.encode_training(ctr_, ctx)
             tenc_ = api.encode_rows(cte_, enc_, ctx)
             return api.fit_evidence_encoded(enc_, tenc_)
@@ -460,8 +465,8 @@ def run_b200(args):
         gc.enable()
         csv_leg = {"value": statistics.median(csv_ms) / 1e3, "unit": "s", "h2d_bytes_per_step": len(csv),
                    "d2h_bytes_per_step": d2h,
-                   "note": "CSV bytes -> ig_ingest_csv (records, numbers, schema, columns on the GPU) -> encode -> "
-                           "fit -> evidence -> A/N; the host parse this replaces is host_prep_s"}
+                   "note": "CSV bytes (page-locked host buffer) -> ig_ingest_csv (records, numbers, schema, columns on "
+                           "the GPU) -> encode -> fit -> evidence -> A/N; the host parse this replaces is host_prep_s"}
 
     # ---- SURVEY.md §8(d) "fit seconds": H2D of the parsed training columns ->
     # tokenise -> enumerate / dedup / support / score / purify -> the pure

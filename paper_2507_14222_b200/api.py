@@ -546,10 +546,19 @@ def ingest_csv(data: bytes, label_column: str = "label", attack_values=(), norma
                train_rows: Optional[int] = None, ratio_k: int = 8,
                ctx: Optional[Context] = None) -> tuple["Schema", "Columns", "Columns"]:
     """Device CSV ingest: (schema, train columns, test columns), resident on the
-    device — the same as read_csv -> slice -> infer_schema -> Columns(...).upload."""
+    device — the same as read_csv -> slice -> infer_schema -> Columns(...).upload.
+    data: bytes, or a uint8 numpy array (e.g. pinned_array: the bytes then
+    cross to the device at full copy-engine speed instead of being staged)."""
     ctx = ctx or default_context()
     hs, ht, he = C.c_void_p(), C.c_void_p(), C.c_void_p()
-    ctx.check(lib.ig_ingest_csv(ctx.handle, data, len(data), label_column.encode(), ",".join(attack_values).encode(),
+    if isinstance(data, np.ndarray):
+        if data.dtype != np.uint8 or not data.flags.c_contiguous:
+            raise ValueError("ingest_csv: a numpy input must be contiguous uint8")
+        nbytes = int(data.size)
+        data = C.cast(C.c_void_p(data.ctypes.data), C.c_char_p)
+    else:
+        nbytes = len(data)
+    ctx.check(lib.ig_ingest_csv(ctx.handle, data, nbytes, label_column.encode(), ",".join(attack_values).encode(),
                                 ",".join(normal_values).encode(), decimals,
                                 -1 if train_rows is None else int(train_rows), ratio_k,
                                 C.byref(hs), C.byref(ht), C.byref(he)))

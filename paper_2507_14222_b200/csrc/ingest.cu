@@ -261,55 +261,90 @@ __global__ void patch_cells(const uint32_t* __restrict__ list, const double* __r
 
 // per column over the training records: text seen (-> categorical) and
 // parsed count
+// per column: any text cell / how many numeric cells among the training rows;
+// a block per (column, row chunk), one atomic per block and column
 __global__ void column_kinds(const uint8_t* __restrict__ st, uint32_t n_rec, uint32_t ntr, int C,
                              int* __restrict__ text, unsigned int* __restrict__ parsed) {
-    const size_t total = (size_t)C * ntr;
-    for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += (size_t)gridDim.x * blockDim.x) {
-        const int c = (int)(q / ntr);
-        const uint8_t k = st[(size_t)c * n_rec + q % ntr];
-        if (k == kText) text[c] = 1;
-        if (k == kNum) atomicAdd(parsed + c, 1u);
+    const int c = blockIdx.y;
+    const uint8_t* k = st + (size_t)c * n_rec;
+    unsigned int cnt = 0;
+    int any_text = 0;
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < ntr; r += gridDim.x * blockDim.x) {
+        const uint8_t x = k[r];
+        any_text |= x == kText;
+        cnt += x == kNum;
+    }
+    for (int o = 16; o; o >>= 1) {
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        any_text |= __shfl_xor_sync(0xffffffffu, any_text, o);
+    }
+    __shared__ unsigned int s_cnt;
+    __shared__ int s_text;
+    if (threadIdx.x == 0) {
+        s_cnt = 0;
+        s_text = 0;
+    }
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&s_cnt, cnt);
+        if (any_text) s_text = 1;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (s_cnt) atomicAdd(parsed + c, s_cnt);
+        if (s_text) text[c] = 1;
     }
 }
 
-// Warp per numeric column: lane 0 adds the training values in row order.
-__global__ void column_stats(const double* __restrict__ val, const uint8_t* __restrict__ st, uint32_t n_rec,
-                             uint32_t ntr, const int* __restrict__ cols, int n_cols, double* __restrict__ mean,
-                             double* __restrict__ sd) {
-    const int lane = threadIdx.x & 31;
-    const int wc = (int)(((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+// A block per numeric column: the training values staged through shared
+// memory in row order, one thread adds them sequentially (the reference's
+// left-to-right double sums, pipeline.cpp:107-129) — the add chain is the
+// only serial part; the staging loads run ahead of it.
+constexpr int kStatChunk = 2048;
+__global__ void __launch_bounds__(256)
+column_stats(const double* __restrict__ val, const uint8_t* __restrict__ st, uint32_t n_rec,
+             uint32_t ntr, const int* __restrict__ cols, int n_cols, double* __restrict__ mean,
+             double* __restrict__ sd) {
+    __shared__ double s_v[kStatChunk];
+    __shared__ uint8_t s_ok[kStatChunk];
+    const int wc = blockIdx.x;
     if (wc >= n_cols) return;
     const int c = cols[wc];
     const double* v = val + (size_t)c * n_rec;
     const uint8_t* k = st + (size_t)c * n_rec;
-    double sum = 0.0;
+    double sum = 0.0, mu = 0.0, ss = 0.0;
     uint32_t cnt = 0;
-    for (uint32_t r0 = 0; r0 < ntr; r0 += 32) {
-        const uint32_t r = r0 + lane;
-        const bool ok = r < ntr && k[r] == kNum;
-        const double x = ok ? v[r] : 0.0;
-        const uint32_t m = __ballot_sync(0xffffffffu, ok);
-        for (int l = 0; l < 32; ++l) {
-            const double y = __shfl_sync(0xffffffffu, x, l);
-            if (lane == 0 && ((m >> l) & 1u)) sum = __dadd_rn(sum, y);
-        }
-        cnt += __popc(m);
-    }
-    const double mu = __ddiv_rn(sum, (double)cnt);
-    double ss = 0.0;
-    for (uint32_t r0 = 0; r0 < ntr; r0 += 32) {
-        const uint32_t r = r0 + lane;
-        const bool ok = r < ntr && k[r] == kNum;
-        const double x = ok ? v[r] : 0.0;
-        const uint32_t m = __ballot_sync(0xffffffffu, ok);
-        for (int l = 0; l < 32; ++l) {
-            const double y = __shfl_sync(0xffffffffu, x, l);
-            if (lane == 0 && ((m >> l) & 1u)) {
-                const double d = __dsub_rn(y, mu);
-                ss = __fma_rn(d, d, ss);  // the reference's contracted ss += d * d (host_pipeline.cpp)
+    for (int pass = 0; pass < 2; ++pass) {
+        for (uint32_t r0 = 0; r0 < ntr; r0 += kStatChunk) {
+            const uint32_t m = min((uint32_t)kStatChunk, ntr - r0);
+            __syncthreads();
+            for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+                const bool ok = k[r0 + i] == kNum;
+                s_ok[i] = ok ? 1 : 0;
+                s_v[i] = ok ? v[r0 + i] : 0.0;
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                if (pass == 0) {
+#pragma unroll 8
+                    for (uint32_t i = 0; i < m; ++i)
+                        if (s_ok[i]) {
+                            sum = __dadd_rn(sum, s_v[i]);
+                            ++cnt;
+                        }
+                } else {
+#pragma unroll 8
+                    for (uint32_t i = 0; i < m; ++i)
+                        if (s_ok[i]) {
+                            const double d = __dsub_rn(s_v[i], mu);
+                            ss = __fma_rn(d, d, ss);  // the reference's contracted ss += d * d (host_pipeline.cpp)
+                        }
+                }
             }
         }
+        if (pass == 0 && threadIdx.x == 0) mu = __ddiv_rn(sum, (double)cnt);
     }
+    const int lane = threadIdx.x;
     if (lane == 0) {
         mean[wc] = mu;
         sd[wc] = __dsqrt_rn(__ddiv_rn(ss, (double)cnt));
@@ -645,8 +680,11 @@ bool ingest_csv(Ctx& ctx, const char* bytes, size_t len, const std::string& labe
     DevBuf text(C * 4, ctx.stream), parsed(C * 4, ctx.stream);
     IGB_CUDA(cudaMemsetAsync(text.p, 0, C * 4, ctx.stream));
     IGB_CUDA(cudaMemsetAsync(parsed.p, 0, C * 4, ctx.stream));
-    IGB_LAUNCH(ctx, column_kinds, grid_for(ctx, (size_t)C * ntr, 256), 256, 0, st.as<uint8_t>(), n_rec, ntr, C,
-               text.as<int>(), parsed.as<unsigned int>());
+    {
+        const dim3 grid((unsigned)std::max<size_t>(1, std::min<size_t>((ntr + 255) / 256, 32)), (unsigned)C);
+        IGB_LAUNCH(ctx, column_kinds, grid, 256, 0, st.as<uint8_t>(), n_rec, ntr, C, text.as<int>(),
+                   parsed.as<unsigned int>());
+    }
     std::vector<int> htext = to_host<int>(ctx, text, C);
     std::vector<unsigned int> hparsed = to_host<unsigned int>(ctx, parsed, C);
     S = ig_schema{};
@@ -674,8 +712,8 @@ bool ingest_csv(Ctx& ctx, const char* bytes, size_t len, const std::string& labe
     if (n_num) IGB_CUDA(cudaMemcpyAsync(d_num.p, num_cols.data(), n_num * 4, cudaMemcpyHostToDevice, ctx.stream));
     if (n_num) {
         DevBuf mean(n_num * 8, ctx.stream), sd(n_num * 8, ctx.stream);
-        IGB_LAUNCH(ctx, column_stats, (n_num * 32 + 127) / 128, 128, 0, val.as<double>(), st.as<uint8_t>(), n_rec,
-                   ntr, d_num.as<int>(), n_num, mean.as<double>(), sd.as<double>());
+        IGB_LAUNCH(ctx, column_stats, n_num, 256, 0, val.as<double>(), st.as<uint8_t>(), n_rec, ntr,
+                   d_num.as<int>(), n_num, mean.as<double>(), sd.as<double>());
         std::vector<double> hm = to_host<double>(ctx, mean, n_num), hs = to_host<double>(ctx, sd, n_num);
         for (int i = 0; i < n_num; ++i) {
             S.mean[num_cols[i]] = hm[i];
