@@ -306,46 +306,53 @@ column_stats(const double* __restrict__ val, const uint8_t* __restrict__ st, uin
              uint32_t ntr, const int* __restrict__ cols, int n_cols, double* __restrict__ mean,
              double* __restrict__ sd) {
     __shared__ double s_v[kStatChunk];
-    __shared__ uint8_t s_ok[kStatChunk];
+    __shared__ uint32_t s_wc[8];
     const int wc = blockIdx.x;
     if (wc >= n_cols) return;
     const int c = cols[wc];
     const double* v = val + (size_t)c * n_rec;
     const uint8_t* k = st + (size_t)c * n_rec;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     double sum = 0.0, mu = 0.0, ss = 0.0;
     uint32_t cnt = 0;
     for (int pass = 0; pass < 2; ++pass) {
         for (uint32_t r0 = 0; r0 < ntr; r0 += kStatChunk) {
             const uint32_t m = min((uint32_t)kStatChunk, ntr - r0);
-            __syncthreads();
-            for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
-                const bool ok = k[r0 + i] == kNum;
-                s_ok[i] = ok ? 1 : 0;
-                s_v[i] = ok ? v[r0 + i] : 0.0;
+            // the chunk's numeric values, compacted in row order (the add
+            // chain then runs over a dense array, no per-row branch)
+            uint32_t base = 0;
+            for (uint32_t i0 = 0; i0 < m; i0 += blockDim.x) {
+                const uint32_t i = i0 + threadIdx.x;
+                const bool ok = i < m && k[r0 + i] == kNum;
+                const double x = ok ? v[r0 + i] : 0.0;
+                const uint32_t bal = __ballot_sync(0xffffffffu, ok);
+                if (lane == 0) s_wc[wid] = __popc(bal);
+                __syncthreads();
+                uint32_t before = 0, tot = 0;
+                for (int w = 0; w < 8; ++w) {
+                    before += w < wid ? s_wc[w] : 0u;
+                    tot += s_wc[w];
+                }
+                if (ok) s_v[base + before + __popc(bal & ((1u << lane) - 1u))] = x;
+                base += tot;
+                __syncthreads();
             }
-            __syncthreads();
             if (threadIdx.x == 0) {
                 if (pass == 0) {
-#pragma unroll 8
-                    for (uint32_t i = 0; i < m; ++i)
-                        if (s_ok[i]) {
-                            sum = __dadd_rn(sum, s_v[i]);
-                            ++cnt;
-                        }
+                    for (uint32_t i = 0; i < base; ++i) sum = __dadd_rn(sum, s_v[i]);
+                    cnt += base;
                 } else {
-#pragma unroll 8
-                    for (uint32_t i = 0; i < m; ++i)
-                        if (s_ok[i]) {
-                            const double d = __dsub_rn(s_v[i], mu);
-                            ss = __fma_rn(d, d, ss);  // the reference's contracted ss += d * d (host_pipeline.cpp)
-                        }
+                    for (uint32_t i = 0; i < base; ++i) {
+                        const double d = __dsub_rn(s_v[i], mu);
+                        ss = __fma_rn(d, d, ss);  // the reference's contracted ss += d * d (host_pipeline.cpp)
+                    }
                 }
             }
+            __syncthreads();  // s_v is refilled next chunk
         }
         if (pass == 0 && threadIdx.x == 0) mu = __ddiv_rn(sum, (double)cnt);
     }
-    const int lane = threadIdx.x;
-    if (lane == 0) {
+    if (threadIdx.x == 0) {
         mean[wc] = mu;
         sd[wc] = __dsqrt_rn(__ddiv_rn(ss, (double)cnt));
     }
