@@ -49,27 +49,53 @@ unsigned grid_for(const Ctx& ctx, size_t work, int threads) {
     return (unsigned)g;
 }
 
-__device__ __forceinline__ bool is_end(const char* b, size_t n, size_t i) {
-    const char c = b[i];
-    return c == '\n' || (c == '\r' && (i + 1 == n || b[i + 1] != '\n'));
+
+// terminator positions in [from, n) (order-preserving compaction) + quote flag.
+// Each thread takes 16 aligned bytes per step (one 16-byte load; the byte
+// after them for a '\r' at the end); bit j of ends16 = byte j ends a record.
+__device__ __forceinline__ uint32_t ends16(const char* __restrict__ b, size_t n, size_t from, size_t lo, size_t hi,
+                                          size_t p, bool& quote) {
+    // p: 16-aligned position; bytes outside [max(lo, from), min(hi, n)) do not count
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (p + 16 <= n) {
+        v = *reinterpret_cast<const uint4*>(b + p);
+    } else {
+        unsigned char t[16] = {0};
+        for (int j = 0; j < 16; ++j)
+            if (p + j < n) t[j] = (unsigned char)b[p + j];
+        memcpy(&v, t, 16);
+    }
+    const unsigned char* c = reinterpret_cast<const unsigned char*>(&v);
+    const unsigned char next = p + 16 < n ? (unsigned char)b[p + 16] : 0;
+    uint32_t m = 0;
+    const size_t a0 = max(lo, from), a1 = min(hi, n);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const size_t i = p + j;
+        if (i < a0 || i >= a1) continue;
+        const unsigned char ch = c[j];
+        const unsigned char nx = j + 1 < 16 ? c[j + 1] : next;
+        const bool last = i + 1 == n;
+        if (ch == '\n' || (ch == '\r' && (last || nx != '\n'))) m |= 1u << j;
+        quote |= ch == '"';
+    }
+    return m;
 }
 
-// terminator positions in [from, n) (order-preserving compaction) + quote flag
 __global__ void mark_ends(const char* __restrict__ b, size_t n, size_t from, uint32_t* __restrict__ cnt_block,
                           int* __restrict__ quote) {
     // pass 1: count per block
     __shared__ uint32_t sc;
     if (threadIdx.x == 0) sc = 0;
     __syncthreads();
-    const size_t chunk = ((n - from) + gridDim.x - 1) / gridDim.x;
+    const size_t chunk = (((n - from) + gridDim.x - 1) / gridDim.x + 15) & ~size_t{15};
     const size_t lo = from + (size_t)blockIdx.x * chunk, hi = min(n, lo + chunk);
     uint32_t c = 0;
     bool q = false;
-    for (size_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-        c += is_end(b, n, i) ? 1u : 0u;
-        q |= b[i] == '"';
-    }
-    atomicAdd(&sc, c);
+    for (size_t p = (lo & ~size_t{15}) + 16 * threadIdx.x; p < hi; p += 16 * (size_t)blockDim.x)
+        c += __popc(ends16(b, n, from, lo, hi, p, q));
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(&sc, c);
     if (q) atomicOr(quote, 1);
     __syncthreads();
     if (threadIdx.x == 0) cnt_block[blockIdx.x] = sc;
@@ -77,26 +103,35 @@ __global__ void mark_ends(const char* __restrict__ b, size_t n, size_t from, uin
 
 __global__ void write_ends(const char* __restrict__ b, size_t n, size_t from, const uint32_t* __restrict__ off_block,
                            uint32_t* __restrict__ ends) {
-    // pass 2: ordered positions inside each block chunk (warp ballots, serial over the chunk)
-    const size_t chunk = ((n - from) + gridDim.x - 1) / gridDim.x;
+    // pass 2: ordered positions inside each block chunk (block prefix of the
+    // per-thread counts, serial over the chunk in 16-byte steps)
+    const size_t chunk = (((n - from) + gridDim.x - 1) / gridDim.x + 15) & ~size_t{15};
     const size_t lo = from + (size_t)blockIdx.x * chunk, hi = min(n, lo + chunk);
     __shared__ uint32_t warp_cnt[32];
     __shared__ uint32_t base;
     if (threadIdx.x == 0) base = off_block[blockIdx.x];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     __syncthreads();
-    for (size_t i0 = lo; i0 < hi; i0 += blockDim.x) {
-        const size_t i = i0 + threadIdx.x;
-        const bool e = i < hi && is_end(b, n, i);
-        const uint32_t m = __ballot_sync(0xffffffffu, e);
-        if (lane == 0) warp_cnt[wid] = __popc(m);
+    bool q = false;
+    for (size_t p0 = lo & ~size_t{15}; p0 < hi; p0 += 16 * (size_t)blockDim.x) {
+        const size_t p = p0 + 16 * threadIdx.x;
+        const uint32_t m = p < hi ? ends16(b, n, from, lo, hi, p, q) : 0u;
+        const uint32_t c = __popc(m);
+        uint32_t incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) warp_cnt[wid] = incl;
         __syncthreads();
         uint32_t before = 0, total = 0;
         for (int w = 0; w < nw; ++w) {
             if (w < wid) before += warp_cnt[w];
             total += warp_cnt[w];
         }
-        if (e) ends[base + before + __popc(m & ((1u << lane) - 1u))] = (uint32_t)i;
+        uint32_t pos = base + before + incl - c;
+        for (uint32_t mm = m; mm; mm &= mm - 1) ends[pos++] = (uint32_t)(p + __ffs(mm) - 1);
         __syncthreads();
         if (threadIdx.x == 0) base += total;
         __syncthreads();
