@@ -355,7 +355,8 @@ void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m, bool enumerate 
                 b->persist();
             tr.mark("pure_index");
         }
-        IGB_CUDA(cudaStreamSynchronize(cx.stream));
+        // (no host sync: for_both_classes joins the class streams on the
+        // device, so phase C's launches queue behind both phase Bs at once)
     }, concurrent);
     m.has_pidx = vertical;
     // phase C (per class): evidence of the test encoding, once both classes'
