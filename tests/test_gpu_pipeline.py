@@ -186,3 +186,41 @@ def test_fused_fit_evidence_matches_separate_calls(api, golden_dir):
     api.fit_evidence_encoded(enc, tenc2, d_A_ptr=dA.data_ptr(), d_N_ptr=dN.data_ptr())
     torch.cuda.synchronize()
     assert np.array_equal(dA.cpu().numpy(), A) and np.array_equal(dN.cpu().numpy(), N)
+
+
+def test_narrow_column_copy_edge_values(api):
+    """ig_columns_prefetch's narrow exact form (host_pipeline.hpp) on values that
+    stress it — negatives, -0.0, empty cells, integers past int16 / int32,
+    many decimals, a column that needs the raw doubles — encodes exactly like
+    the raw path (the host checks every code bitwise; this checks the decode)."""
+    rng = np.random.default_rng(11)
+    n = 3000
+    cols = {
+        "small": rng.integers(-100, 100, n).astype(str),
+        "wide": rng.integers(-(2 ** 40), 2 ** 40, n).astype(str),
+        "mid": rng.integers(-70000, 70000, n).astype(str),
+        "rate": np.char.mod("%.2f", rng.random(n)),
+        "fine": np.char.mod("%.6f", rng.normal(0, 1, n)),
+        "raw": np.char.mod("%.17g", rng.normal(0, 1e-3, n)),
+        "negzero": np.where(rng.random(n) < 0.5, "-0.0", "0.5"),
+    }
+    for k in cols:
+        cols[k] = np.where(rng.random(n) < 0.05, "", cols[k])  # empty cells
+    label = np.where(rng.random(n) < 0.4, "attack", "normal")
+    head = ",".join(list(cols) + ["label"])
+    body = "\n".join(",".join([cols[k][i] for k in cols] + [label[i]]) for i in range(n))
+    table = api.read_csv((head + "\n" + body + "\n").encode())
+    tr, te = table.slice(0, 1000), table.slice(1000, n)
+    schema = api.infer_schema(tr, "label", decimals=2)
+    ctx = api.default_context()
+    want = api.encode_training(api.Columns(tr, schema, True), ctx)
+    ctr, cte = api.Columns(tr, schema, True), api.Columns(te, schema, False)
+    assert cte.nbytes < (n - 1000) * 8 * len(cols)  # the narrow form is smaller than the doubles
+    ctr.prefetch(ctx)
+    got = api.encode_training(ctr, ctx)
+    assert got.vocabulary == want.vocabulary
+    for c in range(2):
+        assert np.array_equal(got.matrix(c), want.matrix(c))
+    t_want = api.encode_rows(api.Columns(te, schema, False), want, ctx).matrix(2)
+    cte.prefetch(ctx)
+    assert np.array_equal(api.encode_rows(cte, want, ctx).matrix(2), t_want)
