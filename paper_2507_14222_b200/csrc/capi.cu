@@ -49,10 +49,14 @@ struct ig_model {
     uint64_t partial_total[2] = {0, 0};  // Σ candidate scores per class (checked)
     ig_candidates cand[2];
     ig_candidates pure[2];
-    // scan index of each pure dictionary (token lists ranked by the training
-    // rows' frequencies, grouped by rarest pair), built by fit; evidence reuses
-    // it for every test batch.  Absent for models assembled from dictionaries.
+    // scan index of each pure dictionary, built by fit; evidence reuses it for
+    // every test batch: the candidates' index (token lists ranked by the
+    // training rows' frequencies, grouped by rarest pair) with the pure
+    // patterns' positions selected (pidx[c].sel), and the candidates' scores
+    // in that index's pattern ids (pscore: the candidate set itself may be
+    // reordered on copy-out).  Absent for models assembled from dictionaries.
     igb::PatternIndex pidx[2];
+    igb::DevBuf pscore[2];
     bool has_pidx = false;
     double ms[6] = {0, 0, 0, 0, 0, 0};
     igb::EnumStats stats[2];
@@ -334,24 +338,24 @@ void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m, bool enumerate 
         P.rows.buf.alloc(std::max<size_t>(np * k, 1) * 8, cx.stream);
         P.support.alloc(std::max<size_t>(np, 1) * 8, cx.stream);
         P.score.alloc(std::max<size_t>(np, 1) * 8, cx.stream);
-        DevBuf kept;  // pure (compacted) position -> candidate index
         P.rows.n = igb::compact_unflagged(cx, C.rows.data(), C.support.as<int64_t>(), C.score.as<int64_t>(),
                                           mask.as<uint8_t>(), np, k, P.rows.data(), P.support.as<int64_t>(),
-                                          P.score.as<int64_t>(), vertical ? &kept : nullptr);
+                                          P.score.as<int64_t>(), nullptr);
         P.has_support = P.has_score = true;
         tr.mark("compact");
-        DevBuf order;  // canonical position -> compacted position
-        igb::canonical_order(cx, P.rows, &P.support, &P.score, vertical ? &order : nullptr);
+        igb::canonical_order(cx, P.rows, &P.support, &P.score, nullptr);
         tr.mark("order");
         if (vertical) {
-            // the pure dictionary's scan index = the candidates' restricted to it
-            const size_t n = P.rows.n;
-            DevBuf src(std::max<size_t>(n, 1) * 4, cx.stream);
-            igb::compose_u32(cx, kept.as<uint32_t>(), order.p ? order.as<uint32_t>() : nullptr, n,
-                             src.as<uint32_t>());
-            igb::subset_pattern_index(cx, CI[c], src.as<uint32_t>(), n, m.pidx[c]);
+            // the pure dictionary's scan index = the candidates' index with the
+            // pure patterns' positions selected (no re-grouping), scores in
+            // candidate ids
+            igb::select_unflagged_positions(cx, CI[c], mask.as<uint8_t>(), P.rows.n);
+            m.pidx[c] = std::move(CI[c]);
+            m.pscore[c].alloc(std::max<size_t>(np, 1) * 8, cx.stream);
+            if (np)
+                IGB_CUDA(cudaMemcpyAsync(m.pscore[c].p, C.score.p, np * 8, cudaMemcpyDeviceToDevice, cx.stream));
             for (DevBuf* b : {&m.pidx[c].beg, &m.pidx[c].len, m.pidx[c].toks.get(), &m.pidx[c].order, &m.pidx[c].gid,
-                              &m.pidx[c].gkey, &m.pidx[c].pid, &m.pidx[c].pkey})
+                              &m.pidx[c].gkey, &m.pidx[c].pid, &m.pidx[c].pkey, &m.pidx[c].sel, &m.pscore[c]})
                 b->persist();
             tr.mark("pure_index");
         }
@@ -373,7 +377,7 @@ void fit_impl(igb::Ctx& ctx, View X[2], uint32_t L, ig_model& m, bool enumerate 
             const ig_candidates& P = m.pure[c];
             // Σ scores <= Σ candidate scores, checked <= INT64_MAX above: unchecked sums
             IGB_CUDA(cudaStreamWaitEvent(cx.stream, ev->job->done, 0));
-            igb::posting_match(cx, P.rows.data(), P.rows.n, k, P.score.as<int64_t>(), ev->job->P, ev->out[c],
+            igb::posting_match(cx, P.rows.data(), P.rows.n, k, m.pscore[c].as<int64_t>(), ev->job->P, ev->out[c],
                                nullptr, true, &m.pidx[c]);
             tr.mark("evidence");
         }, concurrent);
@@ -447,8 +451,9 @@ void evidence_impl(igb::Ctx& ctx, const ig_model& m, const int64_t* d_tests, siz
             const ig_candidates& P = m.pure[c];
             // the fit checked Σ candidate scores <= INT64_MAX (total_score); pure ⊆ candidates
             igb::Trace trc(cx, "evidence", c);
-            igb::posting_match(cx, P.rows.data(), P.rows.n, k, P.score.as<int64_t>(), PT, c == 0 ? d_A : d_N,
-                               flag.as<int>(), m.sum_fits, m.has_pidx ? &m.pidx[c] : nullptr);
+            igb::posting_match(cx, P.rows.data(), P.rows.n, k,
+                               m.has_pidx ? m.pscore[c].as<int64_t>() : P.score.as<int64_t>(), PT,
+                               c == 0 ? d_A : d_N, flag.as<int>(), m.sum_fits, m.has_pidx ? &m.pidx[c] : nullptr);
             trc.mark("match");
         }, m.pure[0].rows.n + m.pure[1].rows.n <= kConcurrentPatterns);
         int h = 0;

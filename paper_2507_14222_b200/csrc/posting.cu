@@ -594,7 +594,7 @@ grouped_scan(const unsigned long long* __restrict__ dense, size_t W, size_t n_ro
              const uint32_t* __restrict__ ew, const unsigned long long* __restrict__ em,
              const int64_t* __restrict__ scores, unsigned long long* __restrict__ acc,
              int64_t* __restrict__ support_out, uint8_t* __restrict__ cover_out, int* __restrict__ flags,
-             unsigned long long* __restrict__ work) {
+             unsigned long long* __restrict__ work, const uint32_t* __restrict__ sel) {
     const int lane = threadIdx.x & 31;
     const size_t warps = ((size_t)gridDim.x * blockDim.x) >> 5;
     // matcher: per warp, the current pattern's tokens 3..34, read four at a
@@ -605,7 +605,8 @@ grouped_scan(const unsigned long long* __restrict__ dense, size_t W, size_t n_ro
     uint32_t* so = s_off[(threadIdx.x >> 5) & 7];
     bool ovf = false;
     unsigned long long nand = 0;  // COUNT only
-    for (size_t i = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < np; i += warps) {
+    for (size_t i0 = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i0 < np; i0 += warps) {
+        const size_t i = sel ? sel[i0] : i0;  // np positions: all, or the selected subset
         const uint32_t p = order[i];
         const uint32_t g = gid[i];
         const uint32_t o = tok_beg[p];
@@ -734,7 +735,8 @@ half_scan(const unsigned long long* __restrict__ dense, size_t W, const uint32_t
           const unsigned long long* __restrict__ goff, const uint32_t* __restrict__ glen,
           const uint32_t* __restrict__ ew, const unsigned long long* __restrict__ em,
           const int64_t* __restrict__ scores, unsigned long long* __restrict__ acc,
-          int64_t* __restrict__ support_out, uint8_t* __restrict__ cover_out, unsigned long long* __restrict__ work) {
+          int64_t* __restrict__ support_out, uint8_t* __restrict__ cover_out, unsigned long long* __restrict__ work,
+          const uint32_t* __restrict__ sel) {
     static_assert(MODE == kSupport || MODE == kCover || MODE == kMatch, "half_scan: support, coverage or match");
     constexpr bool kSmemTok = MODE == kMatch;
     const int lane = threadIdx.x & 31, half = lane >> 4, hl = lane & 15;
@@ -747,11 +749,12 @@ half_scan(const unsigned long long* __restrict__ dense, size_t W, const uint32_t
     const size_t npairs = (np + 1) / 2;
     unsigned long long nand = 0;
     for (size_t pi = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; pi < npairs; pi += warps) {
-        const size_t ih = 2 * pi + (size_t)half;
-        const bool has = ih < np;
+        const size_t ih0 = 2 * pi + (size_t)half;
+        const bool has = ih0 < np;
         uint32_t p = 0, o = 0, m = 0, len = 0;
         unsigned long long base = 0, sc = 0;
         if (has) {
+            const size_t ih = sel ? sel[ih0] : ih0;  // np positions: all, or the selected subset
             p = order[ih];
             const uint32_t g = gid[ih];
             o = tok_beg[p];
@@ -1026,7 +1029,8 @@ void launch_scan(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Post
         I = &local;
         tr.mark("pattern_index");
     }
-    if (I->np != np) fail(IG_E_CUDA, "pattern index does not match the pattern set");
+    const uint32_t* sel = I->sel.p ? I->sel.as<uint32_t>() : nullptr;
+    if ((sel ? I->nsel : I->np) != np) fail(IG_E_CUDA, "pattern index does not match the pattern set");
     const size_t G = I->G, G2 = I->G2;
     // parent (t1, t2) lists S2 = non-zero (w, post[t1][w] & post[t2][w]) in P,
     // then each (t1, t2, t3) group's list S = S2 filtered by post[t3]
@@ -1094,7 +1098,7 @@ void launch_scan(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Post
                            I->beg.as<uint32_t>(), I->len.as<uint32_t>(), I->toks->as<uint16_t>(), np,
                            I->order.as<uint32_t>(), I->gid.as<uint32_t>(), goff.as<unsigned long long>(),
                            glen.as<uint32_t>(), ew.as<uint32_t>(), em.as<unsigned long long>(), scores, acc, support,
-                           cover, work);
+                           cover, work, sel);
                 return;
             }
         }
@@ -1102,7 +1106,7 @@ void launch_scan(Ctx& ctx, const int64_t* d_pat, size_t np, size_t k, const Post
                    P.n, I->beg.as<uint32_t>(), I->len.as<uint32_t>(), I->toks->as<uint16_t>(), np,
                    I->order.as<uint32_t>(), I->gid.as<uint32_t>(), goff.as<unsigned long long>(),
                    glen.as<uint32_t>(), ew.as<uint32_t>(), em.as<unsigned long long>(), scores, acc, support,
-                   cover, flags, work);
+                   cover, flags, work, sel);
     };
     launch(std::false_type{}, nullptr);
     tr.mark("grouped_scan");
@@ -1314,6 +1318,34 @@ void subset_pattern_index(Ctx& ctx, const PatternIndex& S, const uint32_t* d_src
                key.as<unsigned long long>());
     group_ids(ctx, key.as<unsigned long long>(), n, I);
     tr.mark("groups");
+}
+
+namespace {
+__global__ void position_keep(const uint32_t* __restrict__ order, size_t n, const uint8_t* __restrict__ flag,
+                              uint8_t* __restrict__ keep, uint32_t* __restrict__ pos) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        keep[i] = flag[order[i]] ? 0 : 1;
+        pos[i] = (uint32_t)i;
+    }
+}
+}  // namespace
+
+size_t select_unflagged_positions(Ctx& ctx, PatternIndex& I, const uint8_t* d_flag, size_t count) {
+    const size_t n = I.np;
+    I.sel.alloc(std::max<size_t>(n, 1) * 4, ctx.stream);
+    I.nsel = 0;
+    if (n == 0) return 0;
+    DevBuf keep(n, ctx.stream), pos(n * 4, ctx.stream), nsel(8, ctx.stream);
+    IGB_LAUNCH(ctx, position_keep, grid_for(ctx, n, 256), 256, 0, I.order.as<uint32_t>(), n, d_flag,
+               keep.as<uint8_t>(), pos.as<uint32_t>());
+    size_t tb = 0;
+    IGB_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, pos.as<uint32_t>(), keep.as<uint8_t>(), I.sel.as<uint32_t>(),
+                                        nsel.as<int64_t>(), (int64_t)n, ctx.stream));
+    DevBuf temp(tb, ctx.stream);
+    IGB_CUDA(cub::DeviceSelect::Flagged(temp.p, tb, pos.as<uint32_t>(), keep.as<uint8_t>(), I.sel.as<uint32_t>(),
+                                        nsel.as<int64_t>(), (int64_t)n, ctx.stream));
+    I.nsel = count;  // (the caller's compaction of the same flags counted them)
+    return I.nsel;
 }
 
 namespace {

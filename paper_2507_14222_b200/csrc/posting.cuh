@@ -46,6 +46,11 @@ struct PatternIndex {
     size_t G2 = 0;   // parent groups (t1, t2)
     DevBuf pid;      // G u32: parent of each group
     DevBuf pkey;     // G2 u32: (t1 << 16) | t2
+    // Optional: scan only these positions (of the group order), nsel of them —
+    // a subset of the patterns (the pure ones among the candidates) without a
+    // re-built index; pattern ids (and scores) stay the full set's.
+    DevBuf sel;
+    size_t nsel = 0;
 };
 
 // descending: most frequent first (default: rarest first)
@@ -65,6 +70,9 @@ void group_ids(Ctx& ctx, const unsigned long long* d_sorted_key, size_t np, Patt
 // index of the patterns S.pattern[d_src_of[i]], i < n (a subset, e.g. the pure
 // patterns among the candidates), without re-ranking or re-sorting
 void subset_pattern_index(Ctx& ctx, const PatternIndex& S, const uint32_t* d_src_of, size_t n, PatternIndex& I);
+// I.sel = the positions (group order) whose pattern is not flagged, in order
+// (count: how many there are, known to the caller)
+size_t select_unflagged_positions(Ctx& ctx, PatternIndex& I, const uint8_t* d_flag, size_t count);
 
 bool postings_supported(uint32_t L, size_t n);
 // canonical: index rows in words::less order (clusters rows that share tokens).
