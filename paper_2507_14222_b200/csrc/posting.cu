@@ -726,7 +726,8 @@ __device__ __forceinline__ void scatter_runs(unsigned long long mw, unsigned lon
 // neighbouring patterns, each on a half-warp, whenever both group lists fit 16
 // words; otherwise it runs them one after the other on the full warp, as
 // grouped_scan does (the matcher's full-warp path reads the pattern's tokens
-// from a per-warp shared-memory row, support / coverage from shuffles).
+// from a per-warp shared-memory row — so does support, whose full-warp lists
+// are long at C4 — coverage from shuffles).
 template <int MODE, bool COUNT = false>
 __global__ void __launch_bounds__(256)
 half_scan(const unsigned long long* __restrict__ dense, size_t W, const uint32_t* __restrict__ tok_beg,
@@ -738,7 +739,7 @@ half_scan(const unsigned long long* __restrict__ dense, size_t W, const uint32_t
           int64_t* __restrict__ support_out, uint8_t* __restrict__ cover_out, unsigned long long* __restrict__ work,
           const uint32_t* __restrict__ sel) {
     static_assert(MODE == kSupport || MODE == kCover || MODE == kMatch, "half_scan: support, coverage or match");
-    constexpr bool kSmemTok = MODE == kMatch;
+    constexpr bool kSmemTok = MODE == kMatch || MODE == kSupport;
     const int lane = threadIdx.x & 31, half = lane >> 4, hl = lane & 15;
     const unsigned hmask = half ? 0xffff0000u : 0x0000ffffu;
     const uint32_t Wu = (uint32_t)W, wb = Wu * 8u;
