@@ -725,9 +725,8 @@ __device__ __forceinline__ void scatter_runs(unsigned long long mw, unsigned lon
 // matcher at C4: 20-22) leave half of a warp's lanes idle: a warp takes two
 // neighbouring patterns, each on a half-warp, whenever both group lists fit 16
 // words; otherwise it runs them one after the other on the full warp, as
-// grouped_scan does (the matcher's full-warp path reads the pattern's tokens
-// from a per-warp shared-memory row — so does support, whose full-warp lists
-// are long at C4 — coverage from shuffles).
+// grouped_scan does, the pattern's tokens read from a per-warp shared-memory
+// row (one 16-byte broadcast per four tokens).
 template <int MODE, bool COUNT = false>
 __global__ void __launch_bounds__(256)
 half_scan(const unsigned long long* __restrict__ dense, size_t W, const uint32_t* __restrict__ tok_beg,
@@ -739,7 +738,6 @@ half_scan(const unsigned long long* __restrict__ dense, size_t W, const uint32_t
           int64_t* __restrict__ support_out, uint8_t* __restrict__ cover_out, unsigned long long* __restrict__ work,
           const uint32_t* __restrict__ sel) {
     static_assert(MODE == kSupport || MODE == kCover || MODE == kMatch, "half_scan: support, coverage or match");
-    constexpr bool kSmemTok = MODE == kMatch || MODE == kSupport;
     const int lane = threadIdx.x & 31, half = lane >> 4, hl = lane & 15;
     const unsigned hmask = half ? 0xffff0000u : 0x0000ffffu;
     const uint32_t Wu = (uint32_t)W, wb = Wu * 8u;
@@ -817,11 +815,9 @@ half_scan(const unsigned long long* __restrict__ dense, size_t W, const uint32_t
             const unsigned long long ss = __shfl_sync(kFull, sc, 16 * h);
             const uint32_t t0 = mm ? (uint32_t)toks[oo] : 0u;
             const uint32_t tl = (uint32_t)lane < mm ? (uint32_t)toks[oo + lane] : t0;
-            if (kSmemTok) {
-                __syncwarp();  // the previous pattern's tokens are read
-                st[0][lane >= 3 ? lane - 3 : 29 + lane] = lane >= 3 ? tl : t0;
-                __syncwarp();
-            }
+            __syncwarp();  // the previous pattern's tokens are read
+            st[0][lane >= 3 ? lane - 3 : 29 + lane] = lane >= 3 ? tl : t0;
+            __syncwarp();
             uint32_t cnt = 0;
             bool hit = false;
             for (uint32_t j0 = 0; j0 < ll; j0 += 32) {
@@ -835,15 +831,7 @@ half_scan(const unsigned long long* __restrict__ dense, size_t W, const uint32_t
                     if ((uint32_t)t >= mm) break;
                     const bool live = mw != 0ull;
                     if (!__any_sync(kFull, live)) break;
-                    uint4 tw;
-                    if (kSmemTok) {
-                        tw = reinterpret_cast<const uint4*>(st[0])[q];
-                    } else {  // compile-time shuffle lanes; 32..34 wrap to tokens 0..2 (no-ops)
-                        tw.x = __shfl_sync(kFull, tl, t);
-                        tw.y = __shfl_sync(kFull, tl, (t + 1) & 31);
-                        tw.z = __shfl_sync(kFull, tl, (t + 2) & 31);
-                        tw.w = __shfl_sync(kFull, tl, (t + 3) & 31);
-                    }
+                    const uint4 tw = reinterpret_cast<const uint4*>(st[0])[q];
                     if (COUNT && live) nand += min(4u, mm - (uint32_t)t);
                     if (live) mw &= (ld_tok(col, tw.x, wb) & ld_tok(col, tw.y, wb)) & (ld_tok(col, tw.z, wb) & ld_tok(col, tw.w, wb));
                 }
