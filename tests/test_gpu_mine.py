@@ -174,3 +174,50 @@ def test_canonical_order_long_and_short_key_runs(api, word0_values, expect):
     assert want.shape[0] > 24576
     cs = api.enumerate_candidates(api.PackedMatrix(X, 64 * k))
     assert np.array_equal(cs.patterns.words, want)
+
+
+def _onehot_rows(rng, n, card):
+    """One-hot records over categorical fields of the given cardinalities
+    (skewed values, like encoded NSL-KDD/CICIDS columns): bool [n, sum(card)]."""
+    B = np.zeros((n, sum(card)), bool)
+    off = 0
+    for c in card:
+        v = np.minimum(rng.geometric(0.35, n) - 1, c - 1)
+        B[np.arange(n), off + v] = True
+        off += c
+    return B
+
+
+@pytest.mark.parametrize("seed", [5, 6])
+def test_fit_fuzz_injected_contradictions(api, seed):
+    """SPEC.md:643 fuzzed pipeline at ~10^6 candidates: encoded-shape records
+    (15 one-hot fields, L = 88), with contradictions injected — 10 % of the
+    normal rows are copies of attack rows (every candidate they hold becomes
+    impure in both classes) and 4 % are attack rows with extra tokens (supersets
+    that cover attack patterns).  Candidates, supports, scores, both pure
+    dictionaries and A/N must equal the oracle's exactly."""
+    from tests.helpers import pack_bits
+    rng = np.random.default_rng(seed)
+    card = [3, 5, 8, 2, 12, 4, 6, 2, 9, 3, 7, 2, 5, 16, 4]
+    L = sum(card)
+    A = _onehot_rows(rng, 2500, card)
+    N = _onehot_rows(rng, 2000, card)
+    N[:250] = A[rng.choice(len(A), 250, replace=False)]
+    N[250:330] = A[rng.choice(len(A), 80, replace=False)] | _onehot_rows(rng, 80, card)
+    N = N[rng.permutation(len(N))]
+    Xa, Xn = pack_bits(A), pack_bits(N)
+    ref = oracle.fit(Xa, Xn)
+    assert len(ref.candidates[0].words) > 500_000
+    assert len(ref.pure[0].words) < len(ref.candidates[0].words) // 4   # the injections bite
+    m = api.fit(Xa, Xn, L)
+    for c in range(2):
+        for which, want in ((0, ref.candidates[c]), (1, ref.pure[c])):
+            d = m.dictionary(c, which)
+            assert np.array_equal(d.words, want.words), (c, which)
+            assert np.array_equal(d.supports, want.supports), (c, which)
+            assert np.array_equal(d.scores, want.scores), (c, which)
+    T = pack_bits(_onehot_rows(rng, 3000, card))
+    T[:200] = Xn[:200]                                       # test rows equal to training rows
+    A_, N_ = m.evidence(T)
+    assert np.array_equal(A_, oracle.fused_score(ref.pure[0].words, ref.pure[0].scores, T))
+    assert np.array_equal(N_, oracle.fused_score(ref.pure[1].words, ref.pure[1].scores, T))
